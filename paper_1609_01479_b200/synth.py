@@ -1,0 +1,60 @@
+"""Seeded synthetic inputs shared by the tests, the oracle leg and the bench.
+
+This module holds random numbers and array shapes only -- none of the
+method's arithmetic (no moments, stencils or equilibria).  Both the CUDA path
+(through the C ABI) and the CPU oracle are fed from here; everything else
+about the initial state is computed by each side on its own (the GPU by
+``lb_init_equilibrium``, the oracle by ``oracle.lb_ref.equilibrium_state``).
+
+Recipe (BASELINE.json configs; reading R15):
+  spinodal   phi = phi0 + amp * (2U - 1), U ~ U[0,1) i.i.d. from NumPy's
+             PCG64 ``default_rng(seed)``, drawn in canonical site order
+             s = x + nx*(y + ny*z); rho = 1, u = 0.
+  rough      phi ~ U(-0.8, 0.8), rho = 1 + 0.05 U, |u_a| <= 0.02, plus noise
+             arrays of amplitude 1e-3 for f and g (exercises every term).
+All arrays are float64, shaped (nz, ny, nx) or (k, nz, ny, nx).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+Q = 19  # number of distribution components per site (D3Q19)
+
+
+def _rng(seed: int) -> np.random.Generator:
+    return np.random.default_rng(seed)
+
+
+def spinodal_phi(nx: int, ny: int, nz: int, seed: int = 0, phi0: float = 0.0, amp: float = 0.01) -> np.ndarray:
+    """Order parameter of a quench into the spinodal region: phi0 +- amp noise."""
+    u = _rng(seed).random(nx * ny * nz)
+    return (phi0 + amp * (2.0 * u - 1.0)).reshape(nz, ny, nx)
+
+
+def spinodal_fields(nx: int, ny: int, nz: int, seed: int = 0, phi0: float = 0.0, amp: float = 0.01):
+    """(rho, u, phi) of the spinodal initial state: rho = 1, u = 0."""
+    rho = np.ones((nz, ny, nx))
+    u = np.zeros((3, nz, ny, nx))
+    return rho, u, spinodal_phi(nx, ny, nz, seed, phi0, amp)
+
+
+def rough_fields(nx: int, ny: int, nz: int, seed: int = 1):
+    """(rho, u, phi, noise_f, noise_g): a rough state that exercises every term."""
+    r = _rng(seed)
+    shape = (nz, ny, nx)
+    phi = r.uniform(-0.8, 0.8, size=shape)
+    rho = 1.0 + 0.05 * r.random(shape)
+    u = r.uniform(-0.02, 0.02, size=(3,) + shape)
+    noise_f = 1e-3 * r.uniform(-1.0, 1.0, size=(Q,) + shape)
+    noise_g = 1e-3 * r.uniform(-1.0, 1.0, size=(Q,) + shape)
+    return rho, u, phi, noise_f, noise_g
+
+
+def sample_sites(nx: int, ny: int, nz: int, n: int, seed: int = 7) -> list[tuple[int, int, int]]:
+    """n distinct sampled sites, always including the 8 corners (wrap-around edges)."""
+    r = _rng(seed)
+    corners = [(x, y, z) for x in (0, nx - 1) for y in (0, ny - 1) for z in (0, nz - 1)]
+    picks = set(corners)
+    while len(picks) < min(n, nx * ny * nz):
+        picks.add((int(r.integers(nx)), int(r.integers(ny)), int(r.integers(nz))))
+    return sorted(picks, key=lambda s: (s[2], s[1], s[0]))
