@@ -1,0 +1,172 @@
+/*
+ * lb.h -- C ABI of the B200-native D3Q19 binary-fluid lattice-Boltzmann step.
+ *
+ * What one step computes (sec. 2.1.1; readings R1-R22 of
+ * DESIGN.md, which spell out the equations the paper only names):
+ *   1. moments rho = sum_i f_i, j = sum_i c_i f_i, phi = sum_i g_i            (A.3)
+ *   2. "Order Parameter Gradients": central grad phi, 7-point lap phi        (A.2)
+ *   3. chemical potential mu and "Chemical Stress" P_ab                       (A.4)
+ *   4. force F = -div P ("the divergence of the 'Chemical stress'")           (A.5)
+ *   5. "Collision": BGK of f with Guo forcing, BGK of g towards g^eq(phi,u,Gamma mu)
+ *                                                                             (A.6-A.7)
+ *   6. "Propagation": "displacing the fluid data one lattice spacing in the
+ *      appropriate direction", periodic                                       (A.8)
+ *   7. halo exchange between z-slabs ("each local sub-domain is surrounded by a
+ *      halo region populated using neighboring sub-domain data")
+ *
+ * Conventions
+ *   - All field values are IEEE fp64 ("a set of double precision values
+ *     at each lattice point").
+ *   - Canonical D3Q19 order: rest first, then the 18 moving velocities in
+ *     descending lexicographic (cx, cy, cz) (reading R1).
+ *   - Site index s = x + nx*(y + ny*z), x fastest.  A distribution array is
+ *     f[p*nloc + s], p = 0..18, nloc = nx*ny*nz_local.
+ *   - State = the PRE-collision (post-propagation) f and g at integer time t (R12).
+ *
+ * Ownership: the caller owns every host array and the library never keeps a
+ * pointer to one after a call returns; the library owns all device memory, its
+ * CUDA stream and (for lb_create_slab) its NCCL communicator.  Host<->device
+ * copies are synchronous: on return the data has been transferred.  Host
+ * arrays may be pageable or page-locked (page-locked is faster).
+ *
+ * Errors: every int-returning call returns LB_OK (0) or a negative code; the
+ * handle's lb_last_error() then holds a one-line message.  After LB_ECUDA or
+ * LB_ENCCL the handle is unusable except for lb_destroy / lb_last_error.
+ * A handle is thread-compatible: one thread at a time.
+ */
+#ifndef LB_H
+#define LB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  LB_OK = 0,
+  LB_EINVAL = -1,   /* null pointer, bad extent, bad parameter, nsteps < 0 ...     */
+  LB_ENOMEM = -2,   /* device or host allocation failed                            */
+  LB_ECUDA = -3,    /* CUDA runtime failure; handle unusable                       */
+  LB_ENCCL = -4,    /* NCCL failure; handle unusable                               */
+  LB_ESTATE = -5,   /* step / get before any set_state or init_equilibrium        */
+  LB_ENUMERIC = -6  /* some site had rho <= 0 or a non-finite value (R22)  */
+};
+
+/* Physical parameters of the problem statement (BASELINE north_star; R2, R10).
+ * Free energy  F[phi] = sum_x A/2 phi^2 + B/4 phi^4 + kappa/2 |grad phi|^2.    */
+typedef struct {
+  double tau_f;    /* BGK relaxation time of f, finite and > 1/2                  */
+  double tau_g;    /* BGK relaxation time of g, finite and > 1/2                  */
+  double A, B;     /* bulk free-energy coefficients, finite                        */
+  double kappa;    /* interfacial coefficient, finite and >= 0                     */
+  double mobility; /* M >= 0; internally Gamma = M / (tau_g - 1/2)   (R10)         */
+} lb_params;
+
+typedef struct lb_ctx lb_t;
+
+/* Library version string (static storage). */
+const char* lb_version(void);
+
+/* Whole periodic lattice nx x ny x nz on the current CUDA device.
+ * Extents must be >= 3.  *out receives the handle (NULL on failure). */
+int lb_create(int nx, int ny, int nz, const lb_params* params, lb_t** out);
+
+/* Same lattice, decomposed inside this handle into nslabs z-slabs of nz/nslabs
+ * planes each, whose halos are exchanged by device-to-device copies on this
+ * GPU ("loopback" transport).  Results are bitwise identical to lb_create; it
+ * exists to exercise the slab index maps on one GPU.  nz % nslabs == 0 and
+ * nz/nslabs >= 2.  The host arrays of set/get are still the whole lattice. */
+int lb_create_loopback(int nx, int ny, int nz, const lb_params* params, int nslabs, lb_t** out);
+
+/* Bootstrap for lb_create_slab: rank 0 fills 128 bytes (an ncclUniqueId); the
+ * caller broadcasts them to all ranks by any means.  */
+int lb_nccl_get_unique_id(void* id128);
+
+/* Rank `rank` of a z-slab decomposition over `nranks` processes, one GPU each
+ * (the current CUDA device).  Rank r owns global z in [r*L, (r+1)*L), L =
+ * nz/nranks >= 2; halos travel by NCCL send/recv to ranks r+-1 (mod nranks).
+ * Collective: every rank must call it.  Host arrays of set/get/init are this
+ * rank's slab only (nloc = nx*ny*L sites).  nranks == 1 is lb_create. */
+int lb_create_slab(int nx, int ny, int nz, const lb_params* params, int nranks, int rank,
+                   const void* id128, lb_t** out);
+
+/* Number of sites this handle's host arrays hold (nloc).  Returns 0 for NULL. */
+size_t lb_local_sites(const lb_t* h);
+
+/* Load the state: f, g are host arrays of 19*nloc doubles each, canonical
+ * layout.  Bitwise: lb_get_state right after returns exactly these bits. */
+int lb_set_state(lb_t* h, const double* f, const double* g);
+
+/* Initialise at local equilibrium from macroscopic host fields (R15):
+ * f = f^eq(rho, u), g = g^eq(phi, u, Gamma*mu[phi]) with mu from the 7-point
+ * Laplacian of phi (A.4).  rho: nloc doubles or NULL (rho = 1); u: 3*nloc
+ * doubles u[a*nloc + s] or NULL (u = 0); phi: nloc doubles (required).
+ * Collective for slabs (exchanges phi halo planes). */
+int lb_init_equilibrium(lb_t* h, const double* rho, const double* u, const double* phi);
+
+/* Advance nsteps >= 0 timesteps; returns after the device has finished.
+ * LB_ENUMERIC if any site had rho <= 0 or a non-finite f/g/phi during these
+ * steps (the flag is checked once, at the end).  Collective for slabs. */
+int lb_step(lb_t* h, int nsteps);
+
+/* Read the state back into host arrays of 19*nloc doubles each. */
+int lb_get_state(lb_t* h, double* f, double* g);
+
+/* Order parameter phi = sum_i g_i of the current state, nloc doubles. */
+int lb_get_phi(lb_t* h, double* phi);
+
+/* Frees device memory, the stream and the communicator.  NULL-safe. */
+void lb_destroy(lb_t* h);
+
+/* Last error message of this handle ("" if none); for a NULL handle, the last
+ * error of a failed lb_create* call in this thread.  Owned by the library. */
+const char* lb_last_error(const lb_t* h);
+
+/* ---- measurement support (bench.py) ------------------------------------ */
+
+/* The cudaStream_t every kernel and copy of this handle is issued on. */
+void* lb_stream(const lb_t* h);
+
+/* Kernels launched by this handle since creation (host-side count). */
+long long lb_launch_count(const lb_t* h);
+
+/* Per-kernel CUDA-event timing.  When enabled, every launch is bracketed by
+ * events on the handle's stream; totals accumulate until reset. */
+int lb_profile_enable(lb_t* h, int on);
+int lb_profile_reset(lb_t* h);
+/* Entry i (0 <= i < lb_profile_count): kernel name (static storage), summed
+ * device milliseconds and number of timed launches. */
+int lb_profile_count(const lb_t* h);
+int lb_profile_entry(const lb_t* h, int i, const char** name, double* total_ms, long long* launches);
+
+/* Algorithmic HBM bytes one site update moves in the step kernel (reads and
+ * writes of f and g once each: 38 * 2 * 8 = 608).  Used for the roofline. */
+double lb_bytes_per_site(void);
+
+/* ---- test support ------------------------------------------------------- */
+
+/* Integer propagation map of A.8 as the device code implements it: the
+ * composition of the kernels' push addressing with the halo plan of an
+ * nslabs-way z-slab decomposition, inverted into a pull map over the GLOBAL
+ * lattice:  out[p*N + s] = canonical global index of the site whose
+ * post-collision component p streams into site s (N = nx*ny*nz, int64).
+ * Host-only; no GPU needed.  LB_EINVAL on bad sizes or if the composition is
+ * not a permutation. */
+int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out);
+
+/* Propagation only (collision = identity) for nsteps steps on the device, with
+ * the same kernel addressing and halo exchanges as lb_step.  Test support. */
+int lb_debug_stream(lb_t* h, int nsteps);
+
+/* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of
+ * nranks, the ranks it sends its +z and -z halo to, and the number of doubles
+ * per message: distributions (10 components x nx*ny) and phi (2 planes x nx*ny).
+ * out[0]=up, out[1]=down, out[2]=dist doubles, out[3]=phi doubles. */
+int lb_halo_plan(int nx, int ny, int nz, int nranks, int rank, int64_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LB_H */

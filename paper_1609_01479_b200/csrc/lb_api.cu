@@ -1,0 +1,591 @@
+// lb_api.cu -- host runtime behind the C ABI of include/lb.h.
+//
+// Owns device memory, the CUDA stream, the halo transport (loopback copies or
+// NCCL send/recv, "halo region populated using neighboring sub-domain
+// data") and per-kernel CUDA-event timing.  One handle = one z-slab set on one
+// GPU.  See DESIGN.md "Boundary" and "Multi-GPU".
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lb.h"
+#include "lb_kernels.cuh"
+
+using namespace lbk;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+enum KernelId { K_PHI = 0, K_STEP, K_INIT, K_PERMUTE, K_HALO_DIST, K_HALO_PHI, K_COUNT };
+const char* const kKernelNames[K_COUNT] = {"k_phi", "k_step", "k_init_eq", "k_permute", "halo_dist", "halo_phi"};
+
+struct Slab {
+  int z0 = 0;  // global z of local plane 0
+  double* A = nullptr;
+  double* B = nullptr;
+  double* phi = nullptr;
+};
+
+struct Pending {
+  int kid;
+  cudaEvent_t e0, e1;
+};
+
+}  // namespace
+
+struct lb_ctx {
+  int nx = 0, ny = 0, nz = 0;
+  int nzl = 0;            // planes per slab
+  int nranks = 1, rank = 0;
+  int nslabs = 1;         // slabs held by this handle (loopback > 1)
+  lb_params prm{};
+  DevParams dp{};
+  Geom G{};
+  std::vector<Slab> slabs;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int* d_flag = nullptr;
+  int* h_flag = nullptr;  // pinned
+  ncclComm_t comm = nullptr;
+  bool have_state = false;
+  bool broken = false;
+  std::string err;
+  long long launches = 0;
+  // profiling
+  bool prof_on = false;
+  double prof_ms[K_COUNT] = {0};
+  long long prof_n[K_COUNT] = {0};
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> ev_pool;
+};
+
+namespace {
+
+int set_err(lb_ctx* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) {
+    h->err = buf;
+    if (code == LB_ECUDA || code == LB_ENCCL) h->broken = true;
+  } else {
+    g_create_error = buf;
+  }
+  return code;
+}
+
+#define CK(h, call)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return set_err((h), e_ == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA, "%s: %s (%s:%d)", #call, \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                            \
+  } while (0)
+
+#define NK(h, call)                                                                                 \
+  do {                                                                                              \
+    ncclResult_t r_ = (call);                                                                       \
+    if (r_ != ncclSuccess)                                                                          \
+      return set_err((h), LB_ENCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+  } while (0)
+
+bool finite(double v) { return std::isfinite(v); }
+
+int check_params(const lb_params* p) {
+  if (!p) return set_err(nullptr, LB_EINVAL, "params is NULL");
+  if (!finite(p->tau_f) || !(p->tau_f > 0.5)) return set_err(nullptr, LB_EINVAL, "tau_f must be finite and > 0.5");
+  if (!finite(p->tau_g) || !(p->tau_g > 0.5)) return set_err(nullptr, LB_EINVAL, "tau_g must be finite and > 0.5");
+  if (!finite(p->A) || !finite(p->B)) return set_err(nullptr, LB_EINVAL, "A and B must be finite");
+  if (!finite(p->kappa) || p->kappa < 0) return set_err(nullptr, LB_EINVAL, "kappa must be finite and >= 0");
+  if (!finite(p->mobility) || p->mobility < 0) return set_err(nullptr, LB_EINVAL, "mobility must be finite and >= 0");
+  return LB_OK;
+}
+
+DevParams derive(const lb_params& p) {
+  DevParams d;
+  d.A = p.A;
+  d.B = p.B;
+  d.kappa = p.kappa;
+  d.inv_tau_f = 1.0 / p.tau_f;
+  d.inv_tau_g = 1.0 / p.tau_g;
+  d.guo_pref = 1.0 - 1.0 / (2.0 * p.tau_f);
+  d.gamma = p.mobility / (p.tau_g - 0.5);
+  return d;
+}
+
+size_t dist_doubles(const Geom& G) { return (size_t)(G.nzl + 2 * GZ) * (size_t)G.plane; }
+size_t phi_doubles(const Geom& G) { return (size_t)(G.nzl + 2 * GP) * (size_t)G.nxy; }
+
+// ---- profiling -------------------------------------------------------------
+template <class Fn>
+cudaError_t timed(lb_ctx* h, int kid, bool is_kernel, Fn&& fn) {
+  if (!h->prof_on) {
+    cudaError_t e = fn();
+    if (is_kernel) ++h->launches;
+    return e;
+  }
+  cudaEvent_t ev[2];
+  for (int k = 0; k < 2; ++k) {
+    if (h->ev_pool.empty()) {
+      cudaError_t e = cudaEventCreate(&ev[k]);
+      if (e != cudaSuccess) return e;
+    } else {
+      ev[k] = h->ev_pool.back();
+      h->ev_pool.pop_back();
+    }
+  }
+  cudaEventRecord(ev[0], h->stream);
+  cudaError_t e = fn();
+  cudaEventRecord(ev[1], h->stream);
+  h->pending.push_back({kid, ev[0], ev[1]});
+  if (is_kernel) ++h->launches;
+  return e;
+}
+
+// after a stream sync: fold pending event pairs into the totals
+void resolve_pending(lb_ctx* h) {
+  for (auto& p : h->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.e0, p.e1) == cudaSuccess) {
+      h->prof_ms[p.kid] += ms;
+      h->prof_n[p.kid] += 1;
+    }
+    h->ev_pool.push_back(p.e0);
+    h->ev_pool.push_back(p.e1);
+  }
+  h->pending.clear();
+}
+
+// ---- allocation ------------------------------------------------------------
+int alloc_slabs(lb_ctx* h) {
+  h->slabs.resize(h->nslabs);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    s.z0 = (h->rank * h->nslabs + r) * h->nzl;
+    CK(h, cudaMalloc(&s.A, dist_doubles(h->G) * sizeof(double)));
+    CK(h, cudaMalloc(&s.B, dist_doubles(h->G) * sizeof(double)));
+    CK(h, cudaMalloc(&s.phi, phi_doubles(h->G) * sizeof(double)));
+    // NaN-fill: a read of a plane nobody wrote shows up as a parity failure
+    CK(h, cudaMemsetAsync(s.A, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
+    CK(h, cudaMemsetAsync(s.B, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
+    CK(h, cudaMemsetAsync(s.phi, 0xff, phi_doubles(h->G) * sizeof(double), h->stream));
+  }
+  CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
+  CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
+  CK(h, cudaMallocHost(&h->h_flag, sizeof(int)));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return LB_OK;
+}
+
+int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, int rank, int nslabs, lb_t** out) {
+  if (!out) return set_err(nullptr, LB_EINVAL, "out is NULL");
+  *out = nullptr;
+  int rc = check_params(params);
+  if (rc) return rc;
+  if (nx < 3 || ny < 3 || nz < 3) return set_err(nullptr, LB_EINVAL, "extents must be >= 3 (got %d x %d x %d)", nx, ny, nz);
+  if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(nullptr, LB_EINVAL, "bad rank %d of %d", rank, nranks);
+  if (nslabs < 1) return set_err(nullptr, LB_EINVAL, "nslabs must be >= 1");
+  const int parts = nranks * nslabs;
+  if (nz % parts != 0) return set_err(nullptr, LB_EINVAL, "nz = %d is not divisible by %d slabs", nz, parts);
+  if (parts > 1 && nz / parts < 2) return set_err(nullptr, LB_EINVAL, "a slab needs >= 2 planes (nz/slabs = %d)", nz / parts);
+  if ((long long)nx * ny > (1LL << 31)) return set_err(nullptr, LB_EINVAL, "nx*ny too large");
+
+  lb_ctx* h = new lb_ctx;
+  h->nx = nx;
+  h->ny = ny;
+  h->nz = nz;
+  h->nranks = nranks;
+  h->rank = rank;
+  h->nslabs = nslabs;
+  h->nzl = nz / parts;
+  h->prm = *params;
+  h->dp = derive(*params);
+  h->G.nx = nx;
+  h->G.ny = ny;
+  h->G.nzl = h->nzl;
+  h->G.zwrap = parts == 1 ? 1 : 0;
+  h->G.nxy = (long long)nx * ny;
+  h->G.plane = (long long)NSLOT * h->G.nxy;
+  cudaError_t e = cudaGetDevice(&h->device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    set_err(nullptr, LB_ECUDA, "CUDA init failed: %s", cudaGetErrorString(e));
+    delete h;
+    return LB_ECUDA;
+  }
+  rc = alloc_slabs(h);
+  if (rc) {
+    g_create_error = h->err;
+    lb_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return LB_OK;
+}
+
+int usable(lb_ctx* h) {
+  if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
+  if (h->broken) return set_err(h, LB_ECUDA, "handle unusable after an earlier CUDA/NCCL failure: %s", h->err.c_str());
+  return LB_OK;
+}
+
+// ---- halo transport ---------------------------------------------------------
+// Distribution halo after a step, on buffer B of every slab:
+//   ghost plane nzl (cz=+1 run, slots [0,10)) -> plane 0 of the slab above, same slots
+//   ghost plane -1  (cz=-1 run, slots [28,38)) -> plane nzl-1 of the slab below
+// phi halo before a step:
+//   planes [nzl-2, nzl) -> ghost planes [-2, 0) of the slab above
+//   planes [0, 2)       -> ghost planes [nzl, nzl+2) of the slab below
+int exchange_dist(lb_ctx* h) {
+  const Geom& G = h->G;
+  const size_t cnt = (size_t)HALO_COMPS * G.nxy;
+  if (h->nranks > 1) {
+    Slab& s = h->slabs[0];
+    const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
+    cudaError_t ce = timed(h, K_HALO_DIST, false, [&]() {
+      ncclGroupStart();
+      ncclSend(s.B + dist_index(G, G.nzl, SLOT_UP_FIRST, 0), cnt, ncclDouble, up, h->comm, h->stream);
+      ncclRecv(s.B + dist_index(G, 0, SLOT_UP_FIRST, 0), cnt, ncclDouble, dn, h->comm, h->stream);
+      ncclSend(s.B + dist_index(G, -1, SLOT_DOWN_FIRST, 0), cnt, ncclDouble, dn, h->comm, h->stream);
+      ncclRecv(s.B + dist_index(G, G.nzl - 1, SLOT_DOWN_FIRST, 0), cnt, ncclDouble, up, h->comm, h->stream);
+      return ncclGroupEnd() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+    });
+    if (ce != cudaSuccess) return set_err(h, LB_ENCCL, "NCCL distribution halo exchange failed");
+    return LB_OK;
+  }
+  if (h->nslabs == 1) return LB_OK;  // periodic single slab: kernels wrap
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    Slab& up = h->slabs[(r + 1) % h->nslabs];
+    Slab& dn = h->slabs[(r - 1 + h->nslabs) % h->nslabs];
+    CK(h, timed(h, K_HALO_DIST, false, [&]() {
+      cudaError_t e = cudaMemcpyAsync(up.B + dist_index(G, 0, SLOT_UP_FIRST, 0), s.B + dist_index(G, G.nzl, SLOT_UP_FIRST, 0),
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
+      if (e != cudaSuccess) return e;
+      return cudaMemcpyAsync(dn.B + dist_index(G, G.nzl - 1, SLOT_DOWN_FIRST, 0), s.B + dist_index(G, -1, SLOT_DOWN_FIRST, 0),
+                             cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
+    }));
+  }
+  return LB_OK;
+}
+
+int exchange_phi(lb_ctx* h) {
+  const Geom& G = h->G;
+  const size_t cnt = (size_t)2 * G.nxy;
+  if (h->nranks > 1) {
+    Slab& s = h->slabs[0];
+    const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
+    cudaError_t ce = timed(h, K_HALO_PHI, false, [&]() {
+      ncclGroupStart();
+      ncclSend(s.phi + phi_plane_index(G, G.nzl - 2), cnt, ncclDouble, up, h->comm, h->stream);
+      ncclRecv(s.phi + phi_plane_index(G, -2), cnt, ncclDouble, dn, h->comm, h->stream);
+      ncclSend(s.phi + phi_plane_index(G, 0), cnt, ncclDouble, dn, h->comm, h->stream);
+      ncclRecv(s.phi + phi_plane_index(G, G.nzl), cnt, ncclDouble, up, h->comm, h->stream);
+      return ncclGroupEnd() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+    });
+    if (ce != cudaSuccess) return set_err(h, LB_ENCCL, "NCCL phi halo exchange failed");
+    return LB_OK;
+  }
+  if (h->nslabs == 1) return LB_OK;
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    Slab& up = h->slabs[(r + 1) % h->nslabs];
+    Slab& dn = h->slabs[(r - 1 + h->nslabs) % h->nslabs];
+    CK(h, timed(h, K_HALO_PHI, false, [&]() {
+      cudaError_t e = cudaMemcpyAsync(up.phi + phi_plane_index(G, -2), s.phi + phi_plane_index(G, G.nzl - 2),
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
+      if (e != cudaSuccess) return e;
+      return cudaMemcpyAsync(dn.phi + phi_plane_index(G, G.nzl), s.phi + phi_plane_index(G, 0), cnt * sizeof(double),
+                             cudaMemcpyDeviceToDevice, h->stream);
+    }));
+  }
+  return LB_OK;
+}
+
+// one timestep on every slab: phi, phi halo, step (A -> B), distribution halo, swap
+int one_step(lb_ctx* h, bool collide) {
+  const Geom& G = h->G;
+  int rc;
+  if (collide) {
+    for (auto& s : h->slabs) CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, G.nzl, h->stream); }));
+    if ((rc = exchange_phi(h))) return rc;
+  }
+  for (auto& s : h->slabs)
+    CK(h, timed(h, K_STEP, true, [&]() {
+         return launch_step(G, h->dp, s.A, s.B, s.phi, 0, G.nzl, h->d_flag, collide, h->stream);
+       }));
+  if ((rc = exchange_dist(h))) return rc;
+  for (auto& s : h->slabs) std::swap(s.A, s.B);
+  return LB_OK;
+}
+
+int finish(lb_ctx* h) {
+  CK(h, cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  if (*h->h_flag) {
+    CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    return set_err(h, LB_ENUMERIC, "rho <= 0 or a non-finite value at some site (numerical-domain error)");
+  }
+  return LB_OK;
+}
+
+// host (whole lattice for loopback, this rank's slab for NCCL) <-> canonical staging in B
+size_t host_nloc(const lb_ctx* h) { return (size_t)h->G.nxy * h->nzl * h->nslabs; }
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* lb_version(void) { return "lb-b200 0.1 (sm_100a, fp64 D3Q19 binary fluid)"; }
+
+int lb_create(int nx, int ny, int nz, const lb_params* params, lb_t** out) {
+  return create_common(nx, ny, nz, params, 1, 0, 1, out);
+}
+
+int lb_create_loopback(int nx, int ny, int nz, const lb_params* params, int nslabs, lb_t** out) {
+  return create_common(nx, ny, nz, params, 1, 0, nslabs, out);
+}
+
+int lb_nccl_get_unique_id(void* id128) {
+  if (!id128) return set_err(nullptr, LB_EINVAL, "id128 is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(nullptr, LB_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  std::memcpy(id128, &id, sizeof id);
+  return LB_OK;
+}
+
+int lb_create_slab(int nx, int ny, int nz, const lb_params* params, int nranks, int rank, const void* id128,
+                   lb_t** out) {
+  if (nranks > 1 && !id128) return set_err(nullptr, LB_EINVAL, "id128 is NULL");
+  int rc = create_common(nx, ny, nz, params, nranks, rank, 1, out);
+  if (rc || nranks == 1) return rc;
+  lb_ctx* h = *out;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    g_create_error = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+    h->comm = nullptr;
+    lb_destroy(h);
+    *out = nullptr;
+    return LB_ENCCL;
+  }
+  return LB_OK;
+}
+
+size_t lb_local_sites(const lb_t* h) { return h ? host_nloc(h) : 0; }
+
+int lb_set_state(lb_t* h, const double* f, const double* g) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (!f || !g) return set_err(h, LB_EINVAL, "f or g is NULL");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    // 19 rows of nloc doubles, host row pitch N (whole lattice) -> staging rows of nloc
+    CK(h, cudaMemcpy2DAsync(s.B, nloc * 8, f + r * nloc, N * 8, nloc * 8, Q, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpy2DAsync(s.B + Q * nloc, nloc * 8, g + r * nloc, N * 8, nloc * 8, Q, cudaMemcpyHostToDevice, h->stream));
+    CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_canon_to_planes(G, s.B, s.A, h->stream); }));
+  }
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  h->have_state = true;
+  return LB_OK;
+}
+
+int lb_get_state(lb_t* h, double* f, double* g) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (!f || !g) return set_err(h, LB_EINVAL, "f or g is NULL");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_planes_to_canon(G, s.A, s.B, h->stream); }));
+    CK(h, cudaMemcpy2DAsync(f + r * nloc, N * 8, s.B, nloc * 8, nloc * 8, Q, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpy2DAsync(g + r * nloc, N * 8, s.B + Q * nloc, nloc * 8, nloc * 8, Q, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  return LB_OK;
+}
+
+int lb_init_equilibrium(lb_t* h, const double* rho, const double* u, const double* phi) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (!phi) return set_err(h, LB_EINVAL, "phi is NULL");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    CK(h, cudaMemcpyAsync(s.phi + phi_plane_index(G, 0), phi + r * nloc, nloc * 8, cudaMemcpyHostToDevice, h->stream));
+    if (rho) CK(h, cudaMemcpyAsync(s.B, rho + r * nloc, nloc * 8, cudaMemcpyHostToDevice, h->stream));
+    if (u) CK(h, cudaMemcpy2DAsync(s.B + nloc, nloc * 8, u + r * nloc, N * 8, nloc * 8, 3, cudaMemcpyHostToDevice, h->stream));
+  }
+  if ((rc = exchange_phi(h))) return rc;
+  for (auto& s : h->slabs)
+    CK(h, timed(h, K_INIT, true, [&]() {
+         return launch_init_eq(G, h->dp, s.phi, rho ? s.B : nullptr, u ? s.B + nloc : nullptr, s.A, h->stream);
+       }));
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  h->have_state = true;
+  return LB_OK;
+}
+
+int lb_step(lb_t* h, int nsteps) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
+  for (int t = 0; t < nsteps; ++t)
+    if ((rc = one_step(h, true))) return rc;
+  return finish(h);
+}
+
+int lb_debug_stream(lb_t* h, int nsteps) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
+  for (int t = 0; t < nsteps; ++t)
+    if ((rc = one_step(h, false))) return rc;
+  return finish(h);
+}
+
+int lb_get_phi(lb_t* h, double* phi) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (!phi) return set_err(h, LB_EINVAL, "phi is NULL");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl;
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, G.nzl, h->stream); }));
+    CK(h, cudaMemcpyAsync(phi + r * nloc, s.phi + phi_plane_index(G, 0), nloc * 8, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  return LB_OK;
+}
+
+void lb_destroy(lb_t* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) ncclCommDestroy(h->comm);
+  for (auto& s : h->slabs) {
+    cudaFree(s.A);
+    cudaFree(s.B);
+    cudaFree(s.phi);
+  }
+  cudaFree(h->d_flag);
+  if (h->h_flag) cudaFreeHost(h->h_flag);
+  for (auto& p : h->pending) {
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
+  }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+const char* lb_last_error(const lb_t* h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+void* lb_stream(const lb_t* h) { return h ? (void*)h->stream : nullptr; }
+
+long long lb_launch_count(const lb_t* h) { return h ? h->launches : 0; }
+
+int lb_profile_enable(lb_t* h, int on) {
+  if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
+  h->prof_on = on != 0;
+  return LB_OK;
+}
+
+int lb_profile_reset(lb_t* h) {
+  if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
+  for (int k = 0; k < K_COUNT; ++k) h->prof_ms[k] = 0, h->prof_n[k] = 0;
+  return LB_OK;
+}
+
+int lb_profile_count(const lb_t* h) { return h ? K_COUNT : 0; }
+
+int lb_profile_entry(const lb_t* h, int i, const char** name, double* total_ms, long long* launches) {
+  if (!h || i < 0 || i >= K_COUNT) return LB_EINVAL;
+  if (name) *name = kKernelNames[i];
+  if (total_ms) *total_ms = h->prof_ms[i];
+  if (launches) *launches = h->prof_n[i];
+  return LB_OK;
+}
+
+double lb_bytes_per_site(void) { return 2.0 * NSLOT * sizeof(double); }
+
+// Host-only: the composition of the kernels' push addressing (push_target) and
+// the halo plan, inverted into a pull map over the GLOBAL lattice:
+// out[p*N + s_dst] = canonical global index of the site whose component p
+// streams into s_dst.  N = nx*ny*nz.  Exercises exactly the integer maps the
+// device code uses, for any slab count.
+int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out) {
+  if (!out || nx < 3 || ny < 3 || nz < 3 || nslabs < 1 || nz % nslabs || (nslabs > 1 && nz / nslabs < 2))
+    return LB_EINVAL;
+  Geom G;
+  G.nx = nx;
+  G.ny = ny;
+  G.nzl = nz / nslabs;
+  G.zwrap = nslabs == 1;
+  G.nxy = (long long)nx * ny;
+  G.plane = (long long)NSLOT * G.nxy;
+  const long long N = G.nxy * nz;
+  for (long long k = 0; k < (long long)Q * N; ++k) out[k] = -1;
+  for (int r = 0; r < nslabs; ++r)
+    for (int z = 0; z < G.nzl; ++z)
+      for (int y = 0; y < ny; ++y)
+        for (int x = 0; x < nx; ++x)
+          for (int i = 0; i < Q; ++i) {
+            const long long d = push_target(G, i, x, y, z);  // plane-relative address without slot
+            const int zz = (int)(d / G.plane) - GZ;          // local destination plane
+            const long long xy = d - (long long)(zz + GZ) * G.plane;
+            int rdst = r, zdst = zz;
+            if (zz == G.nzl) {  // ghost above: halo run goes to plane 0 of slab r+1
+              if (slot(0, i) < SLOT_UP_FIRST || slot(0, i) >= SLOT_UP_FIRST + HALO_COMPS) return LB_EINVAL;
+              rdst = (r + 1) % nslabs, zdst = 0;
+            } else if (zz == -1) {  // ghost below: goes to plane nzl-1 of slab r-1
+              if (slot(0, i) < SLOT_DOWN_FIRST || slot(0, i) >= SLOT_DOWN_FIRST + HALO_COMPS) return LB_EINVAL;
+              rdst = (r - 1 + nslabs) % nslabs, zdst = G.nzl - 1;
+            }
+            const long long sdst = xy + G.nxy * ((long long)rdst * G.nzl + zdst);
+            const long long ssrc = x + (long long)nx * (y + (long long)ny * ((long long)r * G.nzl + z));
+            if (out[(long long)i * N + sdst] != -1) return LB_EINVAL;  // not a permutation
+            out[(long long)i * N + sdst] = ssrc;
+          }
+  return LB_OK;
+}
+
+int lb_halo_plan(int nx, int ny, int nz, int nranks, int rank, int64_t out[4]) {
+  if (!out || nx < 3 || ny < 3 || nz < 3 || nranks < 1 || rank < 0 || rank >= nranks || nz % nranks ||
+      (nranks > 1 && nz / nranks < 2))
+    return LB_EINVAL;
+  out[0] = (rank + 1) % nranks;
+  out[1] = (rank - 1 + nranks) % nranks;
+  out[2] = (int64_t)HALO_COMPS * nx * ny;
+  out[3] = (int64_t)2 * nx * ny;
+  return LB_OK;
+}
+
+}  // extern "C"

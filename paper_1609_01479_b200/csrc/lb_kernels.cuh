@@ -1,0 +1,62 @@
+// lb_kernels.cuh -- internal (C++) interface between the host runtime and the
+// sm_100a kernels.  Not part of the C ABI (include/lb.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "d3q19.cuh"
+
+namespace lbk {
+
+// Constants of the step derived once on the host from lb_params (R2, R7-R10).
+struct DevParams {
+  double A, B, kappa;
+  double inv_tau_f;   // 1 / tau_f
+  double inv_tau_g;   // 1 / tau_g
+  double guo_pref;    // 1 - 1/(2 tau_f)   (R7)
+  double gamma;       // M / (tau_g - 1/2) (R10)
+};
+
+// Geometry of one z-slab as the kernels see it.
+struct Geom {
+  int nx, ny, nzl;  // local extents
+  int zwrap;        // 1: this slab is the whole periodic z extent (no ghosts used)
+  long long nxy;    // nx * ny
+  long long plane;  // NSLOT * nxy doubles per distribution plane
+};
+
+// Buffer addressing.  dist buffer: (nzl + 2*GZ) planes; phi buffer: (nzl + 2*GP) planes.
+__host__ __device__ inline long long dist_index(const Geom& G, int z, int s, long long xy) {
+  return (long long)(z + GZ) * G.plane + (long long)s * G.nxy + xy;
+}
+__host__ __device__ inline long long phi_plane_index(const Geom& G, int z) {
+  return (long long)(z + GP) * G.nxy;
+}
+__host__ __device__ inline int wrap_n(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+
+// Where the kernels PUSH the post-collision component i of local site (x,y,z):
+// (x + cx, y + cy) periodic in the plane; z + cz wraps when G.zwrap, otherwise
+// z + cz in [-1, nzl] (planes -1 and nzl are the ghost planes sent to the
+// neighbouring slabs).  Shared by the step kernel and the host-side map check.
+__host__ __device__ inline long long push_target(const Geom& G, int i, int x, int y, int z) {
+  const int xd = wrap_n(x + cx(i), G.nx);
+  const int yd = wrap_n(y + cy(i), G.ny);
+  int zd = z + cz(i);
+  if (G.zwrap) zd = wrap_n(zd, G.nzl);
+  return (long long)(zd + GZ) * G.plane + (long long)xd + (long long)G.nx * yd;  // + slot*nxy by caller
+}
+
+// ---- launchers (lb_kernels.cu) -------------------------------------------
+// All launch on `st`, return cudaGetLastError().
+cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st);
+cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phi,
+                        int z0, int z1, int* flag, bool collide, cudaStream_t st);
+cudaError_t launch_init_eq(const Geom& G, const DevParams& p, const double* phi, const double* rho,
+                           const double* u, double* A, cudaStream_t st);
+// canonical [2][19][nloc] (f block then g block) <-> plane-major buffer
+cudaError_t launch_canon_to_planes(const Geom& G, const double* canon, double* buf, cudaStream_t st);
+cudaError_t launch_planes_to_canon(const Geom& G, const double* buf, double* canon, cudaStream_t st);
+
+}  // namespace lbk

@@ -1,0 +1,273 @@
+"""Thin ctypes binding of the C ABI in include/lb.h (argument marshalling only).
+
+Every step of the path runs in liblb.so's CUDA kernels; this module only
+converts arrays to pointers and return codes to exceptions.  There is no CPU
+fallback: if liblb.so is missing or fails to load, importing this module
+raises.  Function names follow the C ABI (``lb_create``, ``lb_set_state``,
+``lb_step``, ``lb_get_state``, ``lb_destroy`` ...); ``Lattice`` is a small
+owning wrapper around a handle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblb.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)"
+    )
+_lib = C.CDLL(_LIB_PATH)
+
+LB_OK, LB_EINVAL, LB_ENOMEM, LB_ECUDA, LB_ENCCL, LB_ESTATE, LB_ENUMERIC = 0, -1, -2, -3, -4, -5, -6
+_NAMES = {-1: "LB_EINVAL", -2: "LB_ENOMEM", -3: "LB_ECUDA", -4: "LB_ENCCL", -5: "LB_ESTATE", -6: "LB_ENUMERIC"}
+Q = 19
+
+
+class LBError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class lb_params(C.Structure):
+    _fields_ = [("tau_f", C.c_double), ("tau_g", C.c_double), ("A", C.c_double), ("B", C.c_double),
+                ("kappa", C.c_double), ("mobility", C.c_double)]
+
+
+_vp, _dp, _i, _ll = C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_longlong
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_lib_version = _sig("lb_version", C.c_char_p)
+_lb_create = _sig("lb_create", _i, _i, _i, _i, C.POINTER(lb_params), C.POINTER(_vp))
+_lb_create_loopback = _sig("lb_create_loopback", _i, _i, _i, _i, C.POINTER(lb_params), _i, C.POINTER(_vp))
+_lb_nccl_get_unique_id = _sig("lb_nccl_get_unique_id", _i, _vp)
+_lb_create_slab = _sig("lb_create_slab", _i, _i, _i, _i, C.POINTER(lb_params), _i, _i, _vp, C.POINTER(_vp))
+_lb_local_sites = _sig("lb_local_sites", C.c_size_t, _vp)
+_lb_set_state = _sig("lb_set_state", _i, _vp, _vp, _vp)
+_lb_init_equilibrium = _sig("lb_init_equilibrium", _i, _vp, _vp, _vp, _vp)
+_lb_step = _sig("lb_step", _i, _vp, _i)
+_lb_debug_stream = _sig("lb_debug_stream", _i, _vp, _i)
+_lb_get_state = _sig("lb_get_state", _i, _vp, _vp, _vp)
+_lb_get_phi = _sig("lb_get_phi", _i, _vp, _vp)
+_lb_destroy = _sig("lb_destroy", None, _vp)
+_lb_last_error = _sig("lb_last_error", C.c_char_p, _vp)
+_lb_stream = _sig("lb_stream", _vp, _vp)
+_lb_launch_count = _sig("lb_launch_count", _ll, _vp)
+_lb_profile_enable = _sig("lb_profile_enable", _i, _vp, _i)
+_lb_profile_reset = _sig("lb_profile_reset", _i, _vp)
+_lb_profile_count = _sig("lb_profile_count", _i, _vp)
+_lb_profile_entry = _sig("lb_profile_entry", _i, _vp, _i, C.POINTER(C.c_char_p), _dp, C.POINTER(_ll))
+_lb_bytes_per_site = _sig("lb_bytes_per_site", C.c_double)
+_lb_debug_propagation_map = _sig("lb_debug_propagation_map", _i, _i, _i, _i, _i, _vp)
+_lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
+
+EXPORTS = [
+    "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
+    "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_get_state", "lb_get_phi", "lb_destroy",
+    "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
+    "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_halo_plan",
+]
+
+
+def _check(rc: int, h) -> None:
+    if rc != LB_OK:
+        raise LBError(rc, (_lb_last_error(h) or b"").decode())
+
+
+def _ptr(a, n: int, writable: bool = False) -> int:
+    """Pointer to n contiguous float64 values: a NumPy array or a (CPU, possibly
+    pinned) torch tensor.  No copies: a non-conforming array raises."""
+    if hasattr(a, "data_ptr"):  # torch tensor
+        if a.device.type != "cpu" or a.dtype.__repr__() != "torch.float64" or not a.is_contiguous() or a.numel() != n:
+            raise ValueError(f"need a contiguous CPU float64 tensor of {n} elements")
+        return a.data_ptr()
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous or a.size != n:
+        raise ValueError(f"need a C-contiguous float64 ndarray of {n} elements")
+    if writable and not a.flags.writeable:
+        raise ValueError("output array is read-only")
+    return a.ctypes.data
+
+
+def make_params(tau_f=0.8, tau_g=1.3, A=-0.0625, B=0.0625, kappa=0.04, mobility=0.05) -> lb_params:
+    return lb_params(tau_f, tau_g, A, B, kappa, mobility)
+
+
+# ---- C ABI names ------------------------------------------------------------
+def lb_version() -> str:
+    return _lib_version().decode()
+
+
+def lb_create(nx: int, ny: int, nz: int, params: lb_params):
+    h = _vp()
+    _check(_lb_create(nx, ny, nz, C.byref(params), C.byref(h)), None)
+    return h
+
+
+def lb_create_loopback(nx: int, ny: int, nz: int, params: lb_params, nslabs: int):
+    h = _vp()
+    _check(_lb_create_loopback(nx, ny, nz, C.byref(params), nslabs, C.byref(h)), None)
+    return h
+
+
+def lb_nccl_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lb_nccl_get_unique_id(buf), None)
+    return buf.raw
+
+
+def lb_create_slab(nx: int, ny: int, nz: int, params: lb_params, nranks: int, rank: int, uid: bytes | None):
+    h = _vp()
+    buf = C.create_string_buffer(uid, 128) if uid is not None else None
+    _check(_lb_create_slab(nx, ny, nz, C.byref(params), nranks, rank, buf, C.byref(h)), None)
+    return h
+
+
+def lb_local_sites(h) -> int:
+    return int(_lb_local_sites(h))
+
+
+def lb_set_state(h, f, g) -> None:
+    n = Q * lb_local_sites(h)
+    _check(_lb_set_state(h, _ptr(f, n), _ptr(g, n)), h)
+
+
+def lb_init_equilibrium(h, rho, u, phi) -> None:
+    n = lb_local_sites(h)
+    _check(_lb_init_equilibrium(h, None if rho is None else _ptr(rho, n), None if u is None else _ptr(u, 3 * n),
+                                _ptr(phi, n)), h)
+
+
+def lb_step(h, nsteps: int) -> None:
+    _check(_lb_step(h, nsteps), h)
+
+
+def lb_debug_stream(h, nsteps: int) -> None:
+    _check(_lb_debug_stream(h, nsteps), h)
+
+
+def lb_get_state(h, f=None, g=None):
+    n = Q * lb_local_sites(h)
+    f = np.empty(n) if f is None else f
+    g = np.empty(n) if g is None else g
+    _check(_lb_get_state(h, _ptr(f, n, True), _ptr(g, n, True)), h)
+    return f, g
+
+
+def lb_get_phi(h, phi=None):
+    n = lb_local_sites(h)
+    phi = np.empty(n) if phi is None else phi
+    _check(_lb_get_phi(h, _ptr(phi, n, True)), h)
+    return phi
+
+
+def lb_destroy(h) -> None:
+    _lb_destroy(h)
+
+
+def lb_last_error(h=None) -> str:
+    return (_lb_last_error(h) or b"").decode()
+
+
+def lb_stream(h) -> int:
+    return int(_lb_stream(h) or 0)
+
+
+def lb_launch_count(h) -> int:
+    return int(_lb_launch_count(h))
+
+
+def lb_profile_enable(h, on: bool) -> None:
+    _check(_lb_profile_enable(h, int(on)), h)
+
+
+def lb_profile_reset(h) -> None:
+    _check(_lb_profile_reset(h), h)
+
+
+def lb_profile(h) -> dict:
+    """{kernel name: (total device ms, timed launches)} from the handle's event timers."""
+    out = {}
+    for i in range(_lb_profile_count(h)):
+        name, ms, n = C.c_char_p(), C.c_double(), _ll()
+        _check(_lb_profile_entry(h, i, C.byref(name), C.byref(ms), C.byref(n)), h)
+        out[name.value.decode()] = (ms.value, n.value)
+    return out
+
+
+def lb_bytes_per_site() -> float:
+    return float(_lb_bytes_per_site())
+
+
+def lb_debug_propagation_map(nx: int, ny: int, nz: int, nslabs: int = 1) -> np.ndarray:
+    out = np.empty(Q * nx * ny * nz, dtype=np.int64)
+    rc = _lb_debug_propagation_map(nx, ny, nz, nslabs, out.ctypes.data)
+    if rc != LB_OK:
+        raise LBError(rc, "propagation map failed (bad sizes or not a permutation)")
+    return out.reshape(Q, nz, ny, nx)
+
+
+def lb_halo_plan(nx: int, ny: int, nz: int, nranks: int, rank: int) -> dict:
+    out = np.empty(4, dtype=np.int64)
+    _check(_lb_halo_plan(nx, ny, nz, nranks, rank, out.ctypes.data), None)
+    return {"up": int(out[0]), "down": int(out[1]), "dist_doubles": int(out[2]), "phi_doubles": int(out[3])}
+
+
+# ---- owning wrapper -----------------------------------------------------------
+class Lattice:
+    """A handle plus its shape.  Arrays at this level are (19, nz, ny, nx)."""
+
+    def __init__(self, nx, ny, nz, params: lb_params | None = None, nslabs: int = 1, nranks: int = 1, rank: int = 0,
+                 uid: bytes | None = None):
+        self.params = params or make_params()
+        if nranks > 1:
+            self.h = lb_create_slab(nx, ny, nz, self.params, nranks, rank, uid)
+            self.shape = (nz // nranks, ny, nx)
+        else:
+            self.h = lb_create_loopback(nx, ny, nz, self.params, nslabs) if nslabs > 1 else lb_create(nx, ny, nz, self.params)
+            self.shape = (nz, ny, nx)
+
+    def close(self):
+        h = getattr(self, "h", None)
+        if h:
+            lb_destroy(h)
+            self.h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_state(self, f, g):
+        lb_set_state(self.h, np.ascontiguousarray(f, dtype=np.float64).reshape(-1),
+                     np.ascontiguousarray(g, dtype=np.float64).reshape(-1))
+
+    def init_equilibrium(self, phi, rho=None, u=None):
+        c = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+        lb_init_equilibrium(self.h, c(rho), c(u), c(phi))
+
+    def step(self, n: int = 1):
+        lb_step(self.h, n)
+
+    def stream_only(self, n: int = 1):
+        lb_debug_stream(self.h, n)
+
+    def get_state(self):
+        f, g = lb_get_state(self.h)
+        return f.reshape((Q,) + self.shape), g.reshape((Q,) + self.shape)
+
+    def get_phi(self):
+        return lb_get_phi(self.h).reshape(self.shape)

@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance (north_star "within 1e-12 relative"; reading R18): norm-wise
+per field, ||x_gpu - x_ref||_inf / ||x_ref||_inf <= 1e-12, separately for f, g
+and the derived phi, rho, u.  Integer maps and pure data movement (set/get,
+propagation-only, slab decompositions, symmetries) are compared bitwise.
+Inputs are the seeded synthetic states of ``paper_1609_01479_b200.synth``;
+initial distributions are built by the oracle on the host and loaded with
+lb_set_state, so no oracle input comes from the GPU.
+"""
+import numpy as np
+import pytest
+
+from oracle import lb_brute as BR
+from oracle import lb_ref as R
+from paper_1609_01479_b200 import lb, synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+P0 = R.Params()
+
+
+def cparams(p: R.Params):
+    return lb.make_params(p.tau_f, p.tau_g, p.A, p.B, p.kappa, p.mobility)
+
+
+def spinodal(nx, ny, nz, seed=0, p=P0):
+    rho, u, phi = synth.spinodal_fields(nx, ny, nz, seed)
+    return R.equilibrium_state(rho, u, phi, p)
+
+
+def rough(nx, ny, nz, seed=1, p=P0):
+    rho, u, phi, nf, ng = synth.rough_fields(nx, ny, nz, seed)
+    f, g = R.equilibrium_state(rho, u, phi, p)
+    return f + nf, g + ng
+
+
+def gpu_run(f, g, p, nsteps, nslabs=1):
+    nz, ny, nx = f.shape[1:]
+    with lb.Lattice(nx, ny, nz, cparams(p), nslabs=nslabs) as L:
+        L.set_state(f, g)
+        L.step(nsteps)
+        return L.get_state()
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def u_scale(f, rho):
+    """R18 for u: u = sum_i c_i f_i / rho cancels, so its error is normalised by the
+    momentum the populations carry, max_s sum_i |c_i| f_i / rho (or |u| if larger)."""
+    cabs = np.sqrt((R.C * R.C).sum(axis=1)).reshape(19, 1, 1, 1)
+    return float((np.abs(f) * cabs).sum(axis=0).__truediv__(rho).max())
+
+
+def assert_parity(fg_gpu, fg_ref, tol=TOL):
+    (f1, g1), (f0, g0) = fg_gpu, fg_ref
+    r1, j1, p1 = R.macroscopic(f1, g1)
+    r0, j0, p0 = R.macroscopic(f0, g0)
+    u1, u0 = j1 / r1, j0 / r0
+    u_err = float(np.abs(u1 - u0).max() / max(np.abs(u0).max(), u_scale(f0, r0)))
+    errs = {"f": rel(f1, f0), "g": rel(g1, g0), "phi": rel(p1, p0), "rho": rel(r1, r0), "u": u_err}
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad, f"parity errors above {tol}: {bad} (all: {errs})"
+    return errs
+
+
+# ------------------------------------------------------------------ data movement
+@pytest.mark.parametrize("nslabs", [1, 2, 4])
+def test_set_get_roundtrip_bitwise(nslabs):
+    r = np.random.default_rng(0)
+    f = r.standard_normal((19, 8, 5, 7))
+    g = r.standard_normal((19, 8, 5, 7))
+    with lb.Lattice(7, 5, 8, nslabs=nslabs) as L:
+        L.set_state(f, g)
+        f1, g1 = L.get_state()
+    assert np.array_equal(f1.view(np.uint64), f.view(np.uint64))
+    assert np.array_equal(g1.view(np.uint64), g.view(np.uint64))
+
+
+@pytest.mark.parametrize("shape,nslabs", [((7, 5, 8), 1), ((7, 5, 8), 2), ((4, 3, 12), 3), ((16, 16, 16), 4)])
+def test_stream_only_equals_oracle_propagation_bitwise(shape, nslabs):
+    nx, ny, nz = shape
+    r = np.random.default_rng(1)
+    f = r.standard_normal((19, nz, ny, nx))
+    g = r.standard_normal((19, nz, ny, nx))
+    with lb.Lattice(nx, ny, nz, nslabs=nslabs) as L:
+        L.set_state(f, g)
+        L.stream_only(3)
+        f1, g1 = L.get_state()
+    for _ in range(3):
+        f, g = R.propagate(f), R.propagate(g)
+    assert np.array_equal(f1, f) and np.array_equal(g1, g)
+
+
+@pytest.mark.parametrize("kind", ["spinodal", "rough"])
+@pytest.mark.parametrize("nslabs", [1, 2])
+def test_init_equilibrium_matches_oracle(kind, nslabs):
+    nx, ny, nz = 12, 10, 8
+    if kind == "spinodal":
+        rho, u, phi = synth.spinodal_fields(nx, ny, nz, 3)
+    else:
+        rho, u, phi, _, _ = synth.rough_fields(nx, ny, nz, 3)
+    f0, g0 = R.equilibrium_state(rho, u, phi, P0)
+    with lb.Lattice(nx, ny, nz, cparams(P0), nslabs=nslabs) as L:
+        L.init_equilibrium(phi, rho if kind == "rough" else None, u if kind == "rough" else None)
+        f1, g1 = L.get_state()
+        ph = L.get_phi()
+    assert rel(f1, f0) <= 1e-14 and rel(g1, g0) <= 1e-14
+    assert rel(ph, phi) <= 1e-14
+
+
+# ------------------------------------------------------------------ parity
+def test_parity_16cubed_10_steps_spinodal():
+    """BASELINE config 1: 16^3, spinodal random phi +- 0.01, 10 steps, fp64."""
+    f, g = spinodal(16, 16, 16)
+    assert_parity(gpu_run(f, g, P0, 10), R.run(f, g, P0, 10))
+
+
+@pytest.mark.parametrize("shape", [(16, 16, 16), (17, 19, 13), (3, 3, 3), (24, 20, 18), (33, 5, 4), (4, 31, 6)])
+def test_parity_rough_ragged(shape):
+    nx, ny, nz = shape
+    f, g = rough(nx, ny, nz)
+    assert_parity(gpu_run(f, g, P0, 5), R.run(f, g, P0, 5))
+
+
+def test_parity_64cubed_10_steps():
+    f, g = spinodal(64, 64, 64, seed=2)
+    assert_parity(gpu_run(f, g, P0, 10), R.run(f, g, P0, 10))
+
+
+def test_parity_100_steps_demo_mobility():
+    p = R.Params(mobility=0.45)
+    f, g = spinodal(16, 16, 16, seed=4, p=p)
+    assert_parity(gpu_run(f, g, p, 100), R.run(f, g, p, 100))
+
+
+@pytest.mark.parametrize("tau", [(1.0, 1.0), (0.55, 2.5)])
+def test_parity_other_relaxation_times(tau):
+    p = R.Params(tau_f=tau[0], tau_g=tau[1], mobility=0.2)
+    f, g = rough(12, 9, 10, seed=5, p=p)
+    assert_parity(gpu_run(f, g, p, 4), R.run(f, g, p, 4))
+
+
+@pytest.mark.parametrize("nx,ny,nz", [(128, 128, 128), (256, 128, 64)])
+def test_parity_full_size_sampled(nx, ny, nz):
+    """Full benchmark-class sizes: one step in the bench's launch configuration,
+    compared at sampled sites (incl. all 8 corners) with the brute-force oracle."""
+    f, g = spinodal(nx, ny, nz, seed=6)
+    f1, g1 = gpu_run(f, g, P0, 1)
+    smp = BR.SiteSampler(f, g, P0)
+    fs, gs, fr, gr = [], [], [], []
+    for (x, y, z) in synth.sample_sites(nx, ny, nz, 48):
+        fo, go = smp.after_step(x, y, z)
+        fr.append(fo), gr.append(go)
+        fs.append(f1[:, z, y, x]), gs.append(g1[:, z, y, x])
+    assert rel(np.array(fs), np.array(fr)) <= TOL
+    assert rel(np.array(gs), np.array(gr)) <= TOL
+
+
+# ------------------------------------------------------------------ bitwise properties of the GPU path
+@pytest.mark.parametrize("nslabs", [2, 4, 8])
+def test_slab_decomposition_is_bitwise_identical(nslabs):
+    f, g = rough(12, 10, 16, seed=7)
+    a = gpu_run(f, g, P0, 6, nslabs=1)
+    b = gpu_run(f, g, P0, 6, nslabs=nslabs)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_determinism_bitwise():
+    f, g = rough(16, 12, 10, seed=8)
+    a = gpu_run(f, g, P0, 5)
+    b = gpu_run(f, g, P0, 5)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_phi_sign_symmetry_bitwise():
+    f, g = rough(10, 9, 8, seed=9)
+    a = gpu_run(f, g, P0, 3)
+    b = gpu_run(f, -g, P0, 3)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(-a[1], b[1])
+
+
+def test_shift_invariance_bitwise():
+    f, g = rough(10, 9, 8, seed=10)
+    a = gpu_run(f, g, P0, 3)
+    for v in [(1, 0, 0), (0, 3, 0), (0, 0, 5), (2, 1, 1)]:
+        sh = lambda x: np.roll(x, shift=(v[2], v[1], v[0]), axis=(1, 2, 3))
+        b = gpu_run(sh(f), sh(g), P0, 3)
+        assert np.array_equal(sh(a[0]), b[0]) and np.array_equal(sh(a[1]), b[1])
+
+
+@pytest.mark.parametrize("u0", [(0.0, 0.0, 0.0), (0.03, -0.02, 0.01)])
+def test_uniform_equilibrium_fixed_point(u0):
+    sh = (6, 5, 4)
+    u = np.stack([np.full(sh, v) for v in u0])
+    f, g = R.equilibrium_state(np.full(sh, 1.1), u, np.full(sh, 0.4), P0)
+    f1, g1 = gpu_run(f, g, P0, 5)
+    # a few ulps per step: the device contracts to FMA and multiplies by 1/tau (R17)
+    assert rel(f1, f) <= 5e-15 and rel(g1, g) <= 5e-15
+
+
+def test_conservation_64cubed_1000_steps():
+    """C2: 64^3, 1000 steps: mass and phi drift <= 1e-12 relative, momentum <= 1e-13 sum|f|."""
+    f, g = spinodal(64, 64, 64, seed=11, p=R.Params(mobility=0.45))
+    m0, j0, p0 = (v.sum(axis=(-1, -2, -3)) for v in R.macroscopic(f, g))
+    f1, g1 = gpu_run(f, g, R.Params(mobility=0.45), 1000)
+    m1, j1, p1 = (v.sum(axis=(-1, -2, -3)) for v in R.macroscopic(f1, g1))
+    assert abs(m1 - m0) <= 1e-12 * abs(m0)
+    assert np.abs(j1 - j0).max() <= 1e-13 * np.abs(f1).sum()
+    assert abs(p1 - p0) <= 1e-12 * np.abs(g1).sum()
+
+
+# ------------------------------------------------------------------ errors
+def test_numeric_error_flag():
+    f, g = rough(8, 8, 8)
+    f[:, 3, 2, 1] = 0.0  # rho = 0 at one site
+    with lb.Lattice(8, 8, 8) as L:
+        L.set_state(f, g)
+        with pytest.raises(lb.LBError) as e:
+            L.step(1)
+        assert e.value.code == lb.LB_ENUMERIC
+    g[5, 1, 1, 1] = np.nan
+    f[:, 3, 2, 1] = 1.0 / 19
+    with lb.Lattice(8, 8, 8) as L:
+        L.set_state(f, g)
+        with pytest.raises(lb.LBError) as e:
+            L.step(2)
+        assert e.value.code == lb.LB_ENUMERIC
+
+
+def test_state_errors_and_zero_steps():
+    with lb.Lattice(8, 8, 8) as L:
+        with pytest.raises(lb.LBError) as e:
+            L.step(1)
+        assert e.value.code == lb.LB_ESTATE
+        with pytest.raises(lb.LBError) as e:
+            L.get_state()
+        assert e.value.code == lb.LB_ESTATE
+        f, g = rough(8, 8, 8)
+        L.set_state(f, g)
+        L.step(0)
+        f1, g1 = L.get_state()
+        assert np.array_equal(f1, f) and np.array_equal(g1, g)
+        with pytest.raises(lb.LBError) as e:
+            L.step(-1)
+        assert e.value.code == lb.LB_EINVAL
+
+
+def test_launch_count_and_profile():
+    f, g = spinodal(16, 16, 16)
+    with lb.Lattice(16, 16, 16) as L:
+        L.set_state(f, g)
+        n0 = lb.lb_launch_count(L.h)
+        lb.lb_profile_enable(L.h, True)
+        L.step(4)
+        prof = lb.lb_profile(L.h)
+        assert lb.lb_launch_count(L.h) > n0
+        assert prof["k_step"][1] == 4 and prof["k_step"][0] > 0
