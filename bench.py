@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- MLUPS and achieved HBM GB/s of the D3Q19 binary-fluid LB step on B200.
+
+Metric (BASELINE.json): lattice site updates per second (MLUPS) and achieved HBM
+GB/s against the measured B200 peak, at 1/2/4/8 GPUs.  One "step" = one full LB
+timestep (every row of SURVEY.md sec. 8(a)) over the whole lattice.
+
+Default workload: BASELINE config 5, weak scaling with a fixed 512 x 512 x 64
+z-slab per GPU (global 512 x 512 x 64N; 512^3 at N = 8; reading R20).  --config
+picks another BASELINE config (c1 16^3, c2 64^3, c3 128^3, c4 256^3 strong).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL halos)
+
+Timing: W >= 3 untimed steps, then exactly K steps bracketed by a barrier and a
+device synchronize, timed with CUDA events on the library's own stream, max over
+ranks.  Inputs are larger than L2 (the per-GPU state is >= 1.2 GB for c3-c5).
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lattice site updates/s (MLUPS) and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
+BYTES_PER_SITE = 608.0  # f and g (38 fp64) read once and written once
+
+# name: (nx, ny, nz_global(N), scaling, description)
+CONFIGS = {
+    "c1": (16, 16, lambda n: 16 * n, "weak", "16^3 per GPU D3Q19 binary fluid, spinodal phi +-0.01 (BASELINE config 1)"),
+    "c2": (64, 64, lambda n: 64 * n, "weak", "64^3 per GPU binary fluid (BASELINE config 2)"),
+    "c3": (128, 128, lambda n: 128 * n, "weak", "128^3 per GPU binary fluid, paper-scale single device (BASELINE config 3)"),
+    "c4": (256, 256, lambda n: 256, "strong", "256^3 binary fluid, strong scaling over z-slabs (BASELINE config 4)"),
+    "c5": (512, 512, lambda n: 64 * n, "weak",
+           "512x512x64 per GPU z-slab binary fluid, weak scaling, 512^3 at 8 GPUs (BASELINE config 5, reading R20)"),
+}
+DEFAULT_CONFIG = "c5"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def src_hash() -> str:
+    h = hashlib.sha1()
+    csrc = os.path.join(ROOT, "paper_1609_01479_b200", "csrc")
+    for f in sorted(os.listdir(csrc)):
+        if f.endswith((".cu", ".cuh")):
+            h.update(open(os.path.join(csrc, f), "rb").read())
+    return h.hexdigest()[:12]
+
+
+def ncu_traffic(kernel: str, config: str):
+    """dram bytes (read + write) per launch of `kernel` from a committed ncu --set full
+    capture (profiles/traffic.json), only if it was taken on the current sources."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        e = t.get(f"{kernel}@{config}")
+        if e and e.get("src_hash") == src_hash():
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.rows, self.marks = [], {}
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append((time.monotonic(), parts))
+
+    def mark(self, name):
+        self.marks[name] = time.monotonic()
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        t0, t1 = self.marks.get("start", 0), self.marks.get("end", 1e30)
+        inside = [p for (t, p) in self.rows if t0 <= t <= t1] or [p for (_, p) in self.rows]
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(p[0]) for p in inside if p[0].replace(".", "").isdigit()]
+        mx = [float(p[1]) for p in inside if p[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for p in inside for k in range(4) if p[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(inside)}
+
+
+# ------------------------------------------------------------------------------ oracle arm
+def oracle_sample_shape(nx: int, ny: int, budget_sites: int):
+    """A periodic nx x ny_s x nz_s sub-lattice of the workload with ~budget_sites sites."""
+    nz_s = 8
+    ny_s = max(4, min(ny, budget_sites // (nx * nz_s)))
+    ny_s = 1 << (ny_s.bit_length() - 1)
+    return nx, ny_s, nz_s
+
+
+def time_oracle(nx, ny, steps: int, seed: int = 0):
+    """The oracle as it stands, 1 thread, on a sample sub-lattice; returns (sites/s, shape)."""
+    from oracle import lb_ref as R
+    from paper_1609_01479_b200 import synth
+
+    sx, sy, sz = oracle_sample_shape(nx, ny, 262144)
+    rho, u, phi = synth.spinodal_fields(sx, sy, sz, seed)
+    p = R.Params()
+    f, g = R.equilibrium_state(rho, u, phi, p)
+    R.step(f, g, p)  # warm
+    t0 = time.perf_counter()
+    f, g = R.run(f, g, p, steps)
+    dt = time.perf_counter() - t0
+    return sx * sy * sz * steps / dt, (sx, sy, sz), dt
+
+
+def run_reference(args):
+    rank, world, _ = env_rank_world()
+    if rank != 0:
+        return 0
+    nx, ny, nzf, scaling, desc = CONFIGS[args.config]
+    sx, sy, sz = oracle_sample_shape(nx, ny, 262144)
+    from oracle import lb_ref as R
+    from paper_1609_01479_b200 import synth
+
+    rho, u, phi = synth.spinodal_fields(sx, sy, sz, 0)
+    p = R.Params()
+    f, g = R.equilibrium_state(rho, u, phi, p)
+    f, g = R.run(f, g, p, max(args.warmup, 0))
+    t0 = time.perf_counter()
+    f, g = R.run(f, g, p, args.steps)
+    dt = time.perf_counter() - t0
+    sites = sx * sy * sz
+    v = sites * args.steps / dt / 1e6
+    sample = f"oracle/lb_ref.py NumPy fp64 step on a periodic {sx}x{sy}x{sz} sub-lattice ({sites} sites) of the workload per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "MLUPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "sample": [sx, sy, sz]},
+        "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ our arm
+def env_rank_world():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def run_ours(args):
+    import torch
+
+    from paper_1609_01479_b200 import dist as D
+    from paper_1609_01479_b200 import lb, synth
+
+    rank, world, local = env_rank_world()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        D.init("nccl")
+    nx, ny, nzf, scaling, desc = CONFIGS[args.config]
+    nz = nzf(world)
+    z0, z1 = D.slab_range(nz, world, rank)
+    nloc = nx * ny * (z1 - z0)
+    params = lb.make_params()  # R16 defaults
+    uid = None
+    if world > 1:
+        uid = D.broadcast_bytes(lb.lb_nccl_get_unique_id() if rank == 0 else None)
+    L = lb.Lattice(nx, ny, nz, params, nranks=world, rank=rank, uid=uid)
+    phi = synth.spinodal_phi_slab(nx, ny, nz, z0, z1, seed=0)
+    L.init_equilibrium(phi)
+
+    W = max(args.warmup, 3)
+    K = args.steps
+    stream = torch.cuda.ExternalStream(lb.lb_stream(L.h))
+    L.step(W)
+
+    clocks = ClockSampler(local)
+    time.sleep(0.25)
+    D.barrier()
+    torch.cuda.synchronize()
+    lb.lb_profile_reset(L.h)
+    lb.lb_profile_enable(L.h, True)
+    n0 = lb.lb_launch_count(L.h)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark("start")
+    e0.record(stream)
+    L.step(K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark("end")
+    D.barrier()
+    launches = lb.lb_launch_count(L.h) - n0
+    lb.lb_profile_enable(L.h, False)
+    prof = lb.lb_profile(L.h)
+    ms = D.max_over_ranks(e0.elapsed_time(e1))
+    clk = clocks.stop()
+
+    sites_total = nx * ny * nz
+    value = sites_total * K / (ms * 1e-3) / 1e6  # MLUPS, whole job
+    peak, peak_src = peaks()
+    ks_ms, ks_n = prof.get("k_step", (0.0, 0))
+    ks_avg = D.max_over_ranks(ks_ms / max(ks_n, 1))
+    achieved = BYTES_PER_SITE * nloc / (ks_avg * 1e-3) / 1e9
+    step_gbs = value * 1e6 * BYTES_PER_SITE / world / 1e9  # per GPU, algorithmic, whole step
+    traffic = ncu_traffic("k_step", args.config)
+    kernel_share = {k: round(v[0] / max(sum(x[0] for x in prof.values()), 1e-30), 4) for k, v in prof.items() if v[1]}
+
+    # ---- e2e: the same metric through the public C ABI with pinned HOST buffers:
+    # every step uploads the state (lb_set_state), advances one step, and reads the
+    # state back (lb_get_state); copies inside the timed region.
+    e2e = None
+    if not args.no_e2e:
+        Ke = min(K, 5)
+        fh = torch.empty(19 * nloc, dtype=torch.float64, pin_memory=True)
+        gh = torch.empty(19 * nloc, dtype=torch.float64, pin_memory=True)
+        lb.lb_get_state(L.h, fh, gh)
+        D.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(Ke):
+            lb.lb_set_state(L.h, fh, gh)
+            lb.lb_step(L.h, 1)
+            lb.lb_get_state(L.h, fh, gh)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        D.barrier()
+        ems = D.max_over_ranks(a0.elapsed_time(a1))
+        e2e = {"value": sites_total * Ke / (ems * 1e-3) / 1e6, "unit": "MLUPS",
+               "h2d_bytes_per_step": 2 * 19 * 8 * nloc, "d2h_bytes_per_step": 2 * 19 * 8 * nloc, "steps": Ke,
+               "mode": "per step: lb_set_state(pinned host f,g) + lb_step(1) + lb_get_state(pinned host f,g)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cv, shp, dt = time_oracle(nx, ny, 20)
+        cpu = {"value": cv / 1e6, "unit": "MLUPS", "cores": 1, "kind": "oracle",
+               "sample": f"oracle/lb_ref.py, 20 steps on a periodic {shp[0]}x{shp[1]}x{shp[2]} sub-lattice of the "
+                         f"workload, 1 thread ({dt:.1f} s of CPU)", "host_cpus": os.cpu_count()}
+
+    L.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "lattice": [nx, ny, nz], "sites_per_gpu": nloc,
+                       "parallelism": f"z-slab x{world}" + (" (NCCL halos)" if world > 1 else ""),
+                       "state_bytes_per_gpu": int(2 * 38 * 8 * nx * ny * (z1 - z0 + 2) + 8 * nx * ny * (z1 - z0 + 4)),
+                       "l2": "inputs larger than L2 (state per GPU >> 126 MB)" if nloc * 608 > 126e6 * 2
+                       else "state comparable to L2: not an HBM roofline point",
+                       "params": {"tau_f": 0.8, "tau_g": 1.3, "A": -0.0625, "B": 0.0625, "kappa": 0.04, "M": 0.05}},
+            "hbm_gbs_step": step_gbs,
+            "roofline": {"bound": "hbm", "kernel": "k_step", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_site": BYTES_PER_SITE, "avg_launch_ms": ks_avg,
+                         "step_frac": step_gbs / peak, "kernel_time_share": kernel_share},
+            "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "src_hash": src_hash(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

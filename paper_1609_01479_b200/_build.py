@@ -11,8 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblb.so")
-SOURCES = ["lb_kernels.cu", "lb_api.cu"]
-HEADERS = ["d3q19.cuh", "lb_kernels.cuh"]
+SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_api.cu"]
+HEADERS = ["d3q19.cuh", "lb_kernels.cuh", "lb_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -43,6 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
+           *os.environ.get("LB_NVCC_FLAGS", "").split(),
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}",
            "-o", LIB + ".tmp"]

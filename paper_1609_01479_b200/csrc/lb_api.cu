@@ -51,6 +51,8 @@ struct lb_ctx {
   std::vector<Slab> slabs;
   cudaStream_t stream = nullptr;
   int device = 0;
+  int num_sms = 148;
+  int zc = 1;             // z-chunk of the step kernel
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
   ncclComm_t comm = nullptr;
@@ -216,12 +218,14 @@ int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, i
   h->G.nxy = (long long)nx * ny;
   h->G.plane = (long long)NSLOT * h->G.nxy;
   cudaError_t e = cudaGetDevice(&h->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     set_err(nullptr, LB_ECUDA, "CUDA init failed: %s", cudaGetErrorString(e));
     delete h;
     return LB_ECUDA;
   }
+  h->zc = step_zchunk(h->G, h->num_sms);
   rc = alloc_slabs(h);
   if (rc) {
     g_create_error = h->err;
@@ -311,18 +315,27 @@ int exchange_phi(lb_ctx* h) {
   return LB_OK;
 }
 
-// one timestep on every slab: phi, phi halo, step (A -> B), distribution halo, swap
+// one timestep on every slab.  Single periodic slab: the fused step alone.
+// Slabs: phi on the two edge planes at each end (K_phi), phi halo exchange, the
+// fused step (A -> B), distribution halo exchange, swap.
 int one_step(lb_ctx* h, bool collide) {
   const Geom& G = h->G;
   int rc;
-  if (collide) {
-    for (auto& s : h->slabs) CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, G.nzl, h->stream); }));
-    if ((rc = exchange_phi(h))) return rc;
+  if (!collide) {
+    for (auto& s : h->slabs) CK(h, timed(h, K_STEP, true, [&]() { return launch_stream(G, s.A, s.B, h->stream); }));
+  } else {
+    if (!G.zwrap) {
+      for (auto& s : h->slabs) {
+        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, 2, h->stream); }));
+        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, G.nzl - 2, G.nzl, h->stream); }));
+      }
+      if ((rc = exchange_phi(h))) return rc;
+    }
+    for (auto& s : h->slabs)
+      CK(h, timed(h, K_STEP, true, [&]() {
+           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, h->stream);
+         }));
   }
-  for (auto& s : h->slabs)
-    CK(h, timed(h, K_STEP, true, [&]() {
-         return launch_step(G, h->dp, s.A, s.B, s.phi, 0, G.nzl, h->d_flag, collide, h->stream);
-       }));
   if ((rc = exchange_dist(h))) return rc;
   for (auto& s : h->slabs) std::swap(s.A, s.B);
   return LB_OK;

@@ -51,8 +51,12 @@ __host__ __device__ inline long long push_target(const Geom& G, int i, int x, in
 // ---- launchers (lb_kernels.cu) -------------------------------------------
 // All launch on `st`, return cudaGetLastError().
 cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st);
-cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phi,
-                        int z0, int z1, int* flag, bool collide, cudaStream_t st);
+// the fused step (lb_step.cu): collide planes [0, nzl) of A into B; phig = phi
+// buffer whose ghost planes are read when !G.zwrap; zc = z-chunk per CTA
+int step_zchunk(const Geom& G, int num_sms);
+cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
+                        int* flag, cudaStream_t st);
+cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st);
 cudaError_t launch_init_eq(const Geom& G, const DevParams& p, const double* phi, const double* rho,
                            const double* u, double* A, cudaStream_t st);
 // canonical [2][19][nloc] (f block then g block) <-> plane-major buffer

@@ -31,6 +31,17 @@ def spinodal_phi(nx: int, ny: int, nz: int, seed: int = 0, phi0: float = 0.0, am
     return (phi0 + amp * (2.0 * u - 1.0)).reshape(nz, ny, nx)
 
 
+def spinodal_phi_slab(nx: int, ny: int, nz: int, z0: int, z1: int, seed: int = 0, phi0: float = 0.0,
+                      amp: float = 0.01) -> np.ndarray:
+    """Planes [z0, z1) of ``spinodal_phi(nx, ny, nz, seed)``, bitwise, without drawing
+    the rest: the PCG64 stream is advanced past the z0*nx*ny earlier sites."""
+    del nz  # the global extent does not change the draws of these planes
+    bg = np.random.PCG64(seed)
+    bg.advance(z0 * nx * ny)
+    u = np.random.Generator(bg).random(nx * ny * (z1 - z0))
+    return (phi0 + amp * (2.0 * u - 1.0)).reshape(z1 - z0, ny, nx)
+
+
 def spinodal_fields(nx: int, ny: int, nz: int, seed: int = 0, phi0: float = 0.0, amp: float = 0.01):
     """(rho, u, phi) of the spinodal initial state: rho = 1, u = 0."""
     rho = np.ones((nz, ny, nx))
