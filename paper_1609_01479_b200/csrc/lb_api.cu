@@ -28,9 +28,10 @@ const char* const kKernelNames[K_COUNT] = {"k_phi", "k_step", "k_init_eq", "k_pe
 
 struct Slab {
   int z0 = 0;  // global z of local plane 0
-  double* A = nullptr;
-  double* B = nullptr;
+  double* A = nullptr;  // current state (pre-collision f, g)
+  double* B = nullptr;  // next state / staging
   double* phi = nullptr;
+  StepMaps mapsA{}, mapsB{};  // TMA descriptors of A and B (swapped with them)
 };
 
 struct Pending {
@@ -180,6 +181,8 @@ int alloc_slabs(lb_ctx* h) {
     CK(h, cudaMemsetAsync(s.A, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
     CK(h, cudaMemsetAsync(s.B, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
     CK(h, cudaMemsetAsync(s.phi, 0xff, phi_doubles(h->G) * sizeof(double), h->stream));
+    if (!make_step_maps(h->G, s.A, &s.mapsA) || !make_step_maps(h->G, s.B, &s.mapsB))
+      return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed for the step kernel's TMA descriptors");
   }
   CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
   CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
@@ -333,11 +336,14 @@ int one_step(lb_ctx* h, bool collide) {
     }
     for (auto& s : h->slabs)
       CK(h, timed(h, K_STEP, true, [&]() {
-           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, h->stream);
+           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream);
          }));
   }
   if ((rc = exchange_dist(h))) return rc;
-  for (auto& s : h->slabs) std::swap(s.A, s.B);
+  for (auto& s : h->slabs) {
+    std::swap(s.A, s.B);
+    std::swap(s.mapsA, s.mapsB);
+  }
   return LB_OK;
 }
 

@@ -46,16 +46,20 @@ __device__ __forceinline__ void stress6(const DevParams& p, double ph, double gx
 // BGK of g towards g^eq(phi, u, Gamma mu).  emit(i, f_i*, g_i*) is called once
 // per component, in canonical order, as soon as it is known (so stores can
 // retire registers early).  Returns rho (for the R22 numerical-domain check).
-template <class Emit>
-__device__ __forceinline__ double collide(const DevParams& p, const double (&f)[Q], const double (&g)[Q], double phi,
-                                          double mu, const double F[3], Emit&& emit) {
+// Same, reading f_i / g_i through accessors (e.g. from shared memory) and
+// emitting only components I0 <= i < I1; the moments always use all 19 f_i in
+// canonical order, so every caller computes identical rho, u.
+template <int I0, int I1, class GetF, class GetG, class Emit>
+__device__ __forceinline__ double collide_range(const DevParams& p, GetF&& getf, GetG&& getg, double phi, double mu,
+                                                const double F[3], Emit&& emit) {
   double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    rho += f[i];
-    if (cx(i)) jx += cx(i) * f[i];
-    if (cy(i)) jy += cy(i) * f[i];
-    if (cz(i)) jz += cz(i) * f[i];
+    const double fi = getf(i);
+    rho += fi;
+    if (cx(i)) jx += cx(i) * fi;
+    if (cy(i)) jy += cy(i) * fi;
+    if (cz(i)) jz += cz(i) * fi;
   }
   const double rinv = 1.0 / rho;
   const double ux = (jx + 0.5 * F[0]) * rinv;  // R7
@@ -65,18 +69,27 @@ __device__ __forceinline__ double collide(const DevParams& p, const double (&f)[
   const double uF = ux * F[0] + uy * F[1] + uz * F[2];
   const double gmu = p.gamma * mu;
 #pragma unroll
-  for (int i = 0; i < Q; ++i) {
+  for (int i = I0; i < I1; ++i) {
     const double cu = cx(i) * ux + cy(i) * uy + cz(i) * uz;
     const double cF = cx(i) * F[0] + cy(i) * F[1] + cz(i) * F[2];
     const double w = wgt(i);
     const double feq = w * rho * (1.0 + 3.0 * cu + 4.5 * cu * cu - 1.5 * uu);  // R8
     const double S = w * (3.0 * (cF - uF) + 9.0 * cu * cF);                      // R7
-    const double fs = f[i] - (f[i] - feq) * p.inv_tau_f + p.guo_pref * S;
+    const double fi = getf(i), gi = getg(i);
+    const double fs = fi - (fi - feq) * p.inv_tau_f + p.guo_pref * S;
     double geq = w * (3.0 * phi * cu + 4.5 * gmu * (double)(csq(i) - 1) + 4.5 * phi * (cu * cu - uu * (1.0 / 3.0)));  // R9
     if (i == 0) geq += phi;
-    emit(i, fs, g[i] - (g[i] - geq) * p.inv_tau_g);
+    emit(i, fs, gi - (gi - geq) * p.inv_tau_g);
   }
   return rho;
 }
+
+template <class Emit>
+__device__ __forceinline__ double collide(const DevParams& p, const double (&f)[Q], const double (&g)[Q], double phi,
+                                          double mu, const double F[3], Emit&& emit) {
+  return collide_range<0, Q>(
+      p, [&](int i) { return f[i]; }, [&](int i) { return g[i]; }, phi, mu, F, emit);
+}
+
 
 }  // namespace lbk

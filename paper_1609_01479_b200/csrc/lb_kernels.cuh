@@ -54,8 +54,15 @@ cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int 
 // the fused step (lb_step.cu): collide planes [0, nzl) of A into B; phig = phi
 // buffer whose ghost planes are read when !G.zwrap; zc = z-chunk per CTA
 int step_zchunk(const Geom& G, int num_sms);
+// TMA descriptors of one distribution buffer (three CUtensorMap, opaque here):
+// the tile box (TX x TY x 38) and the g halo boxes (x 5 and x 9 components).
+struct alignas(64) StepMaps {
+  unsigned char tile[128], g5[128], g9[128];
+  bool ok;
+};
+bool make_step_maps(const Geom& G, const double* buf, StepMaps* out);
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, cudaStream_t st);
+                        int* flag, const StepMaps* mapsA, cudaStream_t st);
 cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st);
 cudaError_t launch_init_eq(const Geom& G, const DevParams& p, const double* phi, const double* rho,
                            const double* u, double* A, cudaStream_t st);

@@ -4,35 +4,50 @@
 // "Order Parameter Gradients", "Chemical Stress", force =
 // "divergence of the 'Chemical stress'", "Collision", "Propagation"):
 //
-//   CTA   = a TX x TY tile of (x, y) columns marching in z over a chunk of
-//           planes (2.5-D blocking); one thread per column.
-//   smem  = sT : f and g of the tile on the plane being collided      (async-copied)
-//           sG : g on the tile + 2-site halo, two planes ahead         (async-copied)
-//           sPhi: ring of 5 phi planes on the halo box (phi = sum_i g_i recomputed
-//                 for the halo: single pass, no phi round trip through HBM)
+//   CTA   = a TX x TY tile of (x, y) columns marching in z over a chunk of planes
+//           (2.5-D blocking); one thread per column.
+//   smem  = sT : f and g of the tile on the plane being collided   (TMA, 1 op)
+//           sG : g on the tile + 2-site halo, two planes ahead      (TMA, 3 ops;
+//                1-D bulk row copies where the halo wraps the periodic edge)
+//           sPhi: ring of 5 phi planes on the halo box (phi = sum_i g_i is
+//                 recomputed for the halo: single pass, no phi round trip to HBM)
 //           sP : chemical stress P_ab of one plane on the tile + 1-site halo
 //   regs  = the z-column pieces of F = -div P: P_az on planes k-1, k, k+1 and the
 //           in-plane divergence of plane k+1.
 //
-// Loads never occupy registers while in flight: both streams (sT, sG) are
-// cp.async copies issued one stage ahead, so every SM always has one of them
-// outstanding while it computes on the other.
+// Loads never occupy registers or LSU slots while in flight: both streams are
+// asynchronous (TMA / bulk copies completing on an mbarrier each), issued one
+// stage ahead by one thread, so the SM always has one of them outstanding while
+// it computes on the other.  Odd nx (rows not 16-byte
+// aligned) falls back to per-thread 8-byte cp.async with the same schedule.
 //
-// Iteration k (collide plane k), cp.async groups in commit order:
-//   wait sG = g(k+2) box           -> phi(k+2) into the ring; issue sG = g(k+3)
-//   P(k+1) on the P box            -> own P_az(k+1), in-plane div P(k+1)
-//   wait sT = f, g(k) tile         -> collide, push f*, g* to x + c_i (A.8);
-//                                     issue sT = f, g(k+1)
+// Iteration k (collide plane k):
+//   wait sG = g(k+2) box     -> phi(k+2) into the ring; issue sG = g(k+3)
+//   P(k+1) on the P box      -> own P_az(k+1), in-plane div P(k+1)
+//   wait sT = f, g(k) tile   -> collide, push f*, g* to x + c_i (A.8); issue sT = f, g(k+1)
 // HBM traffic per site: f and g read once, written once = 608 B;
 // the halo part of sG and the re-read of g(k) hit L2.
 // Slab edges (z < 0 or z >= nzl, multi-slab only) take phi from the ghost planes
 // of the phi buffer, filled by K_phi + the halo exchange.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "lb_device.cuh"
 
 namespace lbk {
 namespace {
+
+#ifndef LB_STEP_TX
+#define LB_STEP_TX 32
+#endif
+#ifndef LB_STEP_TY
+#define LB_STEP_TY 8
+#endif
+#ifndef LB_STEP_WAVES
+#define LB_STEP_WAVES 4
+#endif
+constexpr int kTX = LB_STEP_TX, kTY = LB_STEP_TY;
 
 __device__ __forceinline__ int slot5(int z) {
   const int s = z % 5;
@@ -41,8 +56,58 @@ __device__ __forceinline__ int slot5(int z) {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+// ---- mbarrier / TMA / bulk-copy primitives (PTX ISA 8.x, sm_90+) ------------
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const double* src, unsigned bytes, unsigned long long* bar,
+                                          unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// L2 policies: the tile copy is the last use of f and g of a plane (evict first);
+// the g box is re-read two planes later by the tile copy (evict last).
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// per-thread copies: wrapped halo boxes (16 B when rows are 16-byte aligned) and
+// everything for odd nx (8 B)
 template <int VEC>
-__device__ __forceinline__ void cp_async(void* dst, const double* src) {
+__device__ __forceinline__ void cp_async_v(void* dst, const double* src) {
   if constexpr (VEC == 2)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
   else
@@ -54,36 +119,36 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// slots of the 19 g components in canonical order
-__device__ __forceinline__ constexpr int gslot(int i) { return slot(1, i); }
+// g components in slot order: rank j = 0..18 <-> slot 5..9 | 19..27 | 33..37
+__host__ __device__ constexpr int gslot_of_rank(int j) { return j < 5 ? 5 + j : (j < 14 ? 19 + (j - 5) : 33 + (j - 14)); }
+__host__ __device__ constexpr int grank(int i) {  // canonical i -> rank
+  return slot(1, i) < 10 ? slot(1, i) - 5 : (slot(1, i) < 28 ? slot(1, i) - 19 + 5 : slot(1, i) - 33 + 14);
+}
 
 template <int TX, int TY>
-struct StepSmem {
+struct alignas(128) StepSmem {
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
   static constexpr int PX = TX + 2, PY = TY + 2, NP = PX * PY;  // P box: tile + 1 halo
   static constexpr int NTILE = TX * TY;
-  double sT[NSLOT][NTILE];  // f, g of the tile, slot order
-  double sG[Q][NB];         // g on the box, canonical order
+  alignas(128) double sT[NSLOT][NTILE];  // f, g of the tile, slot order      (TMA box TX x TY x 38)
+  alignas(128) double sG[Q][NB];         // g on the box, slot-rank order      (TMA boxes BX x BY x 5|9|5)
   double sPhi[5][NB];
   double sP[6][NP];
+  unsigned long long bar_tile, bar_box;
 };
 
-template <int TX, int TY, int VEC>
+// USE_TMA: nx even (16-byte rows): TMA + bulk copies.  Otherwise 8-byte cp.async.
+template <int TX, int TY, bool USE_TMA>
 __global__ void __launch_bounds__(TX* TY, 1)
     k_step_async(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-                 const double* __restrict__ phig, int zc, int* __restrict__ flag) {
+                 const double* __restrict__ phig, int zc, int* __restrict__ flag,
+                 const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_g5,
+                 const __grid_constant__ CUtensorMap tm_g9) {
   using S = StepSmem<TX, TY>;
   constexpr int NT = TX * TY;
-  constexpr int BX = S::BX, NB = S::NB, PX = S::PX, NP = S::NP;
-  constexpr int NBR = (NB + NT - 1) / NT;
-  constexpr int NPR = (NP + NT - 1) / NT;
-  // copy work: units of VEC doubles along x
-  constexpr int TROWU = TX / VEC;                  // units per tile row
-  constexpr int BROWU = BX / VEC;                  // units per box row
-  constexpr int NTU = NSLOT * TY * TROWU;          // tile units
-  constexpr int NBU = Q * S::BY * BROWU;           // box units
-  static_assert(TX % VEC == 0 && BX % VEC == 0, "tile width must be a multiple of VEC");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
+  constexpr unsigned TILE_BYTES = NSLOT * NT * 8, BOX_BYTES = Q * NB * 8;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
   const int tid = threadIdx.x;
@@ -94,26 +159,15 @@ __global__ void __launch_bounds__(TX* TY, 1)
   const int zA = blockIdx.z * zc;
   const int zB = min(zA + zc, G.nzl);
   const long long nxy = G.nxy;
+  // box fully inside the plane: TMA tensor copies; else per-thread cp.async
+  const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
 
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
-  auto zsrc = [&](int zp, bool& ghost) {
-    ghost = false;
-    if (G.zwrap) { zp %= G.nzl; return zp < 0 ? zp + G.nzl : zp; }
-    ghost = zp < 0 || zp >= G.nzl;
-    return zp;
-  };
 
-  // Copy plans, fixed over z: each thread copies the same (row, column-unit)
-  // positions of every component; only the component (slot) changes.
-  //   box : per component BY*BROWU units, thread takes units tid + r*NT
-  //   tile: per slot TY*TROWU units; NT is a multiple of it, so a thread's
-  //         position is fixed and it covers slots s0, s0 + NT/(TY*TROWU), ...
-  constexpr int BOXU = S::BY * BROWU;
-  constexpr int BOXR = (BOXU + NT - 1) / NT;
-  constexpr int TILEU = TY * TROWU;
-  static_assert(NT % TILEU == 0, "tile copy plan needs NT % (TY * TX/VEC) == 0");
-  constexpr int TSTEP = NT / TILEU;
+  // per-thread copy plan of the halo box (fixed over z): units of VEC doubles
+  constexpr int VEC = USE_TMA ? 2 : 1;
+  constexpr int BROWU = BX / VEC, BOXU = BY * BROWU, BOXR = (BOXU + NT - 1) / NT;
   long long box_src[BOXR];
   int box_dst[BOXR];
 #pragma unroll
@@ -123,56 +177,105 @@ __global__ void __launch_bounds__(TX* TY, 1)
     box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * VEC);
     box_dst[r] = u < BOXU ? row * BX + cu * VEC : -1;
   }
-  const int t_unit = tid % TILEU, t_s0 = tid / TILEU;
-  const long long tile_src =
-      (long long)wrapy(y0 + t_unit / TROWU) * G.nx + wrapx(x0 + (t_unit % TROWU) * VEC);  // wrap: partial tiles
-  const int tile_dst = (t_unit / TROWU) * TX + (t_unit % TROWU) * VEC;
+  auto zsrc = [&](int zp, bool& ghost) {
+    ghost = false;
+    if (G.zwrap) { zp %= G.nzl; return zp < 0 ? zp + G.nzl : zp; }
+    ghost = zp < 0 || zp >= G.nzl;
+    return zp;
+  };
 
-  // ---- async copy issue: g box of plane zp into sm.sG (nothing if ghost plane)
-  auto issue_box = [&](int zp) {
+  unsigned long long pol_first = 0, pol_last = 0;
+  if (USE_TMA && tid < 32) pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  if (USE_TMA && tid == 0) {
+    mbar_init(&sm.bar_tile, 1);
+    mbar_init(&sm.bar_box, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph_tile = 0, ph_box = 0;  // mbarrier parities
+
+  // ---- copy issue: g box of plane zp into sm.sG (returns false for a ghost plane)
+  auto issue_box = [&](int zp) -> bool {
     bool ghost;
     const int zs = zsrc(zp, ghost);
-    if (!ghost) {
+    if (ghost) return false;
+    if (USE_TMA && box_interior) {
+      // three TMA boxes (g slots 5..9, 19..27, 33..37), one thread
+      if (tid == 0) {
+        const int cpl = (zs + GZ) * NSLOT;  // component-plane index of slot 0
+        fence_proxy_async();
+        mbar_expect_tx(&sm.bar_box, BOX_BYTES);
+        tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
+        tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
+        tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
+      }
+    } else {
+      // the halo wraps the periodic edge (or odd nx): every thread copies its
+      // fixed box positions of all 19 components (cp.async, one group)
       const double* base = A + (long long)(zs + GZ) * G.plane;
 #pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        const double* bi = base + (long long)gslot(i) * nxy;
+      for (int j = 0; j < Q; ++j) {
+        const double* bj = base + (long long)gslot_of_rank(j) * nxy;
 #pragma unroll
         for (int r = 0; r < BOXR; ++r)
-          if (box_dst[r] >= 0) cp_async<VEC>(&sm.sG[i][box_dst[r]], bi + box_src[r]);
+          if (box_dst[r] >= 0) cp_async_v<VEC>(&sm.sG[j][box_dst[r]], bj + box_src[r]);
       }
+      cp_commit();
     }
-    cp_commit();
+    return true;
   };
-  // ---- async copy issue: f, g of the tile at plane zp (always interior) into sm.sT
-  auto issue_tile = [&](int zp) {
-    if (zp < zB) {
-      const double* base = A + (long long)(zp + GZ) * G.plane + tile_src;
-#pragma unroll
-      for (int s = t_s0; s < NSLOT; s += TSTEP) cp_async<VEC>(&sm.sT[s][tile_dst], base + (long long)s * nxy);
+  auto wait_box = [&](bool issued) {
+    if (!issued) return;
+    if (USE_TMA && box_interior) {
+      mbar_wait(&sm.bar_box, ph_box);
+      ph_box ^= 1;
+    } else {
+      cp_wait<0>();  // only box copies use cp.async groups
     }
-    cp_commit();
+  };
+  // ---- copy issue: f, g of the tile at plane zp (always a local plane) into sm.sT
+  auto issue_tile = [&](int zp) {
+    if constexpr (USE_TMA) {
+      if (zp < zB && tid == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&sm.bar_tile, TILE_BYTES);
+        tma_load_3d(&sm.sT[0][0], &tm_tile, x0, y0, (zp + GZ) * NSLOT, &sm.bar_tile, pol_first);
+      }
+    } else {
+      // odd nx: one 8-byte copy per (slot, site), wrap only for partial tiles
+      if (zp < zB) {
+        const double* base =
+            A + (long long)(zp + GZ) * G.plane + (long long)wrapy(y0 + ly) * G.nx + wrapx(x0 + lx);
+#pragma unroll
+        for (int s = 0; s < NSLOT; ++s) cp_async_v<1>(&sm.sT[s][tid], base + (long long)s * nxy);
+      }
+      cp_commit();
+    }
+  };
+  auto wait_tile = [&]() {
+    if constexpr (USE_TMA) {
+      mbar_wait(&sm.bar_tile, ph_tile);
+      ph_tile ^= 1;
+    } else {
+      cp_wait<0>();
+    }
   };
   // ---- phi of plane zp on the box -> ring (from sG, or from the ghost phi planes)
   auto make_phi = [&](int zp) {
     bool ghost;
     const int zs = zsrc(zp, ghost);
     double* ring = sm.sPhi[slot5(zp)];
+    for (int b = tid; b < NB; b += NT) {
+      double v;
+      if (ghost) {
+        const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
+        v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
+      } else {
+        v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
 #pragma unroll
-    for (int r = 0; r < NBR; ++r) {
-      const int b = tid + r * NT;
-      if (b < NB) {
-        double v;
-        if (ghost) {
-          const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
-          v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
-        } else {
-          v = sm.sG[0][b];  // A.3, canonical order (same as phi_sum)
-#pragma unroll
-          for (int i = 1; i < Q; ++i) v += sm.sG[i][b];
-        }
-        ring[b] = v;
+        for (int i = 1; i < Q; ++i) v += sm.sG[grank(i)][b];
       }
+      ring[b] = v;
     }
   };
   // ---- chemical stress on plane zp over the P box (needs phi planes zp-1..zp+1)
@@ -180,21 +283,17 @@ __global__ void __launch_bounds__(TX* TY, 1)
     const double* f0 = sm.sPhi[slot5(zp - 1)];
     const double* f1 = sm.sPhi[slot5(zp)];
     const double* f2 = sm.sPhi[slot5(zp + 1)];
+    for (int e = tid; e < NP; e += NT) {
+      const int c = (e / PX + 1) * BX + (e % PX + 1);
+      const double ph = f1[c];
+      const double xp = f1[c + 1], xm = f1[c - 1];
+      const double yp = f1[c + BX], ym = f1[c - BX];
+      const double zp_ = f2[c], zm = f0[c];
+      const double lap = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * ph;  // A.2
+      double P[6];
+      stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp_ - zm), lap, P);
 #pragma unroll
-    for (int r = 0; r < NPR; ++r) {
-      const int e = tid + r * NT;
-      if (e < NP) {
-        const int c = (e / PX + 1) * BX + (e % PX + 1);
-        const double ph = f1[c];
-        const double xp = f1[c + 1], xm = f1[c - 1];
-        const double yp = f1[c + BX], ym = f1[c - BX];
-        const double zp_ = f2[c], zm = f0[c];
-        const double lap = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * ph;  // A.2
-        double P[6];
-        stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp_ - zm), lap, P);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
-      }
+      for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
     }
   };
   // ---- own-site pieces of F = -div P (A.5): P_az, and the b = x, y terms
@@ -211,8 +310,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
 
   // ---- prologue: phi on zA-2 .. zA+1; P on zA-1, zA; then prime both streams
   for (int zp = zA - 2; zp <= zA + 1; ++zp) {
-    issue_box(zp);
-    cp_wait<0>();
+    wait_box(issue_box(zp));
     __syncthreads();
     make_phi(zp);
     __syncthreads();
@@ -225,29 +323,29 @@ __global__ void __launch_bounds__(TX* TY, 1)
   compute_P(zA);
   __syncthreads();
   own_P(Pz_cur, Fxy_cur);
-  issue_box(zA + 2);
+  bool box_issued = issue_box(zA + 2);
   issue_tile(zA);
 
   // push targets: wrapped neighbour columns/rows of this thread's site
   const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
-  const int ct = ly * TX + lx;
   const int cbox = (ly + 2) * BX + (lx + 2);
+  const double* sTc = &sm.sT[0][tid];
 
   for (int k = zA; k < zB; ++k) {
-    // pending groups: [box(k+2), tile(k)]
-    cp_wait<1>();
+    wait_box(box_issued);  // g(k+2) box landed
     __syncthreads();
     make_phi(k + 2);
     __syncthreads();  // sG consumed, ring written
-    if (k + 1 < zB)
-      issue_box(k + 3);  // pending: [tile(k), box(k+3)]
-    else
-      cp_commit();
+    if (k + 1 < zB) {
+      box_issued = issue_box(k + 3);
+    } else {
+      box_issued = false;
+    }
     compute_P(k + 1);
     __syncthreads();
     double Pz_next[3], Fxy_next[3];
     own_P(Pz_next, Fxy_next);
-    cp_wait<1>();  // tile(k) landed
+    wait_tile();  // f, g(k) tile landed
     __syncthreads();
     if (active) {
       const double* r0 = sm.sPhi[slot5(k)];
@@ -258,16 +356,11 @@ __global__ void __launch_bounds__(TX* TY, 1)
       double F[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) F[a] = Fxy_cur[a] - 0.5 * (Pz_next[a] - Pz_prev[a]);
-      double f[Q], g[Q];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        f[i] = sm.sT[slot(0, i)][ct];
-        g[i] = sm.sT[slot(1, i)][ct];
-      }
-      const long long zoff[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ,
-                                 (long long)k + GZ,
+      const long long zoff[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
                                  (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
-      const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
+      auto getf = [&](int i) { return sTc[slot(0, i) * NT]; };
+      auto getg = [&](int i) { return sTc[slot(1, i) * NT]; };
+      const double rho = collide_range<0, Q>(p, getf, getg, ph, mu, F, [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
         double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;  // A.8 push
@@ -277,7 +370,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
       if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
     }
     __syncthreads();  // sT consumed
-    issue_tile(k + 1);  // pending: [box(k+3), tile(k+1)]
+    issue_tile(k + 1);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       Pz_prev[a] = Pz_cur[a];
@@ -288,36 +381,68 @@ __global__ void __launch_bounds__(TX* TY, 1)
   cp_wait<0>();
 }
 
-#ifndef LB_STEP_TX
-#define LB_STEP_TX 32
-#endif
-#ifndef LB_STEP_TY
-#define LB_STEP_TY 8
-#endif
-constexpr int kTX = LB_STEP_TX, kTY = LB_STEP_TY;
+// ---- host: tensor maps ---------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
 
-template <int VEC>
+// buffer viewed as a 3-D fp64 tensor {x: nx, y: ny, component-plane: (nzl+2GZ)*38}
+bool encode(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsigned by, unsigned bz) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)G.nx, (cuuint64_t)G.ny, (cuuint64_t)(G.nzl + 2 * GZ) * NSLOT};
+  cuuint64_t strides[2] = {(cuuint64_t)G.nx * 8, (cuuint64_t)G.nxy * 8};
+  cuuint32_t box[3] = {bx, by, bz};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(buf), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool USE_TMA>
 cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                     int* flag, cudaStream_t st) {
+                     int* flag, const StepMaps* maps, cudaStream_t st) {
   constexpr size_t smem = sizeof(StepSmem<kTX, kTY>);
-  auto kern = k_step_async<kTX, kTY, VEC>;
+  auto kern = k_step_async<kTX, kTY, USE_TMA>;
   static bool attr = false;  // per-process, per-instantiation
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  static_assert(sizeof(CUtensorMap) == sizeof(maps->tile), "CUtensorMap size");
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps);
   dim3 grid((G.nx + kTX - 1) / kTX, (G.ny + kTY - 1) / kTY, (G.nzl + zc - 1) / zc);
-  kern<<<grid, kTX * kTY, smem, st>>>(G, p, A, B, phig, zc, flag);
+  kern<<<grid, kTX * kTY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2]);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+bool make_step_maps(const Geom& G, const double* buf, StepMaps* out) {
+  out->ok = false;
+  if (G.nx % 2 != 0) return true;  // odd rows: the cp.async path needs no maps
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
+  const unsigned BX = kTX + 4, BY = kTY + 4;
+  if (!encode(&m[0], G, buf, kTX, kTY, NSLOT)) return false;
+  if (!encode(&m[1], G, buf, BX, BY, 5)) return false;
+  if (!encode(&m[2], G, buf, BX, BY, 9)) return false;
+  out->ok = true;
+  return true;
+}
+
 // number of z-chunks: enough CTAs to fill the GPU several times, chunks >= 8 planes
 int step_zchunk(const Geom& G, int num_sms) {
   const long long tiles = (long long)((G.nx + kTX - 1) / kTX) * ((G.ny + kTY - 1) / kTY);
-  const long long target = 4LL * num_sms;
+  const long long target = (long long)LB_STEP_WAVES * num_sms;
   long long nchunks = (target + tiles - 1) / tiles;
   const long long maxchunks = G.nzl >= 16 ? G.nzl / 8 : 1;
   if (nchunks > maxchunks) nchunks = maxchunks;
@@ -326,10 +451,10 @@ int step_zchunk(const Geom& G, int num_sms) {
 }
 
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, cudaStream_t st) {
-  // 16-byte copies need even rows (every row start then 16-byte aligned)
-  if (G.nx % 2 == 0) return launch_t<2>(G, p, A, B, phig, zc, flag, st);
-  return launch_t<1>(G, p, A, B, phig, zc, flag, st);
+                        int* flag, const StepMaps* maps, cudaStream_t st) {
+  if (maps && maps->ok) return launch_t<true>(G, p, A, B, phig, zc, flag, maps, st);
+  StepMaps dummy{};
+  return launch_t<false>(G, p, A, B, phig, zc, flag, &dummy, st);
 }
 
 }  // namespace lbk
