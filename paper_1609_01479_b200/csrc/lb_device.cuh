@@ -42,16 +42,17 @@ __device__ __forceinline__ void stress6(const DevParams& p, double ph, double gx
   P[PYZ] = p.kappa * gy * gz;
 }
 
-// A.3, A.6, A.7: moments, velocity u = (j + F/2)/rho, BGK of f with Guo source,
-// BGK of g towards g^eq(phi, u, Gamma mu).  emit(i, f_i*, g_i*) is called once
-// per component, in canonical order, as soon as it is known (so stores can
-// retire registers early).  Returns rho (for the R22 numerical-domain check).
-// Same, reading f_i / g_i through accessors (e.g. from shared memory) and
-// emitting only components I0 <= i < I1; the moments always use all 19 f_i in
-// canonical order, so every caller computes identical rho, u.
-template <int I0, int I1, class GetF, class GetG, class Emit>
-__device__ __forceinline__ double collide_range(const DevParams& p, GetF&& getf, GetG&& getg, double phi, double mu,
-                                                const double F[3], Emit&& emit) {
+// A.3, A.6, A.7: moments, velocity u = (j + F/2)/rho, BGK of f with the Guo
+// source, BGK of g towards g^eq(phi, u, Gamma mu):
+//   f_i* = f_i (1 - 1/tau_f) + f_i^eq / tau_f + (1 - 1/(2 tau_f)) S_i
+//   g_i* = g_i (1 - 1/tau_g) + g_i^eq / tau_g
+// Evaluated per antipodal pair (i, 19 - i): c_{19-i} = -c_i and w equal, so each
+// of f^eq, S, g^eq splits into a part even in c (shared by the pair) and a part
+// odd in c (sign-flipped), which roughly halves the fp64 work.  emit(i, f_i*, g_i*)
+// is called once per component.  Returns rho (for the R22 numerical-domain check).
+template <class GetF, class GetG, class Emit>
+__device__ __forceinline__ double collide_acc(const DevParams& p, GetF&& getf, GetG&& getg, double phi, double mu,
+                                              const double F[3], Emit&& emit) {
   double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
@@ -68,18 +69,34 @@ __device__ __forceinline__ double collide_range(const DevParams& p, GetF&& getf,
   const double uu = ux * ux + uy * uy + uz * uz;
   const double uF = ux * F[0] + uy * F[1] + uz * F[2];
   const double gmu = p.gamma * mu;
+  const double omf = p.inv_tau_f, omg = p.inv_tau_g, keepf = 1.0 - p.inv_tau_f, keepg = 1.0 - p.inv_tau_g;
+  // parts of f^eq (R8), S (R7), g^eq (R9) that depend only on |c|^2 (weight class)
+  const double rho_even = rho * (1.0 - 1.5 * uu);   // f^eq/w without the c.u terms
+  const double s_even = -3.0 * uF;                  // S/w without the c terms
+  const double phi_even = -1.5 * phi * uu;          // g^eq/w: -4.5 phi uu/3
+  {  // rest particle: c = 0, |c|^2 - 1 = -1
+    const double w = wgt(0);
+    const double feq = w * rho_even, S = w * s_even;
+    const double geq = w * (phi_even - 4.5 * gmu) + phi;
+    emit(0, keepf * getf(0) + (omf * feq + p.guo_pref * S), keepg * getg(0) + omg * geq);
+  }
 #pragma unroll
-  for (int i = I0; i < I1; ++i) {
+  for (int i = 1; i <= 9; ++i) {
+    const int ia = Q - i;  // antipode (Appendix B)
+    const double w = wgt(i);
     const double cu = cx(i) * ux + cy(i) * uy + cz(i) * uz;
     const double cF = cx(i) * F[0] + cy(i) * F[1] + cz(i) * F[2];
-    const double w = wgt(i);
-    const double feq = w * rho * (1.0 + 3.0 * cu + 4.5 * cu * cu - 1.5 * uu);  // R8
-    const double S = w * (3.0 * (cF - uF) + 9.0 * cu * cF);                      // R7
-    const double fi = getf(i), gi = getg(i);
-    const double fs = fi - (fi - feq) * p.inv_tau_f + p.guo_pref * S;
-    double geq = w * (3.0 * phi * cu + 4.5 * gmu * (double)(csq(i) - 1) + 4.5 * phi * (cu * cu - uu * (1.0 / 3.0)));  // R9
-    if (i == 0) geq += phi;
-    emit(i, fs, gi - (gi - geq) * p.inv_tau_g);
+    const double cu2 = cu * cu;
+    // even / odd parts, each already times w
+    const double feq_e = w * (rho_even + 4.5 * rho * cu2), feq_o = (3.0 * w * rho) * cu;
+    const double S_e = w * (s_even + 9.0 * cu * cF), S_o = (3.0 * w) * cF;
+    const double geq_e = w * (4.5 * gmu * (double)(csq(i) - 1) + phi_even + 4.5 * phi * cu2);
+    const double geq_o = (3.0 * w * phi) * cu;
+    const double sym = omf * feq_e + p.guo_pref * S_e;
+    const double anti = omf * feq_o + p.guo_pref * S_o;
+    const double gsym = omg * geq_e, ganti = omg * geq_o;
+    emit(i, keepf * getf(i) + sym + anti, keepg * getg(i) + gsym + ganti);
+    emit(ia, keepf * getf(ia) + sym - anti, keepg * getg(ia) + gsym - ganti);
   }
   return rho;
 }
@@ -87,9 +104,8 @@ __device__ __forceinline__ double collide_range(const DevParams& p, GetF&& getf,
 template <class Emit>
 __device__ __forceinline__ double collide(const DevParams& p, const double (&f)[Q], const double (&g)[Q], double phi,
                                           double mu, const double F[3], Emit&& emit) {
-  return collide_range<0, Q>(
+  return collide_acc(
       p, [&](int i) { return f[i]; }, [&](int i) { return g[i]; }, phi, mu, F, emit);
 }
-
 
 }  // namespace lbk

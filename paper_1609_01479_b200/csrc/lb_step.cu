@@ -347,6 +347,16 @@ __global__ void __launch_bounds__(TX* TY, 1)
     own_P(Pz_next, Fxy_next);
     wait_tile();  // f, g(k) tile landed
     __syncthreads();
+    // pull this site's f, g out of sT, then free sT for the next tile copy so
+    // it overlaps the collision arithmetic and the next phi/P phases
+    double f[Q], g[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      f[i] = sTc[slot(0, i) * NT];
+      g[i] = sTc[slot(1, i) * NT];
+    }
+    __syncthreads();  // sT consumed
+    issue_tile(k + 1);
     if (active) {
       const double* r0 = sm.sPhi[slot5(k)];
       const double ph = r0[cbox];
@@ -358,9 +368,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
       for (int a = 0; a < 3; ++a) F[a] = Fxy_cur[a] - 0.5 * (Pz_next[a] - Pz_prev[a]);
       const long long zoff[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
                                  (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
-      auto getf = [&](int i) { return sTc[slot(0, i) * NT]; };
-      auto getg = [&](int i) { return sTc[slot(1, i) * NT]; };
-      const double rho = collide_range<0, Q>(p, getf, getg, ph, mu, F, [&](int i, double fs, double gs) {
+      const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
         double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;  // A.8 push
@@ -369,8 +377,6 @@ __global__ void __launch_bounds__(TX* TY, 1)
       });
       if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
     }
-    __syncthreads();  // sT consumed
-    issue_tile(k + 1);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       Pz_prev[a] = Pz_cur[a];
