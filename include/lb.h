@@ -160,6 +160,13 @@ int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out);
  * the same kernel addressing and halo exchanges as lb_step.  Test support. */
 int lb_debug_stream(lb_t* h, int nsteps);
 
+/* Measurement probe: nsteps launches of the step kernel with its copies and
+ * stores but without the physics (mode 1: tile copy + propagation stores only;
+ * mode 2: also the halo-box copies and the phi / stress stencils).  The state
+ * afterwards is a propagated copy, not a solution.  Gives the memory-side
+ * ceiling of the step kernel's access pattern for the roofline analysis. */
+int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
+
 /* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of
  * nranks, the ranks it sends its +z and -z halo to, and the number of doubles
  * per message: distributions (10 components x nx*ny) and phi (2 planes x nx*ny).

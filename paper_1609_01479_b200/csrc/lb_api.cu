@@ -321,10 +321,11 @@ int exchange_phi(lb_ctx* h) {
 // one timestep on every slab.  Single periodic slab: the fused step alone.
 // Slabs: phi on the two edge planes at each end (K_phi), phi halo exchange, the
 // fused step (A -> B), distribution halo exchange, swap.
-int one_step(lb_ctx* h, bool collide) {
+// mode: -1 propagation only (k_stream), 0 the step, 1/2 step-kernel memory probes
+int one_step(lb_ctx* h, int mode) {
   const Geom& G = h->G;
   int rc;
-  if (!collide) {
+  if (mode < 0) {
     for (auto& s : h->slabs) CK(h, timed(h, K_STEP, true, [&]() { return launch_stream(G, s.A, s.B, h->stream); }));
   } else {
     if (!G.zwrap) {
@@ -336,7 +337,7 @@ int one_step(lb_ctx* h, bool collide) {
     }
     for (auto& s : h->slabs)
       CK(h, timed(h, K_STEP, true, [&]() {
-           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream);
+           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, mode);
          }));
   }
   if ((rc = exchange_dist(h))) return rc;
@@ -474,7 +475,17 @@ int lb_step(lb_t* h, int nsteps) {
   if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
   for (int t = 0; t < nsteps; ++t)
-    if ((rc = one_step(h, true))) return rc;
+    if ((rc = one_step(h, 0))) return rc;
+  return finish(h);
+}
+
+int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (nsteps < 0 || mode < 1 || mode > 2) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2} required");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
+  for (int t = 0; t < nsteps; ++t)
+    if ((rc = one_step(h, mode))) return rc;
   return finish(h);
 }
 
@@ -484,7 +495,7 @@ int lb_debug_stream(lb_t* h, int nsteps) {
   if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
   for (int t = 0; t < nsteps; ++t)
-    if ((rc = one_step(h, false))) return rc;
+    if ((rc = one_step(h, -1))) return rc;
   return finish(h);
 }
 

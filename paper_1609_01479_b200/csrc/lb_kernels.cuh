@@ -54,15 +54,16 @@ cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int 
 // the fused step (lb_step.cu): collide planes [0, nzl) of A into B; phig = phi
 // buffer whose ghost planes are read when !G.zwrap; zc = z-chunk per CTA
 int step_zchunk(const Geom& G, int num_sms);
-// TMA descriptors of one distribution buffer (three CUtensorMap, opaque here):
-// the tile box (TX x TY x 38) and the g halo boxes (x 5 and x 9 components).
+// TMA descriptors of one distribution buffer (four CUtensorMap, opaque here):
+// tile boxes TX x TY x {5, 9} components, halo boxes (TX+4) x (TY+4) x {5, 9}.
 struct alignas(64) StepMaps {
-  unsigned char tile[128], g5[128], g9[128];
+  unsigned char m[4][128];
   bool ok;
 };
 bool make_step_maps(const Geom& G, const double* buf, StepMaps* out);
+// mode 0 = the step; 1, 2 = memory probes (lb_debug_step_probe)
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* mapsA, cudaStream_t st);
+                        int* flag, const StepMaps* mapsA, cudaStream_t st, int mode = 0);
 cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st);
 cudaError_t launch_init_eq(const Geom& G, const DevParams& p, const double* phi, const double* rho,
                            const double* u, double* A, cudaStream_t st);

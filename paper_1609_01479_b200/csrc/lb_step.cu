@@ -119,6 +119,8 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// f components in slot order: rank j = 0..18 <-> slot 0..4 | 10..18 | 28..32
+__host__ __device__ constexpr int fslot_of_rank(int j) { return j < 5 ? j : (j < 14 ? 10 + (j - 5) : 28 + (j - 14)); }
 // g components in slot order: rank j = 0..18 <-> slot 5..9 | 19..27 | 33..37
 __host__ __device__ constexpr int gslot_of_rank(int j) { return j < 5 ? 5 + j : (j < 14 ? 19 + (j - 5) : 33 + (j - 14)); }
 __host__ __device__ constexpr int grank(int i) {  // canonical i -> rank
@@ -130,24 +132,34 @@ struct alignas(128) StepSmem {
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
   static constexpr int PX = TX + 2, PY = TY + 2, NP = PX * PY;  // P box: tile + 1 halo
   static constexpr int NTILE = TX * TY;
-  alignas(128) double sT[NSLOT][NTILE];  // f, g of the tile, slot order      (TMA box TX x TY x 38)
-  alignas(128) double sG[Q][NB];         // g on the box, slot-rank order      (TMA boxes BX x BY x 5|9|5)
+  alignas(128) double sTf[Q][NTILE];  // f of the tile, f-slot order   (TMA boxes TX x TY x 5|9|5)
+  alignas(128) double sTg[Q][NTILE];  // g of the tile, g-slot order   (TMA boxes TX x TY x 5|9|5)
+  alignas(128) double sG[Q][NB];      // g on the box, g-slot order     (TMA boxes BX x BY x 5|9|5)
   double sPhi[5][NB];
   double sP[6][NP];
-  unsigned long long bar_tile, bar_box;
+  unsigned long long bar_f, bar_g, bar_box;
 };
 
+// f components in slot order: rank j = 0..18 <-> slot 0..4 | 10..18 | 28..32
+__host__ __device__ constexpr int frank(int i) {  // canonical i -> rank
+  return slot(0, i) < 5 ? slot(0, i) : (slot(0, i) < 19 ? slot(0, i) - 10 + 5 : slot(0, i) - 28 + 14);
+}
+
 // USE_TMA: nx even (16-byte rows): TMA + bulk copies.  Otherwise 8-byte cp.async.
-template <int TX, int TY, bool USE_TMA>
+// The tile's f and g are separate streams: f (from HBM) is consumed first and
+// re-issued for the next plane at the top of an iteration, so it has a whole
+// iteration of lead time; g (an L2 hit: the box brought it in two planes ago)
+// follows.
+template <int TX, int TY, bool USE_TMA, int MODE>
 __global__ void __launch_bounds__(TX* TY, 1)
     k_step_async(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
                  const double* __restrict__ phig, int zc, int* __restrict__ flag,
-                 const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_g5,
-                 const __grid_constant__ CUtensorMap tm_g9) {
+                 const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
+                 const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
   using S = StepSmem<TX, TY>;
   constexpr int NT = TX * TY;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
-  constexpr unsigned TILE_BYTES = NSLOT * NT * 8, BOX_BYTES = Q * NB * 8;
+  constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
@@ -187,12 +199,13 @@ __global__ void __launch_bounds__(TX* TY, 1)
   unsigned long long pol_first = 0, pol_last = 0;
   if (USE_TMA && tid < 32) pol_first = policy_evict_first(), pol_last = policy_evict_last();
   if (USE_TMA && tid == 0) {
-    mbar_init(&sm.bar_tile, 1);
+    mbar_init(&sm.bar_f, 1);
+    mbar_init(&sm.bar_g, 1);
     mbar_init(&sm.bar_box, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  unsigned ph_tile = 0, ph_box = 0;  // mbarrier parities
+  unsigned ph_f = 0, ph_g = 0, ph_box = 0;  // mbarrier parities
 
   // ---- copy issue: g box of plane zp into sm.sG (returns false for a ghost plane)
   auto issue_box = [&](int zp) -> bool {
@@ -234,28 +247,40 @@ __global__ void __launch_bounds__(TX* TY, 1)
     }
   };
   // ---- copy issue: f, g of the tile at plane zp (always a local plane) into sm.sT
-  auto issue_tile = [&](int zp) {
+  // dist 0: f slots 0..4 | 10..18 | 28..32 -> sTf;  dist 1: g slots 5..9 | 19..27 | 33..37 -> sTg
+  auto issue_tile = [&](int zp, int dist) {
+    double(*dst)[NT] = dist == 0 ? sm.sTf : sm.sTg;
     if constexpr (USE_TMA) {
       if (zp < zB && tid == 0) {
+        unsigned long long* bar = dist == 0 ? &sm.bar_f : &sm.bar_g;
+        const int cp0 = (zp + GZ) * NSLOT + (dist == 0 ? 0 : 5);
         fence_proxy_async();
-        mbar_expect_tx(&sm.bar_tile, TILE_BYTES);
-        tma_load_3d(&sm.sT[0][0], &tm_tile, x0, y0, (zp + GZ) * NSLOT, &sm.bar_tile, pol_first);
+        mbar_expect_tx(bar, TILE_BYTES);
+        tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol_first);
+        tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
+        tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol_first);
       }
     } else {
-      // odd nx: one 8-byte copy per (slot, site), wrap only for partial tiles
+      // odd nx: one 8-byte copy per (component, site), wrap only for partial tiles
       if (zp < zB) {
         const double* base =
             A + (long long)(zp + GZ) * G.plane + (long long)wrapy(y0 + ly) * G.nx + wrapx(x0 + lx);
 #pragma unroll
-        for (int s = 0; s < NSLOT; ++s) cp_async_v<1>(&sm.sT[s][tid], base + (long long)s * nxy);
+        for (int j = 0; j < Q; ++j)
+          cp_async_v<1>(&dst[j][tid], base + (long long)(dist == 0 ? fslot_of_rank(j) : gslot_of_rank(j)) * nxy);
       }
       cp_commit();
     }
   };
-  auto wait_tile = [&]() {
+  auto wait_tile = [&](int dist) {
     if constexpr (USE_TMA) {
-      mbar_wait(&sm.bar_tile, ph_tile);
-      ph_tile ^= 1;
+      if (dist == 0) {
+        mbar_wait(&sm.bar_f, ph_f);
+        ph_f ^= 1;
+      } else {
+        mbar_wait(&sm.bar_g, ph_g);
+        ph_g ^= 1;
+      }
     } else {
       cp_wait<0>();
     }
@@ -308,56 +333,68 @@ __global__ void __launch_bounds__(TX* TY, 1)
     Fxy[2] = -0.5 * (P[PXZ][e + 1] - P[PXZ][e - 1]) - 0.5 * (P[PYZ][e + PX] - P[PYZ][e - PX]);
   };
 
-  // ---- prologue: phi on zA-2 .. zA+1; P on zA-1, zA; then prime both streams
+  // ---- prologue: phi on zA-2 .. zA+1; P on zA-1, zA; then prime the streams
+  issue_tile(zA, 0);
   for (int zp = zA - 2; zp <= zA + 1; ++zp) {
     wait_box(issue_box(zp));
     __syncthreads();
     make_phi(zp);
     __syncthreads();
   }
-  compute_P(zA - 1);
-  __syncthreads();
-  double Pz_prev[3], Pz_cur[3], Fxy_cur[3], unused[3];
-  own_P(Pz_prev, unused);
-  __syncthreads();
-  compute_P(zA);
-  __syncthreads();
-  own_P(Pz_cur, Fxy_cur);
+  double Pz_prev[3] = {0, 0, 0}, Pz_cur[3] = {0, 0, 0}, Fxy_cur[3] = {0, 0, 0};
+  if (MODE != 1) {
+    compute_P(zA - 1);
+    __syncthreads();
+    double unused[3];
+    own_P(Pz_prev, unused);
+    __syncthreads();
+    compute_P(zA);
+    __syncthreads();
+    own_P(Pz_cur, Fxy_cur);
+  }
   bool box_issued = issue_box(zA + 2);
-  issue_tile(zA);
+  issue_tile(zA, 1);
 
   // push targets: wrapped neighbour columns/rows of this thread's site
   const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
   const int cbox = (ly + 2) * BX + (lx + 2);
-  const double* sTc = &sm.sT[0][tid];
 
   for (int k = zA; k < zB; ++k) {
-    wait_box(box_issued);  // g(k+2) box landed
-    __syncthreads();
-    make_phi(k + 2);
-    __syncthreads();  // sG consumed, ring written
-    if (k + 1 < zB) {
-      box_issued = issue_box(k + 3);
-    } else {
-      box_issued = false;
-    }
-    compute_P(k + 1);
-    __syncthreads();
-    double Pz_next[3], Fxy_next[3];
-    own_P(Pz_next, Fxy_next);
-    wait_tile();  // f, g(k) tile landed
-    __syncthreads();
-    // pull this site's f, g out of sT, then free sT for the next tile copy so
-    // it overlaps the collision arithmetic and the next phi/P phases
+    // f(k) to registers, then free sTf for f(k+1): a whole iteration of lead time
     double f[Q], g[Q];
+    wait_tile(0);
 #pragma unroll
-    for (int i = 0; i < Q; ++i) {
-      f[i] = sTc[slot(0, i) * NT];
-      g[i] = sTc[slot(1, i) * NT];
+    for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
+    wait_box(box_issued);  // g(k+2) box landed
+    __syncthreads();       // sTf consumed by all threads; sG visible
+    issue_tile(k + 1, 0);
+    double Pz_next[3] = {0, 0, 0}, Fxy_next[3] = {0, 0, 0};
+    if (MODE != 1) make_phi(k + 2);
+    __syncthreads();  // sG consumed, ring written
+    box_issued = (k + 1 < zB) ? issue_box(k + 3) : false;
+    if (MODE != 1) {
+      compute_P(k + 1);
+      __syncthreads();
+      own_P(Pz_next, Fxy_next);
     }
-    __syncthreads();  // sT consumed
-    issue_tile(k + 1);
-    if (active) {
+    wait_tile(1);  // g(k) tile landed
+#pragma unroll
+    for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
+    __syncthreads();  // sTg consumed
+    issue_tile(k + 1, 1);
+    if (MODE != 0 && active) {
+      const long long zo[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
+                               (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
+        const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+        double* d = B + zo[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;
+        __stcs(d + (long long)slot(0, i) * nxy, f[i]);
+        __stcs(d + (long long)slot(1, i) * nxy, g[i]);
+      }
+    }
+    if (MODE == 0 && active) {
       const double* r0 = sm.sPhi[slot5(k)];
       const double ph = r0[cbox];
       const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) +
@@ -413,22 +450,32 @@ bool encode(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsig
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool USE_TMA>
+template <bool USE_TMA, int MODE>
 cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                      int* flag, const StepMaps* maps, cudaStream_t st) {
   constexpr size_t smem = sizeof(StepSmem<kTX, kTY>);
-  auto kern = k_step_async<kTX, kTY, USE_TMA>;
+  auto kern = k_step_async<kTX, kTY, USE_TMA, MODE>;
   static bool attr = false;  // per-process, per-instantiation
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  static_assert(sizeof(CUtensorMap) == sizeof(maps->tile), "CUtensorMap size");
-  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps);
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   dim3 grid((G.nx + kTX - 1) / kTX, (G.ny + kTY - 1) / kTY, (G.nzl + zc - 1) / zc);
-  kern<<<grid, kTX * kTY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2]);
+  kern<<<grid, kTX * kTY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
   return cudaGetLastError();
+}
+
+template <bool USE_TMA>
+cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
+                        int* flag, const StepMaps* maps, cudaStream_t st, int mode) {
+  switch (mode) {
+    case 1: return launch_t<USE_TMA, 1>(G, p, A, B, phig, zc, flag, maps, st);
+    case 2: return launch_t<USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st);
+    default: return launch_t<USE_TMA, 0>(G, p, A, B, phig, zc, flag, maps, st);
+  }
 }
 
 }  // namespace
@@ -436,11 +483,12 @@ cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double*
 bool make_step_maps(const Geom& G, const double* buf, StepMaps* out) {
   out->ok = false;
   if (G.nx % 2 != 0) return true;  // odd rows: the cp.async path needs no maps
-  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out->m);
   const unsigned BX = kTX + 4, BY = kTY + 4;
-  if (!encode(&m[0], G, buf, kTX, kTY, NSLOT)) return false;
-  if (!encode(&m[1], G, buf, BX, BY, 5)) return false;
-  if (!encode(&m[2], G, buf, BX, BY, 9)) return false;
+  if (!encode(&m[0], G, buf, kTX, kTY, 5)) return false;
+  if (!encode(&m[1], G, buf, kTX, kTY, 9)) return false;
+  if (!encode(&m[2], G, buf, BX, BY, 5)) return false;
+  if (!encode(&m[3], G, buf, BX, BY, 9)) return false;
   out->ok = true;
   return true;
 }
@@ -457,10 +505,10 @@ int step_zchunk(const Geom& G, int num_sms) {
 }
 
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st) {
-  if (maps && maps->ok) return launch_t<true>(G, p, A, B, phig, zc, flag, maps, st);
+                        int* flag, const StepMaps* maps, cudaStream_t st, int mode) {
+  if (maps && maps->ok) return launch_mode<true>(G, p, A, B, phig, zc, flag, maps, st, mode);
   StepMaps dummy{};
-  return launch_t<false>(G, p, A, B, phig, zc, flag, &dummy, st);
+  return launch_mode<false>(G, p, A, B, phig, zc, flag, &dummy, st, mode);
 }
 
 }  // namespace lbk
