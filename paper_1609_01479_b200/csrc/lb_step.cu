@@ -38,14 +38,17 @@
 namespace lbk {
 namespace {
 
+// Tile 32 x 4 (128 threads, ~104 KB smem): two CTAs per SM, so one CTA's copies
+// are in flight while the other computes (measured best of 32x8, 32x4, 64x4,
+// 16x8 at 512x512x64 and 128^3).
 #ifndef LB_STEP_TX
 #define LB_STEP_TX 32
 #endif
 #ifndef LB_STEP_TY
-#define LB_STEP_TY 8
+#define LB_STEP_TY 4
 #endif
 #ifndef LB_STEP_WAVES
-#define LB_STEP_WAVES 4
+#define LB_STEP_WAVES 8
 #endif
 constexpr int kTX = LB_STEP_TX, kTY = LB_STEP_TY;
 

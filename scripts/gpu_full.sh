@@ -1,0 +1,11 @@
+# full round check: GPU tests, smoke, bench lines, reference arm, ncu launch list + full capture
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo tests=$?; tail -2 gpurun_out/gpu_tests.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench=$?
+timeout 300 python bench.py --config c3 --no-cpu-baseline > gpurun_out/bench_c3.json 2>/dev/null; echo bench_c3=$?
+timeout 300 python bench.py --config c2 --steps 1000 --no-cpu-baseline > gpurun_out/bench_c2.json 2>/dev/null; echo bench_c2=$?
+timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>/dev/null; echo ref=$?
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 50 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo ncu_launches=$?
+$CMD > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/prof_kstep_c5 $CMD > gpurun_out/ncu2.log 2>&1; echo ncu_full=$?

@@ -29,9 +29,11 @@ def main(path, sites=None):
         top = sorted(stalls.items(), key=lambda kv: -kv[1])[:8]
         print("  top stalls (warps per issue):", ", ".join(f"{k.split('stalled_')[1].split('_per')[0]}={v:.2f}" for k, v in top))
         if sites:
-            rb = float(d["dram__bytes_read.sum"].replace(",", "")) * (1e6 if units[h.index("dram__bytes_read.sum")] == "Mbyte" else 1)
-            wb = float(d["dram__bytes_write.sum"].replace(",", "")) * (1e6 if units[h.index("dram__bytes_write.sum")] == "Mbyte" else 1)
-            print(f"  dram bytes/site: read {rb/sites:.1f} write {wb/sites:.1f}")
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rb = float(d["dram__bytes_read.sum"].replace(",", "")) * scale[units[h.index("dram__bytes_read.sum")]]
+            wb = float(d["dram__bytes_write.sum"].replace(",", "")) * scale[units[h.index("dram__bytes_write.sum")]]
+            print(f"  dram bytes/site: read {rb/sites:.1f} write {wb/sites:.1f}  (algorithmic 304 + 304)")
+            print(f"  dram bytes/launch: {rb + wb:.6e}")
 
 
 if __name__ == "__main__":

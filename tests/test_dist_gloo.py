@@ -1,0 +1,159 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2-4): no GPU needed.
+
+* dist helpers used by bench.py / lb_create_slab bootstrap: broadcast of the
+  128-byte NCCL unique id, max-over-ranks timing reduction, slab ranges.
+* the z-slab halo plan of the C library (lb_halo_plan: peers and message
+  sizes) driving a slab-decomposed run of the CPU oracle, with the same
+  exchanges the CUDA path does (phi: 2 planes per direction before the step;
+  distributions: the 10 components with c_z = +-1 of the boundary planes after
+  it).  The decomposed result must equal the whole-lattice oracle bitwise
+  (sub-domains surrounded by halos filled from neighbours).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import lb_ref as R
+from paper_1609_01479_b200 import dist as D
+from paper_1609_01479_b200 import lb, synth
+
+P0 = R.Params(mobility=0.2)
+CZ_UP = [i for i in range(19) if R.C[i, 2] == 1]
+CZ_DN = [i for i in range(19) if R.C[i, 2] == -1]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _run(fn, world, *args):
+    port = _free_port()
+    mp.spawn(_entry, args=(world, port, fn, args), nprocs=world, join=True)
+
+
+def _entry(rank, world, port, fn, args):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RANK"], os.environ["WORLD_SIZE"] = str(rank), str(world)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fn(rank, world, *args)
+    finally:
+        dist.destroy_process_group()
+
+
+def _sendrecv(send_arr, dst, recv_shape, src):
+    """Paired exchange (isend + recv) of float64 arrays."""
+    out = torch.empty(recv_shape, dtype=torch.float64)
+    req = dist.isend(torch.from_numpy(np.ascontiguousarray(send_arr)), dst)
+    dist.recv(out, src)
+    req.wait()
+    return out.numpy()
+
+
+# ---------------------------------------------------------------- helpers
+def _helpers_body(rank, world):
+    uid = lb.lb_nccl_get_unique_id() if rank == 0 else None
+    got = D.broadcast_bytes(uid)
+    ref = [None]
+    if rank == 0:
+        ref = [got]
+    dist.broadcast_object_list(ref, 0)
+    assert len(got) == 128 and got == ref[0]
+    assert D.max_over_ranks(float(rank) * 1.5) == 1.5 * (world - 1)
+    assert D.sum_over_ranks(1.0) == float(world)
+    z0, z1 = D.slab_range(8 * world, world, rank)
+    assert (z0, z1) == (8 * rank, 8 * rank + 8)
+    D.barrier()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_helpers_gloo(world):
+    _run(_helpers_body, world)
+
+
+def test_slab_range_rejects_thin_slabs():
+    with pytest.raises(ValueError):
+        D.slab_range(6, 4, 0)
+    with pytest.raises(ValueError):
+        D.slab_range(3, 2, 0)
+
+
+# ---------------------------------------------------------------- slab-decomposed oracle
+def slab_step(f, g, p, plan, L):
+    """One oracle step on a z-slab with the library's halo exchanges (A.8, R14)."""
+    up, dn = plan["up"], plan["down"]
+    nz_, ny, nx = f.shape[1:]
+    assert nz_ == L
+    # phi halo: planes [L-2, L) go up, [0, 2) go down (lb_api.cu exchange_phi)
+    phi = R.order_parameter(g)
+    assert plan["phi_doubles"] == 2 * nx * ny
+    below = _sendrecv(phi[L - 2:], up, (2, ny, nx), dn)
+    above = _sendrecv(phi[:2], dn, (2, ny, nx), up)
+    ext = np.concatenate([below, phi, above])  # planes -2 .. L+1
+    grad, lap = R.gradient(ext), R.laplacian(ext)
+    F = R.force(R.chemical_stress(ext, grad, lap, p))[:, 2:L + 2]
+    mu = R.chemical_potential(ext, lap, p)[2:L + 2]
+    rho, j = R.density(f), R.momentum(f)
+    R.check_domain(f, g, rho)
+    u = R.velocity(rho, j, F)
+    fs, gs = R.collide_f(f, rho, u, F, p), R.collide_g(g, phi, u, mu, p)
+    # push with ghost planes -1 and L, then the distribution halo exchange
+    outs = []
+    for a in (fs, gs):
+        o = np.zeros((19, L + 2, ny, nx))
+        for i in range(19):
+            shifted = np.roll(a[i], shift=(int(R.C[i, 1]), int(R.C[i, 0])), axis=(1, 2))
+            o[i, 1 + int(R.C[i, 2]):L + 1 + int(R.C[i, 2])] += shifted
+        outs.append(o)
+    msg_up = np.stack([o[i, L + 1] for o in outs for i in CZ_UP])  # ghost plane L, c_z = +1
+    msg_dn = np.stack([o[i, 0] for o in outs for i in CZ_DN])  # ghost plane -1, c_z = -1
+    assert plan["dist_doubles"] == msg_up.size == msg_dn.size
+    from_dn = _sendrecv(msg_up, up, msg_up.shape, dn)
+    from_up = _sendrecv(msg_dn, dn, msg_dn.shape, up)
+    k = 0
+    for o in outs:
+        for i in CZ_UP:
+            o[i, 1] = from_dn[k]
+            k += 1
+    k = 0
+    for o in outs:
+        for i in CZ_DN:
+            o[i, L] = from_up[k]
+            k += 1
+    return outs[0][:, 1:L + 1], outs[1][:, 1:L + 1]
+
+
+def _slab_body(rank, world, shape, steps, out_dir):
+    nx, ny, nz = shape
+    plan = lb.lb_halo_plan(nx, ny, nz, world, rank)
+    z0, z1 = D.slab_range(nz, world, rank)
+    rho, u, phi, nf, ng = synth.rough_fields(nx, ny, nz, seed=3)
+    f, g = R.equilibrium_state(rho, u, phi, P0)
+    f, g = (f + nf)[:, z0:z1].copy(), (g + ng)[:, z0:z1].copy()
+    for _ in range(steps):
+        f, g = slab_step(f, g, P0, plan, z1 - z0)
+    np.save(os.path.join(out_dir, f"f{rank}.npy"), f)
+    np.save(os.path.join(out_dir, f"g{rank}.npy"), g)
+
+
+@pytest.mark.parametrize("world,shape", [(2, (6, 5, 8)), (3, (5, 4, 9)), (4, (4, 5, 8))])
+def test_slab_decomposed_oracle_equals_whole_lattice(world, shape, tmp_path):
+    steps = 3
+    _run(_slab_body, world, shape, steps, str(tmp_path))
+    nx, ny, nz = shape
+    rho, u, phi, nf, ng = synth.rough_fields(nx, ny, nz, seed=3)
+    f, g = R.equilibrium_state(rho, u, phi, P0)
+    f, g = R.run(f + nf, g + ng, P0, steps)
+    fs = np.concatenate([np.load(tmp_path / f"f{r}.npy") for r in range(world)], axis=1)
+    gs = np.concatenate([np.load(tmp_path / f"g{r}.npy") for r in range(world)], axis=1)
+    assert np.array_equal(fs, f) and np.array_equal(gs, g)
