@@ -160,12 +160,18 @@ int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out);
  * the same kernel addressing and halo exchanges as lb_step.  Test support. */
 int lb_debug_stream(lb_t* h, int nsteps);
 
-/* Measurement probe: nsteps launches of the step kernel with its copies and
- * stores but without the physics (mode 1: tile copy + propagation stores only;
- * mode 2: also the halo-box copies and the phi / stress stencils).  The state
- * afterwards is a propagated copy, not a solution.  Gives the memory-side
- * ceiling of the step kernel's access pattern for the roofline analysis. */
+/* Measurement probe: nsteps launches of the tile step kernel with its copies and
+ * stores but without the physics (mode 1: tile copies + halo box + propagation
+ * stores; mode 2: also the phi / stress stencils; mode 3: tile copies and stores
+ * only).  The state afterwards is a propagated copy, not a solution.  Gives the
+ * memory-side ceiling of the access pattern for the roofline analysis. */
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
+
+/* Which step kernel lb_step uses: 0 = default (the tile kernel), 1 = the tile
+ * kernel (halo box per CTA), 2 = the cluster kernel (phi halos shared through
+ * distributed shared memory; needs nx % 64 == 0 and ny % 16 == 0, else
+ * LB_EINVAL).  Both give bitwise identical results.  Test / measurement support. */
+int lb_debug_step_kernel(lb_t* h, int which);
 
 /* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of
  * nranks, the ranks it sends its +z and -z halo to, and the number of doubles

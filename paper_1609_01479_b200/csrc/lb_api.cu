@@ -31,7 +31,8 @@ struct Slab {
   double* A = nullptr;  // current state (pre-collision f, g)
   double* B = nullptr;  // next state / staging
   double* phi = nullptr;
-  StepMaps mapsA{}, mapsB{};  // TMA descriptors of A and B (swapped with them)
+  StepMaps mapsA{}, mapsB{};        // TMA descriptors of A and B (swapped with them)
+  ClusterMaps cmapsA{}, cmapsB{};  // same, for the cluster step kernel
 };
 
 struct Pending {
@@ -54,6 +55,9 @@ struct lb_ctx {
   int device = 0;
   int num_sms = 148;
   int zc = 1;             // z-chunk of the step kernel
+  int ty = 8;             // tile rows of the step kernel
+  int czc = 1;            // z-chunk of the cluster step kernel
+  int kernel_choice = 0;  // 0 auto (cluster kernel where it fits), 1 tile kernel, 2 cluster kernel
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
   ncclComm_t comm = nullptr;
@@ -181,7 +185,8 @@ int alloc_slabs(lb_ctx* h) {
     CK(h, cudaMemsetAsync(s.A, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
     CK(h, cudaMemsetAsync(s.B, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
     CK(h, cudaMemsetAsync(s.phi, 0xff, phi_doubles(h->G) * sizeof(double), h->stream));
-    if (!make_step_maps(h->G, s.A, &s.mapsA) || !make_step_maps(h->G, s.B, &s.mapsB))
+    if (!make_step_maps(h->G, s.A, h->ty, &s.mapsA) || !make_step_maps(h->G, s.B, h->ty, &s.mapsB) ||
+        !make_cluster_maps(h->G, s.A, &s.cmapsA) || !make_cluster_maps(h->G, s.B, &s.cmapsB))
       return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed for the step kernel's TMA descriptors");
   }
   CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
@@ -228,7 +233,9 @@ int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, i
     delete h;
     return LB_ECUDA;
   }
-  h->zc = step_zchunk(h->G, h->num_sms);
+  h->ty = step_tile_rows(h->G, h->num_sms);
+  h->zc = step_zchunk(h->G, h->num_sms, h->ty);
+  h->czc = cluster_zchunk(h->G, h->num_sms);
   rc = alloc_slabs(h);
   if (rc) {
     g_create_error = h->err;
@@ -337,6 +344,10 @@ int one_step(lb_ctx* h, int mode) {
     }
     for (auto& s : h->slabs)
       CK(h, timed(h, K_STEP, true, [&]() {
+           // the cluster kernel is opt-in: measured slower than the tile kernel in round 1
+           // (cluster barrier per plane)
+           const bool cluster = mode == 0 && s.cmapsA.ok && h->kernel_choice == 2;
+           if (cluster) return launch_step_cluster(G, h->dp, s.A, s.B, s.phi, h->czc, h->d_flag, &s.cmapsA, h->stream);
            return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, mode);
          }));
   }
@@ -344,6 +355,7 @@ int one_step(lb_ctx* h, int mode) {
   for (auto& s : h->slabs) {
     std::swap(s.A, s.B);
     std::swap(s.mapsA, s.mapsB);
+    std::swap(s.cmapsA, s.cmapsB);
   }
   return LB_OK;
 }
@@ -482,11 +494,19 @@ int lb_step(lb_t* h, int nsteps) {
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
   int rc = usable(h);
   if (rc) return rc;
-  if (nsteps < 0 || mode < 1 || mode > 2) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2} required");
+  if (nsteps < 0 || mode < 1 || mode > 3) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2, 3} required");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
   for (int t = 0; t < nsteps; ++t)
     if ((rc = one_step(h, mode))) return rc;
   return finish(h);
+}
+
+int lb_debug_step_kernel(lb_t* h, int which) {
+  if (!h || which < 0 || which > 2) return set_err(h, LB_EINVAL, "which must be 0 (auto), 1 (tile) or 2 (cluster)");
+  if (which == 2 && !h->slabs.empty() && !h->slabs[0].cmapsA.ok)
+    return set_err(h, LB_EINVAL, "the cluster kernel needs nx %% 64 == 0 and ny %% 16 == 0");
+  h->kernel_choice = which;
+  return LB_OK;
 }
 
 int lb_debug_stream(lb_t* h, int nsteps) {

@@ -53,17 +53,30 @@ __host__ __device__ inline long long push_target(const Geom& G, int i, int x, in
 cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st);
 // the fused step (lb_step.cu): collide planes [0, nzl) of A into B; phig = phi
 // buffer whose ghost planes are read when !G.zwrap; zc = z-chunk per CTA
-int step_zchunk(const Geom& G, int num_sms);
+int step_tile_rows(const Geom& G, int num_sms);  // 4 or 8
+int step_zchunk(const Geom& G, int num_sms, int ty);
 // TMA descriptors of one distribution buffer (four CUtensorMap, opaque here):
 // tile boxes TX x TY x {5, 9} components, halo boxes (TX+4) x (TY+4) x {5, 9}.
 struct alignas(64) StepMaps {
   unsigned char m[4][128];
+  int ty;  // tile rows of the kernel these maps were made for
   bool ok;
 };
-bool make_step_maps(const Geom& G, const double* buf, StepMaps* out);
+bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out);
 // mode 0 = the step; 1, 2 = memory probes (lb_debug_step_probe)
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                         int* flag, const StepMaps* mapsA, cudaStream_t st, int mode = 0);
+// the cluster variant of the step (lb_step_cluster.cu): phi halos shared through
+// distributed shared memory; for nx % 64 == 0 and ny % 16 == 0
+struct alignas(64) ClusterMaps {
+  unsigned char m[2][128];
+  bool ok;
+};
+bool cluster_step_fits(const Geom& G);
+bool make_cluster_maps(const Geom& G, const double* buf, ClusterMaps* out);
+int cluster_zchunk(const Geom& G, int num_sms);
+cudaError_t launch_step_cluster(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                                int zc, int* flag, const ClusterMaps* mapsA, cudaStream_t st);
 cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st);
 cudaError_t launch_init_eq(const Geom& G, const DevParams& p, const double* phi, const double* rho,
                            const double* u, double* A, cudaStream_t st);

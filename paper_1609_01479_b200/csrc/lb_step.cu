@@ -38,19 +38,19 @@
 namespace lbk {
 namespace {
 
-// Tile 32 x 4 (128 threads, ~104 KB smem): two CTAs per SM, so one CTA's copies
-// are in flight while the other computes (measured best of 32x8, 32x4, 64x4,
-// 16x8 at 512x512x64 and 128^3).
+// Tile 32 x 8 (256 threads, ~177 KB smem, one CTA per SM): the halo box is 1.69x
+// the tile (2.25x for 32 x 4); measured best at 512x512x64 with z-chunks giving
+// ~8 waves.
 #ifndef LB_STEP_TX
 #define LB_STEP_TX 32
 #endif
 #ifndef LB_STEP_TY
-#define LB_STEP_TY 4
+#define LB_STEP_TY 8
 #endif
 #ifndef LB_STEP_WAVES
 #define LB_STEP_WAVES 8
 #endif
-constexpr int kTX = LB_STEP_TX, kTY = LB_STEP_TY;
+constexpr int kTX = LB_STEP_TX;
 
 __device__ __forceinline__ int slot5(int z) {
   const int s = z % 5;
@@ -338,14 +338,14 @@ __global__ void __launch_bounds__(TX* TY, 1)
 
   // ---- prologue: phi on zA-2 .. zA+1; P on zA-1, zA; then prime the streams
   issue_tile(zA, 0);
-  for (int zp = zA - 2; zp <= zA + 1; ++zp) {
+  for (int zp = zA - 2; zp <= zA + 1 && MODE != 3; ++zp) {
     wait_box(issue_box(zp));
     __syncthreads();
     make_phi(zp);
     __syncthreads();
   }
   double Pz_prev[3] = {0, 0, 0}, Pz_cur[3] = {0, 0, 0}, Fxy_cur[3] = {0, 0, 0};
-  if (MODE != 1) {
+  if (MODE != 1 && MODE != 3) {
     compute_P(zA - 1);
     __syncthreads();
     double unused[3];
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     __syncthreads();
     own_P(Pz_cur, Fxy_cur);
   }
-  bool box_issued = issue_box(zA + 2);
+  bool box_issued = MODE != 3 ? issue_box(zA + 2) : false;
   issue_tile(zA, 1);
 
   // push targets: wrapped neighbour columns/rows of this thread's site
@@ -372,10 +372,10 @@ __global__ void __launch_bounds__(TX* TY, 1)
     __syncthreads();       // sTf consumed by all threads; sG visible
     issue_tile(k + 1, 0);
     double Pz_next[3] = {0, 0, 0}, Fxy_next[3] = {0, 0, 0};
-    if (MODE != 1) make_phi(k + 2);
+    if (MODE != 1 && MODE != 3) make_phi(k + 2);
     __syncthreads();  // sG consumed, ring written
-    box_issued = (k + 1 < zB) ? issue_box(k + 3) : false;
-    if (MODE != 1) {
+    box_issued = (k + 1 < zB && MODE != 3) ? issue_box(k + 3) : false;
+    if (MODE != 1 && MODE != 3) {
       compute_P(k + 1);
       __syncthreads();
       own_P(Pz_next, Fxy_next);
@@ -453,11 +453,11 @@ bool encode(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsig
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool USE_TMA, int MODE>
+template <int TY, bool USE_TMA, int MODE>
 cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                      int* flag, const StepMaps* maps, cudaStream_t st) {
-  constexpr size_t smem = sizeof(StepSmem<kTX, kTY>);
-  auto kern = k_step_async<kTX, kTY, USE_TMA, MODE>;
+  constexpr size_t smem = sizeof(StepSmem<kTX, TY>);
+  auto kern = k_step_async<kTX, TY, USE_TMA, MODE>;
   static bool attr = false;  // per-process, per-instantiation
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -466,30 +466,40 @@ cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double*
   }
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
-  dim3 grid((G.nx + kTX - 1) / kTX, (G.ny + kTY - 1) / kTY, (G.nzl + zc - 1) / zc);
-  kern<<<grid, kTX * kTY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
+  dim3 grid((G.nx + kTX - 1) / kTX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc);
+  kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
   return cudaGetLastError();
 }
 
-template <bool USE_TMA>
+template <int TY, bool USE_TMA>
 cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                         int* flag, const StepMaps* maps, cudaStream_t st, int mode) {
   switch (mode) {
-    case 1: return launch_t<USE_TMA, 1>(G, p, A, B, phig, zc, flag, maps, st);
-    case 2: return launch_t<USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st);
-    default: return launch_t<USE_TMA, 0>(G, p, A, B, phig, zc, flag, maps, st);
+    case 1: return launch_t<TY, USE_TMA, 1>(G, p, A, B, phig, zc, flag, maps, st);
+    case 2: return launch_t<TY, USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st);
+    case 3: return launch_t<TY, USE_TMA, 3>(G, p, A, B, phig, zc, flag, maps, st);
+    default: return launch_t<TY, USE_TMA, 0>(G, p, A, B, phig, zc, flag, maps, st);
   }
 }
 
 }  // namespace
 
-bool make_step_maps(const Geom& G, const double* buf, StepMaps* out) {
+// Tile rows: 8 (one CTA per SM, halo box 1.69x the tile) when the plane has enough
+// tiles to fill the GPU several times over; 4 (two CTAs per SM) for smaller planes,
+// where longer z-chunks matter more than the smaller halo.
+int step_tile_rows(const Geom& G, int num_sms) {
+  const long long tiles8 = (long long)((G.nx + kTX - 1) / kTX) * ((G.ny + 7) / 8);
+  return (LB_STEP_TY == 8 && tiles8 >= 4LL * num_sms) ? 8 : 4;
+}
+
+bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out) {
   out->ok = false;
+  out->ty = ty;
   if (G.nx % 2 != 0) return true;  // odd rows: the cp.async path needs no maps
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out->m);
-  const unsigned BX = kTX + 4, BY = kTY + 4;
-  if (!encode(&m[0], G, buf, kTX, kTY, 5)) return false;
-  if (!encode(&m[1], G, buf, kTX, kTY, 9)) return false;
+  const unsigned BX = kTX + 4, BY = ty + 4;
+  if (!encode(&m[0], G, buf, kTX, ty, 5)) return false;
+  if (!encode(&m[1], G, buf, kTX, ty, 9)) return false;
   if (!encode(&m[2], G, buf, BX, BY, 5)) return false;
   if (!encode(&m[3], G, buf, BX, BY, 9)) return false;
   out->ok = true;
@@ -497,8 +507,8 @@ bool make_step_maps(const Geom& G, const double* buf, StepMaps* out) {
 }
 
 // number of z-chunks: enough CTAs to fill the GPU several times, chunks >= 8 planes
-int step_zchunk(const Geom& G, int num_sms) {
-  const long long tiles = (long long)((G.nx + kTX - 1) / kTX) * ((G.ny + kTY - 1) / kTY);
+int step_zchunk(const Geom& G, int num_sms, int ty) {
+  const long long tiles = (long long)((G.nx + kTX - 1) / kTX) * ((G.ny + ty - 1) / ty);
   const long long target = (long long)LB_STEP_WAVES * num_sms;
   long long nchunks = (target + tiles - 1) / tiles;
   const long long maxchunks = G.nzl >= 16 ? G.nzl / 8 : 1;
@@ -509,9 +519,13 @@ int step_zchunk(const Geom& G, int num_sms) {
 
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                         int* flag, const StepMaps* maps, cudaStream_t st, int mode) {
-  if (maps && maps->ok) return launch_mode<true>(G, p, A, B, phig, zc, flag, maps, st, mode);
-  StepMaps dummy{};
-  return launch_mode<false>(G, p, A, B, phig, zc, flag, &dummy, st, mode);
+  if (!maps) return cudaErrorInvalidValue;
+  const bool tma = maps->ok;
+  if (maps->ty == 8)
+    return tma ? launch_mode<8, true>(G, p, A, B, phig, zc, flag, maps, st, mode)
+               : launch_mode<8, false>(G, p, A, B, phig, zc, flag, maps, st, mode);
+  return tma ? launch_mode<4, true>(G, p, A, B, phig, zc, flag, maps, st, mode)
+             : launch_mode<4, false>(G, p, A, B, phig, zc, flag, maps, st, mode);
 }
 
 }  // namespace lbk

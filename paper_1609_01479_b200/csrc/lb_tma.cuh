@@ -1,0 +1,119 @@
+// lb_tma.cuh -- asynchronous-copy building blocks for the step kernels (sm_90+ PTX):
+// mbarriers, TMA tensor copies with L2 cache hints, cp.async, cluster barriers and
+// distributed shared memory, plus the host-side tensor-map encoder.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include "lb_kernels.cuh"
+
+namespace lbk {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// TMA 3-D tile copy global -> this CTA's shared memory, completing on `bar`.
+// The box start must be 16-byte aligned in x (even fp64 index).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+// L2 policies
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// per-thread async copies (16 B needs 16-byte aligned source and destination)
+template <int VEC>
+__device__ __forceinline__ void cp_async_v(void* dst, const double* src) {
+  if constexpr (VEC == 2)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// thread-block clusters: rank, barrier, distributed shared memory
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Cluster barrier for shared-memory hand-offs only: the caller has already made
+// its shared-memory writes complete CTA-wide (bar.sync), so the arrive is relaxed
+// -- a release here would also wait for every outstanding global store.
+__device__ __forceinline__ void cluster_sync_smem() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `local` (a shared-memory variable) in CTA `rank`
+__device__ __forceinline__ unsigned dsmem_addr(const void* local, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double ld_dsmem(unsigned addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// f / g components in slot order (d3q19.cuh): three contiguous runs each
+//   f: 0..4 | 10..18 | 28..32      g: 5..9 | 19..27 | 33..37
+__host__ __device__ constexpr int fslot_of_rank(int j) { return j < 5 ? j : (j < 14 ? 10 + (j - 5) : 28 + (j - 14)); }
+__host__ __device__ constexpr int gslot_of_rank(int j) { return j < 5 ? 5 + j : (j < 14 ? 19 + (j - 5) : 33 + (j - 14)); }
+__host__ __device__ constexpr int frank(int i) {  // canonical i -> rank
+  return slot(0, i) < 5 ? slot(0, i) : (slot(0, i) < 19 ? slot(0, i) - 10 + 5 : slot(0, i) - 28 + 14);
+}
+__host__ __device__ constexpr int grank(int i) {
+  return slot(1, i) < 10 ? slot(1, i) - 5 : (slot(1, i) < 28 ? slot(1, i) - 19 + 5 : slot(1, i) - 33 + 14);
+}
+// first slot of run r (0, 1, 2) of f (dist 0) or g (dist 1), and its length
+__host__ __device__ constexpr int run_first(int dist, int r) { return (r == 0 ? 0 : (r == 1 ? 10 : 28)) + (dist ? (r == 1 ? 9 : 5) : 0); }
+__host__ __device__ constexpr int run_len(int r) { return r == 1 ? 9 : 5; }
+__host__ __device__ constexpr int run_rank0(int r) { return r == 0 ? 0 : (r == 1 ? 5 : 14); }
+
+// host: 3-D fp64 tensor map of a distribution buffer {x: nx, y: ny, comp-plane: (nzl+2GZ)*38}
+bool encode_dist_map(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsigned by, unsigned bz);
+
+}  // namespace lbk

@@ -59,6 +59,7 @@ _lb_init_equilibrium = _sig("lb_init_equilibrium", _i, _vp, _vp, _vp, _vp)
 _lb_step = _sig("lb_step", _i, _vp, _i)
 _lb_debug_stream = _sig("lb_debug_stream", _i, _vp, _i)
 _lb_debug_step_probe = _sig("lb_debug_step_probe", _i, _vp, _i, _i)
+_lb_debug_step_kernel = _sig("lb_debug_step_kernel", _i, _vp, _i)
 _lb_get_state = _sig("lb_get_state", _i, _vp, _vp, _vp)
 _lb_get_phi = _sig("lb_get_phi", _i, _vp, _vp)
 _lb_destroy = _sig("lb_destroy", None, _vp)
@@ -75,7 +76,7 @@ _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
 
 EXPORTS = [
     "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
-    "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_get_state", "lb_get_phi", "lb_destroy",
+    "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_halo_plan",
 ]
@@ -155,6 +156,10 @@ def lb_step(h, nsteps: int) -> None:
 
 def lb_debug_stream(h, nsteps: int) -> None:
     _check(_lb_debug_stream(h, nsteps), h)
+
+
+def lb_debug_step_kernel(h, which: int) -> None:
+    _check(_lb_debug_step_kernel(h, which), h)
 
 
 def lb_debug_step_probe(h, nsteps: int, mode: int) -> None:

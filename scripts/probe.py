@@ -44,6 +44,7 @@ def main():
     out["step"] = timed(lambda n: L.step(n))
     out["probe1_copy_push"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 1))
     out["probe2_plus_halo_phi_P"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 2))
+    out["probe3_tile_only"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 3))
     out["k_stream_site_parallel"] = timed(lambda n: lb.lb_debug_stream(L.h, n))
     n = nx * ny * nz * 38
     x = torch.empty(n, dtype=torch.float64, device="cuda")

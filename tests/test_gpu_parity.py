@@ -36,9 +36,11 @@ def rough(nx, ny, nz, seed=1, p=P0):
     return f + nf, g + ng
 
 
-def gpu_run(f, g, p, nsteps, nslabs=1):
+def gpu_run(f, g, p, nsteps, nslabs=1, kernel=0):
+    """kernel: 0 automatic, 1 tile step kernel, 2 cluster step kernel (lb_debug_step_kernel)."""
     nz, ny, nx = f.shape[1:]
     with lb.Lattice(nx, ny, nz, cparams(p), nslabs=nslabs) as L:
+        lb.lb_debug_step_kernel(L.h, kernel)
         L.set_state(f, g)
         L.step(nsteps)
         return L.get_state()
@@ -158,6 +160,36 @@ def test_parity_full_size_sampled(nx, ny, nz):
         fs.append(f1[:, z, y, x]), gs.append(g1[:, z, y, x])
     assert rel(np.array(fs), np.array(fr)) <= TOL
     assert rel(np.array(gs), np.array(gr)) <= TOL
+
+
+# ------------------------------------------------------------------ the cluster step kernel
+@pytest.mark.parametrize("shape", [(64, 16, 8), (128, 32, 12), (64, 48, 5), (192, 16, 3)])
+def test_cluster_kernel_parity_and_bitwise_equal_to_tile_kernel(shape):
+    """lb_step_cluster.cu (phi halos through distributed shared memory) gives the same
+    bits as the tile kernel and meets the parity tolerance against the oracle."""
+    nx, ny, nz = shape
+    f, g = rough(nx, ny, nz, seed=12)
+    a = gpu_run(f, g, P0, 4, kernel=2)
+    b = gpu_run(f, g, P0, 4, kernel=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert_parity(a, R.run(f, g, P0, 4))
+
+
+@pytest.mark.parametrize("nslabs", [2, 4])
+def test_cluster_kernel_slabs_bitwise(nslabs):
+    f, g = rough(64, 16, 16, seed=13)
+    a = gpu_run(f, g, P0, 5, nslabs=1, kernel=2)
+    b = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=2)
+    c = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(a[0], c[0]) and np.array_equal(a[1], c[1])
+
+
+def test_cluster_kernel_rejects_unfit_lattice():
+    with lb.Lattice(24, 16, 8) as L:
+        with pytest.raises(lb.LBError) as e:
+            lb.lb_debug_step_kernel(L.h, 2)
+        assert e.value.code == lb.LB_EINVAL
 
 
 # ------------------------------------------------------------------ bitwise properties of the GPU path
