@@ -51,6 +51,15 @@ namespace {
 #define LB_STEP_WAVES 8
 #endif
 constexpr int kTX = LB_STEP_TX;
+#ifndef LB_CLUSTER_SYNC_EVERY
+#define LB_CLUSTER_SYNC_EVERY 0
+#endif
+#ifndef LB_CLUSTER_X
+#define LB_CLUSTER_X 1
+#endif
+#ifndef LB_CLUSTER_Y
+#define LB_CLUSTER_Y 2
+#endif
 
 __device__ __forceinline__ int slot5(int z) {
   const int s = z % 5;
@@ -363,6 +372,13 @@ __global__ void __launch_bounds__(TX* TY, 1)
   const int cbox = (ly + 2) * BX + (lx + 2);
 
   for (int k = zA; k < zB; ++k) {
+#if LB_CLUSTER_SYNC_EVERY > 0
+    // keep the CTAs of a cluster (neighbouring tiles) within a few planes of each
+    // other, so the halo rows one loads are still in L2 when the owner loads them
+    if ((k - zA) % LB_CLUSTER_SYNC_EVERY == 0) {
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+    }
+#endif
     // f(k) to registers, then free sTf for f(k+1): a whole iteration of lead time
     double f[Q], g[Q];
     wait_tile(0);
@@ -467,6 +483,24 @@ cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double*
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   dim3 grid((G.nx + kTX - 1) / kTX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc);
+#if LB_CLUSTER_SYNC_EVERY > 0
+  if (grid.x % LB_CLUSTER_X == 0 && grid.y % LB_CLUSTER_Y == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kTX * TY, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = LB_CLUSTER_X;
+    at[0].val.clusterDim.y = LB_CLUSTER_Y;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
+  }
+  return cudaErrorInvalidConfiguration;
+#endif
   kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
   return cudaGetLastError();
 }
