@@ -163,14 +163,19 @@ int lb_debug_stream(lb_t* h, int nsteps);
 /* Measurement probe: nsteps launches of the tile step kernel with its copies and
  * stores but without the physics (mode 1: tile copies + halo box + propagation
  * stores; mode 2: also the phi / stress stencils; mode 3: tile copies and stores
- * only).  The state afterwards is a propagated copy, not a solution.  Gives the
+ * only; mode 4: like mode 1, but g taken from the halo box instead of a second
+ * tile copy).  The state afterwards is a propagated copy, not a solution.  Gives the
  * memory-side ceiling of the access pattern for the roofline analysis. */
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
 
-/* Which step kernel lb_step uses: 0 = default (the tile kernel), 1 = the tile
+/* Which step kernel lb_step uses: 0 = default (the warp-specialised kernel
+ * when the plane is large enough for 32 x 8 tiles and nx is even, else the tile
+ * kernel), 1 = the tile
  * kernel (halo box per CTA), 2 = the cluster kernel (phi halos shared through
  * distributed shared memory; needs nx % 64 == 0 and ny % 16 == 0, else
- * LB_EINVAL).  Both give bitwise identical results.  Test / measurement support. */
+ * LB_EINVAL), 3 = the warp-specialised tile kernel (stencil and collision on
+ * separate warps; needs nx even, else LB_EINVAL).  All give bitwise identical
+ * results.  Test / measurement support. */
 int lb_debug_step_kernel(lb_t* h, int which);
 
 /* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of

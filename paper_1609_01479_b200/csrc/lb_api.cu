@@ -57,7 +57,7 @@ struct lb_ctx {
   int zc = 1;             // z-chunk of the step kernel
   int ty = 8;             // tile rows of the step kernel
   int czc = 1;            // z-chunk of the cluster step kernel
-  int kernel_choice = 0;  // 0 auto (cluster kernel where it fits), 1 tile kernel, 2 cluster kernel
+  int kernel_choice = 0;  // 0 default, 1 tile kernel, 2 cluster kernel, 3 warp-specialised kernel
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
   ncclComm_t comm = nullptr;
@@ -348,6 +348,11 @@ int one_step(lb_ctx* h, int mode) {
            // (cluster barrier per plane)
            const bool cluster = mode == 0 && s.cmapsA.ok && h->kernel_choice == 2;
            if (cluster) return launch_step_cluster(G, h->dp, s.A, s.B, s.phi, h->czc, h->d_flag, &s.cmapsA, h->stream);
+           // default: the warp-specialised kernel for 32 x 8 tiles (large planes), the
+           // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
+           const bool ws = mode == 0 && step_ws_fits(&s.mapsA) &&
+                           (h->kernel_choice == 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
+           if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream);
            return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, mode);
          }));
   }
@@ -494,7 +499,7 @@ int lb_step(lb_t* h, int nsteps) {
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
   int rc = usable(h);
   if (rc) return rc;
-  if (nsteps < 0 || mode < 1 || mode > 3) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2, 3} required");
+  if (nsteps < 0 || mode < 1 || mode > 4) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2, 3, 4} required");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
   for (int t = 0; t < nsteps; ++t)
     if ((rc = one_step(h, mode))) return rc;
@@ -502,9 +507,12 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
 }
 
 int lb_debug_step_kernel(lb_t* h, int which) {
-  if (!h || which < 0 || which > 2) return set_err(h, LB_EINVAL, "which must be 0 (auto), 1 (tile) or 2 (cluster)");
+  if (!h || which < 0 || which > 3)
+    return set_err(h, LB_EINVAL, "which must be 0 (auto), 1 (tile), 2 (cluster) or 3 (warp-specialised)");
   if (which == 2 && !h->slabs.empty() && !h->slabs[0].cmapsA.ok)
     return set_err(h, LB_EINVAL, "the cluster kernel needs nx %% 64 == 0 and ny %% 16 == 0");
+  if (which == 3 && !h->slabs.empty() && !step_ws_fits(&h->slabs[0].mapsA))
+    return set_err(h, LB_EINVAL, "the warp-specialised kernel needs nx even (TMA rows)");
   h->kernel_choice = which;
   return LB_OK;
 }

@@ -74,11 +74,12 @@ __device__ __forceinline__ double collide_acc(const DevParams& p, GetF&& getf, G
   const double rho_even = rho * (1.0 - 1.5 * uu);   // f^eq/w without the c.u terms
   const double s_even = -3.0 * uF;                  // S/w without the c terms
   const double phi_even = -1.5 * phi * uu;          // g^eq/w: -4.5 phi uu/3
-  {  // rest particle: c = 0, |c|^2 - 1 = -1
+  {  // rest particle: c = 0, |c|^2 - 1 = -1.  g is written with explicit roundings:
+     // left to the compiler, its FMA contraction differed between kernels (1 ulp)
     const double w = wgt(0);
     const double feq = w * rho_even, S = w * s_even;
-    const double geq = w * (phi_even - 4.5 * gmu) + phi;
-    emit(0, keepf * getf(0) + (omf * feq + p.guo_pref * S), keepg * getg(0) + omg * geq);
+    const double geq = __fma_rn(w, __fma_rn(-4.5, gmu, phi_even), phi);
+    emit(0, keepf * getf(0) + (omf * feq + p.guo_pref * S), __fma_rn(keepg, getg(0), __dmul_rn(omg, geq)));
   }
 #pragma unroll
   for (int i = 1; i <= 9; ++i) {

@@ -48,6 +48,29 @@ __host__ __device__ inline long long push_target(const Geom& G, int i, int x, in
   return (long long)(zd + GZ) * G.plane + (long long)xd + (long long)G.nx * yd;  // + slot*nxy by caller
 }
 
+// Tile of a step-kernel block: the linear block index walks the plane in strips
+// of w tiles in x, y fastest within a strip, z-chunk slowest.  w >= tiles per
+// row is plain row-major order, the fastest measured: narrow strips put y
+// neighbours (which share halo rows) closer in launch order, but the CTAs
+// resident at one time then read 256-byte pieces of many 4 KB rows instead of
+// whole rows, and lost more in DRAM locality than they gained in L2 reuse
+// (DESIGN.md "Tuning").
+struct TileId {
+  int bx, by, bz;
+};
+__host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int w) {
+  const int ntiles = ntx * nty;
+  TileId t;
+  t.bz = L / ntiles;
+  const int r = L - t.bz * ntiles;
+  const int band = w * nty;
+  const int strip = r / band, rem = r - strip * band;
+  const int ws = ntx - strip * w < w ? ntx - strip * w : w;
+  t.by = rem / ws;
+  t.bx = strip * w + (rem - t.by * ws);
+  return t;
+}
+
 // ---- launchers (lb_kernels.cu) -------------------------------------------
 // All launch on `st`, return cudaGetLastError().
 cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st);
@@ -66,6 +89,10 @@ bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out);
 // mode 0 = the step; 1, 2 = memory probes (lb_debug_step_probe)
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                         int* flag, const StepMaps* mapsA, cudaStream_t st, int mode = 0);
+// the warp-specialised variant of the step (lb_step_ws.cu): same maps, nx even
+bool step_ws_fits(const StepMaps* maps);
+cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
+                           int* flag, const StepMaps* mapsA, cudaStream_t st);
 // the cluster variant of the step (lb_step_cluster.cu): phi halos shared through
 // distributed shared memory; for nx % 64 == 0 and ny % 16 == 0
 struct alignas(64) ClusterMaps {

@@ -47,18 +47,18 @@ namespace {
 #ifndef LB_STEP_TY
 #define LB_STEP_TY 8
 #endif
+// planes ahead of the asynchronous copies at which the same boxes are prefetched
+// into L2 (0: off)
+#ifndef LB_PF_DIST
+#define LB_PF_DIST 0
+#endif
 #ifndef LB_STEP_WAVES
 #define LB_STEP_WAVES 8
 #endif
 constexpr int kTX = LB_STEP_TX;
-#ifndef LB_CLUSTER_SYNC_EVERY
-#define LB_CLUSTER_SYNC_EVERY 0
-#endif
-#ifndef LB_CLUSTER_X
-#define LB_CLUSTER_X 1
-#endif
-#ifndef LB_CLUSTER_Y
-#define LB_CLUSTER_Y 2
+// strip width of the block -> tile order (tile_of_block)
+#ifndef LB_STRIP_W
+#define LB_STRIP_W (1 << 20)
 #endif
 
 __device__ __forceinline__ int slot5(int z) {
@@ -103,6 +103,11 @@ __device__ __forceinline__ void bulk_load(void* dst, const double* src, unsigned
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
 }
 // L2 policies: the tile copy is the last use of f and g of a plane (evict first);
 // the g box is re-read two planes later by the tile copy (evict last).
@@ -177,10 +182,11 @@ __global__ void __launch_bounds__(TX* TY, 1)
 
   const int tid = threadIdx.x;
   const int lx = tid % TX, ly = tid / TX;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, LB_STRIP_W);
+  const int x0 = tb.bx * TX, y0 = tb.by * TY;
   const int x = x0 + lx, y = y0 + ly;
   const bool active = (x < G.nx) && (y < G.ny);
-  const int zA = blockIdx.z * zc;
+  const int zA = tb.bz * zc;
   const int zB = min(zA + zc, G.nzl);
   const long long nxy = G.nxy;
   // box fully inside the plane: TMA tensor copies; else per-thread cp.async
@@ -233,6 +239,13 @@ __global__ void __launch_bounds__(TX* TY, 1)
         tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
         tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
         tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
+        const int zq = G.zwrap ? wrap_n(zp + LB_PF_DIST, G.nzl) : zp + LB_PF_DIST;
+        if (LB_PF_DIST > 0 && zp + LB_PF_DIST <= zB + 1 && zq >= 0 && zq < G.nzl) {
+          const int cq = (zq + GZ) * NSLOT;
+          tma_prefetch_3d(&tm_g5, x0 - 2, y0 - 2, cq + 5);
+          tma_prefetch_3d(&tm_g9, x0 - 2, y0 - 2, cq + 19);
+          tma_prefetch_3d(&tm_g5, x0 - 2, y0 - 2, cq + 33);
+        }
       }
     } else {
       // the halo wraps the periodic edge (or odd nx): every thread copies its
@@ -271,6 +284,12 @@ __global__ void __launch_bounds__(TX* TY, 1)
         tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol_first);
         tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
         tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol_first);
+        if (LB_PF_DIST > 0 && dist == 0 && zp + LB_PF_DIST < zB) {
+          const int cq = (zp + LB_PF_DIST + GZ) * NSLOT;
+          tma_prefetch_3d(&tm_t5, x0, y0, cq);
+          tma_prefetch_3d(&tm_t9, x0, y0, cq + 10);
+          tma_prefetch_3d(&tm_t5, x0, y0, cq + 28);
+        }
       }
     } else {
       // odd nx: one 8-byte copy per (component, site), wrap only for partial tiles
@@ -354,7 +373,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     __syncthreads();
   }
   double Pz_prev[3] = {0, 0, 0}, Pz_cur[3] = {0, 0, 0}, Fxy_cur[3] = {0, 0, 0};
-  if (MODE != 1 && MODE != 3) {
+  if (MODE == 0 || MODE == 2) {
     compute_P(zA - 1);
     __syncthreads();
     double unused[3];
@@ -365,20 +384,13 @@ __global__ void __launch_bounds__(TX* TY, 1)
     own_P(Pz_cur, Fxy_cur);
   }
   bool box_issued = MODE != 3 ? issue_box(zA + 2) : false;
-  issue_tile(zA, 1);
+  if (MODE != 4) issue_tile(zA, 1);
 
   // push targets: wrapped neighbour columns/rows of this thread's site
   const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
   const int cbox = (ly + 2) * BX + (lx + 2);
 
   for (int k = zA; k < zB; ++k) {
-#if LB_CLUSTER_SYNC_EVERY > 0
-    // keep the CTAs of a cluster (neighbouring tiles) within a few planes of each
-    // other, so the halo rows one loads are still in L2 when the owner loads them
-    if ((k - zA) % LB_CLUSTER_SYNC_EVERY == 0) {
-      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-    }
-#endif
     // f(k) to registers, then free sTf for f(k+1): a whole iteration of lead time
     double f[Q], g[Q];
     wait_tile(0);
@@ -388,19 +400,25 @@ __global__ void __launch_bounds__(TX* TY, 1)
     __syncthreads();       // sTf consumed by all threads; sG visible
     issue_tile(k + 1, 0);
     double Pz_next[3] = {0, 0, 0}, Fxy_next[3] = {0, 0, 0};
-    if (MODE != 1 && MODE != 3) make_phi(k + 2);
+    if (MODE == 4) {  // probe: g from the box interior instead of a second tile copy
+#pragma unroll
+      for (int i = 0; i < Q; ++i) g[i] = sm.sG[grank(i)][(ly + 2) * BX + (lx + 2)];
+    }
+    if (MODE != 1 && MODE != 3 && MODE != 4) make_phi(k + 2);
     __syncthreads();  // sG consumed, ring written
     box_issued = (k + 1 < zB && MODE != 3) ? issue_box(k + 3) : false;
-    if (MODE != 1 && MODE != 3) {
+    if (MODE != 1 && MODE != 3 && MODE != 4) {
       compute_P(k + 1);
       __syncthreads();
       own_P(Pz_next, Fxy_next);
     }
-    wait_tile(1);  // g(k) tile landed
+    if (MODE != 4) {
+      wait_tile(1);  // g(k) tile landed
 #pragma unroll
-    for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
-    __syncthreads();  // sTg consumed
-    issue_tile(k + 1, 1);
+      for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
+      __syncthreads();  // sTg consumed
+      issue_tile(k + 1, 1);
+    }
     if (MODE != 0 && active) {
       const long long zo[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
                                (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
@@ -482,25 +500,8 @@ cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double*
   }
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
-  dim3 grid((G.nx + kTX - 1) / kTX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc);
-#if LB_CLUSTER_SYNC_EVERY > 0
-  if (grid.x % LB_CLUSTER_X == 0 && grid.y % LB_CLUSTER_Y == 0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(kTX * TY, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = LB_CLUSTER_X;
-    at[0].val.clusterDim.y = LB_CLUSTER_Y;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
-  }
-  return cudaErrorInvalidConfiguration;
-#endif
+  const unsigned nblk = (unsigned)(((G.nx + kTX - 1) / kTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc));
+  dim3 grid(nblk);
   kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
   return cudaGetLastError();
 }
@@ -512,6 +513,7 @@ cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, doub
     case 1: return launch_t<TY, USE_TMA, 1>(G, p, A, B, phig, zc, flag, maps, st);
     case 2: return launch_t<TY, USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st);
     case 3: return launch_t<TY, USE_TMA, 3>(G, p, A, B, phig, zc, flag, maps, st);
+    case 4: return launch_t<TY, USE_TMA, 4>(G, p, A, B, phig, zc, flag, maps, st);
     default: return launch_t<TY, USE_TMA, 0>(G, p, A, B, phig, zc, flag, maps, st);
   }
 }

@@ -1,0 +1,393 @@
+// lb_step_ws.cu -- warp-specialised variant of the fused D3Q19 binary-fluid step.
+//
+// Same arithmetic, same HBM traffic and same results (bit for bit) as the tile
+// kernel of lb_step.cu, but the two
+// halves of an iteration run CONCURRENTLY on different warps of the CTA instead
+// of one after the other between __syncthreads:
+//
+//   collision warps (TX*TY threads, one per column): wait for the TMA tile of
+//       f, g at plane k, take phi, mu, F of plane k from the hand-off buffer sQ,
+//       collide (A.6, A.7) and push f*, g* to x + c_i (A.8).  They are the only
+//       warps that store, so the store stream never pauses for stencil work.
+//   stencil warpgroup (128 threads): runs one or two planes ahead -- waits for
+//       the g box of plane j+2 (TMA), phi(j+2) = sum_i g_i on the box (A.3),
+//       the chemical stress P(j+1) (A.4), the force F(j) = -div P (A.5) and
+//       mu(j) (A.4) -- and hands phi, mu, F of plane j over through sQ (two
+//       slots, mbarrier full/empty pairs).
+//
+// The tile kernel is one CTA per SM at 32 x 8 tiles; there, every __syncthreads
+// between the phi/P phases and the collision phase stalled the store stream
+// (DESIGN.md "Tuning").  Needs 16-byte rows (nx even: TMA).
+#include "lb_device.cuh"
+#include "lb_tma.cuh"
+
+namespace lbk {
+namespace {
+
+constexpr int kWTX = 32;
+constexpr int kNA = 128;  // stencil warpgroup
+// L2 policies (policy_of): g box (re-read by the g tile two planes later), f and g
+// tiles (last use), stores (-1: st.global.cs)
+#ifndef LB_WS_BOX_POL
+#define LB_WS_BOX_POL 2
+#endif
+#ifndef LB_WS_TILE_POL
+#define LB_WS_TILE_POL 1
+#endif
+#ifndef LB_WS_ST_POL
+#define LB_WS_ST_POL (-1)
+#endif
+#ifndef LB_WS_STRIP_W
+#define LB_WS_STRIP_W (1 << 20)
+#endif
+
+__device__ __forceinline__ int wslot5(int z) {
+  const int s = z % 5;
+  return s < 0 ? s + 5 : s;
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// NBOX: g boxes in flight (1: issued one plane ahead; 2: two planes ahead).
+// GDIRECT: the collision warps read g(k) straight from global memory (an L2 hit:
+// the box brought it on chip two planes earlier) instead of a TMA tile, which
+// frees the shared memory for the second box buffer.
+template <int TY, int NBOX, bool GDIRECT>
+struct alignas(128) WsSmem {
+  static constexpr int TX = kWTX, NT = TX * TY;
+  static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
+  static constexpr int PX = TX + 2, PY = TY + 2, NP = PX * PY;  // P box: tile + 1 halo
+  alignas(128) double sTf[Q][NT];                // f of the tile, f-slot order (TMA boxes TX x TY x 5|9|5)
+  alignas(128) double sTg[GDIRECT ? 1 : Q][NT];  // g of the tile, g-slot order
+  alignas(128) double sG[NBOX][Q][NB];           // g on the box, g-slot order  (TMA boxes BX x BY x 5|9|5)
+  double sPhi[5][NB];                            // ring of phi planes on the box
+  double sP[6][NP];                              // chemical stress of one plane on the P box
+  double sQ[2][5][NT];                           // hand-off: phi, mu, Fx, Fy, Fz of a plane
+  unsigned long long bar_f, bar_g, bar_box[NBOX], q_full[2], q_empty[2];
+};
+
+template <int TY, int NBOX, bool GDIRECT>
+__global__ void __launch_bounds__(kWTX* TY + kNA, 1)
+    k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
+              const double* __restrict__ phig, int zc, int* __restrict__ flag, const __grid_constant__ CUtensorMap tm_t5,
+              const __grid_constant__ CUtensorMap tm_t9, const __grid_constant__ CUtensorMap tm_g5,
+              const __grid_constant__ CUtensorMap tm_g9) {
+  using S = WsSmem<TY, NBOX, GDIRECT>;
+  constexpr int TX = kWTX, NT = S::NT;
+  constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
+  constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
+  constexpr int SPT = NT / kNA;  // sites per stencil thread
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, LB_WS_STRIP_W);
+  const int x0 = tb.bx * TX, y0 = tb.by * TY;
+  const int zA = tb.bz * zc;
+  const int zB = min(zA + zc, G.nzl);
+  const long long nxy = G.nxy;
+
+  auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
+  auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
+
+  if (tid == 0) {
+    mbar_init(&sm.bar_f, 1);
+    mbar_init(&sm.bar_g, 1);
+    for (int b = 0; b < NBOX; ++b) mbar_init(&sm.bar_box[b], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.q_full[s], kNA);
+      mbar_init(&sm.q_empty[s], NT);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (tid >= NT) {
+    // ============================ stencil warpgroup ============================
+    // Box n (n = 0 .. nlast) is the g box of plane zA - 2 + n, in buffer n % NBOX.
+    const int a = tid - NT;
+    const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
+    const unsigned long long pol_last = policy_of<LB_WS_BOX_POL>();
+    // per-thread copy plan of a wrapped halo box: 16-byte units
+    constexpr int BROWU = BX / 2, BOXU = BY * BROWU, BOXR = (BOXU + kNA - 1) / kNA;
+    long long box_src[BOXR];
+    int box_dst[BOXR];
+#pragma unroll
+    for (int r = 0; r < BOXR; ++r) {
+      const int u = a + r * kNA;
+      const int row = u / BROWU, cu = u - row * BROWU;
+      box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
+      box_dst[r] = u < BOXU ? row * BX + cu * 2 : -1;
+    }
+    auto zsrc = [&](int zp, bool& ghost) {
+      ghost = false;
+      if (G.zwrap) { zp %= G.nzl; return zp < 0 ? zp + G.nzl : zp; }
+      ghost = zp < 0 || zp >= G.nzl;
+      return zp;
+    };
+    const int nlast = zB - zA + 3;  // box of plane zB + 1
+    unsigned ph_box = 0;            // bit b: parity of bar_box[b]
+    // issue box n; the cp.async path commits exactly one group per call (empty
+    // for a ghost plane) so that the group count stays regular
+    auto issue_box = [&](int n) {
+      const int zp = zA - 2 + n;
+      bool ghost;
+      const int zs = zsrc(zp, ghost);
+      double(*dst)[NB] = sm.sG[n % NBOX];
+      if (box_interior) {
+        if (!ghost && a == 0) {
+          const int cpl = (zs + GZ) * NSLOT;
+          unsigned long long* bar = &sm.bar_box[n % NBOX];
+          fence_proxy_async();
+          mbar_expect_tx(bar, BOX_BYTES);
+          tma_load_3d(&dst[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, bar, pol_last);
+          tma_load_3d(&dst[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, bar, pol_last);
+          tma_load_3d(&dst[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, bar, pol_last);
+        }
+      } else {
+        if (!ghost) {
+          const double* base = A + (long long)(zs + GZ) * G.plane;
+#pragma unroll
+          for (int j = 0; j < Q; ++j) {
+            const double* bj = base + (long long)gslot_of_rank(j) * nxy;
+#pragma unroll
+            for (int r = 0; r < BOXR; ++r)
+              if (box_dst[r] >= 0) cp_async_v<2>(&dst[j][box_dst[r]], bj + box_src[r]);
+          }
+        }
+        cp_commit();
+      }
+    };
+    // wait for box n, then make it visible to the whole warpgroup
+    auto wait_box = [&](int n) {
+      bool ghost;
+      zsrc(zA - 2 + n, ghost);
+      if (box_interior) {
+        if (!ghost) {
+          const int b = n % NBOX;
+          mbar_wait(&sm.bar_box[b], (ph_box >> b) & 1);
+          ph_box ^= 1u << b;
+        }
+      } else {
+        // groups committed after box n: boxes n+1 .. min(n+NBOX-1, nlast)
+        if (NBOX == 2 && n + 1 <= nlast) cp_wait<1>();
+        else cp_wait<0>();
+      }
+      named_sync(2, kNA);
+    };
+    auto make_phi = [&](int n) {
+      const int zp = zA - 2 + n;
+      bool ghost;
+      const int zs = zsrc(zp, ghost);
+      double* ring = sm.sPhi[wslot5(zp)];
+      const double(*src)[NB] = sm.sG[n % NBOX];
+      for (int b = a; b < NB; b += kNA) {
+        double v;
+        if (ghost) {
+          const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
+          v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
+        } else {
+          v = src[grank(0)][b];  // A.3, canonical order (same as phi_sum)
+#pragma unroll
+          for (int i = 1; i < Q; ++i) v += src[grank(i)][b];
+        }
+        ring[b] = v;
+      }
+    };
+    auto compute_P = [&](int zp) {
+      const double* f0 = sm.sPhi[wslot5(zp - 1)];
+      const double* f1 = sm.sPhi[wslot5(zp)];
+      const double* f2 = sm.sPhi[wslot5(zp + 1)];
+      for (int e = a; e < NP; e += kNA) {
+        const int c = (e / PX + 1) * BX + (e % PX + 1);
+        const double ph = f1[c];
+        const double xp = f1[c + 1], xm = f1[c - 1];
+        const double yp = f1[c + BX], ym = f1[c - BX];
+        const double zp_ = f2[c], zm = f0[c];
+        const double lap = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * ph;  // A.2
+        double P[6];
+        stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp_ - zm), lap, P);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
+      }
+    };
+    auto own_P = [&](int site, double Pz[3], double Fxy[3]) {
+      const int e = (site / TX + 1) * PX + (site % TX + 1);
+      const auto& P = sm.sP;
+      Pz[0] = P[PXZ][e];
+      Pz[1] = P[PYZ][e];
+      Pz[2] = P[PZZ][e];
+      Fxy[0] = -0.5 * (P[PXX][e + 1] - P[PXX][e - 1]) - 0.5 * (P[PXY][e + PX] - P[PXY][e - PX]);
+      Fxy[1] = -0.5 * (P[PXY][e + 1] - P[PXY][e - 1]) - 0.5 * (P[PYY][e + PX] - P[PYY][e - PX]);
+      Fxy[2] = -0.5 * (P[PXZ][e + 1] - P[PXZ][e - 1]) - 0.5 * (P[PYZ][e + PX] - P[PYZ][e - PX]);
+    };
+
+    double Pz_prev[SPT][3], Pz_cur[SPT][3], Fxy_cur[SPT][3];
+    for (int n = 0; n < NBOX && n <= nlast; ++n) issue_box(n);
+    for (int n = 0; n <= nlast; ++n) {
+      const int zp = zA - 2 + n;
+      wait_box(n);  // (also: everyone is past the previous hand-off)
+      make_phi(n);
+      named_sync(2, kNA);  // sG[n % NBOX] consumed, ring written
+      if (n + NBOX <= nlast) issue_box(n + NBOX);
+      if (n < 2) continue;
+      compute_P(zp - 1);  // needs phi(zp-2 .. zp)
+      named_sync(2, kNA);
+      if (n == 2) {
+#pragma unroll
+        for (int s = 0; s < SPT; ++s) {
+          double unused[3];
+          own_P(a + s * kNA, Pz_prev[s], unused);
+        }
+        continue;
+      }
+      if (n == 3) {
+#pragma unroll
+        for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_cur[s], Fxy_cur[s]);
+        continue;
+      }
+      double Pz_next[SPT][3], Fxy_next[SPT][3];
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_next[s], Fxy_next[s]);
+      // hand phi, mu, F of plane j = zp - 2 to the collision warps
+      const int j = zp - 2;
+      const int idx = j - zA, q = idx & 1, u = idx >> 1;
+      if (u >= 1) mbar_wait(&sm.q_empty[q], (u - 1) & 1);
+      const double* r0 = sm.sPhi[wslot5(j)];
+      const double* rm = sm.sPhi[wslot5(j - 1)];
+      const double* rp = sm.sPhi[wslot5(j + 1)];
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) {
+        const int site = a + s * kNA;
+        const int cbox = (site / TX + 2) * BX + (site % TX + 2);
+        const double ph = r0[cbox];
+        const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) + (rp[cbox] + rm[cbox]) -
+                           6.0 * ph;
+        sm.sQ[q][0][site] = ph;
+        sm.sQ[q][1][site] = chem_pot(p, ph, lap);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          sm.sQ[q][2 + c][site] = Fxy_cur[s][c] - 0.5 * (Pz_next[s][c] - Pz_prev[s][c]);
+          Pz_prev[s][c] = Pz_cur[s][c];
+          Pz_cur[s][c] = Pz_next[s][c];
+          Fxy_cur[s][c] = Fxy_next[s][c];
+        }
+      }
+      mbar_arrive(&sm.q_full[q]);
+    }
+    cp_wait<0>();
+    return;
+  }
+
+  // ============================== collision warps ==============================
+  const int lx = tid % TX, ly = tid / TX;
+  const int x = x0 + lx, y = y0 + ly;
+  const bool active = (x < G.nx) && (y < G.ny);
+  const unsigned long long pol_first = policy_of<LB_WS_TILE_POL>();
+  const unsigned long long pol_st = policy_of<(LB_WS_ST_POL < 0 ? 1 : LB_WS_ST_POL)>();
+  unsigned ph_f = 0, ph_g = 0;
+  auto issue_tile = [&](int zp, int dist) {
+    if (zp < zB && tid == 0) {
+      double(*dst)[NT] = dist == 0 ? sm.sTf : sm.sTg;
+      unsigned long long* bar = dist == 0 ? &sm.bar_f : &sm.bar_g;
+      const int cp0 = (zp + GZ) * NSLOT + (dist == 0 ? 0 : 5);
+      fence_proxy_async();
+      mbar_expect_tx(bar, TILE_BYTES);
+      tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol_first);
+      tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
+      tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol_first);
+    }
+  };
+  issue_tile(zA, 0);
+  if (!GDIRECT) issue_tile(zA, 1);
+  const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
+  const long long xy = (long long)(active ? y : 0) * G.nx + (active ? x : 0);
+
+  for (int k = zA; k < zB; ++k) {
+    double f[Q], g[Q];
+    if (GDIRECT) {  // g(k): last use, an L2 hit
+      const double* gk = A + (long long)(k + GZ) * G.plane + xy;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) g[i] = __ldcs(gk + (long long)slot(1, i) * nxy);
+    }
+    mbar_wait(&sm.bar_f, ph_f);
+    ph_f ^= 1;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
+    named_sync(1, NT);  // sTf consumed
+    issue_tile(k + 1, 0);
+    const int idx = k - zA, q = idx & 1, u = idx >> 1;
+    mbar_wait(&sm.q_full[q], u & 1);
+    const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];
+    const double F[3] = {sm.sQ[q][2][tid], sm.sQ[q][3][tid], sm.sQ[q][4][tid]};
+    mbar_arrive(&sm.q_empty[q]);
+    if (!GDIRECT) {
+      mbar_wait(&sm.bar_g, ph_g);
+      ph_g ^= 1;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
+      named_sync(1, NT);  // sTg consumed
+      issue_tile(k + 1, 1);
+    }
+    if (active) {
+      const long long zoff[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
+                                 (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
+      const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
+        const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
+        const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+        double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;  // A.8 push
+        if (LB_WS_ST_POL < 0) {
+          __stcs(d + (long long)slot(0, i) * nxy, fs);
+          __stcs(d + (long long)slot(1, i) * nxy, gs);
+        } else {
+          st_hint(d + (long long)slot(0, i) * nxy, fs, pol_st);
+          st_hint(d + (long long)slot(1, i) * nxy, gs, pol_st);
+        }
+      });
+      if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
+    }
+  }
+}
+
+#ifndef LB_WS_NBOX
+#define LB_WS_NBOX 1
+#endif
+#ifndef LB_WS_GDIRECT
+#define LB_WS_GDIRECT 0
+#endif
+
+template <int TY>
+cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
+                        int* flag, const StepMaps* maps, cudaStream_t st) {
+  constexpr size_t smem = sizeof(WsSmem<TY, LB_WS_NBOX, LB_WS_GDIRECT>);
+  static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
+  auto kern = k_step_ws<TY, LB_WS_NBOX, LB_WS_GDIRECT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
+  const unsigned nblk = (unsigned)(((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc));
+  dim3 grid(nblk);
+  kern<<<grid, kWTX * TY + kNA, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool step_ws_fits(const StepMaps* maps) { return maps && maps->ok && (maps->ty == 8 || maps->ty == 4); }
+
+cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
+                           int* flag, const StepMaps* maps, cudaStream_t st) {
+  if (!step_ws_fits(maps)) return cudaErrorInvalidValue;
+  if (maps->ty == 8) return launch_ws_t<8>(G, p, A, B, phig, zc, flag, maps, st);
+  return launch_ws_t<4>(G, p, A, B, phig, zc, flag, maps, st);
+}
+
+}  // namespace lbk

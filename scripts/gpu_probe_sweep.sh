@@ -14,7 +14,7 @@ for rep in $(seq 1 ${REPEAT:-1}); do
   for v in "${VS[@]}"; do
     cp gpurun_out/var$n/liblb.so paper_1609_01479_b200/liblb.so
     for cfg in ${CFGS:-c5}; do
-      python scripts/probe.py --config $cfg > gpurun_out/var$n/probe_${cfg}_$rep.json 2>gpurun_out/probe_v.err || { echo "probe_fail [$v]"; tail -3 gpurun_out/probe_v.err; }
+      python scripts/probe.py --config $cfg ${PROBE_ONLY:+--only $PROBE_ONLY} > gpurun_out/var$n/probe_${cfg}_$rep.json 2>gpurun_out/probe_v.err || { echo "probe_fail [$v]"; tail -3 gpurun_out/probe_v.err; }
     done
     n=$((n+1))
   done
@@ -26,10 +26,10 @@ for v in "${VS[@]}"; do
 import glob, json, statistics, sys
 v, cfg, d = sys.argv[1:4]
 runs = [json.load(open(f)) for f in sorted(glob.glob(f"{d}/probe_{cfg}_*.json"))]
-keys = ("step", "probe1_copy_push", "probe2_plus_halo_phi_P", "probe3_tile_only", "k_stream_site_parallel")
-med = {k: round(statistics.median(r[k]["mlups"] for r in runs)) for k in keys if k in runs[0]}
+keys = [k for k, x in runs[0].items() if isinstance(x, dict) and "mlups" in x]
+med = {k: round(statistics.median(r[k]["mlups"] for r in runs)) for k in keys}
 print(f"[{v}] {cfg} n={len(runs)}", " ".join(f"{k}={x}" for k, x in med.items()),
-      "steps:", [round(r["step"]["mlups"]) for r in runs])
+      "runs:", {k: [round(r[k]["mlups"]) for r in runs] for k in keys})
 PY
   done
   n=$((n+1))

@@ -22,6 +22,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c5")
     ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--only", default="", help="comma-separated subset of the timings")
+    ap.add_argument("--ab", default="", help="interleaved A/B of step kernels, e.g. 1,3 (lb_debug_step_kernel)")
+    ap.add_argument("--rounds", type=int, default=20)
     a = ap.parse_args()
     nx, ny, nzf, _, desc = bench.CONFIGS[a.config]
     nz = nzf(1)
@@ -30,7 +33,11 @@ def main():
     stream = torch.cuda.ExternalStream(lb.lb_stream(L.h))
     out = {"config": a.config, "sites": nx * ny * nz}
 
-    def timed(fn):
+    only = set(a.only.split(",")) if a.only else None
+
+    def timed(fn, name=None):
+        if only is not None and name not in only:
+            return None
         fn(3)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -41,11 +48,40 @@ def main():
         ms = e0.elapsed_time(e1) / a.steps
         return {"ms_per_step": ms, "mlups": nx * ny * nz / ms / 1e3, "gbs_608": nx * ny * nz * 608 / ms / 1e6}
 
-    out["step"] = timed(lambda n: L.step(n))
-    out["probe1_copy_push"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 1))
-    out["probe2_plus_halo_phi_P"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 2))
-    out["probe3_tile_only"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 3))
-    out["k_stream_site_parallel"] = timed(lambda n: lb.lb_debug_stream(L.h, n))
+    if a.ab:
+        ks = [int(v) for v in a.ab.split(",")]
+        tot = {k: 0.0 for k in ks}
+        L.step(5)
+        for r in range(a.rounds):
+            for k in (ks if r % 2 == 0 else ks[::-1]):
+                lb.lb_debug_step_kernel(L.h, k)
+                L.step(2)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                L.step(a.steps)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tot[k] += e0.elapsed_time(e1)
+        for k in ks:
+            out[f"ab_kernel{k}"] = {"mlups": nx * ny * nz * a.steps * a.rounds / tot[k] / 1e3}
+        lb.lb_debug_step_kernel(L.h, 0)
+        L.close()
+        print(json.dumps(out))
+        return
+    out["step"] = timed(lambda n: L.step(n), "step")
+    for name, which in (("step_ws", 3), ("step_tile", 1)):
+        try:
+            lb.lb_debug_step_kernel(L.h, which)
+            out[name] = timed(lambda n: L.step(n), name)
+        except lb.LBError as e:
+            out[name] = str(e)
+    lb.lb_debug_step_kernel(L.h, 0)
+    out["probe1_copy_push"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 1), "probe1_copy_push")
+    out["probe2_plus_halo_phi_P"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 2), "probe2_plus_halo_phi_P")
+    out["probe3_tile_only"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 3), "probe3_tile_only")
+    out["probe4_box_no_gtile"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 4), "probe4_box_no_gtile")
+    out["k_stream_site_parallel"] = timed(lambda n: lb.lb_debug_stream(L.h, n), "k_stream_site_parallel")
     n = nx * ny * nz * 38
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)

@@ -1,4 +1,5 @@
-"""Short run for ncu: one launch each of the step kernel in modes 0, 1, 2 (after warm-up)."""
+"""Short run for ncu: one launch each of the step kernel (tile), its probe modes
+1-4, and the warp-specialised step kernel, after warm-up."""
 import os
 import sys
 
@@ -13,9 +14,12 @@ nx, ny, nzf, _, _ = bench.CONFIGS[cfg]
 nz = nzf(1)
 L = lb.Lattice(nx, ny, nz)
 L.init_equilibrium(synth.spinodal_phi(nx, ny, nz))
+lb.lb_debug_step_kernel(L.h, 1)
 L.step(2)
 L.step(1)
-lb.lb_debug_step_probe(L.h, 1, 1)
-lb.lb_debug_step_probe(L.h, 1, 2)
+for mode in (1, 2, 3, 4):
+    lb.lb_debug_step_probe(L.h, 1, mode)
+lb.lb_debug_step_kernel(L.h, 3)
+L.step(1)
 L.close()
 print("ok")

@@ -37,7 +37,7 @@ def rough(nx, ny, nz, seed=1, p=P0):
 
 
 def gpu_run(f, g, p, nsteps, nslabs=1, kernel=0):
-    """kernel: 0 automatic, 1 tile step kernel, 2 cluster step kernel (lb_debug_step_kernel)."""
+    """kernel: 0 default, 1 tile, 2 cluster, 3 warp-specialised step kernel (lb_debug_step_kernel)."""
     nz, ny, nx = f.shape[1:]
     with lb.Lattice(nx, ny, nz, cparams(p), nslabs=nslabs) as L:
         lb.lb_debug_step_kernel(L.h, kernel)
@@ -189,6 +189,54 @@ def test_cluster_kernel_rejects_unfit_lattice():
     with lb.Lattice(24, 16, 8) as L:
         with pytest.raises(lb.LBError) as e:
             lb.lb_debug_step_kernel(L.h, 2)
+        assert e.value.code == lb.LB_EINVAL
+
+
+# ------------------------------------------------------------------ the warp-specialised step kernel
+@pytest.mark.parametrize("shape", [(16, 16, 16), (24, 20, 18), (34, 10, 7), (64, 64, 16), (4, 31, 6)])
+def test_ws_kernel_parity_and_bitwise_equal_to_tile_kernel(shape):
+    """lb_step_ws.cu (stencil warpgroup + collision warps) gives the same bits as the
+    tile kernel -- wrapped and partial tiles, 32 x 4 tiles -- and meets the parity
+    tolerance against the oracle."""
+    nx, ny, nz = shape
+    f, g = rough(nx, ny, nz, seed=14)
+    a = gpu_run(f, g, P0, 4, kernel=3)
+    b = gpu_run(f, g, P0, 4, kernel=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert_parity(a, R.run(f, g, P0, 4))
+
+
+def test_ws_kernel_32x8_tiles_and_z_chunks():
+    """A plane with >= 4 x 148 tiles of 32 x 8 (the bench's tile shape) and two
+    z-chunks: bitwise equal to the tile kernel, and sampled sites against the
+    brute-force oracle."""
+    nx, ny, nz = 512, 304, 16
+    f, g = spinodal(nx, ny, nz, seed=15)
+    a = gpu_run(f, g, P0, 1, kernel=3)
+    b = gpu_run(f, g, P0, 1, kernel=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    smp = BR.SiteSampler(f, g, P0)
+    fs, gs, fr, gr = [], [], [], []
+    for (x, y, z) in synth.sample_sites(nx, ny, nz, 32):
+        fo, go = smp.after_step(x, y, z)
+        fr.append(fo), gr.append(go)
+        fs.append(a[0][:, z, y, x]), gs.append(a[1][:, z, y, x])
+    assert rel(np.array(fs), np.array(fr)) <= TOL
+    assert rel(np.array(gs), np.array(gr)) <= TOL
+
+
+@pytest.mark.parametrize("nslabs", [2, 4])
+def test_ws_kernel_slabs_bitwise(nslabs):
+    f, g = rough(32, 16, 16, seed=16)
+    a = gpu_run(f, g, P0, 5, nslabs=1, kernel=1)
+    b = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=3)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_ws_kernel_rejects_odd_nx():
+    with lb.Lattice(7, 16, 8) as L:
+        with pytest.raises(lb.LBError) as e:
+            lb.lb_debug_step_kernel(L.h, 3)
         assert e.value.code == lb.LB_EINVAL
 
 
