@@ -178,6 +178,25 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
  * results.  Test / measurement support. */
 int lb_debug_step_kernel(lb_t* h, int which);
 
+/* Halo transport of a slab handle.  mode -1: returns the current mode (0 or 1);
+ * 0: exchange -- kernels push into ghost planes, then device copies (loopback) or
+ *    NCCL send/recv (ranks) move them, and the phi ghost planes likewise;
+ * 1: peer (fused) -- the step kernel stores the components leaving the slab
+ *    directly into the neighbour's next-state buffer, and K_phi its edge planes
+ *    into the neighbour's phi ghost planes (same GPU for loopback; NVLink P2P
+ *    through CUDA IPC mappings between ranks); only a one-double NCCL send/recv
+ *    per phase orders the ranks.
+ * Default: 1 for loopback and for ranks whose neighbours' memory could be mapped
+ * (checked end to end at lb_create_slab), else 0; environment LB_HALO=nccl (or
+ * copy) forces 0.  Both give bitwise identical results.  LB_EINVAL for a single
+ * periodic slab or a rank handle without peer mappings. */
+int lb_debug_halo_mode(lb_t* h, int mode);
+
+/* lb_debug_propagation_map for the peer transport: the destinations come from the
+ * kernels' own address arithmetic with the neighbouring slabs' buffers (no ghost
+ * planes, no halo plan).  Must equal lb_debug_propagation_map.  Host-only. */
+int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* out);
+
 /* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of
  * nranks, the ranks it sends its +z and -z halo to, and the number of doubles
  * per message: distributions (10 components x nx*ny) and phi (2 planes x nx*ny).

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -61,6 +62,16 @@ struct lb_ctx {
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
   ncclComm_t comm = nullptr;
+  // halo transport: 0 = exchange (ghost planes + copies / NCCL send-recv after the
+  // kernels), 1 = peer (fused: the kernels store into the neighbours' buffers)
+  int halo_mode = 0;
+  // peer transport between ranks: the neighbours' A, B and phi buffers mapped by
+  // CUDA IPC ([0] = slab below, [1] = slab above; the same mapping when nranks == 2)
+  double* peerA[2] = {nullptr, nullptr};
+  double* peerB[2] = {nullptr, nullptr};
+  double* peerPhi[2] = {nullptr, nullptr};
+  std::vector<void*> ipc_opened;
+  double* d_token = nullptr;  // 4 doubles: NCCL barrier tokens
   bool have_state = false;
   bool broken = false;
   std::string err;
@@ -233,6 +244,11 @@ int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, i
     delete h;
     return LB_ECUDA;
   }
+  {
+    const char* env = std::getenv("LB_HALO");
+    const bool force_exchange = env && (!std::strcmp(env, "copy") || !std::strcmp(env, "nccl"));
+    h->halo_mode = (parts > 1 && nranks == 1 && !force_exchange) ? 1 : 0;  // ranks: after IPC setup
+  }
   h->ty = step_tile_rows(h->G, h->num_sms);
   h->zc = step_zchunk(h->G, h->num_sms, h->ty);
   h->czc = cluster_zchunk(h->G, h->num_sms);
@@ -325,6 +341,48 @@ int exchange_phi(lb_ctx* h) {
   return LB_OK;
 }
 
+// ---- fused halo (peer transport) ----------------------------------------------
+// Neighbour buffers of slab r: other slabs of this handle (loopback) or the IPC
+// mappings of the neighbouring ranks' buffers.
+Peers peers_of(const lb_ctx* h, int r) {
+  Peers P;
+  if (h->halo_mode != 1 || h->G.zwrap) return P;
+  if (h->nranks > 1) {
+    P.dn = h->peerB[0];
+    P.up = h->peerB[1];
+    P.phi_dn = h->peerPhi[0];
+    P.phi_up = h->peerPhi[1];
+  } else {
+    const Slab& dn = h->slabs[(r - 1 + h->nslabs) % h->nslabs];
+    const Slab& up = h->slabs[(r + 1) % h->nslabs];
+    P.dn = dn.B;
+    P.up = up.B;
+    P.phi_dn = dn.phi;
+    P.phi_up = up.phi;
+  }
+  return P;
+}
+
+// Ordering point of the peer transport between ranks: a one-double NCCL send/recv
+// with both neighbours on the stream.  A neighbour's send is issued after its
+// kernel (which ended with __threadfence_system), so once both receives have
+// completed, every P2P store the neighbours made into this rank's buffers is
+// visible to the kernels that follow.  Loopback slabs share one stream: no-op.
+int halo_barrier(lb_ctx* h, int kid) {
+  if (h->nranks == 1) return LB_OK;
+  const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
+  cudaError_t ce = timed(h, kid, false, [&]() {
+    ncclGroupStart();
+    ncclSend(h->d_token, 1, ncclDouble, up, h->comm, h->stream);
+    ncclRecv(h->d_token + 1, 1, ncclDouble, dn, h->comm, h->stream);
+    ncclSend(h->d_token, 1, ncclDouble, dn, h->comm, h->stream);
+    ncclRecv(h->d_token + 2, 1, ncclDouble, up, h->comm, h->stream);
+    return ncclGroupEnd() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+  });
+  if (ce != cudaSuccess) return set_err(h, LB_ENCCL, "NCCL halo barrier failed");
+  return LB_OK;
+}
+
 // one timestep on every slab.  Single periodic slab: the fused step alone.
 // Slabs: phi on the two edge planes at each end (K_phi), phi halo exchange, the
 // fused step (A -> B), distribution halo exchange, swap.
@@ -332,36 +390,48 @@ int exchange_phi(lb_ctx* h) {
 int one_step(lb_ctx* h, int mode) {
   const Geom& G = h->G;
   int rc;
+  const bool peer = h->halo_mode == 1 && !G.zwrap;
   if (mode < 0) {
-    for (auto& s : h->slabs) CK(h, timed(h, K_STEP, true, [&]() { return launch_stream(G, s.A, s.B, h->stream); }));
+    for (int r = 0; r < h->nslabs; ++r) {
+      Slab& s = h->slabs[r];
+      const Peers pr = peers_of(h, r);
+      CK(h, timed(h, K_STEP, true, [&]() { return launch_stream(G, s.A, s.B, h->stream, pr); }));
+    }
   } else {
     if (!G.zwrap) {
-      for (auto& s : h->slabs) {
-        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, 2, h->stream); }));
-        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, G.nzl - 2, G.nzl, h->stream); }));
+      for (int r = 0; r < h->nslabs; ++r) {
+        Slab& s = h->slabs[r];
+        const Peers pr = peers_of(h, r);
+        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, 2, h->stream, pr); }));
+        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, G.nzl - 2, G.nzl, h->stream, pr); }));
       }
-      if ((rc = exchange_phi(h))) return rc;
+      if ((rc = peer ? halo_barrier(h, K_HALO_PHI) : exchange_phi(h))) return rc;
     }
-    for (auto& s : h->slabs)
+    for (int r = 0; r < h->nslabs; ++r) {
+      Slab& s = h->slabs[r];
+      const Peers pr = peers_of(h, r);
       CK(h, timed(h, K_STEP, true, [&]() {
            // the cluster kernel is opt-in: measured slower than the tile kernel in round 1
            // (cluster barrier per plane)
            const bool cluster = mode == 0 && s.cmapsA.ok && h->kernel_choice == 2;
-           if (cluster) return launch_step_cluster(G, h->dp, s.A, s.B, s.phi, h->czc, h->d_flag, &s.cmapsA, h->stream);
+           if (cluster)
+             return launch_step_cluster(G, h->dp, s.A, s.B, s.phi, h->czc, h->d_flag, &s.cmapsA, h->stream, pr);
            // default: the warp-specialised kernel for 32 x 8 tiles (large planes), the
            // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
            const bool ws = mode == 0 && step_ws_fits(&s.mapsA) &&
                            (h->kernel_choice == 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
-           if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream);
-           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, mode);
+           if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr);
+           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, mode, pr);
          }));
+    }
   }
-  if ((rc = exchange_dist(h))) return rc;
+  if ((rc = peer ? halo_barrier(h, K_HALO_DIST) : exchange_dist(h))) return rc;
   for (auto& s : h->slabs) {
     std::swap(s.A, s.B);
     std::swap(s.mapsA, s.mapsB);
     std::swap(s.cmapsA, s.cmapsB);
   }
+  for (int k = 0; k < 2; ++k) std::swap(h->peerA[k], h->peerB[k]);  // the neighbours swapped too
   return LB_OK;
 }
 
@@ -374,6 +444,91 @@ int finish(lb_ctx* h) {
     CK(h, cudaStreamSynchronize(h->stream));
     return set_err(h, LB_ENUMERIC, "rho <= 0 or a non-finite value at some site (numerical-domain error)");
   }
+  return LB_OK;
+}
+
+__global__ void k_poke(double* p, double v) {
+  *p = v;
+  __threadfence_system();
+}
+
+void close_peers(lb_ctx* h) {
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  h->ipc_opened.clear();
+  for (int k = 0; k < 2; ++k) h->peerA[k] = h->peerB[k] = h->peerPhi[k] = nullptr;
+}
+
+// Peer transport between ranks (collective): exchange CUDA IPC handles of A, B and
+// phi over NCCL, map the neighbours' buffers, and check the mapping end to end --
+// each rank stores a token into both neighbours' phi ghost planes with a kernel
+// and reads back what its neighbours stored.  On success halo_mode = 1; if the
+// neighbours' memory cannot be mapped (no peer access) or the check fails on any
+// rank, every rank keeps the NCCL exchange (the decision is agreed by an
+// all-reduce).  Only a NCCL/CUDA error on the way is an error.
+int open_peers(lb_ctx* h) {
+  const Geom& G = h->G;
+  Slab& s = h->slabs[0];
+  CK(h, cudaMalloc(&h->d_token, 4 * sizeof(double)));
+  CK(h, cudaMemsetAsync(h->d_token, 0, 4 * sizeof(double), h->stream));
+  struct Handles {
+    cudaIpcMemHandle_t a, b, phi;
+  } mine{};
+  int ok = 1;
+  if (cudaIpcGetMemHandle(&mine.a, s.A) != cudaSuccess || cudaIpcGetMemHandle(&mine.b, s.B) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine.phi, s.phi) != cudaSuccess)
+    ok = 0;
+  cudaGetLastError();
+  std::vector<Handles> all(h->nranks);
+  char* d_all = nullptr;
+  CK(h, cudaMalloc(&d_all, sizeof(Handles) * h->nranks));
+  CK(h, cudaMemcpyAsync(d_all + sizeof(Handles) * h->rank, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
+  NK(h, ncclAllGather(d_all + sizeof(Handles) * h->rank, d_all, sizeof(Handles), ncclChar, h->comm, h->stream));
+  CK(h, cudaMemcpyAsync(all.data(), d_all, sizeof(Handles) * h->nranks, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(d_all);
+  const int nb[2] = {(h->rank - 1 + h->nranks) % h->nranks, (h->rank + 1) % h->nranks};
+  for (int k = 0; k < 2 && ok; ++k) {
+    if (k == 1 && nb[1] == nb[0]) {
+      h->peerA[1] = h->peerA[0], h->peerB[1] = h->peerB[0], h->peerPhi[1] = h->peerPhi[0];
+      break;
+    }
+    const cudaIpcMemHandle_t* hs[3] = {&all[nb[k]].a, &all[nb[k]].b, &all[nb[k]].phi};
+    double** dst[3] = {&h->peerA[k], &h->peerB[k], &h->peerPhi[k]};
+    for (int j = 0; j < 3 && ok; ++j) {
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, *hs[j], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        ok = 0;
+        cudaGetLastError();
+      } else {
+        h->ipc_opened.push_back(p);
+        *dst[j] = static_cast<double*>(p);
+      }
+    }
+  }
+  // end-to-end check of the mapping with kernel stores (the barrier is collective:
+  // every rank takes part, mapped or not)
+  if (ok) {
+    k_poke<<<1, 1, 0, h->stream>>>(h->peerPhi[1] + phi_plane_index(G, -GP), 1000.0 + h->rank);
+    k_poke<<<1, 1, 0, h->stream>>>(h->peerPhi[0] + phi_plane_index(G, G.nzl) + 1, 2000.0 + h->rank);
+    CK(h, cudaGetLastError());
+  }
+  int rc = halo_barrier(h, K_HALO_PHI);
+  if (rc) return rc;
+  double got[2] = {0, 0};
+  CK(h, cudaMemcpyAsync(&got[0], s.phi + phi_plane_index(G, -GP), 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(&got[1], s.phi + phi_plane_index(G, G.nzl) + 1, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  ok = ok && got[0] == 1000.0 + nb[0] && got[1] == 2000.0 + nb[1];
+  // every rank must agree (a neighbour that could not map falls back with us)
+  int* d_ok = nullptr;
+  CK(h, cudaMalloc(&d_ok, sizeof(int)));
+  CK(h, cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  NK(h, ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
+  CK(h, cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(d_ok);
+  if (!ok) close_peers(h);
+  h->halo_mode = ok ? 1 : 0;
   return LB_OK;
 }
 
@@ -420,6 +575,15 @@ int lb_create_slab(int nx, int ny, int nz, const lb_params* params, int nranks, 
     lb_destroy(h);
     *out = nullptr;
     return LB_ENCCL;
+  }
+  const char* env = std::getenv("LB_HALO");
+  const bool force_exchange = env && (!std::strcmp(env, "nccl") || !std::strcmp(env, "copy"));
+  rc = force_exchange ? LB_OK : open_peers(h);
+  if (rc) {
+    g_create_error = h->err;
+    lb_destroy(h);
+    *out = nullptr;
+    return rc;
   }
   return LB_OK;
 }
@@ -547,6 +711,8 @@ int lb_get_phi(lb_t* h, double* phi) {
 void lb_destroy(lb_t* h) {
   if (!h) return;
   if (h->stream) cudaStreamSynchronize(h->stream);
+  close_peers(h);
+  cudaFree(h->d_token);
   if (h->comm) ncclCommDestroy(h->comm);
   for (auto& s : h->slabs) {
     cudaFree(s.A);
@@ -632,6 +798,60 @@ int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out) {
             if (out[(long long)i * N + sdst] != -1) return LB_EINVAL;  // not a permutation
             out[(long long)i * N + sdst] = ssrc;
           }
+  return LB_OK;
+}
+
+int lb_debug_halo_mode(lb_t* h, int mode) {
+  if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
+  if (mode == -1) return h->halo_mode;
+  if (mode != 0 && mode != 1) return set_err(h, LB_EINVAL, "mode must be -1 (query), 0 (exchange) or 1 (peer)");
+  if (mode == 1 && h->nranks > 1 && !h->peerB[0]) return set_err(h, LB_EINVAL, "no peer mapping on this handle");
+  if (mode == 1 && h->G.zwrap) return set_err(h, LB_EINVAL, "a single periodic slab has no halo");
+  h->halo_mode = mode;
+  return LB_OK;
+}
+
+int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* out) {
+  if (!out || nx < 3 || ny < 3 || nz < 3 || nslabs < 1 || nz % nslabs || (nslabs > 1 && nz / nslabs < 2))
+    return LB_EINVAL;
+  Geom G;
+  G.nx = nx;
+  G.ny = ny;
+  G.nzl = nz / nslabs;
+  G.zwrap = nslabs == 1;
+  G.nxy = (long long)nx * ny;
+  G.plane = (long long)NSLOT * G.nxy;
+  const long long N = G.nxy * nz, per = (long long)(G.nzl + 2 * GZ) * G.plane;
+  // the slabs' next-state buffers as one host array: the kernels' own address
+  // arithmetic (push_plane with the neighbours' buffers) decides the destination
+  std::vector<double> buf((size_t)(per * nslabs));
+  for (long long k = 0; k < (long long)Q * N; ++k) out[k] = -1;
+  for (int r = 0; r < nslabs; ++r) {
+    Peers P;
+    if (!G.zwrap) {
+      P.dn = buf.data() + per * ((r - 1 + nslabs) % nslabs);
+      P.up = buf.data() + per * ((r + 1) % nslabs);
+    }
+    double* B = buf.data() + per * r;
+    for (int z = 0; z < G.nzl; ++z)
+      for (int y = 0; y < ny; ++y)
+        for (int x = 0; x < nx; ++x)
+          for (int i = 0; i < Q; ++i) {
+            const double* d = push_plane(G, B, P, z + cz(i)) + push_in_plane(G, i, x, y) + (long long)slot(0, i) * G.nxy;
+            const long long off = d - buf.data();
+            const int rdst = (int)(off / per);
+            const long long in = off - per * rdst;
+            const int zz = (int)(in / G.plane) - GZ;
+            if (zz < 0 || zz >= G.nzl) return LB_EINVAL;  // a ghost plane: the fused halo must not use them
+            const long long rem = in - (long long)(zz + GZ) * G.plane;
+            if (rem / G.nxy != slot(0, i)) return LB_EINVAL;
+            const long long xy = rem - (long long)slot(0, i) * G.nxy;
+            const long long sdst = xy + G.nxy * ((long long)rdst * G.nzl + zz);
+            const long long ssrc = x + (long long)nx * (y + (long long)ny * ((long long)r * G.nzl + z));
+            if (out[(long long)i * N + sdst] != -1) return LB_EINVAL;  // not a permutation
+            out[(long long)i * N + sdst] = ssrc;
+          }
+  }
   return LB_OK;
 }
 

@@ -26,18 +26,25 @@ __device__ __forceinline__ double phi_at(const Geom& G, const double* __restrict
 }
 
 // K_phi: phi = sum_i g_i over local planes [z0, z1) (A.3).
+// With peers (fused halo), planes 0, 1 are also stored into ghost planes nzl, nzl+1
+// of the slab below and planes nzl-2, nzl-1 into ghost planes -2, -1 of the slab
+// above (P2P stores over NVLink between GPUs).
 __global__ void __launch_bounds__(TPB) k_phi(Geom G, const double* __restrict__ A, double* __restrict__ phi, int z0,
-                                             int z1) {
+                                             int z1, Peers pr) {
   const long long t = (long long)blockIdx.x * TPB + threadIdx.x;
   if (t >= G.nxy * (z1 - z0)) return;
   const int z = z0 + (int)(t / G.nxy);
   const long long xy = t - (long long)(z - z0) * G.nxy;
-  phi[phi_plane_index(G, z) + xy] = phi_sum(A + dist_index(G, z, 0, xy), G.nxy);
+  const double v = phi_sum(A + dist_index(G, z, 0, xy), G.nxy);
+  phi[phi_plane_index(G, z) + xy] = v;
+  if (pr.phi_dn && z < GP) pr.phi_dn[phi_plane_index(G, G.nzl + z) + xy] = v;
+  if (pr.phi_up && z >= G.nzl - GP) pr.phi_up[phi_plane_index(G, z - G.nzl) + xy] = v;
+  if (pr.phi_dn || pr.phi_up) __threadfence_system();
 }
 
 // Propagation only (test support, lb_debug_stream): the push of A.8 with the
 // same addressing (push_target) and slot map as the step kernel.
-__global__ void __launch_bounds__(TPB) k_stream(Geom G, const double* __restrict__ A, double* __restrict__ B) {
+__global__ void __launch_bounds__(TPB) k_stream(Geom G, const double* __restrict__ A, double* __restrict__ B, Peers pr) {
   const long long t = (long long)blockIdx.x * TPB + threadIdx.x;
   if (t >= G.nxy * G.nzl) return;
   const int z = (int)(t / G.nxy);
@@ -47,10 +54,12 @@ __global__ void __launch_bounds__(TPB) k_stream(Geom G, const double* __restrict
   const double* a = A + dist_index(G, z, 0, xy);
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    const long long d = push_target(G, i, x, y, z);
-    B[d + (long long)slot(0, i) * G.nxy] = a[(long long)slot(0, i) * G.nxy];
-    B[d + (long long)slot(1, i) * G.nxy] = a[(long long)slot(1, i) * G.nxy];
+    const long long d = push_in_plane(G, i, x, y);
+    double* b = push_plane(G, B, pr, z + cz(i));
+    b[d + (long long)slot(0, i) * G.nxy] = a[(long long)slot(0, i) * G.nxy];
+    b[d + (long long)slot(1, i) * G.nxy] = a[(long long)slot(1, i) * G.nxy];
   }
+  if (pr.dn || pr.up) __threadfence_system();
 }
 
 // Initial state at local equilibrium (R15): f = f^eq(rho, u), g = g^eq(phi, u, Gamma mu),
@@ -116,15 +125,15 @@ __global__ void __launch_bounds__(TPB) k_permute(Geom G, const double* __restric
 
 }  // namespace
 
-cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st) {
+cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st, const Peers& pr) {
   const long long n = G.nxy * (z1 - z0);
   if (n <= 0) return cudaSuccess;
-  k_phi<<<blocks_for(n), TPB, 0, st>>>(G, A, phi, z0, z1);
+  k_phi<<<blocks_for(n), TPB, 0, st>>>(G, A, phi, z0, z1, pr);
   return cudaGetLastError();
 }
 
-cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st) {
-  k_stream<<<blocks_for(G.nxy * G.nzl), TPB, 0, st>>>(G, A, B);
+cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st, const Peers& pr) {
+  k_stream<<<blocks_for(G.nxy * G.nzl), TPB, 0, st>>>(G, A, B, pr);
   return cudaGetLastError();
 }
 

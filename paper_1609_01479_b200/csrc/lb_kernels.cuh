@@ -40,40 +40,69 @@ __host__ __device__ inline int wrap_n(int v, int n) { return v < 0 ? v + n : (v 
 // (x + cx, y + cy) periodic in the plane; z + cz wraps when G.zwrap, otherwise
 // z + cz in [-1, nzl] (planes -1 and nzl are the ghost planes sent to the
 // neighbouring slabs).  Shared by the step kernel and the host-side map check.
-__host__ __device__ inline long long push_target(const Geom& G, int i, int x, int y, int z) {
-  const int xd = wrap_n(x + cx(i), G.nx);
-  const int yd = wrap_n(y + cy(i), G.ny);
-  int zd = z + cz(i);
+__host__ __device__ inline long long push_plane_offset(const Geom& G, int zd) {
   if (G.zwrap) zd = wrap_n(zd, G.nzl);
-  return (long long)(zd + GZ) * G.plane + (long long)xd + (long long)G.nx * yd;  // + slot*nxy by caller
+  return (long long)(zd + GZ) * G.plane;
+}
+__host__ __device__ inline long long push_in_plane(const Geom& G, int i, int x, int y) {
+  return (long long)wrap_n(x + cx(i), G.nx) + (long long)G.nx * wrap_n(y + cy(i), G.ny);
+}
+__host__ __device__ inline long long push_target(const Geom& G, int i, int x, int y, int z) {
+  return push_plane_offset(G, z + cz(i)) + push_in_plane(G, i, x, y);  // + slot*nxy by caller
 }
 
-// Tile of a step-kernel block: the linear block index walks the plane in strips
-// of w tiles in x, y fastest within a strip, z-chunk slowest.  w >= tiles per
-// row is plain row-major order, the fastest measured: narrow strips put y
-// neighbours (which share halo rows) closer in launch order, but the CTAs
-// resident at one time then read 256-byte pieces of many 4 KB rows instead of
-// whole rows, and lost more in DRAM locality than they gained in L2 reuse
-// (DESIGN.md "Tuning").
+// Tile and z-chunk of a step-kernel block.  Blocks start in launch order, about
+// `resid` of them resident at a time, each taking about as long as the others.
+// The order is: groups of `resid` tiles (row-major); inside a group, all tiles of
+// chunk 0, then all of chunk 1, ...  So chunk c of a tile starts when chunk c-1
+// of the same tile ends, and its first planes (the box loads of planes zA-2 ..
+// zA+1, which the previous chunk loaded last) are still in L2 -- with chunks in
+// separate waves they were read from DRAM twice.  Row-major order inside a group
+// keeps the CTAs resident at one time on whole 4 KB rows (narrow strips, tried
+// to bring y neighbours closer in launch order, lost more in DRAM locality than
+// they gained in L2 reuse).
 struct TileId {
   int bx, by, bz;
 };
-__host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int w) {
+__host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch, int resid) {
   const int ntiles = ntx * nty;
-  TileId t;
-  t.bz = L / ntiles;
-  const int r = L - t.bz * ntiles;
-  const int band = w * nty;
-  const int strip = r / band, rem = r - strip * band;
-  const int ws = ntx - strip * w < w ? ntx - strip * w : w;
-  t.by = rem / ws;
-  t.bx = strip * w + (rem - t.by * ws);
-  return t;
+  if (resid > ntiles || resid < 1) resid = ntiles;
+  const int per_group = resid * nch;
+  const int grp = L / per_group;
+  const int r = L - grp * per_group;
+  const int rg = ntiles - grp * resid < resid ? ntiles - grp * resid : resid;
+  const int c = r / rg;
+  const int t = grp * resid + (r - c * rg);
+  return TileId{t % ntx, t / ntx, c};
+}
+
+// Fused halo ("peer" transport): the buffers of the
+// neighbouring slabs, on this GPU (loopback) or mapped from a peer GPU over
+// NVLink (CUDA IPC).  With them the step kernel stores the components it pushes
+// out of the slab straight into the neighbour's next state, and K_phi its edge
+// planes straight into the neighbour's phi ghost planes -- no separate exchange.
+// nullptr: ghost planes here + a copy / NCCL exchange afterwards.
+struct Peers {
+  double* dn = nullptr;      // next-state buffer (B) of the slab below
+  double* up = nullptr;      // next-state buffer (B) of the slab above
+  double* phi_dn = nullptr;  // phi buffer of the slab below
+  double* phi_up = nullptr;  // phi buffer of the slab above
+};
+// Base of the distribution plane that local plane zd in [-1, nzl] is pushed to:
+// this slab's plane (wrapping when G.zwrap, else its ghost planes -1 / nzl), or,
+// with peers, plane nzl-1 of the slab below / plane 0 of the slab above -- the
+// very slots the exchange would have copied the ghost planes to.
+__host__ __device__ inline double* push_plane(const Geom& G, double* B, const Peers& P, int zd) {
+  if (!G.zwrap && zd < 0 && P.dn) return P.dn + push_plane_offset(G, G.nzl - 1);
+  if (!G.zwrap && zd >= G.nzl && P.up) return P.up + push_plane_offset(G, 0);
+  return B + push_plane_offset(G, zd);
 }
 
 // ---- launchers (lb_kernels.cu) -------------------------------------------
 // All launch on `st`, return cudaGetLastError().
-cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st);
+// K_phi on local planes [z0, z1); with peers, edge planes also go to the neighbours' ghost planes
+cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st,
+                       const Peers& pr = Peers{});
 // the fused step (lb_step.cu): collide planes [0, nzl) of A into B; phig = phi
 // buffer whose ghost planes are read when !G.zwrap; zc = z-chunk per CTA
 int step_tile_rows(const Geom& G, int num_sms);  // 4 or 8
@@ -88,11 +117,11 @@ struct alignas(64) StepMaps {
 bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out);
 // mode 0 = the step; 1, 2 = memory probes (lb_debug_step_probe)
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* mapsA, cudaStream_t st, int mode = 0);
+                        int* flag, const StepMaps* mapsA, cudaStream_t st, int mode = 0, const Peers& pr = Peers{});
 // the warp-specialised variant of the step (lb_step_ws.cu): same maps, nx even
 bool step_ws_fits(const StepMaps* maps);
 cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                           int* flag, const StepMaps* mapsA, cudaStream_t st);
+                           int* flag, const StepMaps* mapsA, cudaStream_t st, const Peers& pr = Peers{});
 // the cluster variant of the step (lb_step_cluster.cu): phi halos shared through
 // distributed shared memory; for nx % 64 == 0 and ny % 16 == 0
 struct alignas(64) ClusterMaps {
@@ -103,8 +132,8 @@ bool cluster_step_fits(const Geom& G);
 bool make_cluster_maps(const Geom& G, const double* buf, ClusterMaps* out);
 int cluster_zchunk(const Geom& G, int num_sms);
 cudaError_t launch_step_cluster(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
-                                int zc, int* flag, const ClusterMaps* mapsA, cudaStream_t st);
-cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st);
+                                int zc, int* flag, const ClusterMaps* mapsA, cudaStream_t st, const Peers& pr = Peers{});
+cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st, const Peers& pr = Peers{});
 cudaError_t launch_init_eq(const Geom& G, const DevParams& p, const double* phi, const double* rho,
                            const double* u, double* A, cudaStream_t st);
 // canonical [2][19][nloc] (f block then g block) <-> plane-major buffer

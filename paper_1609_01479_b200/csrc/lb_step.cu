@@ -57,9 +57,6 @@ namespace {
 #endif
 constexpr int kTX = LB_STEP_TX;
 // strip width of the block -> tile order (tile_of_block)
-#ifndef LB_STRIP_W
-#define LB_STRIP_W (1 << 20)
-#endif
 
 __device__ __forceinline__ int slot5(int z) {
   const int s = z % 5;
@@ -170,7 +167,7 @@ __host__ __device__ constexpr int frank(int i) {  // canonical i -> rank
 template <int TX, int TY, bool USE_TMA, int MODE>
 __global__ void __launch_bounds__(TX* TY, 1)
     k_step_async(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-                 const double* __restrict__ phig, int zc, int* __restrict__ flag,
+                 const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
                  const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
                  const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
   using S = StepSmem<TX, TY>;
@@ -182,7 +179,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
 
   const int tid = threadIdx.x;
   const int lx = tid % TX, ly = tid / TX;
-  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, LB_STRIP_W);
+  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc, resid);
   const int x0 = tb.bx * TX, y0 = tb.by * TY;
   const int x = x0 + lx, y = y0 + ly;
   const bool active = (x < G.nx) && (y < G.ny);
@@ -419,14 +416,13 @@ __global__ void __launch_bounds__(TX* TY, 1)
       __syncthreads();  // sTg consumed
       issue_tile(k + 1, 1);
     }
+    double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
     if (MODE != 0 && active) {
-      const long long zo[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
-                               (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-        double* d = B + zo[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;
+        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
         __stcs(d + (long long)slot(0, i) * nxy, f[i]);
         __stcs(d + (long long)slot(1, i) * nxy, g[i]);
       }
@@ -440,12 +436,10 @@ __global__ void __launch_bounds__(TX* TY, 1)
       double F[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) F[a] = Fxy_cur[a] - 0.5 * (Pz_next[a] - Pz_prev[a]);
-      const long long zoff[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
-                                 (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
       const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-        double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;  // A.8 push
+        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
         __stcs(d + (long long)slot(0, i) * nxy, fs);
         __stcs(d + (long long)slot(1, i) * nxy, gs);
       });
@@ -459,6 +453,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     }
   }
   cp_wait<0>();
+  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
 }
 
 // ---- host: tensor maps ---------------------------------------------------------
@@ -489,7 +484,7 @@ bool encode(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsig
 
 template <int TY, bool USE_TMA, int MODE>
 cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                     int* flag, const StepMaps* maps, cudaStream_t st) {
+                     int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
   constexpr size_t smem = sizeof(StepSmem<kTX, TY>);
   auto kern = k_step_async<kTX, TY, USE_TMA, MODE>;
   static bool attr = false;  // per-process, per-instantiation
@@ -502,19 +497,30 @@ cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double*
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   const unsigned nblk = (unsigned)(((G.nx + kTX - 1) / kTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc));
   dim3 grid(nblk);
-  kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
+  static int resid = 0;  // CTAs resident at a time (tile_of_block)
+  if (!resid) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTX * TY, smem);
+    resid = sms * (per_sm > 0 ? per_sm : 1);
+#ifdef LB_RESID_OVERRIDE
+    resid = LB_RESID_OVERRIDE;
+#endif
+  }
+  kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3]);
   return cudaGetLastError();
 }
 
 template <int TY, bool USE_TMA>
 cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st, int mode) {
+                        int* flag, const StepMaps* maps, cudaStream_t st, int mode, const Peers& pr) {
   switch (mode) {
-    case 1: return launch_t<TY, USE_TMA, 1>(G, p, A, B, phig, zc, flag, maps, st);
-    case 2: return launch_t<TY, USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st);
-    case 3: return launch_t<TY, USE_TMA, 3>(G, p, A, B, phig, zc, flag, maps, st);
-    case 4: return launch_t<TY, USE_TMA, 4>(G, p, A, B, phig, zc, flag, maps, st);
-    default: return launch_t<TY, USE_TMA, 0>(G, p, A, B, phig, zc, flag, maps, st);
+    case 1: return launch_t<TY, USE_TMA, 1>(G, p, A, B, phig, zc, flag, maps, st, pr);
+    case 2: return launch_t<TY, USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st, pr);
+    case 3: return launch_t<TY, USE_TMA, 3>(G, p, A, B, phig, zc, flag, maps, st, pr);
+    case 4: return launch_t<TY, USE_TMA, 4>(G, p, A, B, phig, zc, flag, maps, st, pr);
+    default: return launch_t<TY, USE_TMA, 0>(G, p, A, B, phig, zc, flag, maps, st, pr);
   }
 }
 
@@ -554,14 +560,14 @@ int step_zchunk(const Geom& G, int num_sms, int ty) {
 }
 
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st, int mode) {
+                        int* flag, const StepMaps* maps, cudaStream_t st, int mode, const Peers& pr) {
   if (!maps) return cudaErrorInvalidValue;
   const bool tma = maps->ok;
   if (maps->ty == 8)
-    return tma ? launch_mode<8, true>(G, p, A, B, phig, zc, flag, maps, st, mode)
-               : launch_mode<8, false>(G, p, A, B, phig, zc, flag, maps, st, mode);
-  return tma ? launch_mode<4, true>(G, p, A, B, phig, zc, flag, maps, st, mode)
-             : launch_mode<4, false>(G, p, A, B, phig, zc, flag, maps, st, mode);
+    return tma ? launch_mode<8, true>(G, p, A, B, phig, zc, flag, maps, st, mode, pr)
+               : launch_mode<8, false>(G, p, A, B, phig, zc, flag, maps, st, mode, pr);
+  return tma ? launch_mode<4, true>(G, p, A, B, phig, zc, flag, maps, st, mode, pr)
+             : launch_mode<4, false>(G, p, A, B, phig, zc, flag, maps, st, mode, pr);
 }
 
 }  // namespace lbk

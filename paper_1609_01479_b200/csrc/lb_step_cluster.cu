@@ -50,7 +50,7 @@ __device__ __forceinline__ int mod_n(int v, int n) {
 template <int MODE>
 __global__ void __launch_bounds__(NT, 2)
     k_step_cluster(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-                   const double* __restrict__ phig, int zc, int* __restrict__ flag,
+                   const double* __restrict__ phig, int zc, int* __restrict__ flag, Peers pr,
                    const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   ClusterSmem& sm = *reinterpret_cast<ClusterSmem*>(smem_raw);
@@ -295,12 +295,11 @@ __global__ void __launch_bounds__(NT, 2)
     __syncthreads();
     own_P(Pz_next, Fxy_next);
     if (x < G.nx && y < G.ny) {
-      const long long zoff[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
-                                 (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
+      double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
       auto emit = [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-        double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;  // A.8 push
+        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
         __stcs(d + (long long)slot(0, i) * nxy, fs);
         __stcs(d + (long long)slot(1, i) * nxy, gs);
       };
@@ -323,6 +322,7 @@ __global__ void __launch_bounds__(NT, 2)
     }
   }
   cp_wait<0>();
+  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
   cluster_sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
@@ -371,7 +371,7 @@ int cluster_zchunk(const Geom& G, int num_sms) {
 }
 
 cudaError_t launch_step_cluster(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
-                                int zc, int* flag, const ClusterMaps* maps, cudaStream_t st) {
+                                int zc, int* flag, const ClusterMaps* maps, cudaStream_t st, const Peers& pr) {
   if (!maps || !maps->ok) return cudaErrorInvalidValue;
   constexpr size_t smem = sizeof(ClusterSmem);
   auto kern = k_step_cluster<0>;
@@ -394,7 +394,7 @@ cudaError_t launch_step_cluster(const Geom& G, const DevParams& p, const double*
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, G, p, A, B, phig, zc, flag, m[0], m[1]);
+  return cudaLaunchKernelEx(&cfg, kern, G, p, A, B, phig, zc, flag, pr, m[0], m[1]);
 }
 
 }  // namespace lbk

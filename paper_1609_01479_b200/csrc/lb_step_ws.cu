@@ -9,7 +9,9 @@
 //       f, g at plane k, take phi, mu, F of plane k from the hand-off buffer sQ,
 //       collide (A.6, A.7) and push f*, g* to x + c_i (A.8).  They are the only
 //       warps that store, so the store stream never pauses for stencil work.
-//   stencil warpgroup (128 threads): runs one or two planes ahead -- waits for
+//   stencil warps (one thread per column for 32 x 8 tiles, with the register
+//       file split between the roles by setmaxnreg; one warpgroup for 32 x 4
+//       tiles): run one or two planes ahead -- wait for
 //       the g box of plane j+2 (TMA), phi(j+2) = sum_i g_i on the box (A.3),
 //       the chemical stress P(j+1) (A.4), the force F(j) = -div P (A.5) and
 //       mu(j) (A.4) -- and hands phi, mu, F of plane j over through sQ (two
@@ -25,7 +27,22 @@ namespace lbk {
 namespace {
 
 constexpr int kWTX = 32;
-constexpr int kNA = 128;  // stencil warpgroup
+#ifndef LB_WS_NA
+#define LB_WS_NA 256
+#endif
+// stencil threads: one or two warpgroups, at most one per site
+__host__ __device__ constexpr int ws_na(int ty) { return LB_WS_NA < kWTX * ty ? LB_WS_NA : kWTX * ty; }
+// register split between the roles for 32 x 8 tiles with 256 stencil threads
+// (setmaxnreg: 512 threads launch at 128 registers; the collision needs ~170)
+#ifndef LB_WS_REGS_STENCIL
+#define LB_WS_REGS_STENCIL 80
+#endif
+#ifndef LB_WS_REGS_COLL
+#define LB_WS_REGS_COLL 176
+#endif
+__host__ __device__ constexpr bool ws_split_regs(int ty) {
+  return LB_WS_REGS_STENCIL > 0 && kWTX * ty == 256 && ws_na(ty) == 256;
+}
 // L2 policies (policy_of): g box (re-read by the g tile two planes later), f and g
 // tiles (last use), stores (-1: st.global.cs)
 #ifndef LB_WS_BOX_POL
@@ -36,9 +53,6 @@ constexpr int kNA = 128;  // stencil warpgroup
 #endif
 #ifndef LB_WS_ST_POL
 #define LB_WS_ST_POL (-1)
-#endif
-#ifndef LB_WS_STRIP_W
-#define LB_WS_STRIP_W (1 << 20)
 #endif
 
 __device__ __forceinline__ int wslot5(int z) {
@@ -71,21 +85,23 @@ struct alignas(128) WsSmem {
 };
 
 template <int TY, int NBOX, bool GDIRECT>
-__global__ void __launch_bounds__(kWTX* TY + kNA, 1)
+__global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-              const double* __restrict__ phig, int zc, int* __restrict__ flag, const __grid_constant__ CUtensorMap tm_t5,
+              const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
+              const __grid_constant__ CUtensorMap tm_t5,
               const __grid_constant__ CUtensorMap tm_t9, const __grid_constant__ CUtensorMap tm_g5,
               const __grid_constant__ CUtensorMap tm_g9) {
   using S = WsSmem<TY, NBOX, GDIRECT>;
   constexpr int TX = kWTX, NT = S::NT;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
   constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
+  constexpr int kNA = ws_na(TY);
   constexpr int SPT = NT / kNA;  // sites per stencil thread
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
   const int tid = threadIdx.x;
-  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, LB_WS_STRIP_W);
+  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc, resid);
   const int x0 = tb.bx * TX, y0 = tb.by * TY;
   const int zA = tb.bz * zc;
   const int zB = min(zA + zc, G.nzl);
@@ -108,6 +124,7 @@ __global__ void __launch_bounds__(kWTX* TY + kNA, 1)
 
   if (tid >= NT) {
     // ============================ stencil warpgroup ============================
+    if constexpr (ws_split_regs(TY)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LB_WS_REGS_STENCIL));
     // Box n (n = 0 .. nlast) is the g box of plane zA - 2 + n, in buffer n % NBOX.
     const int a = tid - NT;
     const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
@@ -284,6 +301,7 @@ __global__ void __launch_bounds__(kWTX* TY + kNA, 1)
   }
 
   // ============================== collision warps ==============================
+  if constexpr (ws_split_regs(TY)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(LB_WS_REGS_COLL));
   const int lx = tid % TX, ly = tid / TX;
   const int x = x0 + lx, y = y0 + ly;
   const bool active = (x < G.nx) && (y < G.ny);
@@ -334,12 +352,11 @@ __global__ void __launch_bounds__(kWTX* TY + kNA, 1)
       issue_tile(k + 1, 1);
     }
     if (active) {
-      const long long zoff[3] = {(long long)(G.zwrap ? wrap_n(k - 1, G.nzl) : k - 1) + GZ, (long long)k + GZ,
-                                 (long long)(G.zwrap ? wrap_n(k + 1, G.nzl) : k + 1) + GZ};
+      double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
       const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-        double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;  // A.8 push
+        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
         if (LB_WS_ST_POL < 0) {
           __stcs(d + (long long)slot(0, i) * nxy, fs);
           __stcs(d + (long long)slot(1, i) * nxy, gs);
@@ -351,6 +368,7 @@ __global__ void __launch_bounds__(kWTX* TY + kNA, 1)
       if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
     }
   }
+  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
 }
 
 #ifndef LB_WS_NBOX
@@ -362,7 +380,7 @@ __global__ void __launch_bounds__(kWTX* TY + kNA, 1)
 
 template <int TY>
 cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st) {
+                        int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
   constexpr size_t smem = sizeof(WsSmem<TY, LB_WS_NBOX, LB_WS_GDIRECT>);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
   auto kern = k_step_ws<TY, LB_WS_NBOX, LB_WS_GDIRECT>;
@@ -375,7 +393,18 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   const unsigned nblk = (unsigned)(((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc));
   dim3 grid(nblk);
-  kern<<<grid, kWTX * TY + kNA, smem, st>>>(G, p, A, B, phig, zc, flag, m[0], m[1], m[2], m[3]);
+  static int resid = 0;  // CTAs resident at a time (tile_of_block)
+  if (!resid) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWTX * TY + ws_na(TY), smem);
+    resid = sms * (per_sm > 0 ? per_sm : 1);
+#ifdef LB_RESID_OVERRIDE
+    resid = LB_RESID_OVERRIDE;
+#endif
+  }
+  kern<<<grid, kWTX * TY + ws_na(TY), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3]);
   return cudaGetLastError();
 }
 
@@ -384,10 +413,10 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
 bool step_ws_fits(const StepMaps* maps) { return maps && maps->ok && (maps->ty == 8 || maps->ty == 4); }
 
 cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                           int* flag, const StepMaps* maps, cudaStream_t st) {
+                           int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
   if (!step_ws_fits(maps)) return cudaErrorInvalidValue;
-  if (maps->ty == 8) return launch_ws_t<8>(G, p, A, B, phig, zc, flag, maps, st);
-  return launch_ws_t<4>(G, p, A, B, phig, zc, flag, maps, st);
+  if (maps->ty == 8) return launch_ws_t<8>(G, p, A, B, phig, zc, flag, maps, st, pr);
+  return launch_ws_t<4>(G, p, A, B, phig, zc, flag, maps, st, pr);
 }
 
 }  // namespace lbk

@@ -72,13 +72,16 @@ _lb_profile_count = _sig("lb_profile_count", _i, _vp)
 _lb_profile_entry = _sig("lb_profile_entry", _i, _vp, _i, C.POINTER(C.c_char_p), _dp, C.POINTER(_ll))
 _lb_bytes_per_site = _sig("lb_bytes_per_site", C.c_double)
 _lb_debug_propagation_map = _sig("lb_debug_propagation_map", _i, _i, _i, _i, _i, _vp)
+_lb_debug_propagation_map_peers = _sig("lb_debug_propagation_map_peers", _i, _i, _i, _i, _i, _vp)
+_lb_debug_halo_mode = _sig("lb_debug_halo_mode", _i, _vp, _i)
 _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
 
 EXPORTS = [
     "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
-    "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_halo_plan",
+    "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
+    "lb_debug_halo_mode", "lb_halo_plan",
 ]
 
 
@@ -225,6 +228,22 @@ def lb_debug_propagation_map(nx: int, ny: int, nz: int, nslabs: int = 1) -> np.n
     if rc != LB_OK:
         raise LBError(rc, "propagation map failed (bad sizes or not a permutation)")
     return out.reshape(Q, nz, ny, nx)
+
+
+def lb_debug_propagation_map_peers(nx: int, ny: int, nz: int, nslabs: int = 1) -> np.ndarray:
+    out = np.empty(Q * nx * ny * nz, dtype=np.int64)
+    rc = _lb_debug_propagation_map_peers(nx, ny, nz, nslabs, out.ctypes.data)
+    if rc != LB_OK:
+        raise LBError(rc, "peer propagation map failed (bad sizes, a ghost-plane store or not a permutation)")
+    return out.reshape(Q, nz, ny, nx)
+
+
+def lb_debug_halo_mode(h, mode: int = -1) -> int:
+    """-1: query (returns 0 exchange / 1 peer); 0 or 1: set (returns 0)."""
+    rc = _lb_debug_halo_mode(h, mode)
+    if rc < 0:
+        _check(rc, h)
+    return rc
 
 
 def lb_halo_plan(nx: int, ny: int, nz: int, nranks: int, rank: int) -> dict:

@@ -74,6 +74,17 @@ def test_propagation_map_equals_oracle_bitwise(shape, nslabs):
     assert np.array_equal(got, _oracle_pull_map(nx, ny, nz))
 
 
+@pytest.mark.parametrize("shape,nslabs", [((4, 5, 6), 1), ((4, 5, 6), 2), ((4, 5, 6), 3), ((3, 3, 3), 1),
+                                          ((7, 3, 8), 4), ((5, 6, 4), 2), ((6, 4, 16), 8)])
+def test_fused_halo_map_equals_oracle_bitwise(shape, nslabs):
+    """The fused (peer) halo: destinations from the kernels' own push_plane address
+    arithmetic into the neighbouring slabs' buffers, never a ghost plane -- the same
+    permutation as np.roll (A.8)."""
+    nx, ny, nz = shape
+    got = lb.lb_debug_propagation_map_peers(nx, ny, nz, nslabs)
+    assert np.array_equal(got, _oracle_pull_map(nx, ny, nz))
+
+
 @pytest.mark.parametrize("nranks", [1, 2, 4, 8])
 def test_halo_plan_ring(nranks):
     for r in range(nranks):

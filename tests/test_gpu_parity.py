@@ -36,11 +36,14 @@ def rough(nx, ny, nz, seed=1, p=P0):
     return f + nf, g + ng
 
 
-def gpu_run(f, g, p, nsteps, nslabs=1, kernel=0):
-    """kernel: 0 default, 1 tile, 2 cluster, 3 warp-specialised step kernel (lb_debug_step_kernel)."""
+def gpu_run(f, g, p, nsteps, nslabs=1, kernel=0, halo=None):
+    """kernel: 0 default, 1 tile, 2 cluster, 3 warp-specialised step kernel (lb_debug_step_kernel);
+    halo: None default, 0 exchange, 1 peer (fused) transport between slabs (lb_debug_halo_mode)."""
     nz, ny, nx = f.shape[1:]
     with lb.Lattice(nx, ny, nz, cparams(p), nslabs=nslabs) as L:
         lb.lb_debug_step_kernel(L.h, kernel)
+        if halo is not None:
+            lb.lb_debug_halo_mode(L.h, halo)
         L.set_state(f, g)
         L.step(nsteps)
         return L.get_state()
@@ -238,6 +241,48 @@ def test_ws_kernel_rejects_odd_nx():
         with pytest.raises(lb.LBError) as e:
             lb.lb_debug_step_kernel(L.h, 3)
         assert e.value.code == lb.LB_EINVAL
+
+
+# ------------------------------------------------------------------ fused (peer) halo transport
+def test_loopback_defaults_to_fused_halo():
+    with lb.Lattice(16, 8, 8, nslabs=2) as L:
+        assert lb.lb_debug_halo_mode(L.h) == 1
+    with lb.Lattice(16, 8, 8) as L:
+        with pytest.raises(lb.LBError):
+            lb.lb_debug_halo_mode(L.h, 1)  # one periodic slab has no halo
+
+
+@pytest.mark.parametrize("kernel", [1, 3])
+@pytest.mark.parametrize("shape,nslabs", [((12, 10, 16), 2), ((32, 16, 16), 4), ((34, 9, 12), 3), ((7, 5, 8), 4)])
+def test_fused_halo_bitwise_equal_to_exchange_and_one_slab(kernel, shape, nslabs):
+    """The step kernel storing the leaving components straight into the neighbour
+    slab's buffer (and K_phi into its phi ghost planes) gives the same bits as the
+    ghost-plane + exchange transport and as the undecomposed lattice."""
+    nx, ny, nz = shape
+    if kernel == 3 and nx % 2:
+        pytest.skip("warp-specialised kernel needs nx even")
+    f, g = rough(nx, ny, nz, seed=17)
+    ref = gpu_run(f, g, P0, 5, nslabs=1, kernel=1)
+    peer = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=kernel, halo=1)
+    exch = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=kernel, halo=0)
+    for a in (peer, exch):
+        assert np.array_equal(a[0], ref[0]) and np.array_equal(a[1], ref[1])
+
+
+def test_fused_halo_cluster_kernel_and_stream_only():
+    f, g = rough(64, 16, 16, seed=18)
+    a = gpu_run(f, g, P0, 3, nslabs=2, kernel=2, halo=1)
+    b = gpu_run(f, g, P0, 3, nslabs=1, kernel=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    with lb.Lattice(64, 16, 16, nslabs=4) as L:
+        assert lb.lb_debug_halo_mode(L.h) == 1
+        L.set_state(f, g)
+        L.stream_only(5)
+        f1, g1 = L.get_state()
+    f0, g0 = f, g
+    for _ in range(5):
+        f0, g0 = R.propagate(f0), R.propagate(g0)
+    assert np.array_equal(f1, f0) and np.array_equal(g1, g0)
 
 
 # ------------------------------------------------------------------ bitwise properties of the GPU path
