@@ -174,8 +174,9 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
  * kernel (halo box per CTA), 2 = the cluster kernel (phi halos shared through
  * distributed shared memory; needs nx % 64 == 0 and ny % 16 == 0, else
  * LB_EINVAL), 3 = the warp-specialised tile kernel (stencil and collision on
- * separate warps; needs nx even, else LB_EINVAL).  All give bitwise identical
- * results.  Test / measurement support. */
+ * separate warps; needs nx even, else LB_EINVAL), 4 = the same with persistent
+ * CTAs taking work items from a counter.  All give bitwise identical results.
+ * Test / measurement support. */
 int lb_debug_step_kernel(lb_t* h, int which);
 
 /* Halo transport of a slab handle.  mode -1: returns the current mode (0 or 1);

@@ -58,9 +58,10 @@ struct lb_ctx {
   int zc = 1;             // z-chunk of the step kernel
   int ty = 8;             // tile rows of the step kernel
   int czc = 1;            // z-chunk of the cluster step kernel
-  int kernel_choice = 0;  // 0 default, 1 tile kernel, 2 cluster kernel, 3 warp-specialised kernel
+  int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
+  WorkCounter wctr;       // work-item counter of the persistent step kernel
   ncclComm_t comm = nullptr;
   // halo transport: 0 = exchange (ghost planes + copies / NCCL send-recv after the
   // kernels), 1 = peer (fused: the kernels store into the neighbours' buffers)
@@ -202,6 +203,8 @@ int alloc_slabs(lb_ctx* h) {
   }
   CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
   CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
+  CK(h, cudaMalloc(&h->wctr.dev, sizeof(unsigned long long)));
+  CK(h, cudaMemsetAsync(h->wctr.dev, 0, sizeof(unsigned long long), h->stream));
   CK(h, cudaMallocHost(&h->h_flag, sizeof(int)));
   CK(h, cudaStreamSynchronize(h->stream));
   return LB_OK;
@@ -419,8 +422,10 @@ int one_step(lb_ctx* h, int mode) {
            // default: the warp-specialised kernel for 32 x 8 tiles (large planes), the
            // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
            const bool ws = mode == 0 && step_ws_fits(&s.mapsA) &&
-                           (h->kernel_choice == 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
-           if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr);
+                           (h->kernel_choice == 3 || h->kernel_choice == 4 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
+           if (ws)
+             return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
+                                   h->kernel_choice == 4);
            return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, mode, pr);
          }));
     }
@@ -671,11 +676,12 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
 }
 
 int lb_debug_step_kernel(lb_t* h, int which) {
-  if (!h || which < 0 || which > 3)
-    return set_err(h, LB_EINVAL, "which must be 0 (auto), 1 (tile), 2 (cluster) or 3 (warp-specialised)");
+  if (!h || which < 0 || which > 4)
+    return set_err(h, LB_EINVAL,
+                   "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised) or 4 (persistent warp-specialised)");
   if (which == 2 && !h->slabs.empty() && !h->slabs[0].cmapsA.ok)
     return set_err(h, LB_EINVAL, "the cluster kernel needs nx %% 64 == 0 and ny %% 16 == 0");
-  if (which == 3 && !h->slabs.empty() && !step_ws_fits(&h->slabs[0].mapsA))
+  if ((which == 3 || which == 4) && !h->slabs.empty() && !step_ws_fits(&h->slabs[0].mapsA))
     return set_err(h, LB_EINVAL, "the warp-specialised kernel needs nx even (TMA rows)");
   h->kernel_choice = which;
   return LB_OK;
@@ -720,6 +726,7 @@ void lb_destroy(lb_t* h) {
     cudaFree(s.phi);
   }
   cudaFree(h->d_flag);
+  cudaFree(h->wctr.dev);
   if (h->h_flag) cudaFreeHost(h->h_flag);
   for (auto& p : h->pending) {
     cudaEventDestroy(p.e0);

@@ -118,10 +118,17 @@ bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out);
 // mode 0 = the step; 1, 2 = memory probes (lb_debug_step_probe)
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                         int* flag, const StepMaps* mapsA, cudaStream_t st, int mode = 0, const Peers& pr = Peers{});
-// the warp-specialised variant of the step (lb_step_ws.cu): same maps, nx even
+// the warp-specialised variant of the step (lb_step_ws.cu): same maps, nx even.
+// Persistent CTAs take work items from a device counter that only grows; `base`
+// is its value at the start of the next launch (advanced by every launch).
+struct WorkCounter {
+  unsigned long long* dev = nullptr;
+  unsigned long long base = 0;
+};
 bool step_ws_fits(const StepMaps* maps);
 cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                           int* flag, const StepMaps* mapsA, cudaStream_t st, const Peers& pr = Peers{});
+                           int* flag, const StepMaps* mapsA, cudaStream_t st, const Peers& pr, WorkCounter* wc,
+                           bool persist);
 // the cluster variant of the step (lb_step_cluster.cu): phi halos shared through
 // distributed shared memory; for nx % 64 == 0 and ny % 16 == 0
 struct alignas(64) ClusterMaps {

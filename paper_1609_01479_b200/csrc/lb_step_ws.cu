@@ -55,6 +55,14 @@ __host__ __device__ constexpr bool ws_split_regs(int ty) {
 #define LB_WS_ST_POL (-1)
 #endif
 
+#ifndef LB_WS_FETCH_EARLY
+#define LB_WS_FETCH_EARLY 0
+#endif
+// persistent CTAs: continue the same tile's next z-chunk without a prologue
+#ifndef LB_WS_CONT
+#define LB_WS_CONT 1
+#endif
+
 __device__ __forceinline__ int wslot5(int z) {
   const int s = z % 5;
   return s < 0 ? s + 5 : s;
@@ -66,32 +74,47 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// NBOX: g boxes in flight (1: issued one plane ahead; 2: two planes ahead).
-// GDIRECT: the collision warps read g(k) straight from global memory (an L2 hit:
-// the box brought it on chip two planes earlier) instead of a TMA tile, which
-// frees the shared memory for the second box buffer.
-template <int TY, int NBOX, bool GDIRECT>
+template <int TY>
 struct alignas(128) WsSmem {
   static constexpr int TX = kWTX, NT = TX * TY;
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
   static constexpr int PX = TX + 2, PY = TY + 2, NP = PX * PY;  // P box: tile + 1 halo
-  alignas(128) double sTf[Q][NT];                // f of the tile, f-slot order (TMA boxes TX x TY x 5|9|5)
-  alignas(128) double sTg[GDIRECT ? 1 : Q][NT];  // g of the tile, g-slot order
-  alignas(128) double sG[NBOX][Q][NB];           // g on the box, g-slot order  (TMA boxes BX x BY x 5|9|5)
-  double sPhi[5][NB];                            // ring of phi planes on the box
-  double sP[6][NP];                              // chemical stress of one plane on the P box
-  double sQ[2][5][NT];                           // hand-off: phi, mu, Fx, Fy, Fz of a plane
-  unsigned long long bar_f, bar_g, bar_box[NBOX], q_full[2], q_empty[2];
+  alignas(128) double sTf[Q][NT];  // f of the tile, f-slot order (TMA boxes TX x TY x 5|9|5)
+  alignas(128) double sTg[Q][NT];  // g of the tile, g-slot order
+  alignas(128) double sG[Q][NB];   // g on the box, g-slot order  (TMA boxes BX x BY x 5|9|5)
+  double sPhi[5][NB];              // ring of phi planes on the box
+  double sP[6][NP];                // chemical stress of one plane on the P box
+  double sQ[2][5][NT];             // hand-off: phi, mu, Fx, Fy, Fz of a plane
+  unsigned long long bar_f, bar_g, bar_box, q_full[2], q_empty[2], item_full[4];
+  int sItem[4];                    // work items, fetched by the stencil warps
 };
 
-template <int TY, int NBOX, bool GDIRECT>
+// Work item L (tile x z-chunk) of the step, in tile_of_block order.
+struct WsItem {
+  int x0, y0, zA, zB;
+};
+
+// PERSIST: one CTA per SM takes work items (L = tile x z-chunk, tile_of_block
+// order) from a global counter until none are left -- the same order the block
+// scheduler would use, so the CTAs working at one time stay on neighbouring
+// tiles (a static L = blockIdx.x + i*gridDim.x split lets fast CTAs run ahead
+// into other bands of tiles: +185 B/site of DRAM reads).  The
+// stencil warps fetch the next item as they start the current one and publish it
+// to the collision warps (sItem ring, item_full mbarriers), so the collision warps
+// prefetch the next item's first f and g tiles while they finish the current
+// one, and the stencil warps fill the next item's pipeline (prologue) while the
+// collision warps drain the current one.  The hand-off counter runs on across
+// items.  When the next item continues the same tile in z, the stencil keeps its
+// phi ring and P state and skips the prologue.  Without PERSIST, one item per
+// CTA (L = blockIdx.x).
+template <int TY, bool PERSIST>
 __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
               const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
-              const __grid_constant__ CUtensorMap tm_t5,
-              const __grid_constant__ CUtensorMap tm_t9, const __grid_constant__ CUtensorMap tm_g5,
-              const __grid_constant__ CUtensorMap tm_g9) {
-  using S = WsSmem<TY, NBOX, GDIRECT>;
+              unsigned long long* __restrict__ wctr, unsigned long long wbase,
+              const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
+              const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
+  using S = WsSmem<TY>;
   constexpr int TX = kWTX, NT = S::NT;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
   constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
@@ -101,11 +124,18 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
   const int tid = threadIdx.x;
-  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc, resid);
-  const int x0 = tb.bx * TX, y0 = tb.by * TY;
-  const int zA = tb.bz * zc;
-  const int zB = min(zA + zc, G.nzl);
+  const int ntx = (G.nx + TX - 1) / TX, nty = (G.ny + TY - 1) / TY, nch = (G.nzl + zc - 1) / zc;
+  const int nitems = ntx * nty * nch;
   const long long nxy = G.nxy;
+  auto item_of = [&](int L) {
+    const TileId tb = tile_of_block(L, ntx, nty, nch, resid);
+    WsItem it;
+    it.x0 = tb.bx * TX;
+    it.y0 = tb.by * TY;
+    it.zA = tb.bz * zc;
+    it.zB = min(it.zA + zc, G.nzl);
+    return it;
+  };
 
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
@@ -113,288 +143,327 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
   if (tid == 0) {
     mbar_init(&sm.bar_f, 1);
     mbar_init(&sm.bar_g, 1);
-    for (int b = 0; b < NBOX; ++b) mbar_init(&sm.bar_box[b], 1);
+    mbar_init(&sm.bar_box, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.q_full[s], kNA);
       mbar_init(&sm.q_empty[s], NT);
     }
+    for (int s = 0; s < 4; ++s) mbar_init(&sm.item_full[s], 1);
     fence_barrier_init();
   }
   __syncthreads();
 
   if (tid >= NT) {
-    // ============================ stencil warpgroup ============================
+    // ============================ stencil warps ============================
     if constexpr (ws_split_regs(TY)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LB_WS_REGS_STENCIL));
-    // Box n (n = 0 .. nlast) is the g box of plane zA - 2 + n, in buffer n % NBOX.
     const int a = tid - NT;
-    const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
     const unsigned long long pol_last = policy_of<LB_WS_BOX_POL>();
-    // per-thread copy plan of a wrapped halo box: 16-byte units
-    constexpr int BROWU = BX / 2, BOXU = BY * BROWU, BOXR = (BOXU + kNA - 1) / kNA;
-    long long box_src[BOXR];
-    int box_dst[BOXR];
-#pragma unroll
-    for (int r = 0; r < BOXR; ++r) {
-      const int u = a + r * kNA;
-      const int row = u / BROWU, cu = u - row * BROWU;
-      box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
-      box_dst[r] = u < BOXU ? row * BX + cu * 2 : -1;
-    }
     auto zsrc = [&](int zp, bool& ghost) {
       ghost = false;
       if (G.zwrap) { zp %= G.nzl; return zp < 0 ? zp + G.nzl : zp; }
       ghost = zp < 0 || zp >= G.nzl;
       return zp;
     };
-    const int nlast = zB - zA + 3;  // box of plane zB + 1
-    unsigned ph_box = 0;            // bit b: parity of bar_box[b]
-    // issue box n; the cp.async path commits exactly one group per call (empty
-    // for a ghost plane) so that the group count stays regular
-    auto issue_box = [&](int n) {
-      const int zp = zA - 2 + n;
-      bool ghost;
-      const int zs = zsrc(zp, ghost);
-      double(*dst)[NB] = sm.sG[n % NBOX];
-      if (box_interior) {
-        if (!ghost && a == 0) {
-          const int cpl = (zs + GZ) * NSLOT;
-          unsigned long long* bar = &sm.bar_box[n % NBOX];
-          fence_proxy_async();
-          mbar_expect_tx(bar, BOX_BYTES);
-          tma_load_3d(&dst[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, bar, pol_last);
-          tma_load_3d(&dst[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, bar, pol_last);
-          tma_load_3d(&dst[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, bar, pol_last);
+    constexpr int BROWU = BX / 2, BOXU = BY * BROWU, BOXR = (BOXU + kNA - 1) / kNA;
+    unsigned ph_box = 0;
+    unsigned seq = 0;  // planes handed off so far: slot seq & 1, use seq >> 1
+    double Pz_prev[SPT][3], Pz_cur[SPT][3], Fxy_cur[SPT][3];
+    WsItem prev{-1, -1, -1, -1};
+    // item m goes to sItem[m % 4]; the value nitems ends the sequence
+    unsigned m = 0;
+    auto fetch_publish = [&](unsigned idx) {
+      if (a == 0) {
+        int L;
+        if (PERSIST) {
+          const unsigned long long v = atomicAdd(wctr, 1ULL) - wbase;
+          L = v < (unsigned long long)nitems ? (int)v : nitems;
+        } else {
+          L = idx == 0 ? (int)blockIdx.x : nitems;
         }
-      } else {
-        if (!ghost) {
+        sm.sItem[idx % 4] = L;
+        mbar_arrive(&sm.item_full[idx % 4]);
+      }
+    };
+    fetch_publish(0);
+    named_sync(2, kNA);
+    int L = sm.sItem[0];
+    while (L < nitems) {
+#if LB_WS_FETCH_EARLY
+      fetch_publish(m + 1);  // early: the collision warps need it at this item's last plane
+#endif
+      const WsItem it = item_of(L);
+      const int x0 = it.x0, y0 = it.y0, zA = it.zA, zB = it.zB;
+      const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
+      // per-thread copy plan of a wrapped halo box: 16-byte units
+      long long box_src[BOXR];
+      int box_dst[BOXR];
+#pragma unroll
+      for (int r = 0; r < BOXR; ++r) {
+        const int u = a + r * kNA;
+        const int row = u / BROWU, cu = u - row * BROWU;
+        box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
+        box_dst[r] = u < BOXU ? row * BX + cu * 2 : -1;
+      }
+      // box n (n = 0 .. nlast) is the g box of plane zA - 2 + n
+      const int nlast = zB - zA + 3;  // plane zB + 1
+      auto issue_box = [&](int n) -> bool {
+        const int zp = zA - 2 + n;
+        bool ghost;
+        const int zs = zsrc(zp, ghost);
+        if (ghost) return false;
+        if (box_interior) {
+          if (a == 0) {
+            const int cpl = (zs + GZ) * NSLOT;
+            fence_proxy_async();
+            mbar_expect_tx(&sm.bar_box, BOX_BYTES);
+            tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
+            tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
+            tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
+          }
+        } else {
           const double* base = A + (long long)(zs + GZ) * G.plane;
 #pragma unroll
           for (int j = 0; j < Q; ++j) {
             const double* bj = base + (long long)gslot_of_rank(j) * nxy;
 #pragma unroll
             for (int r = 0; r < BOXR; ++r)
-              if (box_dst[r] >= 0) cp_async_v<2>(&dst[j][box_dst[r]], bj + box_src[r]);
+              if (box_dst[r] >= 0) cp_async_v<2>(&sm.sG[j][box_dst[r]], bj + box_src[r]);
+          }
+          cp_commit();
+        }
+        return true;
+      };
+      // wait for the box, then make it visible to the whole role
+      auto wait_box = [&](bool issued) {
+        if (issued) {
+          if (box_interior) {
+            mbar_wait(&sm.bar_box, ph_box);
+            ph_box ^= 1;
+          } else {
+            cp_wait<0>();
           }
         }
-        cp_commit();
-      }
-    };
-    // wait for box n, then make it visible to the whole warpgroup
-    auto wait_box = [&](int n) {
-      bool ghost;
-      zsrc(zA - 2 + n, ghost);
-      if (box_interior) {
-        if (!ghost) {
-          const int b = n % NBOX;
-          mbar_wait(&sm.bar_box[b], (ph_box >> b) & 1);
-          ph_box ^= 1u << b;
-        }
-      } else {
-        // groups committed after box n: boxes n+1 .. min(n+NBOX-1, nlast)
-        if (NBOX == 2 && n + 1 <= nlast) cp_wait<1>();
-        else cp_wait<0>();
-      }
-      named_sync(2, kNA);
-    };
-    auto make_phi = [&](int n) {
-      const int zp = zA - 2 + n;
-      bool ghost;
-      const int zs = zsrc(zp, ghost);
-      double* ring = sm.sPhi[wslot5(zp)];
-      const double(*src)[NB] = sm.sG[n % NBOX];
-      for (int b = a; b < NB; b += kNA) {
-        double v;
-        if (ghost) {
-          const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
-          v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
-        } else {
-          v = src[grank(0)][b];  // A.3, canonical order (same as phi_sum)
+        named_sync(2, kNA);
+      };
+      auto make_phi = [&](int zp) {
+        bool ghost;
+        const int zs = zsrc(zp, ghost);
+        double* ring = sm.sPhi[wslot5(zp)];
+        for (int b = a; b < NB; b += kNA) {
+          double v;
+          if (ghost) {
+            const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
+            v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
+          } else {
+            v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
 #pragma unroll
-          for (int i = 1; i < Q; ++i) v += src[grank(i)][b];
+            for (int i = 1; i < Q; ++i) v += sm.sG[grank(i)][b];
+          }
+          ring[b] = v;
         }
-        ring[b] = v;
-      }
-    };
-    auto compute_P = [&](int zp) {
-      const double* f0 = sm.sPhi[wslot5(zp - 1)];
-      const double* f1 = sm.sPhi[wslot5(zp)];
-      const double* f2 = sm.sPhi[wslot5(zp + 1)];
-      for (int e = a; e < NP; e += kNA) {
-        const int c = (e / PX + 1) * BX + (e % PX + 1);
-        const double ph = f1[c];
-        const double xp = f1[c + 1], xm = f1[c - 1];
-        const double yp = f1[c + BX], ym = f1[c - BX];
-        const double zp_ = f2[c], zm = f0[c];
-        const double lap = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * ph;  // A.2
-        double P[6];
-        stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp_ - zm), lap, P);
+      };
+      auto compute_P = [&](int zp) {
+        const double* f0 = sm.sPhi[wslot5(zp - 1)];
+        const double* f1 = sm.sPhi[wslot5(zp)];
+        const double* f2 = sm.sPhi[wslot5(zp + 1)];
+        for (int e = a; e < NP; e += kNA) {
+          const int c = (e / PX + 1) * BX + (e % PX + 1);
+          const double ph = f1[c];
+          const double xp = f1[c + 1], xm = f1[c - 1];
+          const double yp = f1[c + BX], ym = f1[c - BX];
+          const double zp_ = f2[c], zm = f0[c];
+          const double lap = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * ph;  // A.2
+          double P[6];
+          stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp_ - zm), lap, P);
 #pragma unroll
-        for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
-      }
-    };
-    auto own_P = [&](int site, double Pz[3], double Fxy[3]) {
-      const int e = (site / TX + 1) * PX + (site % TX + 1);
-      const auto& P = sm.sP;
-      Pz[0] = P[PXZ][e];
-      Pz[1] = P[PYZ][e];
-      Pz[2] = P[PZZ][e];
-      Fxy[0] = -0.5 * (P[PXX][e + 1] - P[PXX][e - 1]) - 0.5 * (P[PXY][e + PX] - P[PXY][e - PX]);
-      Fxy[1] = -0.5 * (P[PXY][e + 1] - P[PXY][e - 1]) - 0.5 * (P[PYY][e + PX] - P[PYY][e - PX]);
-      Fxy[2] = -0.5 * (P[PXZ][e + 1] - P[PXZ][e - 1]) - 0.5 * (P[PYZ][e + PX] - P[PYZ][e - PX]);
-    };
+          for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
+        }
+      };
+      auto own_P = [&](int site, double Pz[3], double Fxy[3]) {
+        const int e = (site / TX + 1) * PX + (site % TX + 1);
+        const auto& P = sm.sP;
+        Pz[0] = P[PXZ][e];
+        Pz[1] = P[PYZ][e];
+        Pz[2] = P[PZZ][e];
+        Fxy[0] = -0.5 * (P[PXX][e + 1] - P[PXX][e - 1]) - 0.5 * (P[PXY][e + PX] - P[PXY][e - PX]);
+        Fxy[1] = -0.5 * (P[PXY][e + 1] - P[PXY][e - 1]) - 0.5 * (P[PYY][e + PX] - P[PYY][e - PX]);
+        Fxy[2] = -0.5 * (P[PXZ][e + 1] - P[PXZ][e - 1]) - 0.5 * (P[PYZ][e + PX] - P[PYZ][e - PX]);
+      };
 
-    double Pz_prev[SPT][3], Pz_cur[SPT][3], Fxy_cur[SPT][3];
-    for (int n = 0; n < NBOX && n <= nlast; ++n) issue_box(n);
-    for (int n = 0; n <= nlast; ++n) {
-      const int zp = zA - 2 + n;
-      wait_box(n);  // (also: everyone is past the previous hand-off)
-      make_phi(n);
-      named_sync(2, kNA);  // sG[n % NBOX] consumed, ring written
-      if (n + NBOX <= nlast) issue_box(n + NBOX);
-      if (n < 2) continue;
-      compute_P(zp - 1);  // needs phi(zp-2 .. zp)
-      named_sync(2, kNA);
-      if (n == 2) {
+      // the same tile continued in z: phi ring, P state and box stream carry on
+      const bool cont = LB_WS_CONT && PERSIST && prev.x0 == x0 && prev.y0 == y0 && prev.zB == zA;
+      const int n0 = cont ? 4 : 0;
+      bool issued = issue_box(n0);
+      for (int n = n0; n <= nlast; ++n) {
+        const int zp = zA - 2 + n;
+        wait_box(issued);  // (also: everyone is past the previous hand-off)
+        make_phi(zp);
+        named_sync(2, kNA);  // sG consumed, ring written
+        issued = n + 1 <= nlast ? issue_box(n + 1) : false;
+        if (n < 2) continue;
+        compute_P(zp - 1);  // needs phi(zp-2 .. zp)
+        named_sync(2, kNA);
+        if (n == 2) {
+#pragma unroll
+          for (int s = 0; s < SPT; ++s) {
+            double unused[3];
+            own_P(a + s * kNA, Pz_prev[s], unused);
+          }
+          continue;
+        }
+        if (n == 3) {
+#pragma unroll
+          for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_cur[s], Fxy_cur[s]);
+          continue;
+        }
+        double Pz_next[SPT][3], Fxy_next[SPT][3];
+#pragma unroll
+        for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_next[s], Fxy_next[s]);
+        // hand phi, mu, F of plane j = zp - 2 to the collision warps
+        const int j = zp - 2;
+        const int q = seq & 1, u = seq >> 1;
+        if (u >= 1) mbar_wait(&sm.q_empty[q], (u - 1) & 1);
+        const double* r0 = sm.sPhi[wslot5(j)];
+        const double* rm = sm.sPhi[wslot5(j - 1)];
+        const double* rp = sm.sPhi[wslot5(j + 1)];
 #pragma unroll
         for (int s = 0; s < SPT; ++s) {
-          double unused[3];
-          own_P(a + s * kNA, Pz_prev[s], unused);
+          const int site = a + s * kNA;
+          const int cbox = (site / TX + 2) * BX + (site % TX + 2);
+          const double ph = r0[cbox];
+          const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) + (rp[cbox] + rm[cbox]) -
+                             6.0 * ph;
+          sm.sQ[q][0][site] = ph;
+          sm.sQ[q][1][site] = chem_pot(p, ph, lap);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            sm.sQ[q][2 + c][site] = Fxy_cur[s][c] - 0.5 * (Pz_next[s][c] - Pz_prev[s][c]);
+            Pz_prev[s][c] = Pz_cur[s][c];
+            Pz_cur[s][c] = Pz_next[s][c];
+            Fxy_cur[s][c] = Fxy_next[s][c];
+          }
         }
-        continue;
+        mbar_arrive(&sm.q_full[q]);
+        ++seq;
       }
-      if (n == 3) {
-#pragma unroll
-        for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_cur[s], Fxy_cur[s]);
-        continue;
-      }
-      double Pz_next[SPT][3], Fxy_next[SPT][3];
-#pragma unroll
-      for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_next[s], Fxy_next[s]);
-      // hand phi, mu, F of plane j = zp - 2 to the collision warps
-      const int j = zp - 2;
-      const int idx = j - zA, q = idx & 1, u = idx >> 1;
-      if (u >= 1) mbar_wait(&sm.q_empty[q], (u - 1) & 1);
-      const double* r0 = sm.sPhi[wslot5(j)];
-      const double* rm = sm.sPhi[wslot5(j - 1)];
-      const double* rp = sm.sPhi[wslot5(j + 1)];
-#pragma unroll
-      for (int s = 0; s < SPT; ++s) {
-        const int site = a + s * kNA;
-        const int cbox = (site / TX + 2) * BX + (site % TX + 2);
-        const double ph = r0[cbox];
-        const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) + (rp[cbox] + rm[cbox]) -
-                           6.0 * ph;
-        sm.sQ[q][0][site] = ph;
-        sm.sQ[q][1][site] = chem_pot(p, ph, lap);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          sm.sQ[q][2 + c][site] = Fxy_cur[s][c] - 0.5 * (Pz_next[s][c] - Pz_prev[s][c]);
-          Pz_prev[s][c] = Pz_cur[s][c];
-          Pz_cur[s][c] = Pz_next[s][c];
-          Fxy_cur[s][c] = Fxy_next[s][c];
-        }
-      }
-      mbar_arrive(&sm.q_full[q]);
+#if !LB_WS_FETCH_EARLY
+      // the next item, taken only now (after the last hand-off) so that the items in
+      // flight stay a window of about one per CTA
+      fetch_publish(m + 1);
+#endif
+      cp_wait<0>();
+      named_sync(2, kNA);  // ring / P of this item done before the next item's box lands; sItem visible
+      prev = it;
+      ++m;
+      L = sm.sItem[m % 4];
     }
-    cp_wait<0>();
     return;
   }
 
   // ============================== collision warps ==============================
   if constexpr (ws_split_regs(TY)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(LB_WS_REGS_COLL));
-  const int lx = tid % TX, ly = tid / TX;
-  const int x = x0 + lx, y = y0 + ly;
-  const bool active = (x < G.nx) && (y < G.ny);
   const unsigned long long pol_first = policy_of<LB_WS_TILE_POL>();
   const unsigned long long pol_st = policy_of<(LB_WS_ST_POL < 0 ? 1 : LB_WS_ST_POL)>();
-  unsigned ph_f = 0, ph_g = 0;
-  auto issue_tile = [&](int zp, int dist) {
-    if (zp < zB && tid == 0) {
+  unsigned ph_f = 0, ph_g = 0, seq = 0;
+  auto issue_tile = [&](const WsItem& it, int zp, int dist) {
+    if (tid == 0) {
       double(*dst)[NT] = dist == 0 ? sm.sTf : sm.sTg;
       unsigned long long* bar = dist == 0 ? &sm.bar_f : &sm.bar_g;
       const int cp0 = (zp + GZ) * NSLOT + (dist == 0 ? 0 : 5);
       fence_proxy_async();
       mbar_expect_tx(bar, TILE_BYTES);
-      tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol_first);
-      tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
-      tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol_first);
+      tma_load_3d(&dst[0][0], &tm_t5, it.x0, it.y0, cp0, bar, pol_first);
+      tma_load_3d(&dst[5][0], &tm_t9, it.x0, it.y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
+      tma_load_3d(&dst[14][0], &tm_t5, it.x0, it.y0, cp0 + 28, bar, pol_first);
     }
   };
-  issue_tile(zA, 0);
-  if (!GDIRECT) issue_tile(zA, 1);
-  const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
-  const long long xy = (long long)(active ? y : 0) * G.nx + (active ? x : 0);
-
-  for (int k = zA; k < zB; ++k) {
-    double f[Q], g[Q];
-    if (GDIRECT) {  // g(k): last use, an L2 hit
-      const double* gk = A + (long long)(k + GZ) * G.plane + xy;
+  unsigned m = 0;
+  mbar_wait(&sm.item_full[0], 0);
+  int L = sm.sItem[0];
+  if (L < nitems) {
+    const WsItem first = item_of(L);
+    issue_tile(first, first.zA, 0);
+    issue_tile(first, first.zA, 1);
+  }
+  while (L < nitems) {
+    const WsItem it = item_of(L);
+    const int lx = tid % TX, ly = tid / TX;
+    const int x = it.x0 + lx, y = it.y0 + ly;
+    const bool active = (x < G.nx) && (y < G.ny);
+    const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
+    int Ln = nitems;
+    WsItem nxt = it;
+    bool got_next = false;
+    // the tile after plane k: plane k+1 of this item, or the next item's first plane
+    auto issue_next = [&](int k, int dist) {
+      if (k + 1 < it.zB) {
+        issue_tile(it, k + 1, dist);
+        return;
+      }
+      if (!got_next) {
+        mbar_wait(&sm.item_full[(m + 1) % 4], ((m + 1) / 4) & 1);
+        Ln = sm.sItem[(m + 1) % 4];
+        if (Ln < nitems) nxt = item_of(Ln);
+        got_next = true;
+      }
+      if (Ln < nitems) issue_tile(nxt, nxt.zA, dist);
+    };
+    for (int k = it.zA; k < it.zB; ++k) {
+      double f[Q], g[Q];
+      mbar_wait(&sm.bar_f, ph_f);
+      ph_f ^= 1;
 #pragma unroll
-      for (int i = 0; i < Q; ++i) g[i] = __ldcs(gk + (long long)slot(1, i) * nxy);
-    }
-    mbar_wait(&sm.bar_f, ph_f);
-    ph_f ^= 1;
-#pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
-    named_sync(1, NT);  // sTf consumed
-    issue_tile(k + 1, 0);
-    const int idx = k - zA, q = idx & 1, u = idx >> 1;
-    mbar_wait(&sm.q_full[q], u & 1);
-    const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];
-    const double F[3] = {sm.sQ[q][2][tid], sm.sQ[q][3][tid], sm.sQ[q][4][tid]};
-    mbar_arrive(&sm.q_empty[q]);
-    if (!GDIRECT) {
+      for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
+      named_sync(1, NT);  // sTf consumed
+      issue_next(k, 0);
+      const int q = seq & 1, u = seq >> 1;
+      mbar_wait(&sm.q_full[q], u & 1);
+      const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];
+      const double F[3] = {sm.sQ[q][2][tid], sm.sQ[q][3][tid], sm.sQ[q][4][tid]};
+      mbar_arrive(&sm.q_empty[q]);
+      ++seq;
       mbar_wait(&sm.bar_g, ph_g);
       ph_g ^= 1;
 #pragma unroll
       for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
       named_sync(1, NT);  // sTg consumed
-      issue_tile(k + 1, 1);
+      issue_next(k, 1);
+      if (active) {
+        double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
+        const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
+          const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
+          const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+          double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
+          if (LB_WS_ST_POL < 0) {
+            __stcs(d + (long long)slot(0, i) * nxy, fs);
+            __stcs(d + (long long)slot(1, i) * nxy, gs);
+          } else {
+            st_hint(d + (long long)slot(0, i) * nxy, fs, pol_st);
+            st_hint(d + (long long)slot(1, i) * nxy, gs, pol_st);
+          }
+        });
+        if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
+      }
     }
-    if (active) {
-      double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
-      const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
-        const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
-        const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
-        if (LB_WS_ST_POL < 0) {
-          __stcs(d + (long long)slot(0, i) * nxy, fs);
-          __stcs(d + (long long)slot(1, i) * nxy, gs);
-        } else {
-          st_hint(d + (long long)slot(0, i) * nxy, fs, pol_st);
-          st_hint(d + (long long)slot(1, i) * nxy, gs, pol_st);
-        }
-      });
-      if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
-    }
+    ++m;
+    L = Ln;
   }
   if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
 }
 
-#ifndef LB_WS_NBOX
-#define LB_WS_NBOX 1
-#endif
-#ifndef LB_WS_GDIRECT
-#define LB_WS_GDIRECT 0
-#endif
 
-template <int TY>
+template <int TY, bool PERSIST>
 cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
-  constexpr size_t smem = sizeof(WsSmem<TY, LB_WS_NBOX, LB_WS_GDIRECT>);
+                        int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc) {
+  constexpr size_t smem = sizeof(WsSmem<TY>);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
-  auto kern = k_step_ws<TY, LB_WS_NBOX, LB_WS_GDIRECT>;
+  auto kern = k_step_ws<TY, PERSIST>;
   static bool attr = false;
+  static int resid = 0;  // CTAs resident at a time (tile_of_block; the persistent grid)
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
-  }
-  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
-  const unsigned nblk = (unsigned)(((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc));
-  dim3 grid(nblk);
-  static int resid = 0;  // CTAs resident at a time (tile_of_block)
-  if (!resid) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -404,7 +473,14 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
     resid = LB_RESID_OVERRIDE;
 #endif
   }
-  kern<<<grid, kWTX * TY + ws_na(TY), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3]);
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
+  const int nitems = ((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc);
+  if (PERSIST && (!wc || !wc->dev)) return cudaErrorInvalidValue;
+  const unsigned nblk = (unsigned)(PERSIST ? (nitems < resid ? nitems : resid) : nitems);
+  kern<<<nblk, kWTX * TY + ws_na(TY), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, wc ? wc->dev : nullptr,
+                                                  wc ? wc->base : 0ULL, m[0], m[1], m[2], m[3]);
+  // every CTA takes one item past the end: the counter moved by nitems + grid
+  if (PERSIST) wc->base += (unsigned long long)nitems + nblk;
   return cudaGetLastError();
 }
 
@@ -413,10 +489,14 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
 bool step_ws_fits(const StepMaps* maps) { return maps && maps->ok && (maps->ty == 8 || maps->ty == 4); }
 
 cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                           int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
+                           int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc,
+                           bool persist) {
   if (!step_ws_fits(maps)) return cudaErrorInvalidValue;
-  if (maps->ty == 8) return launch_ws_t<8>(G, p, A, B, phig, zc, flag, maps, st, pr);
-  return launch_ws_t<4>(G, p, A, B, phig, zc, flag, maps, st, pr);
+  if (persist)
+    return maps->ty == 8 ? launch_ws_t<8, true>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
+                         : launch_ws_t<4, true>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
+  return maps->ty == 8 ? launch_ws_t<8, false>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
+                       : launch_ws_t<4, false>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
 }
 
 }  // namespace lbk

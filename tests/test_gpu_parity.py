@@ -37,7 +37,7 @@ def rough(nx, ny, nz, seed=1, p=P0):
 
 
 def gpu_run(f, g, p, nsteps, nslabs=1, kernel=0, halo=None):
-    """kernel: 0 default, 1 tile, 2 cluster, 3 warp-specialised step kernel (lb_debug_step_kernel);
+    """kernel: 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised (lb_debug_step_kernel);
     halo: None default, 0 exchange, 1 peer (fused) transport between slabs (lb_debug_halo_mode)."""
     nz, ny, nx = f.shape[1:]
     with lb.Lattice(nx, ny, nz, cparams(p), nslabs=nslabs) as L:
@@ -205,7 +205,9 @@ def test_ws_kernel_parity_and_bitwise_equal_to_tile_kernel(shape):
     f, g = rough(nx, ny, nz, seed=14)
     a = gpu_run(f, g, P0, 4, kernel=3)
     b = gpu_run(f, g, P0, 4, kernel=1)
+    c = gpu_run(f, g, P0, 4, kernel=4)  # persistent CTAs
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(c[0], b[0]) and np.array_equal(c[1], b[1])
     assert_parity(a, R.run(f, g, P0, 4))
 
 
@@ -217,7 +219,10 @@ def test_ws_kernel_32x8_tiles_and_z_chunks():
     f, g = spinodal(nx, ny, nz, seed=15)
     a = gpu_run(f, g, P0, 1, kernel=3)
     b = gpu_run(f, g, P0, 1, kernel=1)
+    c = gpu_run(f, g, P0, 2, kernel=4)
+    d = gpu_run(f, g, P0, 2, kernel=3)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(c[0], d[0]) and np.array_equal(c[1], d[1])
     smp = BR.SiteSampler(f, g, P0)
     fs, gs, fr, gr = [], [], [], []
     for (x, y, z) in synth.sample_sites(nx, ny, nz, 32):
@@ -252,14 +257,14 @@ def test_loopback_defaults_to_fused_halo():
             lb.lb_debug_halo_mode(L.h, 1)  # one periodic slab has no halo
 
 
-@pytest.mark.parametrize("kernel", [1, 3])
+@pytest.mark.parametrize("kernel", [1, 3, 4])
 @pytest.mark.parametrize("shape,nslabs", [((12, 10, 16), 2), ((32, 16, 16), 4), ((34, 9, 12), 3), ((7, 5, 8), 4)])
 def test_fused_halo_bitwise_equal_to_exchange_and_one_slab(kernel, shape, nslabs):
     """The step kernel storing the leaving components straight into the neighbour
     slab's buffer (and K_phi into its phi ghost planes) gives the same bits as the
     ghost-plane + exchange transport and as the undecomposed lattice."""
     nx, ny, nz = shape
-    if kernel == 3 and nx % 2:
+    if kernel in (3, 4) and nx % 2:
         pytest.skip("warp-specialised kernel needs nx even")
     f, g = rough(nx, ny, nz, seed=17)
     ref = gpu_run(f, g, P0, 5, nslabs=1, kernel=1)
