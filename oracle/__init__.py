@@ -11,6 +11,8 @@ Modules
 lb_ref    plain NumPy fp64 transcription of the step, ``np.roll`` for every shift
 lb_brute  per-site scalar loops (pure Python floats) for tiny lattices and for
           single sampled sites of large lattices
+lb_mrt    the NEXT-3 collision variant: chemical stress in f's equilibrium,
+          three-rate MRT (readings R23-R27)
 
 Citations: ``P:NNN`` = PAPER.md line NNN (Gray & Stratford, arXiv 1609.01479);
 ``S:NNN`` = SPEC.md line NNN; ``Rk`` = reading k of the DESIGN.md ledger (the
