@@ -168,6 +168,19 @@ int lb_debug_stream(lb_t* h, int nsteps);
  * memory-side ceiling of the access pattern for the roofline analysis. */
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
 
+/* Collision model of f (readings R23-R27).
+ *   model 0 (default, the paper path): BGK of f with tau_f of lb_params and the
+ *     Guo force F = -div P (R5, R7); the tau arguments are ignored.
+ *   model 1: the chemical stress P in the second moment of f's equilibrium
+ *     (no force, u = j/rho) and a three-rate MRT of f: the traceless stress
+ *     relaxes with tau_shear (viscosity (tau_shear - 1/2)/3), its trace with
+ *     tau_bulk, the ghost modes with tau_ghost; tau_f of lb_params is unused.
+ *     g is unchanged (BGK with tau_g, R9/R10), with the force-free u.
+ * Each tau finite and > 1/2, else LB_EINVAL; LB_EINVAL also for model 1 while
+ * the cluster kernel is selected (it implements model 0 only).  Takes effect at
+ * the next lb_step. */
+int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, double tau_ghost);
+
 /* Which step kernel lb_step uses: 0 = default (the warp-specialised kernel
  * when the plane is large enough for 32 x 8 tiles and nx is even, else the tile
  * kernel), 1 = the tile

@@ -138,6 +138,8 @@ DevParams derive(const lb_params& p) {
   d.inv_tau_g = 1.0 / p.tau_g;
   d.guo_pref = 1.0 - 1.0 / (2.0 * p.tau_f);
   d.gamma = p.mobility / (p.tau_g - 0.5);
+  d.coll = 0;
+  d.inv_tau_s = d.inv_tau_b = d.inv_tau_ghost = d.inv_tau_f;
   return d;
 }
 
@@ -416,7 +418,7 @@ int one_step(lb_ctx* h, int mode) {
       CK(h, timed(h, K_STEP, true, [&]() {
            // the cluster kernel is opt-in: measured slower than the tile kernel in round 1
            // (cluster barrier per plane)
-           const bool cluster = mode == 0 && s.cmapsA.ok && h->kernel_choice == 2;
+           const bool cluster = mode == 0 && s.cmapsA.ok && h->kernel_choice == 2 && h->dp.coll == 0;
            if (cluster)
              return launch_step_cluster(G, h->dp, s.A, s.B, s.phi, h->czc, h->d_flag, &s.cmapsA, h->stream, pr);
            // default: the warp-specialised kernel for 32 x 8 tiles (large planes), the
@@ -679,6 +681,8 @@ int lb_debug_step_kernel(lb_t* h, int which) {
   if (!h || which < 0 || which > 4)
     return set_err(h, LB_EINVAL,
                    "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised) or 4 (persistent warp-specialised)");
+  if (which == 2 && h->dp.coll != 0)
+    return set_err(h, LB_EINVAL, "the cluster kernel implements only the BGK + force collision (model 0)");
   if (which == 2 && !h->slabs.empty() && !h->slabs[0].cmapsA.ok)
     return set_err(h, LB_EINVAL, "the cluster kernel needs nx %% 64 == 0 and ny %% 16 == 0");
   if ((which == 3 || which == 4) && !h->slabs.empty() && !step_ws_fits(&h->slabs[0].mapsA))
@@ -805,6 +809,24 @@ int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out) {
             if (out[(long long)i * N + sdst] != -1) return LB_EINVAL;  // not a permutation
             out[(long long)i * N + sdst] = ssrc;
           }
+  return LB_OK;
+}
+
+int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, double tau_ghost) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (model == 0) {
+    h->dp.coll = 0;
+    return LB_OK;
+  }
+  if (model != 1) return set_err(h, LB_EINVAL, "model must be 0 (BGK + force) or 1 (stress in f^eq, MRT)");
+  for (double t : {tau_shear, tau_bulk, tau_ghost})
+    if (!std::isfinite(t) || !(t > 0.5)) return set_err(h, LB_EINVAL, "MRT relaxation times must be finite and > 0.5");
+  if (h->kernel_choice == 2) return set_err(h, LB_EINVAL, "the cluster kernel implements only model 0");
+  h->dp.coll = 1;
+  h->dp.inv_tau_s = 1.0 / tau_shear;
+  h->dp.inv_tau_b = 1.0 / tau_bulk;
+  h->dp.inv_tau_ghost = 1.0 / tau_ghost;
   return LB_OK;
 }
 

@@ -102,6 +102,94 @@ __device__ __forceinline__ double collide_acc(const DevParams& p, GetF&& getf, G
   return rho;
 }
 
+// NEXT-3 variant (readings R23-R26): the chemical stress P in the second moment of
+// f's equilibrium, no force, u = j / rho, and a three-rate MRT of f in projection
+// form.  With X = P + rho u u and f^neq = f - f^eq, Pi = sum c c f^neq,
+// t = tr Pi, S = Pi - t/3 I, h_i = 4.5 w_i (S:c c + t/3 (|c|^2 - 1)):
+//   f_i^eq = w_i [rho + 3 rho c.u + 4.5 (X:c c - tr X/3)]
+//   f_i*   = f_i^eq + 4.5 w_i [k_s S:c c + k_b t/3 (|c|^2 - 1)] + k_g (f_i^neq - h_i)
+//          = f_i^eq + k_g f_i^neq + 4.5 w_i [(k_s - k_g) S:c c + (k_b - k_g) t/3 (|c|^2 - 1)]
+// with k_s = 1 - 1/tau_s, k_b = 1 - 1/tau_b, k_g = 1 - 1/tau_ghost; g as in collide_acc
+// with the force-free u.  Evaluated per antipodal pair: X:c c, S:c c and |c|^2 are
+// even in c, c.u is odd.  P6 = (xx, yy, zz, xy, xz, yz).  Returns rho.
+template <class Emit>
+__device__ __forceinline__ double collide_mrt(const DevParams& p, double (&f)[Q], const double (&g)[Q], double phi,
+                                              double mu, const double P6[6], Emit&& emit) {
+  double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    rho += f[i];
+    if (cx(i)) jx += cx(i) * f[i];
+    if (cy(i)) jy += cy(i) * f[i];
+    if (cz(i)) jz += cz(i) * f[i];
+  }
+  const double rinv = 1.0 / rho;
+  const double ux = jx * rinv, uy = jy * rinv, uz = jz * rinv;  // R23
+  const double X[6] = {P6[PXX] + rho * ux * ux, P6[PYY] + rho * uy * uy, P6[PZZ] + rho * uz * uz,
+                       P6[PXY] + rho * ux * uy, P6[PXZ] + rho * ux * uz, P6[PYZ] + rho * uy * uz};
+  const double trX3 = (X[0] + X[1] + X[2]) * (1.0 / 3.0);
+  auto cMc = [](int i, const double M[6]) {  // c_i . M . c_i (even in c)
+    double v = 0.0;
+    if (cx(i)) v += M[0];
+    if (cy(i)) v += M[1];
+    if (cz(i)) v += M[2];
+    if (cx(i) && cy(i)) v += 2.0 * cx(i) * cy(i) * M[3];
+    if (cx(i) && cz(i)) v += 2.0 * cx(i) * cz(i) * M[4];
+    if (cy(i) && cz(i)) v += 2.0 * cy(i) * cz(i) * M[5];
+    return v;
+  };
+  // pass 1: f^neq in place, and its second moment Pi
+  double Pi[6] = {0, 0, 0, 0, 0, 0};
+  f[0] -= wgt(0) * (rho - 4.5 * trX3);  // rest: X:cc = 0
+#pragma unroll
+  for (int i = 1; i <= 9; ++i) {
+    const int ia = Q - i;
+    const double w = wgt(i);
+    const double e = w * (rho + 4.5 * (cMc(i, X) - trX3));
+    const double o = (3.0 * w * rho) * (cx(i) * ux + cy(i) * uy + cz(i) * uz);
+    f[i] -= e + o;
+    f[ia] -= e - o;
+    const double s = f[i] + f[ia];  // c c is even: the pair contributes c c (f_i + f_ia)
+    if (cx(i)) Pi[0] += s;
+    if (cy(i)) Pi[1] += s;
+    if (cz(i)) Pi[2] += s;
+    if (cx(i) && cy(i)) Pi[3] += cx(i) * cy(i) * s;
+    if (cx(i) && cz(i)) Pi[4] += cx(i) * cz(i) * s;
+    if (cy(i) && cz(i)) Pi[5] += cy(i) * cz(i) * s;
+  }
+  const double t3 = (Pi[0] + Pi[1] + Pi[2]) * (1.0 / 3.0);
+  const double S[6] = {Pi[0] - t3, Pi[1] - t3, Pi[2] - t3, Pi[3], Pi[4], Pi[5]};
+  const double kg = 1.0 - p.inv_tau_ghost;
+  const double dks = (1.0 - p.inv_tau_s) - kg, dkb = (1.0 - p.inv_tau_b) - kg;
+  // g (R26): as collide_acc with F = 0
+  const double uu = ux * ux + uy * uy + uz * uz;
+  const double gmu = p.gamma * mu;
+  const double omg = p.inv_tau_g, keepg = 1.0 - p.inv_tau_g;
+  const double phi_even = -1.5 * phi * uu;
+  {  // rest particle
+    const double w = wgt(0);
+    const double feq = w * (rho - 4.5 * trX3);
+    const double fs = feq + kg * f[0] + 4.5 * w * (dkb * t3 * -1.0);
+    const double geq = __fma_rn(w, __fma_rn(-4.5, gmu, phi_even), phi);
+    emit(0, fs, __fma_rn(keepg, g[0], __dmul_rn(omg, geq)));
+  }
+#pragma unroll
+  for (int i = 1; i <= 9; ++i) {
+    const int ia = Q - i;
+    const double w = wgt(i);
+    const double e = w * (rho + 4.5 * (cMc(i, X) - trX3));
+    const double cu = cx(i) * ux + cy(i) * uy + cz(i) * uz;
+    const double o = (3.0 * w * rho) * cu;
+    const double even = 4.5 * w * (dks * cMc(i, S) + dkb * t3 * (double)(csq(i) - 1));
+    const double geq_e = w * (4.5 * gmu * (double)(csq(i) - 1) + phi_even + 4.5 * phi * cu * cu);
+    const double geq_o = (3.0 * w * phi) * cu;
+    const double gsym = omg * geq_e, ganti = omg * geq_o;
+    emit(i, (e + o) + kg * f[i] + even, keepg * g[i] + gsym + ganti);
+    emit(ia, (e - o) + kg * f[ia] + even, keepg * g[ia] + gsym - ganti);
+  }
+  return rho;
+}
+
 template <class Emit>
 __device__ __forceinline__ double collide(const DevParams& p, const double (&f)[Q], const double (&g)[Q], double phi,
                                           double mu, const double F[3], Emit&& emit) {

@@ -17,6 +17,10 @@ struct DevParams {
   double inv_tau_g;   // 1 / tau_g
   double guo_pref;    // 1 - 1/(2 tau_f)   (R7)
   double gamma;       // M / (tau_g - 1/2) (R10)
+  // collision of f: 0 = BGK with the Guo force F = -div P (R5, R7; the paper path),
+  // 1 = chemical stress in f^eq + three-rate MRT (NEXT-3, R23-R26)
+  int coll;
+  double inv_tau_s, inv_tau_b, inv_tau_ghost;  // MRT rates (coll 1)
 };
 
 // Geometry of one z-slab as the kernels see it.

@@ -164,7 +164,7 @@ __host__ __device__ constexpr int frank(int i) {  // canonical i -> rank
 // re-issued for the next plane at the top of an iteration, so it has a whole
 // iteration of lead time; g (an L2 hit: the box brought it in two planes ago)
 // follows.
-template <int TX, int TY, bool USE_TMA, int MODE>
+template <int TX, int TY, bool USE_TMA, int MODE, int COLL>
 __global__ void __launch_bounds__(TX* TY, 1)
     k_step_async(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
                  const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
@@ -361,6 +361,13 @@ __global__ void __launch_bounds__(TX* TY, 1)
     Fxy[2] = -0.5 * (P[PXZ][e + 1] - P[PXZ][e - 1]) - 0.5 * (P[PYZ][e + PX] - P[PYZ][e - PX]);
   };
 
+  // ---- own-site P (all six components), for the stress-in-equilibrium collision
+  auto own_P6 = [&](double P6[6]) {
+    const int e = (ly + 1) * PX + (lx + 1);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) P6[q] = sm.sP[q][e];
+  };
+
   // ---- prologue: phi on zA-2 .. zA+1; P on zA-1, zA; then prime the streams
   issue_tile(zA, 0);
   for (int zp = zA - 2; zp <= zA + 1 && MODE != 3; ++zp) {
@@ -370,6 +377,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     __syncthreads();
   }
   double Pz_prev[3] = {0, 0, 0}, Pz_cur[3] = {0, 0, 0}, Fxy_cur[3] = {0, 0, 0};
+  double P6_cur[6] = {0, 0, 0, 0, 0, 0};  // COLL 1: P at this site, plane k
   if (MODE == 0 || MODE == 2) {
     compute_P(zA - 1);
     __syncthreads();
@@ -379,6 +387,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     compute_P(zA);
     __syncthreads();
     own_P(Pz_cur, Fxy_cur);
+    if (COLL == 1) own_P6(P6_cur);
   }
   bool box_issued = MODE != 3 ? issue_box(zA + 2) : false;
   if (MODE != 4) issue_tile(zA, 1);
@@ -397,6 +406,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     __syncthreads();       // sTf consumed by all threads; sG visible
     issue_tile(k + 1, 0);
     double Pz_next[3] = {0, 0, 0}, Fxy_next[3] = {0, 0, 0};
+    double P6_next[6] = {0, 0, 0, 0, 0, 0};
     if (MODE == 4) {  // probe: g from the box interior instead of a second tile copy
 #pragma unroll
       for (int i = 0; i < Q; ++i) g[i] = sm.sG[grank(i)][(ly + 2) * BX + (lx + 2)];
@@ -408,6 +418,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
       compute_P(k + 1);
       __syncthreads();
       own_P(Pz_next, Fxy_next);
+      if (COLL == 1) own_P6(P6_next);
     }
     if (MODE != 4) {
       wait_tile(1);  // g(k) tile landed
@@ -433,16 +444,22 @@ __global__ void __launch_bounds__(TX* TY, 1)
       const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) +
                          (sm.sPhi[slot5(k + 1)][cbox] + sm.sPhi[slot5(k - 1)][cbox]) - 6.0 * ph;
       const double mu = chem_pot(p, ph, lap);
-      double F[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) F[a] = Fxy_cur[a] - 0.5 * (Pz_next[a] - Pz_prev[a]);
-      const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
+      auto push = [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
         double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
         __stcs(d + (long long)slot(0, i) * nxy, fs);
         __stcs(d + (long long)slot(1, i) * nxy, gs);
-      });
+      };
+      double rho;
+      if constexpr (COLL == 1) {
+        rho = collide_mrt(p, f, g, ph, mu, P6_cur, push);
+      } else {
+        double F[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) F[a] = Fxy_cur[a] - 0.5 * (Pz_next[a] - Pz_prev[a]);
+        rho = collide(p, f, g, ph, mu, F, push);
+      }
       if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
     }
 #pragma unroll
@@ -451,6 +468,8 @@ __global__ void __launch_bounds__(TX* TY, 1)
       Pz_cur[a] = Pz_next[a];
       Fxy_cur[a] = Fxy_next[a];
     }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) P6_cur[q] = P6_next[q];
   }
   cp_wait<0>();
   if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
@@ -482,11 +501,11 @@ bool encode(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsig
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TY, bool USE_TMA, int MODE>
+template <int TY, bool USE_TMA, int MODE, int COLL = 0>
 cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                      int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
   constexpr size_t smem = sizeof(StepSmem<kTX, TY>);
-  auto kern = k_step_async<kTX, TY, USE_TMA, MODE>;
+  auto kern = k_step_async<kTX, TY, USE_TMA, MODE, COLL>;
   static bool attr = false;  // per-process, per-instantiation
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -520,7 +539,9 @@ cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, doub
     case 2: return launch_t<TY, USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st, pr);
     case 3: return launch_t<TY, USE_TMA, 3>(G, p, A, B, phig, zc, flag, maps, st, pr);
     case 4: return launch_t<TY, USE_TMA, 4>(G, p, A, B, phig, zc, flag, maps, st, pr);
-    default: return launch_t<TY, USE_TMA, 0>(G, p, A, B, phig, zc, flag, maps, st, pr);
+    default:
+      return p.coll == 1 ? launch_t<TY, USE_TMA, 0, 1>(G, p, A, B, phig, zc, flag, maps, st, pr)
+                         : launch_t<TY, USE_TMA, 0, 0>(G, p, A, B, phig, zc, flag, maps, st, pr);
   }
 }
 

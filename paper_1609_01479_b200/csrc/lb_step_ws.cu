@@ -40,6 +40,13 @@ __host__ __device__ constexpr int ws_na(int ty) { return LB_WS_NA < kWTX * ty ? 
 #ifndef LB_WS_REGS_COLL
 #define LB_WS_REGS_COLL 176
 #endif
+// the MRT collision (COLL 1) keeps more values live
+#ifndef LB_WS_REGS_STENCIL_MRT
+#define LB_WS_REGS_STENCIL_MRT 64
+#endif
+#ifndef LB_WS_REGS_COLL_MRT
+#define LB_WS_REGS_COLL_MRT 192
+#endif
 __host__ __device__ constexpr bool ws_split_regs(int ty) {
   return LB_WS_REGS_STENCIL > 0 && kWTX * ty == 256 && ws_na(ty) == 256;
 }
@@ -74,8 +81,9 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int TY>
+template <int TY, int COLL>
 struct alignas(128) WsSmem {
+  static constexpr int NQ = COLL == 1 ? 8 : 5;  // hand-off values per site
   static constexpr int TX = kWTX, NT = TX * TY;
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
   static constexpr int PX = TX + 2, PY = TY + 2, NP = PX * PY;  // P box: tile + 1 halo
@@ -84,7 +92,7 @@ struct alignas(128) WsSmem {
   alignas(128) double sG[Q][NB];   // g on the box, g-slot order  (TMA boxes BX x BY x 5|9|5)
   double sPhi[5][NB];              // ring of phi planes on the box
   double sP[6][NP];                // chemical stress of one plane on the P box
-  double sQ[2][5][NT];             // hand-off: phi, mu, Fx, Fy, Fz of a plane
+  double sQ[2][NQ][NT];            // hand-off: phi, mu, then Fx, Fy, Fz (COLL 0) or P (COLL 1)
   unsigned long long bar_f, bar_g, bar_box, q_full[2], q_empty[2], item_full[4];
   int sItem[4];                    // work items, fetched by the stencil warps
 };
@@ -107,14 +115,14 @@ struct WsItem {
 // items.  When the next item continues the same tile in z, the stencil keeps its
 // phi ring and P state and skips the prologue.  Without PERSIST, one item per
 // CTA (L = blockIdx.x).
-template <int TY, bool PERSIST>
+template <int TY, bool PERSIST, int COLL>
 __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
               const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
               unsigned long long* __restrict__ wctr, unsigned long long wbase,
               const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
               const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
-  using S = WsSmem<TY>;
+  using S = WsSmem<TY, COLL>;
   constexpr int TX = kWTX, NT = S::NT;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
   constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
@@ -155,7 +163,8 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
 
   if (tid >= NT) {
     // ============================ stencil warps ============================
-    if constexpr (ws_split_regs(TY)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LB_WS_REGS_STENCIL));
+    if constexpr (ws_split_regs(TY))
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(COLL == 1 ? LB_WS_REGS_STENCIL_MRT : LB_WS_REGS_STENCIL));
     const int a = tid - NT;
     const unsigned long long pol_last = policy_of<LB_WS_BOX_POL>();
     auto zsrc = [&](int zp, bool& ghost) {
@@ -168,6 +177,7 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
     unsigned ph_box = 0;
     unsigned seq = 0;  // planes handed off so far: slot seq & 1, use seq >> 1
     double Pz_prev[SPT][3], Pz_cur[SPT][3], Fxy_cur[SPT][3];
+    double P6_cur[SPT][COLL == 1 ? 6 : 1];  // COLL 1: P at the site, plane j
     WsItem prev{-1, -1, -1, -1};
     // item m goes to sItem[m % 4]; the value nitems ends the sequence
     unsigned m = 0;
@@ -279,6 +289,11 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
           for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
         }
       };
+      auto own_P6 = [&](int site, double* P6) {
+        const int e = (site / TX + 1) * PX + (site % TX + 1);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) P6[q] = sm.sP[q][e];
+      };
       auto own_P = [&](int site, double Pz[3], double Fxy[3]) {
         const int e = (site / TX + 1) * PX + (site % TX + 1);
         const auto& P = sm.sP;
@@ -313,12 +328,19 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
         }
         if (n == 3) {
 #pragma unroll
-          for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_cur[s], Fxy_cur[s]);
+          for (int s = 0; s < SPT; ++s) {
+            own_P(a + s * kNA, Pz_cur[s], Fxy_cur[s]);
+            if constexpr (COLL == 1) own_P6(a + s * kNA, P6_cur[s]);
+          }
           continue;
         }
         double Pz_next[SPT][3], Fxy_next[SPT][3];
+        double P6_next[SPT][COLL == 1 ? 6 : 1];
 #pragma unroll
-        for (int s = 0; s < SPT; ++s) own_P(a + s * kNA, Pz_next[s], Fxy_next[s]);
+        for (int s = 0; s < SPT; ++s) {
+          own_P(a + s * kNA, Pz_next[s], Fxy_next[s]);
+          if constexpr (COLL == 1) own_P6(a + s * kNA, P6_next[s]);
+        }
         // hand phi, mu, F of plane j = zp - 2 to the collision warps
         const int j = zp - 2;
         const int q = seq & 1, u = seq >> 1;
@@ -335,12 +357,20 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
                              6.0 * ph;
           sm.sQ[q][0][site] = ph;
           sm.sQ[q][1][site] = chem_pot(p, ph, lap);
+          if constexpr (COLL == 1) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            sm.sQ[q][2 + c][site] = Fxy_cur[s][c] - 0.5 * (Pz_next[s][c] - Pz_prev[s][c]);
-            Pz_prev[s][c] = Pz_cur[s][c];
-            Pz_cur[s][c] = Pz_next[s][c];
-            Fxy_cur[s][c] = Fxy_next[s][c];
+            for (int c = 0; c < 6; ++c) {
+              sm.sQ[q][2 + c][site] = P6_cur[s][c];
+              P6_cur[s][c] = P6_next[s][c];
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              sm.sQ[q][2 + c][site] = Fxy_cur[s][c] - 0.5 * (Pz_next[s][c] - Pz_prev[s][c]);
+              Pz_prev[s][c] = Pz_cur[s][c];
+              Pz_cur[s][c] = Pz_next[s][c];
+              Fxy_cur[s][c] = Fxy_next[s][c];
+            }
           }
         }
         mbar_arrive(&sm.q_full[q]);
@@ -361,7 +391,8 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
   }
 
   // ============================== collision warps ==============================
-  if constexpr (ws_split_regs(TY)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(LB_WS_REGS_COLL));
+  if constexpr (ws_split_regs(TY))
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(COLL == 1 ? LB_WS_REGS_COLL_MRT : LB_WS_REGS_COLL));
   const unsigned long long pol_first = policy_of<LB_WS_TILE_POL>();
   const unsigned long long pol_st = policy_of<(LB_WS_ST_POL < 0 ? 1 : LB_WS_ST_POL)>();
   unsigned ph_f = 0, ph_g = 0, seq = 0;
@@ -419,7 +450,9 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
       const int q = seq & 1, u = seq >> 1;
       mbar_wait(&sm.q_full[q], u & 1);
       const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];
-      const double F[3] = {sm.sQ[q][2][tid], sm.sQ[q][3][tid], sm.sQ[q][4][tid]};
+      double V[S::NQ - 2];  // F (COLL 0) or P (COLL 1)
+#pragma unroll
+      for (int c = 0; c < S::NQ - 2; ++c) V[c] = sm.sQ[q][2 + c][tid];
       mbar_arrive(&sm.q_empty[q]);
       ++seq;
       mbar_wait(&sm.bar_g, ph_g);
@@ -430,7 +463,7 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
       issue_next(k, 1);
       if (active) {
         double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
-        const double rho = collide(p, f, g, ph, mu, F, [&](int i, double fs, double gs) {
+        auto push = [&](int i, double fs, double gs) {
           const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
           const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
           double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
@@ -441,7 +474,10 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
             st_hint(d + (long long)slot(0, i) * nxy, fs, pol_st);
             st_hint(d + (long long)slot(1, i) * nxy, gs, pol_st);
           }
-        });
+        };
+        double rho;
+        if constexpr (COLL == 1) rho = collide_mrt(p, f, g, ph, mu, V, push);
+        else rho = collide(p, f, g, ph, mu, V, push);
         if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
       }
     }
@@ -452,12 +488,12 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
 }
 
 
-template <int TY, bool PERSIST>
+template <int TY, bool PERSIST, int COLL>
 cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                         int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc) {
-  constexpr size_t smem = sizeof(WsSmem<TY>);
+  constexpr size_t smem = sizeof(WsSmem<TY, COLL>);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
-  auto kern = k_step_ws<TY, PERSIST>;
+  auto kern = k_step_ws<TY, PERSIST, COLL>;
   static bool attr = false;
   static int resid = 0;  // CTAs resident at a time (tile_of_block; the persistent grid)
   if (!attr) {
@@ -492,11 +528,19 @@ cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, d
                            int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc,
                            bool persist) {
   if (!step_ws_fits(maps)) return cudaErrorInvalidValue;
+  const bool t8 = maps->ty == 8;
+  if (p.coll == 1) {
+    if (persist)
+      return t8 ? launch_ws_t<8, true, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
+                : launch_ws_t<4, true, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
+    return t8 ? launch_ws_t<8, false, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
+              : launch_ws_t<4, false, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
+  }
   if (persist)
-    return maps->ty == 8 ? launch_ws_t<8, true>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
-                         : launch_ws_t<4, true>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
-  return maps->ty == 8 ? launch_ws_t<8, false>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
-                       : launch_ws_t<4, false>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
+    return t8 ? launch_ws_t<8, true, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
+              : launch_ws_t<4, true, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
+  return t8 ? launch_ws_t<8, false, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
+            : launch_ws_t<4, false, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
 }
 
 }  // namespace lbk

@@ -75,13 +75,14 @@ _lb_debug_propagation_map = _sig("lb_debug_propagation_map", _i, _i, _i, _i, _i,
 _lb_debug_propagation_map_peers = _sig("lb_debug_propagation_map_peers", _i, _i, _i, _i, _i, _vp)
 _lb_debug_halo_mode = _sig("lb_debug_halo_mode", _i, _vp, _i)
 _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
+_lb_set_collision = _sig("lb_set_collision", _i, _vp, _i, C.c_double, C.c_double, C.c_double)
 
 EXPORTS = [
     "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
-    "lb_debug_halo_mode", "lb_halo_plan",
+    "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision",
 ]
 
 
@@ -236,6 +237,11 @@ def lb_debug_propagation_map_peers(nx: int, ny: int, nz: int, nslabs: int = 1) -
     if rc != LB_OK:
         raise LBError(rc, "peer propagation map failed (bad sizes, a ghost-plane store or not a permutation)")
     return out.reshape(Q, nz, ny, nx)
+
+
+def lb_set_collision(h, model: int, tau_shear: float = 0.8, tau_bulk: float = 1.0, tau_ghost: float = 1.0) -> None:
+    """0: BGK + Guo force (default); 1: chemical stress in f^eq with a three-rate MRT."""
+    _check(_lb_set_collision(h, model, tau_shear, tau_bulk, tau_ghost), h)
 
 
 def lb_debug_halo_mode(h, mode: int = -1) -> int:

@@ -25,12 +25,15 @@ def main():
     ap.add_argument("--only", default="", help="comma-separated subset of the timings")
     ap.add_argument("--ab", default="", help="interleaved A/B of step kernels, e.g. 1,3 (lb_debug_step_kernel)")
     ap.add_argument("--rounds", type=int, default=20)
+    ap.add_argument("--mrt", action="store_true", help="collision model 1 (stress in f^eq, MRT)")
     a = ap.parse_args()
     nx, ny, nzf, _, desc = bench.CONFIGS[a.config]
     nz = nzf(1)
     L = lb.Lattice(nx, ny, nz)
     L.init_equilibrium(synth.spinodal_phi(nx, ny, nz))
     stream = torch.cuda.ExternalStream(lb.lb_stream(L.h))
+    if a.mrt:
+        lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
     out = {"config": a.config, "sites": nx * ny * nz}
 
     only = set(a.only.split(",")) if a.only else None
