@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--collision", default="bgk", choices=["bgk", "mrt"],
+                    help="bgk: BGK + Guo force (the paper path, default); mrt: stress in f^eq + MRT (NEXT-3)")
     return ap.parse_args()
 
 
@@ -150,18 +152,29 @@ def oracle_sample_shape(nx: int, ny: int, budget_sites: int):
     return nx, ny_s, nz_s
 
 
-def time_oracle(nx, ny, steps: int, seed: int = 0):
+def oracle_stepper(collision: str):
+    """(module name, step function, run function, params) of the oracle for a collision model."""
+    from oracle import lb_mrt as M
+    from oracle import lb_ref as R
+
+    if collision == "mrt":
+        p = M.MrtParams(base=R.Params(), tau_s=0.8, tau_b=1.1, tau_ghost=1.0)
+        return "oracle/lb_mrt.py", M.step, M.run, p
+    return "oracle/lb_ref.py", R.step, R.run, R.Params()
+
+
+def time_oracle(nx, ny, steps: int, seed: int = 0, collision: str = "bgk"):
     """The oracle as it stands, 1 thread, on a sample sub-lattice; returns (sites/s, shape)."""
     from oracle import lb_ref as R
     from paper_1609_01479_b200 import synth
 
+    _, step, run, p = oracle_stepper(collision)
     sx, sy, sz = oracle_sample_shape(nx, ny, 262144)
     rho, u, phi = synth.spinodal_fields(sx, sy, sz, seed)
-    p = R.Params()
-    f, g = R.equilibrium_state(rho, u, phi, p)
-    R.step(f, g, p)  # warm
+    f, g = R.equilibrium_state(rho, u, phi, R.Params())
+    step(f, g, p)  # warm
     t0 = time.perf_counter()
-    f, g = R.run(f, g, p, steps)
+    f, g = run(f, g, p, steps)
     dt = time.perf_counter() - t0
     return sx * sy * sz * steps / dt, (sx, sy, sz), dt
 
@@ -175,16 +188,16 @@ def run_reference(args):
     from oracle import lb_ref as R
     from paper_1609_01479_b200 import synth
 
+    name, _, run, p = oracle_stepper(args.collision)
     rho, u, phi = synth.spinodal_fields(sx, sy, sz, 0)
-    p = R.Params()
-    f, g = R.equilibrium_state(rho, u, phi, p)
-    f, g = R.run(f, g, p, max(args.warmup, 0))
+    f, g = R.equilibrium_state(rho, u, phi, R.Params())
+    f, g = run(f, g, p, max(args.warmup, 0))
     t0 = time.perf_counter()
-    f, g = R.run(f, g, p, args.steps)
+    f, g = run(f, g, p, args.steps)
     dt = time.perf_counter() - t0
     sites = sx * sy * sz
     v = sites * args.steps / dt / 1e6
-    sample = f"oracle/lb_ref.py NumPy fp64 step on a periodic {sx}x{sy}x{sz} sub-lattice ({sites} sites) of the workload per step"
+    sample = f"{name} NumPy fp64 step on a periodic {sx}x{sy}x{sz} sub-lattice ({sites} sites) of the workload per step"
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "MLUPS", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": scaling,
@@ -223,6 +236,9 @@ def run_ours(args):
     if world > 1:
         uid = D.broadcast_bytes(lb.lb_nccl_get_unique_id() if rank == 0 else None)
     L = lb.Lattice(nx, ny, nz, params, nranks=world, rank=rank, uid=uid)
+    if args.collision == "mrt":
+        lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
+    halo = ("peer (fused P2P stores)" if lb.lb_debug_halo_mode(L.h) == 1 else "NCCL send/recv") if world > 1 else None
     phi = synth.spinodal_phi_slab(nx, ny, nz, z0, z1, seed=0)
     L.init_equilibrium(phi)
 
@@ -289,9 +305,9 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cv, shp, dt = time_oracle(nx, ny, 20)
+        cv, shp, dt = time_oracle(nx, ny, 20, collision=args.collision)
         cpu = {"value": cv / 1e6, "unit": "MLUPS", "cores": 1, "kind": "oracle",
-               "sample": f"oracle/lb_ref.py, 20 steps on a periodic {shp[0]}x{shp[1]}x{shp[2]} sub-lattice of the "
+               "sample": f"{oracle_stepper(args.collision)[0]}, 20 steps on a periodic {shp[0]}x{shp[1]}x{shp[2]} sub-lattice of the "
                          f"workload, 1 thread ({dt:.1f} s of CPU)", "host_cpus": os.cpu_count()}
 
     L.close()
@@ -301,7 +317,9 @@ def run_ours(args):
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "lattice": [nx, ny, nz], "sites_per_gpu": nloc,
-                       "parallelism": f"z-slab x{world}" + (" (NCCL halos)" if world > 1 else ""),
+                       "parallelism": f"z-slab x{world}" + (f" ({halo} halos)" if world > 1 else ""),
+                       "collision": ("BGK + Guo force F = -div P (paper path)" if args.collision == "bgk" else
+                                     "chemical stress in f^eq, MRT tau_s 0.8 / tau_b 1.1 / tau_ghost 1.0 (NEXT-3)"),
                        "state_bytes_per_gpu": int(2 * 38 * 8 * nx * ny * (z1 - z0 + 2) + 8 * nx * ny * (z1 - z0 + 4)),
                        "l2": "inputs larger than L2 (state per GPU >> 126 MB)" if nloc * 608 > 126e6 * 2
                        else "state comparable to L2: not an HBM roofline point",
