@@ -13,6 +13,8 @@ lb_brute  per-site scalar loops (pure Python floats) for tiny lattices and for
           single sampled sites of large lattices
 lb_mrt    the NEXT-3 collision variant: chemical stress in f's equilibrium,
           three-rate MRT (readings R23-R27)
+lb_ch     the NEXT-2 variant: phi as a field, finite-difference Cahn-Hilliard
+          with first-order upwind advection (readings R29-R33)
 
 Citations: ``P:NNN`` = PAPER.md line NNN (Gray & Stratford, arXiv 1609.01479);
 ``S:NNN`` = SPEC.md line NNN; ``Rk`` = reading k of the DESIGN.md ledger (the
