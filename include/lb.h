@@ -168,6 +168,22 @@ int lb_debug_stream(lb_t* h, int nsteps);
  * memory-side ceiling of the access pattern for the roofline analysis. */
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
 
+/* ---- NEXT-2 variant: finite-difference Cahn-Hilliard (R29-R33) ----
+ * A handle whose state is (f, phi): phi is a field updated each step by
+ *   phi <- phi - sum_a [J_a(x + e_a/2) - J_a(x - e_a/2)] + M lap mu,
+ *   J = u_f * phi_upwind, u_f = (u(x) + u(x + e_a))/2, u = j/rho   (R30, R31)
+ * instead of the g distribution, and f collides with the chemical stress in
+ * its equilibrium and a three-rate MRT (model 1 of lb_set_collision, R32).
+ * One periodic lattice on the current GPU (no slabs); nx even, else LB_EINVAL;
+ * tau_f and tau_g of params are unused, M enters the update directly.
+ * lb_step, lb_get_phi, lb_init_equilibrium (f = f^eq(rho, u) of R8, phi as
+ * given), lb_destroy work as for other handles; lb_set_state / lb_get_state
+ * return LB_EINVAL (use the _ch pair: f canonical 19*nloc doubles, phi nloc). */
+int lb_create_ch(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk,
+                 double tau_ghost, lb_t** out);
+int lb_set_state_ch(lb_t* h, const double* f, const double* phi);
+int lb_get_state_ch(lb_t* h, double* f, double* phi);
+
 /* Collision model of f (readings R23-R27).
  *   model 0 (default, the paper path): BGK of f with tau_f of lb_params and the
  *     Guo force F = -div P (R5, R7); the tau arguments are ignored.

@@ -32,6 +32,8 @@ struct Slab {
   double* A = nullptr;  // current state (pre-collision f, g)
   double* B = nullptr;  // next state / staging
   double* phi = nullptr;
+  double* phi2 = nullptr;  // finite-difference Cahn-Hilliard handles: next phi
+  ChMaps chA{}, chB{};     // and the TMA descriptors of their f box
   StepMaps mapsA{}, mapsB{};        // TMA descriptors of A and B (swapped with them)
   ClusterMaps cmapsA{}, cmapsB{};  // same, for the cluster step kernel
 };
@@ -58,6 +60,7 @@ struct lb_ctx {
   int zc = 1;             // z-chunk of the step kernel
   int ty = 8;             // tile rows of the step kernel
   int czc = 1;            // z-chunk of the cluster step kernel
+  bool ch = false;        // NEXT-2 handle: state (f, phi), lb_create_ch
   int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
@@ -140,6 +143,7 @@ DevParams derive(const lb_params& p) {
   d.gamma = p.mobility / (p.tau_g - 0.5);
   d.coll = 0;
   d.inv_tau_s = d.inv_tau_b = d.inv_tau_ghost = d.inv_tau_f;
+  d.mob = p.mobility;
   return d;
 }
 
@@ -396,6 +400,18 @@ int one_step(lb_ctx* h, int mode) {
   const Geom& G = h->G;
   int rc;
   const bool peer = h->halo_mode == 1 && !G.zwrap;
+  if (h->ch && mode >= 0) {
+    Slab& s = h->slabs[0];
+    CK(h, timed(h, K_STEP, true, [&]() {
+         return launch_step_ch(G, h->dp, s.A, s.B, s.phi, s.phi2, h->zc, h->d_flag, &s.chA, h->stream);
+       }));
+    std::swap(s.A, s.B);
+    std::swap(s.mapsA, s.mapsB);
+    std::swap(s.cmapsA, s.cmapsB);
+    std::swap(s.chA, s.chB);
+    std::swap(s.phi, s.phi2);
+    return LB_OK;
+  }
   if (mode < 0) {
     for (int r = 0; r < h->nslabs; ++r) {
       Slab& s = h->slabs[r];
@@ -600,6 +616,7 @@ size_t lb_local_sites(const lb_t* h) { return h ? host_nloc(h) : 0; }
 int lb_set_state(lb_t* h, const double* f, const double* g) {
   int rc = usable(h);
   if (rc) return rc;
+  if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle holds (f, phi): use lb_set_state_ch");
   if (!f || !g) return set_err(h, LB_EINVAL, "f or g is NULL");
   const Geom& G = h->G;
   const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
@@ -619,6 +636,7 @@ int lb_set_state(lb_t* h, const double* f, const double* g) {
 int lb_get_state(lb_t* h, double* f, double* g) {
   int rc = usable(h);
   if (rc) return rc;
+  if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle holds (f, phi): use lb_get_state_ch");
   if (!f || !g) return set_err(h, LB_EINVAL, "f or g is NULL");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
   const Geom& G = h->G;
@@ -671,6 +689,7 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
   int rc = usable(h);
   if (rc) return rc;
   if (nsteps < 0 || mode < 1 || mode > 4) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2, 3, 4} required");
+  if (h->ch) return set_err(h, LB_EINVAL, "no memory probes for a Cahn-Hilliard handle");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
   for (int t = 0; t < nsteps; ++t)
     if ((rc = one_step(h, mode))) return rc;
@@ -678,6 +697,7 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
 }
 
 int lb_debug_step_kernel(lb_t* h, int which) {
+  if (h && h->ch && which != 0) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle has one step kernel");
   if (!h || which < 0 || which > 4)
     return set_err(h, LB_EINVAL,
                    "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised) or 4 (persistent warp-specialised)");
@@ -710,7 +730,8 @@ int lb_get_phi(lb_t* h, double* phi) {
   const size_t nloc = (size_t)G.nxy * G.nzl;
   for (int r = 0; r < h->nslabs; ++r) {
     Slab& s = h->slabs[r];
-    CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, G.nzl, h->stream); }));
+    if (!h->ch)  // phi = sum g; a Cahn-Hilliard handle holds phi itself
+      CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, G.nzl, h->stream); }));
     CK(h, cudaMemcpyAsync(phi + r * nloc, s.phi + phi_plane_index(G, 0), nloc * 8, cudaMemcpyDeviceToHost, h->stream));
   }
   CK(h, cudaStreamSynchronize(h->stream));
@@ -728,6 +749,7 @@ void lb_destroy(lb_t* h) {
     cudaFree(s.A);
     cudaFree(s.B);
     cudaFree(s.phi);
+    cudaFree(s.phi2);
   }
   cudaFree(h->d_flag);
   cudaFree(h->wctr.dev);
@@ -812,9 +834,71 @@ int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out) {
   return LB_OK;
 }
 
+int lb_create_ch(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk, double tau_ghost,
+                 lb_t** out) {
+  if (nx % 2 != 0) return set_err(nullptr, LB_EINVAL, "the Cahn-Hilliard variant needs nx even (TMA rows)");
+  for (double t : {tau_shear, tau_bulk, tau_ghost})
+    if (!std::isfinite(t) || !(t > 0.5)) return set_err(nullptr, LB_EINVAL, "MRT relaxation times must be finite and > 0.5");
+  int rc = create_common(nx, ny, nz, params, 1, 0, 1, out);
+  if (rc) return rc;
+  lb_ctx* h = *out;
+  h->ch = true;
+  h->dp.coll = 1;
+  h->dp.inv_tau_s = 1.0 / tau_shear;
+  h->dp.inv_tau_b = 1.0 / tau_bulk;
+  h->dp.inv_tau_ghost = 1.0 / tau_ghost;
+  Slab& s = h->slabs[0];
+  cudaError_t e = cudaMalloc(&s.phi2, phi_doubles(h->G) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(s.phi2, 0xff, phi_doubles(h->G) * sizeof(double), h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess || !make_ch_maps(h->G, s.A, h->ty, &s.chA) || !make_ch_maps(h->G, s.B, h->ty, &s.chB)) {
+    g_create_error = "Cahn-Hilliard handle: allocation or TMA descriptor failed";
+    lb_destroy(h);
+    *out = nullptr;
+    return e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA;
+  }
+  return LB_OK;
+}
+
+int lb_set_state_ch(lb_t* h, const double* f, const double* phi) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (!h->ch) return set_err(h, LB_EINVAL, "not a Cahn-Hilliard handle");
+  if (!f || !phi) return set_err(h, LB_EINVAL, "f or phi is NULL");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl;
+  Slab& s = h->slabs[0];
+  CK(h, cudaMemcpyAsync(s.B, f, Q * nloc * 8, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemsetAsync(s.B + Q * nloc, 0, Q * nloc * 8, h->stream));  // the g slots are not used
+  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_canon_to_planes(G, s.B, s.A, h->stream); }));
+  CK(h, cudaMemcpyAsync(s.phi + phi_plane_index(G, 0), phi, nloc * 8, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  h->have_state = true;
+  return LB_OK;
+}
+
+int lb_get_state_ch(lb_t* h, double* f, double* phi) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (!h->ch) return set_err(h, LB_EINVAL, "not a Cahn-Hilliard handle");
+  if (!f || !phi) return set_err(h, LB_EINVAL, "f or phi is NULL");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state_ch or lb_init_equilibrium first");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl;
+  Slab& s = h->slabs[0];
+  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_planes_to_canon(G, s.A, s.B, h->stream); }));
+  CK(h, cudaMemcpyAsync(f, s.B, Q * nloc * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(phi, s.phi + phi_plane_index(G, 0), nloc * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  return LB_OK;
+}
+
 int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, double tau_ghost) {
   int rc = usable(h);
   if (rc) return rc;
+  if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle's collision is fixed at lb_create_ch");
   if (model == 0) {
     h->dp.coll = 0;
     return LB_OK;

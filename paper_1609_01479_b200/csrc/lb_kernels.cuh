@@ -21,6 +21,7 @@ struct DevParams {
   // 1 = chemical stress in f^eq + three-rate MRT (NEXT-3, R23-R26)
   int coll;
   double inv_tau_s, inv_tau_b, inv_tau_ghost;  // MRT rates (coll 1)
+  double mob;  // M itself: the finite-difference Cahn-Hilliard variant (R30)
 };
 
 // Geometry of one z-slab as the kernels see it.
@@ -133,6 +134,16 @@ bool step_ws_fits(const StepMaps* maps);
 cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                            int* flag, const StepMaps* mapsA, cudaStream_t st, const Peers& pr, WorkCounter* wc,
                            bool persist);
+// the finite-difference Cahn-Hilliard variant (lb_step_ch.cu, NEXT-2): state f and
+// a phi field; one TMA map (f box of one component, (32+4) x (ty+2)); one slab
+struct alignas(64) ChMaps {
+  unsigned char m[128];
+  int ty;
+  bool ok;
+};
+bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out);
+cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
+                           double* phiB, int zc, int* flag, const ChMaps* mapsA, cudaStream_t st);
 // the cluster variant of the step (lb_step_cluster.cu): phi halos shared through
 // distributed shared memory; for nx % 64 == 0 and ny % 16 == 0
 struct alignas(64) ClusterMaps {

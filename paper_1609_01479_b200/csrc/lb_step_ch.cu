@@ -1,0 +1,290 @@
+// lb_step_ch.cu -- the NEXT-2 variant of the step (DESIGN.md readings
+// R29-R33): phi is a field evolved by a finite-difference Cahn-Hilliard update
+// with first-order upwind advective fluxes, instead of the g distribution
+// ("Advection" and the finite-difference order-parameter update of Ludwig,
+// PAPER.md P:176-183); f collides with the chemical stress in its
+// equilibrium and a three-rate MRT (R23-R25, `collide_mrt`), so u = j / rho.
+//
+// One fused single pass per step, like the main step kernel: per site f is read
+// and written once (304 B) and phi read and written once (16 B) -- 320 B/site
+// instead of 608.  A CTA owns a TX x TY tile and marches in z:
+//
+//   sF  : f of planes k and k+1 on the tile + 1-site halo (TMA, one copy per
+//         component into 128-byte-aligned slots; per-thread 16-byte cp.async
+//         where the halo wraps), two buffers
+//   sPhi: ring of 5 phi planes on the tile + 2-site halo (cp.async)
+//   sU  : ring of 3 planes of u = j / rho on the tile + 1 halo (R32)
+//   sMu : ring of 3 planes of mu on the tile + 1 halo (R3)
+//
+// Iteration k: wait f(k+1), phi(k+2) -> u(k+1), mu(k+1) on the halo box; f(k)
+// to registers; issue f(k+2), phi(k+3); P(k) at the site (R4); collide f and
+// push (A.8); phi(k+1 step) = phi - div J + M lap mu (R30, R31) -> next phi
+// buffer.  Single periodic slab (the slab transport of this variant would also
+// have to carry f's edge planes for u at z +- 1: not built).
+#include "lb_device.cuh"
+#include "lb_tma.cuh"
+
+namespace lbk {
+namespace {
+
+constexpr int kCX = 32;
+
+__device__ __forceinline__ int cmod(int z, int n) {
+  const int s = z % n;
+  return s < 0 ? s + n : s;
+}
+
+template <int TY>
+struct alignas(128) ChSmem {
+  static constexpr int TX = kCX, NT = TX * TY;
+  static constexpr int FX = TX + 4, FY = TY + 2;              // f box: x0-2 .. x0+TX+1 (16-byte start), y +- 1
+  static constexpr int FS = ((FX * FY + 15) / 16) * 16;       // component slot, 128-byte multiple
+  static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: +- 2
+  static constexpr int UX = TX + 2, UY = TY + 2, NU = UX * UY;  // u, mu box: +- 1
+  alignas(128) double sF[2][Q][FS];
+  alignas(128) double sPhi[5][NB];
+  double sU[3][3][NU];
+  double sMu[3][NU];
+  unsigned long long bar[2];
+};
+
+template <int TY>
+__global__ void __launch_bounds__(kCX* TY, 1)
+    k_step_ch(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
+              const double* __restrict__ phiA, double* __restrict__ phiB, int zc, int* __restrict__ flag,
+              const __grid_constant__ CUtensorMap tm_f1) {
+  using S = ChSmem<TY>;
+  constexpr int TX = kCX, NT = S::NT;
+  constexpr int FX = S::FX, FY = S::FY, FS = S::FS, BX = S::BX, NB = S::NB, UX = S::UX, NU = S::NU;
+  constexpr unsigned FBOX_BYTES = Q * FX * FY * 8;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int lx = tid % TX, ly = tid / TX;
+  const int ntx = (G.nx + TX - 1) / TX, nty = (G.ny + TY - 1) / TY;
+  const int tile = blockIdx.x % (ntx * nty);
+  const int x0 = (tile % ntx) * TX, y0 = (tile / ntx) * TY;
+  const int zA = (blockIdx.x / (ntx * nty)) * zc;
+  const int zB = min(zA + zc, G.nzl);
+  const int x = x0 + lx, y = y0 + ly;
+  const bool active = x < G.nx && y < G.ny;
+  const long long nxy = G.nxy;
+  const bool fbox_tma = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 1 && y0 + TY + 1 <= G.ny;
+
+  auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
+  auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
+  auto wz = [&](int z) { return cmod(z, G.nzl); };
+
+  if (tid == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  unsigned ph[2] = {0, 0};
+  const unsigned long long pol_f = policy_evict_last();  // the halo rows are re-read by the neighbours
+
+  // ---- f box of plane zp -> buffer zp & 1 (TMA per component, or per-thread copies)
+  constexpr int FROWU = FX / 2, FBU = FY * FROWU, FBR = (FBU + NT - 1) / NT;
+  long long fb_src[FBR];
+  int fb_dst[FBR];
+#pragma unroll
+  for (int r = 0; r < FBR; ++r) {
+    const int u = tid + r * NT;
+    const int row = u / FROWU, cu = u - row * FROWU;
+    fb_src[r] = (long long)wrapy(y0 - 1 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
+    fb_dst[r] = u < FBU ? row * FX + cu * 2 : -1;
+  }
+  auto issue_f = [&](int zp) {
+    const int b = zp & 1;
+    const int zs = wz(zp);
+    if (fbox_tma) {
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&sm.bar[b], FBOX_BYTES);
+        const int cpl = (zs + GZ) * NSLOT;
+#pragma unroll 1
+        for (int j = 0; j < Q; ++j)
+          tma_load_3d(&sm.sF[b][j][0], &tm_f1, x0 - 2, y0 - 1, cpl + fslot_of_rank(j), &sm.bar[b], pol_f);
+      }
+    } else {
+      const double* base = A + (long long)(zs + GZ) * G.plane;
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const double* bj = base + (long long)fslot_of_rank(j) * nxy;
+#pragma unroll
+        for (int r = 0; r < FBR; ++r)
+          if (fb_dst[r] >= 0) cp_async_v<2>(&sm.sF[b][j][fb_dst[r]], bj + fb_src[r]);
+      }
+    }
+  };
+  auto wait_f = [&](int zp) {
+    const int b = zp & 1;
+    if (fbox_tma) {
+      mbar_wait(&sm.bar[b], ph[b]);
+      ph[b] ^= 1;
+    }
+  };
+  // ---- phi box of plane zp -> ring slot zp % 5 (per-thread 16-byte copies)
+  constexpr int PROWU = BX / 2, PBU = (TY + 4) * PROWU, PBR = (PBU + NT - 1) / NT;
+  long long pb_src[PBR];
+  int pb_dst[PBR];
+#pragma unroll
+  for (int r = 0; r < PBR; ++r) {
+    const int u = tid + r * NT;
+    const int row = u / PROWU, cu = u - row * PROWU;
+    pb_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
+    pb_dst[r] = u < PBU ? row * BX + cu * 2 : -1;
+  }
+  auto issue_phi = [&](int zp) {
+    const double* base = phiA + phi_plane_index(G, wz(zp));
+    double* ring = sm.sPhi[cmod(zp, 5)];
+#pragma unroll
+    for (int r = 0; r < PBR; ++r)
+      if (pb_dst[r] >= 0) cp_async_v<2>(&ring[pb_dst[r]], base + pb_src[r]);
+  };
+
+  // ---- u and mu of plane zp on the +-1 box (needs f box zp, phi zp-1 .. zp+1)
+  auto make_u_mu = [&](int zp) {
+    const double(*fb)[FS] = sm.sF[zp & 1];
+    double(*u3)[NU] = sm.sU[cmod(zp, 3)];
+    double* mu = sm.sMu[cmod(zp, 3)];
+    const double* f0 = sm.sPhi[cmod(zp - 1, 5)];
+    const double* f1 = sm.sPhi[cmod(zp, 5)];
+    const double* f2 = sm.sPhi[cmod(zp + 1, 5)];
+    for (int e = tid; e < NU; e += NT) {
+      const int ex = e % UX, ey = e / UX;
+      const int fi = ey * FX + ex + 1;  // f box: x offset 2, y offset 1; u box: offsets 1, 1
+      double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {  // A.3, canonical order
+        const double v = fb[frank(i)][fi];
+        rho += v;
+        if (cx(i)) jx += cx(i) * v;
+        if (cy(i)) jy += cy(i) * v;
+        if (cz(i)) jz += cz(i) * v;
+      }
+      const double rinv = 1.0 / rho;
+      u3[0][e] = jx * rinv;  // R32
+      u3[1][e] = jy * rinv;
+      u3[2][e] = jz * rinv;
+      const int c = (ey + 1) * BX + (ex + 1);
+      const double phc = f1[c];
+      const double lap = (f1[c + 1] + f1[c - 1]) + (f1[c + BX] + f1[c - BX]) + (f2[c] + f0[c]) - 6.0 * phc;
+      mu[e] = chem_pot(p, phc, lap);
+    }
+  };
+
+  // ---- prologue: phi zA-2 .. zA+1, f boxes zA-1, zA; u, mu of zA-1 and zA
+  for (int zp = zA - 2; zp <= zA + 1; ++zp) issue_phi(zp);
+  issue_f(zA - 1);
+  issue_f(zA);
+  cp_commit();
+  cp_wait<0>();
+  wait_f(zA - 1);
+  __syncthreads();
+  make_u_mu(zA - 1);
+  __syncthreads();
+  issue_f(zA + 1);  // into the buffer of zA - 1
+  issue_phi(zA + 2);
+  cp_commit();
+  wait_f(zA);
+  __syncthreads();
+  make_u_mu(zA);
+
+  const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
+  const int cb = (ly + 2) * BX + (lx + 2);  // own site in the phi box
+  const int cu = (ly + 1) * UX + (lx + 1);  // own site in the u / mu box
+  const int cf = (ly + 1) * FX + (lx + 2);  // own site in the f box
+
+  for (int k = zA; k < zB; ++k) {
+    cp_wait<0>();  // phi(k+2)
+    wait_f(k + 1);
+    __syncthreads();  // (also: everyone is past iteration k-1)
+    make_u_mu(k + 1);
+    double f[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = sm.sF[k & 1][frank(i)][cf];
+    __syncthreads();  // f(k) consumed, u / mu (k+1) written
+    if (k + 2 <= zB) issue_f(k + 2);
+    if (k + 3 <= zB + 1) issue_phi(k + 3);
+    cp_commit();
+    if (!active) continue;
+    // P(k) at the site (R4, A.2)
+    const double* r0 = sm.sPhi[cmod(k, 5)];
+    const double* rm = sm.sPhi[cmod(k - 1, 5)];
+    const double* rp = sm.sPhi[cmod(k + 1, 5)];
+    const double ph = r0[cb];
+    const double xp = r0[cb + 1], xm = r0[cb - 1], yp = r0[cb + BX], ym = r0[cb - BX], zp = rp[cb], zm = rm[cb];
+    const double lap = (xp + xm) + (yp + ym) + (zp + zm) - 6.0 * ph;
+    double P6[6];
+    stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp - zm), lap, P6);
+    // collide f (R23-R25) and push (A.8); g is not used in this variant
+    const long long zoff[3] = {(long long)wz(k - 1) + GZ, (long long)k + GZ, (long long)wz(k + 1) + GZ};
+    const double g0[Q] = {};
+    const double rho = collide_mrt(p, f, g0, 0.0, 0.0, P6, [&](int i, double fs, double) {
+      const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
+      const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+      double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;
+      __stcs(d + (long long)slot(0, i) * nxy, fs);
+    });
+    // phi update (R30, R31): upwind fluxes through the six faces, M lap mu
+    const double* uk = &sm.sU[cmod(k, 3)][0][0];
+    const double* ukm = &sm.sU[cmod(k - 1, 3)][0][0];
+    const double* ukp = &sm.sU[cmod(k + 1, 3)][0][0];
+    auto flux = [](double ua, double ub, double pa, double pb) {  // face between a and b = a + e
+      const double uf = 0.5 * (ua + ub);
+      return uf * (uf > 0.0 ? pa : pb);
+    };
+    double div = 0.0;
+    div = div + (flux(uk[cu], uk[cu + 1], ph, xp) - flux(uk[cu - 1], uk[cu], xm, ph));
+    div = div + (flux(uk[NU + cu], uk[NU + cu + UX], ph, yp) - flux(uk[NU + cu - UX], uk[NU + cu], ym, ph));
+    div = div + (flux(uk[2 * NU + cu], ukp[2 * NU + cu], ph, zp) - flux(ukm[2 * NU + cu], uk[2 * NU + cu], zm, ph));
+    const double* mk = sm.sMu[cmod(k, 3)];
+    const double lapmu = (mk[cu + 1] + mk[cu - 1]) + (mk[cu + UX] + mk[cu - UX]) +
+                         (sm.sMu[cmod(k + 1, 3)][cu] + sm.sMu[cmod(k - 1, 3)][cu]) - 6.0 * mk[cu];
+    const double phn = (ph - div) + p.mob * lapmu;
+    phiB[phi_plane_index(G, k) + (long long)y * G.nx + x] = phn;
+    if (!(rho > 0.0) || !isfinite(rho) || !isfinite(phn)) *flag = 1;  // R22
+  }
+  cp_wait<0>();
+}
+
+template <int TY>
+cudaError_t launch_ch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
+                        double* phiB, int zc, int* flag, const ChMaps* maps, cudaStream_t st) {
+  constexpr size_t smem = sizeof(ChSmem<TY>);
+  static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
+  auto kern = k_step_ch<TY>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = ((G.nx + kCX - 1) / kCX) * ((G.ny + TY - 1) / TY);
+  const int nblk = tiles * ((G.nzl + zc - 1) / zc);
+  kern<<<nblk, kCX * TY, smem, st>>>(G, p, A, B, phiA, phiB, zc, flag, *reinterpret_cast<const CUtensorMap*>(maps->m));
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out) {
+  out->ok = false;
+  out->ty = ty;
+  if (G.nx % 2 != 0) return false;
+  if (!encode_dist_map(reinterpret_cast<CUtensorMap*>(out->m), G, buf, kCX + 4, ty + 2, 1)) return false;
+  out->ok = true;
+  return true;
+}
+
+cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
+                           double* phiB, int zc, int* flag, const ChMaps* maps, cudaStream_t st) {
+  if (!maps || !maps->ok || !G.zwrap) return cudaErrorInvalidValue;
+  if (maps->ty == 8) return launch_ch_t<8>(G, p, A, B, phiA, phiB, zc, flag, maps, st);
+  return launch_ch_t<4>(G, p, A, B, phiA, phiB, zc, flag, maps, st);
+}
+
+}  // namespace lbk

@@ -76,13 +76,17 @@ _lb_debug_propagation_map_peers = _sig("lb_debug_propagation_map_peers", _i, _i,
 _lb_debug_halo_mode = _sig("lb_debug_halo_mode", _i, _vp, _i)
 _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
 _lb_set_collision = _sig("lb_set_collision", _i, _vp, _i, C.c_double, C.c_double, C.c_double)
+_lb_create_ch = _sig("lb_create_ch", _i, _i, _i, _i, C.POINTER(lb_params), C.c_double, C.c_double, C.c_double,
+                     C.POINTER(_vp))
+_lb_set_state_ch = _sig("lb_set_state_ch", _i, _vp, _vp, _vp)
+_lb_get_state_ch = _sig("lb_get_state_ch", _i, _vp, _vp, _vp)
 
 EXPORTS = [
     "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
-    "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision",
+    "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_set_state_ch", "lb_get_state_ch",
 ]
 
 
@@ -244,6 +248,25 @@ def lb_set_collision(h, model: int, tau_shear: float = 0.8, tau_bulk: float = 1.
     _check(_lb_set_collision(h, model, tau_shear, tau_bulk, tau_ghost), h)
 
 
+def lb_create_ch(nx: int, ny: int, nz: int, params: lb_params, tau_shear=0.8, tau_bulk=1.1, tau_ghost=1.0):
+    h = _vp()
+    _check(_lb_create_ch(nx, ny, nz, C.byref(params), tau_shear, tau_bulk, tau_ghost, C.byref(h)), None)
+    return h.value
+
+
+def lb_set_state_ch(h, f, phi) -> None:
+    n = lb_local_sites(h)
+    _check(_lb_set_state_ch(h, _ptr(f, Q * n), _ptr(phi, n)), h)
+
+
+def lb_get_state_ch(h, f=None, phi=None):
+    n = lb_local_sites(h)
+    f = np.empty(Q * n) if f is None else f
+    phi = np.empty(n) if phi is None else phi
+    _check(_lb_get_state_ch(h, _ptr(f, Q * n, True), _ptr(phi, n, True)), h)
+    return f, phi
+
+
 def lb_debug_halo_mode(h, mode: int = -1) -> int:
     """-1: query (returns 0 exchange / 1 peer); 0 or 1: set (returns 0)."""
     rc = _lb_debug_halo_mode(h, mode)
@@ -306,3 +329,20 @@ class Lattice:
 
     def get_phi(self):
         return lb_get_phi(self.h).reshape(self.shape)
+
+
+class ChLattice(Lattice):
+    """A finite-difference Cahn-Hilliard handle (lb_create_ch): state (f, phi)."""
+
+    def __init__(self, nx, ny, nz, params: lb_params | None = None, tau_shear=0.8, tau_bulk=1.1, tau_ghost=1.0):
+        self.params = params or make_params()
+        self.h = lb_create_ch(nx, ny, nz, self.params, tau_shear, tau_bulk, tau_ghost)
+        self.shape = (nz, ny, nx)
+
+    def set_state(self, f, phi):
+        lb_set_state_ch(self.h, np.ascontiguousarray(f, dtype=np.float64).reshape(-1),
+                        np.ascontiguousarray(phi, dtype=np.float64).reshape(-1))
+
+    def get_state(self):
+        f, phi = lb_get_state_ch(self.h)
+        return f.reshape((Q,) + self.shape), phi.reshape(self.shape)

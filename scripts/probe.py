@@ -26,9 +26,25 @@ def main():
     ap.add_argument("--ab", default="", help="interleaved A/B of step kernels, e.g. 1,3 (lb_debug_step_kernel)")
     ap.add_argument("--rounds", type=int, default=20)
     ap.add_argument("--mrt", action="store_true", help="collision model 1 (stress in f^eq, MRT)")
+    ap.add_argument("--ch", action="store_true", help="the finite-difference Cahn-Hilliard variant (lb_create_ch)")
     a = ap.parse_args()
     nx, ny, nzf, _, desc = bench.CONFIGS[a.config]
     nz = nzf(1)
+    if a.ch:
+        L = lb.ChLattice(nx, ny, nz)
+        L.init_equilibrium(synth.spinodal_phi(nx, ny, nz))
+        st = torch.cuda.ExternalStream(lb.lb_stream(L.h))
+        L.step(3)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        L.step(a.steps)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.steps
+        print(json.dumps({"config": a.config, "ch_mlups": nx * ny * nz / ms / 1e3, "gbs_320": nx * ny * nz * 320 / ms / 1e6}))
+        L.close()
+        return
     L = lb.Lattice(nx, ny, nz)
     L.init_equilibrium(synth.spinodal_phi(nx, ny, nz))
     stream = torch.cuda.ExternalStream(lb.lb_stream(L.h))

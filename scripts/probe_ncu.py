@@ -22,4 +22,8 @@ for mode in (1, 2, 3, 4):
 lb.lb_debug_step_kernel(L.h, 3)
 L.step(1)
 L.close()
+L = lb.ChLattice(nx, ny, nz)
+L.init_equilibrium(synth.spinodal_phi(nx, ny, nz))
+L.step(2)
+L.close()
 print("ok")
