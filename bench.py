@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "lattice site updates/s (MLUPS) and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
 BYTES_PER_SITE = 608.0  # f and g (38 fp64) read once and written once
+BYTES_PER_SITE_CH = 320.0  # NEXT-2: f (19 fp64) and phi read once and written once
 
 # name: (nx, ny, nz_global(N), scaling, description)
 CONFIGS = {
@@ -59,8 +60,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--collision", default="bgk", choices=["bgk", "mrt"],
-                    help="bgk: BGK + Guo force (the paper path, default); mrt: stress in f^eq + MRT (NEXT-3)")
+    ap.add_argument("--collision", default="bgk", choices=["bgk", "mrt", "ch"],
+                    help="bgk: BGK + Guo force (the paper path, default); mrt: stress in f^eq + MRT (NEXT-3); "
+                         "ch: phi by finite-difference Cahn-Hilliard instead of g, f as mrt (NEXT-2)")
     return ap.parse_args()
 
 
@@ -160,7 +162,20 @@ def oracle_stepper(collision: str):
     if collision == "mrt":
         p = M.MrtParams(base=R.Params(), tau_s=0.8, tau_b=1.1, tau_ghost=1.0)
         return "oracle/lb_mrt.py", M.step, M.run, p
+    if collision == "ch":
+        from oracle import lb_ch as CH
+
+        return "oracle/lb_ch.py", CH.step, CH.run, CH.ChParams(base=R.Params(), tau_s=0.8, tau_b=1.1, tau_ghost=1.0)
     return "oracle/lb_ref.py", R.step, R.run, R.Params()
+
+
+def oracle_state(rho, u, phi, collision: str):
+    """Initial state of the oracle: (f, g) at equilibrium, or (f, phi) for the ch variant."""
+    from oracle import lb_ref as R
+
+    if collision == "ch":
+        return R.f_equilibrium(rho, u), phi
+    return R.equilibrium_state(rho, u, phi, R.Params())
 
 
 def time_oracle(nx, ny, steps: int, seed: int = 0, collision: str = "bgk"):
@@ -171,7 +186,7 @@ def time_oracle(nx, ny, steps: int, seed: int = 0, collision: str = "bgk"):
     _, step, run, p = oracle_stepper(collision)
     sx, sy, sz = oracle_sample_shape(nx, ny, 262144)
     rho, u, phi = synth.spinodal_fields(sx, sy, sz, seed)
-    f, g = R.equilibrium_state(rho, u, phi, R.Params())
+    f, g = oracle_state(rho, u, phi, collision)
     step(f, g, p)  # warm
     t0 = time.perf_counter()
     f, g = run(f, g, p, steps)
@@ -190,7 +205,7 @@ def run_reference(args):
 
     name, _, run, p = oracle_stepper(args.collision)
     rho, u, phi = synth.spinodal_fields(sx, sy, sz, 0)
-    f, g = R.equilibrium_state(rho, u, phi, R.Params())
+    f, g = oracle_state(rho, u, phi, args.collision)
     f, g = run(f, g, p, max(args.warmup, 0))
     t0 = time.perf_counter()
     f, g = run(f, g, p, args.steps)
@@ -235,7 +250,13 @@ def run_ours(args):
     uid = None
     if world > 1:
         uid = D.broadcast_bytes(lb.lb_nccl_get_unique_id() if rank == 0 else None)
-    L = lb.Lattice(nx, ny, nz, params, nranks=world, rank=rank, uid=uid)
+    if args.collision == "ch":
+        if world > 1:
+            raise SystemExit("--collision ch: the Cahn-Hilliard variant is single-slab (one GPU)")
+        L = lb.ChLattice(nx, ny, nz, params, 0.8, 1.1, 1.0)
+    else:
+        L = lb.Lattice(nx, ny, nz, params, nranks=world, rank=rank, uid=uid)
+    bps = BYTES_PER_SITE_CH if args.collision == "ch" else BYTES_PER_SITE
     if args.collision == "mrt":
         lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
     halo = ("peer (fused P2P stores)" if lb.lb_debug_halo_mode(L.h) == 1 else "NCCL send/recv") if world > 1 else None
@@ -273,9 +294,9 @@ def run_ours(args):
     peak, peak_src = peaks()
     ks_ms, ks_n = prof.get("k_step", (0.0, 0))
     ks_avg = D.max_over_ranks(ks_ms / max(ks_n, 1))
-    achieved = BYTES_PER_SITE * nloc / (ks_avg * 1e-3) / 1e9
-    step_gbs = value * 1e6 * BYTES_PER_SITE / world / 1e9  # per GPU, algorithmic, whole step
-    traffic = ncu_traffic("k_step", args.config)
+    achieved = bps * nloc / (ks_avg * 1e-3) / 1e9
+    step_gbs = value * 1e6 * bps / world / 1e9  # per GPU, algorithmic, whole step
+    traffic = ncu_traffic("k_step", args.config if args.collision == "bgk" else f"{args.config}-{args.collision}")
     kernel_share = {k: round(v[0] / max(sum(x[0] for x in prof.values()), 1e-30), 4) for k, v in prof.items() if v[1]}
 
     # ---- e2e: the same metric through the public C ABI with pinned HOST buffers:
@@ -284,24 +305,29 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         Ke = min(K, 5)
+        ch = args.collision == "ch"
+        ng = nloc if ch else 19 * nloc  # second array: phi (ch) or g
         fh = torch.empty(19 * nloc, dtype=torch.float64, pin_memory=True)
-        gh = torch.empty(19 * nloc, dtype=torch.float64, pin_memory=True)
-        lb.lb_get_state(L.h, fh, gh)
+        gh = torch.empty(ng, dtype=torch.float64, pin_memory=True)
+        set_state, get_state = (lb.lb_set_state_ch, lb.lb_get_state_ch) if ch else (lb.lb_set_state, lb.lb_get_state)
+        get_state(L.h, fh, gh)
         D.barrier()
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         for _ in range(Ke):
-            lb.lb_set_state(L.h, fh, gh)
+            set_state(L.h, fh, gh)
             lb.lb_step(L.h, 1)
-            lb.lb_get_state(L.h, fh, gh)
+            get_state(L.h, fh, gh)
         a1.record(stream)
         torch.cuda.synchronize()
         D.barrier()
         ems = D.max_over_ranks(a0.elapsed_time(a1))
+        nbytes = 8 * (19 * nloc + ng)
         e2e = {"value": sites_total * Ke / (ems * 1e-3) / 1e6, "unit": "MLUPS",
-               "h2d_bytes_per_step": 2 * 19 * 8 * nloc, "d2h_bytes_per_step": 2 * 19 * 8 * nloc, "steps": Ke,
-               "mode": "per step: lb_set_state(pinned host f,g) + lb_step(1) + lb_get_state(pinned host f,g)"}
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": Ke,
+               "mode": "per step: lb_set_state%s(pinned host state) + lb_step(1) + lb_get_state%s(pinned host state)"
+                       % (("_ch", "_ch") if ch else ("", ""))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -318,8 +344,10 @@ def run_ours(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "lattice": [nx, ny, nz], "sites_per_gpu": nloc,
                        "parallelism": f"z-slab x{world}" + (f" ({halo} halos)" if world > 1 else ""),
-                       "collision": ("BGK + Guo force F = -div P (paper path)" if args.collision == "bgk" else
-                                     "chemical stress in f^eq, MRT tau_s 0.8 / tau_b 1.1 / tau_ghost 1.0 (NEXT-3)"),
+                       "collision": {"bgk": "BGK + Guo force F = -div P (paper path)",
+                                     "mrt": "chemical stress in f^eq, MRT tau_s 0.8 / tau_b 1.1 / tau_ghost 1.0 (NEXT-3)",
+                                     "ch": "phi by finite-difference Cahn-Hilliard + upwind advection (NEXT-2); "
+                                           "f: chemical stress in f^eq, MRT 0.8 / 1.1 / 1.0"}[args.collision],
                        "state_bytes_per_gpu": int(2 * 38 * 8 * nx * ny * (z1 - z0 + 2) + 8 * nx * ny * (z1 - z0 + 4)),
                        "l2": "inputs larger than L2 (state per GPU >> 126 MB)" if nloc * 608 > 126e6 * 2
                        else "state comparable to L2: not an HBM roofline point",
@@ -327,7 +355,7 @@ def run_ours(args):
             "hbm_gbs_step": step_gbs,
             "roofline": {"bound": "hbm", "kernel": "k_step", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_site": BYTES_PER_SITE, "avg_launch_ms": ks_avg,
+                         "bytes_per_site": bps, "avg_launch_ms": ks_avg,
                          "step_frac": step_gbs / peak, "kernel_time_share": kernel_share},
             "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "src_hash": src_hash(),
         }
