@@ -34,18 +34,21 @@ __device__ __forceinline__ int cmod(int z, int n) {
   return s < 0 ? s + n : s;
 }
 
+// f box buffers: 3 (the box of plane k+2 goes out while plane k is collided: two
+// iterations of lead) where shared memory allows, else 2
 template <int TY>
 struct alignas(128) ChSmem {
+  static constexpr int NBUF = TY == 8 ? 3 : 2;
   static constexpr int TX = kCX, NT = TX * TY;
   static constexpr int FX = TX + 4, FY = TY + 2;              // f box: x0-2 .. x0+TX+1 (16-byte start), y +- 1
   static constexpr int FS = ((FX * FY + 15) / 16) * 16;       // component slot, 128-byte multiple
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: +- 2
   static constexpr int UX = TX + 2, UY = TY + 2, NU = UX * UY;  // u, mu box: +- 1
-  alignas(128) double sF[2][Q][FS];
+  alignas(128) double sF[NBUF][Q][FS];
   alignas(128) double sPhi[5][NB];
   double sU[3][3][NU];
   double sMu[3][NU];
-  unsigned long long bar[2];
+  unsigned long long bar[NBUF];
 };
 
 template <int TY>
@@ -55,7 +58,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
               const __grid_constant__ CUtensorMap tm_f1) {
   using S = ChSmem<TY>;
   constexpr int TX = kCX, NT = S::NT;
-  constexpr int FX = S::FX, FY = S::FY, FS = S::FS, BX = S::BX, NB = S::NB, UX = S::UX, NU = S::NU;
+  constexpr int FX = S::FX, FY = S::FY, FS = S::FS, BX = S::BX, UX = S::UX, NU = S::NU, NBUF = S::NBUF;
   constexpr unsigned FBOX_BYTES = Q * FX * FY * 8;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
@@ -77,15 +80,14 @@ __global__ void __launch_bounds__(kCX* TY, 1)
   auto wz = [&](int z) { return cmod(z, G.nzl); };
 
   if (tid == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
+    for (int b = 0; b < NBUF; ++b) mbar_init(&sm.bar[b], 1);
     fence_barrier_init();
   }
   __syncthreads();
-  unsigned ph[2] = {0, 0};
+  unsigned ph = 0;  // bit b: parity of bar[b]
   const unsigned long long pol_f = policy_evict_last();  // the halo rows are re-read by the neighbours
 
-  // ---- f box of plane zp -> buffer zp & 1 (TMA per component, or per-thread copies)
+  // ---- f box of plane zp -> buffer zp % NBUF (TMA per component, or per-thread copies)
   constexpr int FROWU = FX / 2, FBU = FY * FROWU, FBR = (FBU + NT - 1) / NT;
   long long fb_src[FBR];
   int fb_dst[FBR];
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     fb_dst[r] = u < FBU ? row * FX + cu * 2 : -1;
   }
   auto issue_f = [&](int zp) {
-    const int b = zp & 1;
+    const int b = cmod(zp, NBUF);
     const int zs = wz(zp);
     if (fbox_tma) {
       if (tid == 0) {
@@ -120,10 +122,10 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     }
   };
   auto wait_f = [&](int zp) {
-    const int b = zp & 1;
+    const int b = cmod(zp, NBUF);
     if (fbox_tma) {
-      mbar_wait(&sm.bar[b], ph[b]);
-      ph[b] ^= 1;
+      mbar_wait(&sm.bar[b], (ph >> b) & 1);
+      ph ^= 1u << b;
     }
   };
   // ---- phi box of plane zp -> ring slot zp % 5 (per-thread 16-byte copies)
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
 
   // ---- u and mu of plane zp on the +-1 box (needs f box zp, phi zp-1 .. zp+1)
   auto make_u_mu = [&](int zp) {
-    const double(*fb)[FS] = sm.sF[zp & 1];
+    const double(*fb)[FS] = sm.sF[cmod(zp, NBUF)];
     double(*u3)[NU] = sm.sU[cmod(zp, 3)];
     double* mu = sm.sMu[cmod(zp, 3)];
     const double* f0 = sm.sPhi[cmod(zp - 1, 5)];
@@ -180,13 +182,14 @@ __global__ void __launch_bounds__(kCX* TY, 1)
   for (int zp = zA - 2; zp <= zA + 1; ++zp) issue_phi(zp);
   issue_f(zA - 1);
   issue_f(zA);
+  if (NBUF == 3) issue_f(zA + 1);
   cp_commit();
   cp_wait<0>();
   wait_f(zA - 1);
   __syncthreads();
   make_u_mu(zA - 1);
   __syncthreads();
-  issue_f(zA + 1);  // into the buffer of zA - 1
+  if (NBUF == 2) issue_f(zA + 1);  // into the buffer of zA - 1
   issue_phi(zA + 2);
   cp_commit();
   wait_f(zA);
@@ -202,12 +205,13 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     cp_wait<0>();  // phi(k+2)
     wait_f(k + 1);
     __syncthreads();  // (also: everyone is past iteration k-1)
+    if (NBUF == 3 && k + 2 <= zB) issue_f(k + 2);  // the buffer of plane k-1 is free
     make_u_mu(k + 1);
     double f[Q];
 #pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = sm.sF[k & 1][frank(i)][cf];
+    for (int i = 0; i < Q; ++i) f[i] = sm.sF[cmod(k, NBUF)][frank(i)][cf];
     __syncthreads();  // f(k) consumed, u / mu (k+1) written
-    if (k + 2 <= zB) issue_f(k + 2);
+    if (NBUF == 2 && k + 2 <= zB) issue_f(k + 2);
     if (k + 3 <= zB + 1) issue_phi(k + 3);
     cp_commit();
     if (!active) continue;
