@@ -148,14 +148,14 @@ __global__ void __launch_bounds__(kCX* TY, 1)
   };
 
   // ---- u and mu of plane zp on the +-1 box (needs f box zp, phi zp-1 .. zp+1)
-  auto make_u_mu = [&](int zp) {
+  auto make_u_mu_at = [&](int zp, int e) {
     const double(*fb)[FS] = sm.sF[cmod(zp, NBUF)];
     double(*u3)[NU] = sm.sU[cmod(zp, 3)];
     double* mu = sm.sMu[cmod(zp, 3)];
     const double* f0 = sm.sPhi[cmod(zp - 1, 5)];
     const double* f1 = sm.sPhi[cmod(zp, 5)];
     const double* f2 = sm.sPhi[cmod(zp + 1, 5)];
-    for (int e = tid; e < NU; e += NT) {
+    {
       const int ex = e % UX, ey = e / UX;
       const int fi = ey * FX + ex + 1;  // f box: x offset 2, y offset 1; u box: offsets 1, 1
       double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
@@ -176,6 +176,17 @@ __global__ void __launch_bounds__(kCX* TY, 1)
       const double lap = (f1[c + 1] + f1[c - 1]) + (f1[c + BX] + f1[c - BX]) + (f2[c] + f0[c]) - 6.0 * phc;
       mu[e] = chem_pot(p, phc, lap);
     }
+  };
+  auto make_u_mu = [&](int zp) {
+    for (int e = tid; e < NU; e += NT) make_u_mu_at(zp, e);
+  };
+  // the ring of the +-1 box around the tile: rows 0 and UY-1, then columns 0 and UX-1
+  constexpr int NRING = NU - NT;
+  auto ring_site = [&](int r) {
+    if (r < UX) return r;
+    if (r < 2 * UX) return (S::UY - 1) * UX + (r - UX);
+    const int t = r - 2 * UX;
+    return (1 + t / 2) * UX + ((t & 1) ? UX - 1 : 0);
   };
 
   // ---- prologue: phi zA-2 .. zA+1, f boxes zA-1, zA; u, mu of zA-1 and zA
@@ -205,15 +216,28 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     cp_wait<0>();  // phi(k+2)
     wait_f(k + 1);
     __syncthreads();  // (also: everyone is past iteration k-1)
-    if (NBUF == 3 && k + 2 <= zB) issue_f(k + 2);  // the buffer of plane k-1 is free
-    make_u_mu(k + 1);
     double f[Q];
+    if constexpr (NBUF == 3) {
+      // one barrier per plane: the buffer of plane k-1 and the ring slots of k-2 are
+      // free; u, mu (k+1) at this thread's own site are computed by this thread (all
+      // the update of plane k reads of plane k+1), the ring of the box by the first
+      // NRING threads (read only after the next barrier)
+      if (k + 2 <= zB) issue_f(k + 2);
+      if (k + 3 <= zB + 1) issue_phi(k + 3);
+      cp_commit();
+      make_u_mu_at(k + 1, cu);
+      if (tid < NRING) make_u_mu_at(k + 1, ring_site(tid));
 #pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = sm.sF[cmod(k, NBUF)][frank(i)][cf];
-    __syncthreads();  // f(k) consumed, u / mu (k+1) written
-    if (NBUF == 2 && k + 2 <= zB) issue_f(k + 2);
-    if (k + 3 <= zB + 1) issue_phi(k + 3);
-    cp_commit();
+      for (int i = 0; i < Q; ++i) f[i] = sm.sF[cmod(k, NBUF)][frank(i)][cf];
+    } else {
+      make_u_mu(k + 1);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) f[i] = sm.sF[cmod(k, NBUF)][frank(i)][cf];
+      __syncthreads();  // f(k) consumed, u / mu (k+1) written
+      if (k + 2 <= zB) issue_f(k + 2);
+      if (k + 3 <= zB + 1) issue_phi(k + 3);
+      cp_commit();
+    }
     if (!active) continue;
     // P(k) at the site (R4, A.2)
     const double* r0 = sm.sPhi[cmod(k, 5)];
