@@ -9,3 +9,5 @@ timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/b
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 50 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo ncu_launches=$?
 $CMD > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/prof_kstep_c5 $CMD > gpurun_out/ncu2.log 2>&1; echo ncu_full=$?
+timeout 300 python bench.py --collision mrt --steps 100 > gpurun_out/bench_mrt.json 2>/dev/null; echo bench_mrt=$?
+timeout 300 python bench.py --collision ch --steps 100 > gpurun_out/bench_ch.json 2>/dev/null; echo bench_ch=$?

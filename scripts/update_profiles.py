@@ -45,7 +45,7 @@ tr = {"k_step@c5": {
 with open(os.path.join(P, "traffic.json"), "w") as fh:
     json.dump(tr, fh, indent=1)
 print("traffic:", tr)
-for f in ("default", "c3", "c2", "ref"):
+for f in ("default", "c3", "c2", "ref", "mrt", "ch"):
     src = os.path.join(G, f"bench_{f}.json")
     if os.path.exists(src) and os.path.getsize(src) > 0:
         shutil.copy(src, os.path.join(P, f"{tag}_bench_{f}.json"))
