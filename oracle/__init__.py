@@ -15,6 +15,8 @@ lb_mrt    the NEXT-3 collision variant: chemical stress in f's equilibrium,
           three-rate MRT (readings R23-R27)
 lb_ch     the NEXT-2 variant: phi as a field, finite-difference Cahn-Hilliard
           with first-order upwind advection (readings R29-R33)
+lb_lc     the NEXT-4 workload: Landau-de Gennes Q tensor, Beris-Edwards LC
+          update and chemical stress driving the LB fluid (readings R34-R45)
 
 Citations: ``P:NNN`` = PAPER.md line NNN (Gray & Stratford, arXiv 1609.01479);
 ``S:NNN`` = SPEC.md line NNN; ``Rk`` = reading k of the DESIGN.md ledger (the

@@ -69,3 +69,26 @@ def sample_sites(nx: int, ny: int, nz: int, n: int, seed: int = 7) -> list[tuple
     while len(picks) < min(n, nx * ny * nz):
         picks.add((int(r.integers(nx)), int(r.integers(ny)), int(r.integers(nz))))
     return sorted(picks, key=lambda s: (s[2], s[1], s[0]))
+
+
+# ---- NEXT-4 liquid-crystal workload (R45) ------------------------
+def random_directors(nx: int, ny: int, nz: int, seed: int = 0) -> np.ndarray:
+    """Unit vectors n (3, nz, ny, nx), isotropically distributed: three standard
+    normals per site from PCG64 ``default_rng(seed)`` (site-major, canonical
+    site order), divided by their length."""
+    v = _rng(seed).standard_normal((nx * ny * nz, 3))
+    v = v / np.sqrt((v * v).sum(axis=1))[:, None]
+    return np.ascontiguousarray(v.T).reshape(3, nz, ny, nx)
+
+
+def rough_lc_fields(nx: int, ny: int, nz: int, seed: int = 3):
+    """(rho, u, q5, noise_f): a rough liquid-crystal state that exercises every term:
+    the five stored Q components ~ U(-0.3, 0.3), rho = 1 + 0.05 U, |u_a| <= 0.02,
+    f noise of amplitude 1e-3."""
+    r = _rng(seed)
+    shape = (nz, ny, nx)
+    q5 = r.uniform(-0.3, 0.3, size=(5,) + shape)
+    rho = 1.0 + 0.05 * r.random(shape)
+    u = r.uniform(-0.02, 0.02, size=(3,) + shape)
+    noise_f = 1e-3 * r.uniform(-1.0, 1.0, size=(Q,) + shape)
+    return rho, u, q5, noise_f
