@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 METRIC = "lattice site updates/s (MLUPS) and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
 BYTES_PER_SITE = 608.0  # f and g (38 fp64) read once and written once
 BYTES_PER_SITE_CH = 320.0  # NEXT-2: f (19 fp64) and phi read once and written once
+BYTES_PER_SITE_LC = 432.0  # NEXT-4: f (19 fp64), Q (5) and the stored u (3) read once and written once
 
 # name: (nx, ny, nz_global(N), scaling, description)
 CONFIGS = {
@@ -60,9 +61,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--collision", default="bgk", choices=["bgk", "mrt", "ch"],
+    ap.add_argument("--collision", default="bgk", choices=["bgk", "mrt", "ch", "lc"],
                     help="bgk: BGK + Guo force (the paper path, default); mrt: stress in f^eq + MRT (NEXT-3); "
-                         "ch: phi by finite-difference Cahn-Hilliard instead of g, f as mrt (NEXT-2)")
+                         "ch: phi by finite-difference Cahn-Hilliard instead of g, f as mrt (NEXT-2); "
+                         "lc: the liquid-crystal workload, Q tensor by Beris-Edwards + Guo-forced f (NEXT-4)")
     return ap.parse_args()
 
 
@@ -166,13 +168,26 @@ def oracle_stepper(collision: str):
         from oracle import lb_ch as CH
 
         return "oracle/lb_ch.py", CH.step, CH.run, CH.ChParams(base=R.Params(), tau_s=0.8, tau_b=1.1, tau_ghost=1.0)
+    if collision == "lc":
+        from oracle import lb_lc as LC
+
+        return "oracle/lb_lc.py", LC.step, LC.run, LC.LcParams()
     return "oracle/lb_ref.py", R.step, R.run, R.Params()
 
 
-def oracle_state(rho, u, phi, collision: str):
-    """Initial state of the oracle: (f, g) at equilibrium, or (f, phi) for the ch variant."""
+def oracle_state(shape, seed: int, collision: str) -> tuple:
+    """Initial state of the oracle on an (nx, ny, nz) sample: (f, g) at equilibrium on the
+    spinodal phi, (f, phi) for the ch variant, (f, Q, u) of the random-director quench (lc)."""
     from oracle import lb_ref as R
+    from paper_1609_01479_b200 import synth
 
+    sx, sy, sz = shape
+    if collision == "lc":
+        from oracle import lb_lc as LC
+
+        n = synth.random_directors(sx, sy, sz, seed)
+        return LC.initial_state(np.ones((sz, sy, sx)), np.zeros((3, sz, sy, sx)), n, LC.LcParams())
+    rho, u, phi = synth.spinodal_fields(sx, sy, sz, seed)
     if collision == "ch":
         return R.f_equilibrium(rho, u), phi
     return R.equilibrium_state(rho, u, phi, R.Params())
@@ -180,16 +195,12 @@ def oracle_state(rho, u, phi, collision: str):
 
 def time_oracle(nx, ny, steps: int, seed: int = 0, collision: str = "bgk"):
     """The oracle as it stands, 1 thread, on a sample sub-lattice; returns (sites/s, shape)."""
-    from oracle import lb_ref as R
-    from paper_1609_01479_b200 import synth
-
     _, step, run, p = oracle_stepper(collision)
-    sx, sy, sz = oracle_sample_shape(nx, ny, 262144)
-    rho, u, phi = synth.spinodal_fields(sx, sy, sz, seed)
-    f, g = oracle_state(rho, u, phi, collision)
-    step(f, g, p)  # warm
+    sx, sy, sz = oracle_sample_shape(nx, ny, 262144 if collision != "lc" else 65536)
+    st = oracle_state((sx, sy, sz), seed, collision)
+    step(*st, p)  # warm
     t0 = time.perf_counter()
-    f, g = run(f, g, p, steps)
+    st = run(*st, p, steps)
     dt = time.perf_counter() - t0
     return sx * sy * sz * steps / dt, (sx, sy, sz), dt
 
@@ -199,16 +210,14 @@ def run_reference(args):
     if rank != 0:
         return 0
     nx, ny, nzf, scaling, desc = CONFIGS[args.config]
-    sx, sy, sz = oracle_sample_shape(nx, ny, 262144)
-    from oracle import lb_ref as R
-    from paper_1609_01479_b200 import synth
-
+    if args.collision == "lc":
+        desc = desc.replace("binary fluid", "liquid crystal (Q tensor + D3Q19 fluid, NEXT-4)")
+    sx, sy, sz = oracle_sample_shape(nx, ny, 262144 if args.collision != "lc" else 65536)
     name, _, run, p = oracle_stepper(args.collision)
-    rho, u, phi = synth.spinodal_fields(sx, sy, sz, 0)
-    f, g = oracle_state(rho, u, phi, args.collision)
-    f, g = run(f, g, p, max(args.warmup, 0))
+    st = oracle_state((sx, sy, sz), 0, args.collision)
+    st = run(*st, p, max(args.warmup, 0))
     t0 = time.perf_counter()
-    f, g = run(f, g, p, args.steps)
+    st = run(*st, p, args.steps)
     dt = time.perf_counter() - t0
     sites = sx * sy * sz
     v = sites * args.steps / dt / 1e6
@@ -243,6 +252,8 @@ def run_ours(args):
     if world > 1:
         D.init("nccl")
     nx, ny, nzf, scaling, desc = CONFIGS[args.config]
+    if args.collision == "lc":
+        desc = desc.replace("binary fluid", "liquid crystal (Q tensor + D3Q19 fluid, NEXT-4)")
     nz = nzf(world)
     z0, z1 = D.slab_range(nz, world, rank)
     nloc = nx * ny * (z1 - z0)
@@ -250,18 +261,22 @@ def run_ours(args):
     uid = None
     if world > 1:
         uid = D.broadcast_bytes(lb.lb_nccl_get_unique_id() if rank == 0 else None)
+    if args.collision in ("ch", "lc") and world > 1:
+        raise SystemExit(f"--collision {args.collision}: this variant is single-slab (one GPU)")
     if args.collision == "ch":
-        if world > 1:
-            raise SystemExit("--collision ch: the Cahn-Hilliard variant is single-slab (one GPU)")
         L = lb.ChLattice(nx, ny, nz, params, 0.8, 1.1, 1.0)
+    elif args.collision == "lc":
+        L = lb.LcLattice(nx, ny, nz, lb.make_lc_params())  # R44 defaults
     else:
         L = lb.Lattice(nx, ny, nz, params, nranks=world, rank=rank, uid=uid)
-    bps = BYTES_PER_SITE_CH if args.collision == "ch" else BYTES_PER_SITE
+    bps = {"ch": BYTES_PER_SITE_CH, "lc": BYTES_PER_SITE_LC}.get(args.collision, BYTES_PER_SITE)
     if args.collision == "mrt":
         lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
     halo = ("peer (fused P2P stores)" if lb.lb_debug_halo_mode(L.h) == 1 else "NCCL send/recv") if world > 1 else None
-    phi = synth.spinodal_phi_slab(nx, ny, nz, z0, z1, seed=0)
-    L.init_equilibrium(phi)
+    if args.collision == "lc":
+        L.init(synth.random_directors(nx, ny, nz, 0))  # R45: quench from random directors
+    else:
+        L.init_equilibrium(synth.spinodal_phi_slab(nx, ny, nz, z0, z1, seed=0))
 
     W = max(args.warmup, 3)
     K = args.steps
@@ -305,29 +320,28 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         Ke = min(K, 5)
-        ch = args.collision == "ch"
-        ng = nloc if ch else 19 * nloc  # second array: phi (ch) or g
-        fh = torch.empty(19 * nloc, dtype=torch.float64, pin_memory=True)
-        gh = torch.empty(ng, dtype=torch.float64, pin_memory=True)
-        set_state, get_state = (lb.lb_set_state_ch, lb.lb_get_state_ch) if ch else (lb.lb_set_state, lb.lb_get_state)
-        get_state(L.h, fh, gh)
+        # host arrays of the state: (f, g), (f, phi) or (f, Q, u), and the ABI pair
+        sizes = {"ch": (19, 1), "lc": (19, 5, 3)}.get(args.collision, (19, 19))
+        host = [torch.empty(k * nloc, dtype=torch.float64, pin_memory=True) for k in sizes]
+        sfx = {"ch": "_ch", "lc": "_lc"}.get(args.collision, "")
+        set_state, get_state = getattr(lb, "lb_set_state" + sfx), getattr(lb, "lb_get_state" + sfx)
+        get_state(L.h, *host)
         D.barrier()
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         for _ in range(Ke):
-            set_state(L.h, fh, gh)
+            set_state(L.h, *host)
             lb.lb_step(L.h, 1)
-            get_state(L.h, fh, gh)
+            get_state(L.h, *host)
         a1.record(stream)
         torch.cuda.synchronize()
         D.barrier()
         ems = D.max_over_ranks(a0.elapsed_time(a1))
-        nbytes = 8 * (19 * nloc + ng)
+        nbytes = 8 * nloc * sum(sizes)
         e2e = {"value": sites_total * Ke / (ems * 1e-3) / 1e6, "unit": "MLUPS",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": Ke,
-               "mode": "per step: lb_set_state%s(pinned host state) + lb_step(1) + lb_get_state%s(pinned host state)"
-                       % (("_ch", "_ch") if ch else ("", ""))}
+               "mode": f"per step: lb_set_state{sfx}(pinned host state) + lb_step(1) + lb_get_state{sfx}(pinned host state)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -347,11 +361,17 @@ def run_ours(args):
                        "collision": {"bgk": "BGK + Guo force F = -div P (paper path)",
                                      "mrt": "chemical stress in f^eq, MRT tau_s 0.8 / tau_b 1.1 / tau_ghost 1.0 (NEXT-3)",
                                      "ch": "phi by finite-difference Cahn-Hilliard + upwind advection (NEXT-2); "
-                                           "f: chemical stress in f^eq, MRT 0.8 / 1.1 / 1.0"}[args.collision],
-                       "state_bytes_per_gpu": int(2 * 38 * 8 * nx * ny * (z1 - z0 + 2) + 8 * nx * ny * (z1 - z0 + 4)),
+                                           "f: chemical stress in f^eq, MRT 0.8 / 1.1 / 1.0",
+                                     "lc": "liquid crystal (NEXT-4): Landau-de Gennes Q tensor, Beris-Edwards LC update "
+                                           "+ upwind advection, f: BGK + Guo force F = div sigma; quench from random "
+                                           "directors (R45)"}[args.collision],
+                       "state_bytes_per_gpu": int(2 * 38 * 8 * nx * ny * (z1 - z0 + 2) + 8 * nx * ny * (z1 - z0 + 4)
+                                                  + (2 * 8 * 8 * nloc if args.collision == "lc" else 0)),
                        "l2": "inputs larger than L2 (state per GPU >> 126 MB)" if nloc * 608 > 126e6 * 2
                        else "state comparable to L2: not an HBM roofline point",
-                       "params": {"tau_f": 0.8, "tau_g": 1.3, "A": -0.0625, "B": 0.0625, "kappa": 0.04, "M": 0.05}},
+                       "params": ({"tau_f": 0.8, "A0": 0.01, "gamma": 3.2, "kappa": 0.01, "xi": 0.7, "Gamma": 0.3}
+                                  if args.collision == "lc" else
+                                  {"tau_f": 0.8, "tau_g": 1.3, "A": -0.0625, "B": 0.0625, "kappa": 0.04, "M": 0.05})},
             "hbm_gbs_step": step_gbs,
             "roofline": {"bound": "hbm", "kernel": "k_step", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

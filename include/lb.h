@@ -184,6 +184,42 @@ int lb_create_ch(int nx, int ny, int nz, const lb_params* params, double tau_she
 int lb_set_state_ch(lb_t* h, const double* f, const double* phi);
 int lb_get_state_ch(lb_t* h, double* f, double* phi);
 
+/* ---- NEXT-4 workload: the paper's liquid crystal (R34-R45) ----------
+ * "an 'order parameter' field (a 3x3 tensor, which is symmetric and traceless)"
+ * evolved by "a finite difference implementation of the Beris-Edwards model with
+ * the Landau-de Gennes free energy functional" ("LC Update") and its "Advection",
+ * coupled to the LB fluid by "the divergence of the 'Chemical stress'"
+ * (PAPER.md P:158-183).  Per step (R43): grad Q and lap Q (R37); molecular field
+ *   H = -A0 (1 - gamma/3) Q + A0 gamma (Q Q - I Q:Q/3) - A0 gamma (Q:Q) Q + kappa lap Q;
+ * stress sigma (R38, Beris-Edwards, p0 = -f); F = div sigma (R39); Guo BGK of f
+ * with tau_f (R40), whose u' = (j + F/2)/rho becomes the stored velocity; LC update
+ *   Q <- Q - div J + S(W, Q) + Gamma H   (R41, R42: upwind J, W = grad u, stored u);
+ * propagation of f.  State (R34): f canonical (19*nloc), Q by its five components
+ * (xx, xy, xz, yy, yz) as q[c*nloc + s], and the stored velocity u[a*nloc + s].
+ * One periodic lattice on the current GPU; nx even, else LB_EINVAL.  lb_step,
+ * lb_destroy, lb_last_error, lb_stream and the profiling calls work as for other
+ * handles; lb_set_state, lb_get_state, lb_init_equilibrium, lb_get_phi and
+ * lb_set_collision return LB_EINVAL. */
+typedef struct {
+  double tau_f;  /* BGK relaxation time of f, finite and > 1/2                     */
+  double A0;     /* Landau-de Gennes bulk constant, finite                          */
+  double gamma;  /* Landau-de Gennes "temperature" parameter, finite                */
+  double kappa;  /* elastic constant, finite and >= 0                               */
+  double xi;     /* flow-aligning parameter, finite                                 */
+  double Gamma;  /* rotational diffusion constant, finite and >= 0                  */
+} lb_lc_params;
+
+int lb_create_lc(int nx, int ny, int nz, const lb_lc_params* params, lb_t** out);
+/* Host arrays: f 19*nloc, q 5*nloc, u 3*nloc doubles (canonical layouts above);
+ * set/get round trip bitwise. */
+int lb_set_state_lc(lb_t* h, const double* f, const double* q, const double* u);
+int lb_get_state_lc(lb_t* h, double* f, double* q, double* u);
+/* R45 initial state from host fields: f = f^eq(rho, u) (R8), Q = S0 (n n - I/3) with
+ * S0 = 1/4 + 3/4 sqrt(1 - 8/(3 gamma)) (needs gamma > 8/3, else LB_EINVAL), stored
+ * velocity = u.  rho: nloc doubles or NULL (1); u: 3*nloc or NULL (0); n: unit
+ * directors, 3*nloc doubles n[a*nloc + s] (required). */
+int lb_init_lc(lb_t* h, const double* rho, const double* u, const double* n);
+
 /* Collision model of f (readings R23-R27).
  *   model 0 (default, the paper path): BGK of f with tau_f of lb_params and the
  *     Guo force F = -div P (R5, R7); the tau arguments are ignored.

@@ -11,7 +11,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblb.so")
-SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_step_cluster.cu", "lb_step_ws.cu", "lb_step_ch.cu", "lb_api.cu"]
+SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_step_cluster.cu", "lb_step_ws.cu", "lb_step_ch.cu", "lb_step_lc.cu", "lb_api.cu"]
 HEADERS = ["d3q19.cuh", "lb_kernels.cuh", "lb_device.cuh", "lb_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

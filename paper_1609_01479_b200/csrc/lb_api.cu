@@ -34,6 +34,13 @@ struct Slab {
   double* phi = nullptr;
   double* phi2 = nullptr;  // finite-difference Cahn-Hilliard handles: next phi
   ChMaps chA{}, chB{};     // and the TMA descriptors of their f box
+  // liquid-crystal handles (NEXT-4): Q (5 components) and the stored velocity u
+  // (3), current and next, plane-major [z][component][y][x]; f tile maps (32 x 8)
+  double* q = nullptr;
+  double* q2 = nullptr;
+  double* u = nullptr;
+  double* u2 = nullptr;
+  StepMaps lcA{}, lcB{};
   StepMaps mapsA{}, mapsB{};        // TMA descriptors of A and B (swapped with them)
   ClusterMaps cmapsA{}, cmapsB{};  // same, for the cluster step kernel
 };
@@ -61,6 +68,8 @@ struct lb_ctx {
   int ty = 8;             // tile rows of the step kernel
   int czc = 1;            // z-chunk of the cluster step kernel
   bool ch = false;        // NEXT-2 handle: state (f, phi), lb_create_ch
+  bool lc = false;        // NEXT-4 handle: state (f, Q, u), lb_create_lc
+  int lczc = 1;           // z-chunk of the liquid-crystal step kernel
   int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
@@ -400,6 +409,19 @@ int one_step(lb_ctx* h, int mode) {
   const Geom& G = h->G;
   int rc;
   const bool peer = h->halo_mode == 1 && !G.zwrap;
+  if (h->lc && mode >= 0) {
+    Slab& s = h->slabs[0];
+    CK(h, timed(h, K_STEP, true, [&]() {
+         return launch_step_lc(G, h->dp, s.A, s.B, s.q, s.q2, s.u, s.u2, h->lczc, h->d_flag, &s.lcA, h->stream);
+       }));
+    std::swap(s.A, s.B);
+    std::swap(s.mapsA, s.mapsB);
+    std::swap(s.cmapsA, s.cmapsB);
+    std::swap(s.lcA, s.lcB);
+    std::swap(s.q, s.q2);
+    std::swap(s.u, s.u2);
+    return LB_OK;
+  }
   if (h->ch && mode >= 0) {
     Slab& s = h->slabs[0];
     CK(h, timed(h, K_STEP, true, [&]() {
@@ -617,6 +639,7 @@ int lb_set_state(lb_t* h, const double* f, const double* g) {
   int rc = usable(h);
   if (rc) return rc;
   if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle holds (f, phi): use lb_set_state_ch");
+  if (h->lc) return set_err(h, LB_EINVAL, "a liquid-crystal handle holds (f, Q, u): use lb_set_state_lc");
   if (!f || !g) return set_err(h, LB_EINVAL, "f or g is NULL");
   const Geom& G = h->G;
   const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
@@ -637,6 +660,7 @@ int lb_get_state(lb_t* h, double* f, double* g) {
   int rc = usable(h);
   if (rc) return rc;
   if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle holds (f, phi): use lb_get_state_ch");
+  if (h->lc) return set_err(h, LB_EINVAL, "a liquid-crystal handle holds (f, Q, u): use lb_get_state_lc");
   if (!f || !g) return set_err(h, LB_EINVAL, "f or g is NULL");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
   const Geom& G = h->G;
@@ -655,6 +679,7 @@ int lb_get_state(lb_t* h, double* f, double* g) {
 int lb_init_equilibrium(lb_t* h, const double* rho, const double* u, const double* phi) {
   int rc = usable(h);
   if (rc) return rc;
+  if (h->lc) return set_err(h, LB_EINVAL, "a liquid-crystal handle is initialised by lb_init_lc");
   if (!phi) return set_err(h, LB_EINVAL, "phi is NULL");
   const Geom& G = h->G;
   const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
@@ -689,7 +714,7 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
   int rc = usable(h);
   if (rc) return rc;
   if (nsteps < 0 || mode < 1 || mode > 4) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2, 3, 4} required");
-  if (h->ch) return set_err(h, LB_EINVAL, "no memory probes for a Cahn-Hilliard handle");
+  if (h->ch || h->lc) return set_err(h, LB_EINVAL, "no memory probes for a Cahn-Hilliard or liquid-crystal handle");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
   for (int t = 0; t < nsteps; ++t)
     if ((rc = one_step(h, mode))) return rc;
@@ -697,7 +722,8 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
 }
 
 int lb_debug_step_kernel(lb_t* h, int which) {
-  if (h && h->ch && which != 0) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle has one step kernel");
+  if (h && (h->ch || h->lc) && which != 0)
+    return set_err(h, LB_EINVAL, "a Cahn-Hilliard or liquid-crystal handle has one step kernel");
   if (!h || which < 0 || which > 4)
     return set_err(h, LB_EINVAL,
                    "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised) or 4 (persistent warp-specialised)");
@@ -725,6 +751,7 @@ int lb_get_phi(lb_t* h, double* phi) {
   int rc = usable(h);
   if (rc) return rc;
   if (!phi) return set_err(h, LB_EINVAL, "phi is NULL");
+  if (h->lc) return set_err(h, LB_EINVAL, "a liquid-crystal handle has no phi (use lb_get_state_lc)");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
   const Geom& G = h->G;
   const size_t nloc = (size_t)G.nxy * G.nzl;
@@ -750,6 +777,10 @@ void lb_destroy(lb_t* h) {
     cudaFree(s.B);
     cudaFree(s.phi);
     cudaFree(s.phi2);
+    cudaFree(s.q);
+    cudaFree(s.q2);
+    cudaFree(s.u);
+    cudaFree(s.u2);
   }
   cudaFree(h->d_flag);
   cudaFree(h->wctr.dev);
@@ -899,6 +930,7 @@ int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, doub
   int rc = usable(h);
   if (rc) return rc;
   if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle's collision is fixed at lb_create_ch");
+  if (h->lc) return set_err(h, LB_EINVAL, "a liquid-crystal handle's collision is fixed at lb_create_lc");
   if (model == 0) {
     h->dp.coll = 0;
     return LB_OK;
@@ -977,6 +1009,148 @@ int lb_halo_plan(int nx, int ny, int nz, int nranks, int rank, int64_t out[4]) {
   out[2] = (int64_t)HALO_COMPS * nx * ny;
   out[3] = (int64_t)2 * nx * ny;
   return LB_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// NEXT-4: the liquid-crystal workload (R34-R45)
+namespace {
+
+lb_ctx* lc_handle(lb_t* h, int* rc) {
+  *rc = usable(h);
+  if (*rc) return nullptr;
+  if (!h->lc) {
+    *rc = set_err(h, LB_EINVAL, "not a liquid-crystal handle");
+    return nullptr;
+  }
+  return h;
+}
+
+// canonical host field a[c*nloc + s] (ncomp components) <-> device [z][c][y][x]
+int lc_field_h2d(lb_ctx* h, double* dev, const double* host, int ncomp) {
+  const Geom& G = h->G;
+  const size_t nxy = (size_t)G.nxy, nloc = nxy * G.nzl;
+  for (int c = 0; c < ncomp; ++c)
+    CK(h, cudaMemcpy2DAsync(dev + c * nxy, ncomp * nxy * 8, host + c * nloc, nxy * 8, nxy * 8, G.nzl,
+                            cudaMemcpyHostToDevice, h->stream));
+  return LB_OK;
+}
+int lc_field_d2h(lb_ctx* h, double* host, const double* dev, int ncomp) {
+  const Geom& G = h->G;
+  const size_t nxy = (size_t)G.nxy, nloc = nxy * G.nzl;
+  for (int c = 0; c < ncomp; ++c)
+    CK(h, cudaMemcpy2DAsync(host + c * nloc, nxy * 8, dev + c * nxy, ncomp * nxy * 8, nxy * 8, G.nzl,
+                            cudaMemcpyDeviceToHost, h->stream));
+  return LB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lb_create_lc(int nx, int ny, int nz, const lb_lc_params* lp, lb_t** out) {
+  if (!out) return set_err(nullptr, LB_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!lp) return set_err(nullptr, LB_EINVAL, "params is NULL");
+  if (nx % 2 != 0) return set_err(nullptr, LB_EINVAL, "the liquid-crystal workload needs nx even (16-byte rows)");
+  if (!std::isfinite(lp->A0) || !std::isfinite(lp->gamma) || !std::isfinite(lp->xi))
+    return set_err(nullptr, LB_EINVAL, "A0, gamma and xi must be finite");
+  if (!std::isfinite(lp->Gamma) || lp->Gamma < 0) return set_err(nullptr, LB_EINVAL, "Gamma must be finite and >= 0");
+  lb_params base{};
+  base.tau_f = lp->tau_f;
+  base.tau_g = 1.0;  // unused
+  base.kappa = lp->kappa;
+  int rc = create_common(nx, ny, nz, &base, 1, 0, 1, out);
+  if (rc) return rc;
+  lb_ctx* h = *out;
+  h->lc = true;
+  h->dp.lc_a0 = lp->A0;
+  h->dp.lc_gamma = lp->gamma;
+  h->dp.lc_xi = lp->xi;
+  h->dp.lc_Gamma = lp->Gamma;
+  h->lczc = lc_zchunk(h->G, h->num_sms);
+  Slab& s = h->slabs[0];
+  const size_t nloc = (size_t)h->G.nxy * h->G.nzl;
+  cudaError_t e = cudaSuccess;
+  for (double** b : {&s.q, &s.q2})
+    if (e == cudaSuccess && (e = cudaMalloc(b, 5 * nloc * sizeof(double))) == cudaSuccess)
+      e = cudaMemsetAsync(*b, 0xff, 5 * nloc * sizeof(double), h->stream);
+  for (double** b : {&s.u, &s.u2})
+    if (e == cudaSuccess && (e = cudaMalloc(b, 3 * nloc * sizeof(double))) == cudaSuccess)
+      e = cudaMemsetAsync(*b, 0xff, 3 * nloc * sizeof(double), h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess || !make_step_maps(h->G, s.A, 8, &s.lcA) || !make_step_maps(h->G, s.B, 8, &s.lcB)) {
+    g_create_error = "liquid-crystal handle: allocation or TMA descriptor failed";
+    lb_destroy(h);
+    *out = nullptr;
+    return e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA;
+  }
+  return LB_OK;
+}
+
+int lb_set_state_lc(lb_t* h_, const double* f, const double* q, const double* u) {
+  int rc;
+  lb_ctx* h = lc_handle(h_, &rc);
+  if (!h) return rc;
+  if (!f || !q || !u) return set_err(h, LB_EINVAL, "f, q or u is NULL");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl;
+  Slab& s = h->slabs[0];
+  CK(h, cudaMemcpyAsync(s.B, f, Q * nloc * 8, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemsetAsync(s.B + Q * nloc, 0, Q * nloc * 8, h->stream));  // the g slots are not used
+  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_canon_to_planes(G, s.B, s.A, h->stream); }));
+  if ((rc = lc_field_h2d(h, s.q, q, 5)) || (rc = lc_field_h2d(h, s.u, u, 3))) return rc;
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  h->have_state = true;
+  return LB_OK;
+}
+
+int lb_get_state_lc(lb_t* h_, double* f, double* q, double* u) {
+  int rc;
+  lb_ctx* h = lc_handle(h_, &rc);
+  if (!h) return rc;
+  if (!f || !q || !u) return set_err(h, LB_EINVAL, "f, q or u is NULL");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state_lc or lb_init_lc first");
+  const Geom& G = h->G;
+  const size_t nloc = (size_t)G.nxy * G.nzl;
+  Slab& s = h->slabs[0];
+  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_planes_to_canon(G, s.A, s.B, h->stream); }));
+  CK(h, cudaMemcpyAsync(f, s.B, Q * nloc * 8, cudaMemcpyDeviceToHost, h->stream));
+  if ((rc = lc_field_d2h(h, q, s.q, 5)) || (rc = lc_field_d2h(h, u, s.u, 3))) return rc;
+  CK(h, cudaStreamSynchronize(h->stream));
+  resolve_pending(h);
+  return LB_OK;
+}
+
+int lb_init_lc(lb_t* h_, const double* rho, const double* u, const double* n) {
+  int rc;
+  lb_ctx* h = lc_handle(h_, &rc);
+  if (!h) return rc;
+  if (!n) return set_err(h, LB_EINVAL, "n is NULL");
+  const double gam = h->dp.lc_gamma;
+  if (!(gam > 8.0 / 3.0)) return set_err(h, LB_EINVAL, "lb_init_lc needs gamma > 8/3 (a nematic bulk minimum)");
+  const size_t nloc = (size_t)h->G.nxy * h->G.nzl;
+  // R45: f = f^eq(rho, u) (R8), Q = S0 (n n - I/3), the stored velocity = u
+  const double S0 = 0.25 + 0.75 * std::sqrt(1.0 - 8.0 / (3.0 * gam));
+  std::vector<double> f(Q * nloc), q(5 * nloc), uu(3 * nloc, 0.0);
+  for (size_t s = 0; s < nloc; ++s) {
+    const double r = rho ? rho[s] : 1.0;
+    double v[3] = {0, 0, 0};
+    if (u)
+      for (int a = 0; a < 3; ++a) v[a] = uu[a * nloc + s] = u[a * nloc + s];
+    const double u2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+    for (int i = 0; i < Q; ++i) {
+      const double cu = cx(i) * v[0] + cy(i) * v[1] + cz(i) * v[2];
+      f[i * nloc + s] = wgt(i) * r * (1.0 + 3.0 * cu + 4.5 * cu * cu - 1.5 * u2);
+    }
+    const double d[3] = {n[s], n[nloc + s], n[2 * nloc + s]};
+    const int ab[5][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}};
+    for (int k = 0; k < 5; ++k)
+      q[k * nloc + s] = S0 * (d[ab[k][0]] * d[ab[k][1]] - (ab[k][0] == ab[k][1] ? 1.0 / 3.0 : 0.0));
+  }
+  return lb_set_state_lc(h, f.data(), q.data(), uu.data());
 }
 
 }  // extern "C"

@@ -50,9 +50,10 @@ __device__ __forceinline__ void stress6(const DevParams& p, double ph, double gx
 // of f^eq, S, g^eq splits into a part even in c (shared by the pair) and a part
 // odd in c (sign-flipped), which roughly halves the fp64 work.  emit(i, f_i*, g_i*)
 // is called once per component.  Returns rho (for the R22 numerical-domain check).
+// uo (optional): receives u = (j + F/2)/rho (the liquid-crystal workload stores it, R40).
 template <class GetF, class GetG, class Emit>
 __device__ __forceinline__ double collide_acc(const DevParams& p, GetF&& getf, GetG&& getg, double phi, double mu,
-                                              const double F[3], Emit&& emit) {
+                                              const double F[3], Emit&& emit, double* uo = nullptr) {
   double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
@@ -66,6 +67,11 @@ __device__ __forceinline__ double collide_acc(const DevParams& p, GetF&& getf, G
   const double ux = (jx + 0.5 * F[0]) * rinv;  // R7
   const double uy = (jy + 0.5 * F[1]) * rinv;
   const double uz = (jz + 0.5 * F[2]) * rinv;
+  if (uo) {
+    uo[0] = ux;
+    uo[1] = uy;
+    uo[2] = uz;
+  }
   const double uu = ux * ux + uy * uy + uz * uz;
   const double uF = ux * F[0] + uy * F[1] + uz * F[2];
   const double gmu = p.gamma * mu;
@@ -192,9 +198,9 @@ __device__ __forceinline__ double collide_mrt(const DevParams& p, double (&f)[Q]
 
 template <class Emit>
 __device__ __forceinline__ double collide(const DevParams& p, const double (&f)[Q], const double (&g)[Q], double phi,
-                                          double mu, const double F[3], Emit&& emit) {
+                                          double mu, const double F[3], Emit&& emit, double* uo = nullptr) {
   return collide_acc(
-      p, [&](int i) { return f[i]; }, [&](int i) { return g[i]; }, phi, mu, F, emit);
+      p, [&](int i) { return f[i]; }, [&](int i) { return g[i]; }, phi, mu, F, emit, uo);
 }
 
 }  // namespace lbk

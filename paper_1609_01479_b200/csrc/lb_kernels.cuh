@@ -22,6 +22,9 @@ struct DevParams {
   int coll;
   double inv_tau_s, inv_tau_b, inv_tau_ghost;  // MRT rates (coll 1)
   double mob;  // M itself: the finite-difference Cahn-Hilliard variant (R30)
+  // liquid-crystal workload (NEXT-4, R35-R42): Landau-de Gennes A0, gamma; flow-aligning
+  // xi; rotational diffusion Gamma (kappa above is the elastic constant)
+  double lc_a0, lc_gamma, lc_xi, lc_Gamma;
 };
 
 // Geometry of one z-slab as the kernels see it.
@@ -144,6 +147,13 @@ struct alignas(64) ChMaps {
 bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out);
 cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
                            double* phiB, int zc, int* flag, const ChMaps* mapsA, cudaStream_t st);
+// the liquid-crystal workload (lb_step_lc.cu, NEXT-4): state f (dist buffer, f slots),
+// Q (five components, q[z][c][y][x]) and u (q[z][a][y][x]); 32 x 8 tiles, the f tile
+// by TMA through maps m[0] (5 components) and m[1] (9) of make_step_maps(.., 8, ..)
+int lc_zchunk(const Geom& G, int num_sms);
+cudaError_t launch_step_lc(const Geom& G, const DevParams& p, const double* A, double* B, const double* qA,
+                           double* qB, const double* uA, double* uB, int zc, int* flag, const StepMaps* mapsA,
+                           cudaStream_t st);
 // the cluster variant of the step (lb_step_cluster.cu): phi halos shared through
 // distributed shared memory; for nx % 64 == 0 and ny % 16 == 0
 struct alignas(64) ClusterMaps {

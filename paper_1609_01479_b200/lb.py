@@ -81,12 +81,24 @@ _lb_create_ch = _sig("lb_create_ch", _i, _i, _i, _i, C.POINTER(lb_params), C.c_d
 _lb_set_state_ch = _sig("lb_set_state_ch", _i, _vp, _vp, _vp)
 _lb_get_state_ch = _sig("lb_get_state_ch", _i, _vp, _vp, _vp)
 
+
+class lb_lc_params(C.Structure):
+    _fields_ = [("tau_f", C.c_double), ("A0", C.c_double), ("gamma", C.c_double), ("kappa", C.c_double),
+                ("xi", C.c_double), ("Gamma", C.c_double)]
+
+
+_lb_create_lc = _sig("lb_create_lc", _i, _i, _i, _i, C.POINTER(lb_lc_params), C.POINTER(_vp))
+_lb_set_state_lc = _sig("lb_set_state_lc", _i, _vp, _vp, _vp, _vp)
+_lb_get_state_lc = _sig("lb_get_state_lc", _i, _vp, _vp, _vp, _vp)
+_lb_init_lc = _sig("lb_init_lc", _i, _vp, _vp, _vp, _vp)
+
 EXPORTS = [
     "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
     "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_set_state_ch", "lb_get_state_ch",
+    "lb_create_lc", "lb_set_state_lc", "lb_get_state_lc", "lb_init_lc",
 ]
 
 
@@ -267,6 +279,37 @@ def lb_get_state_ch(h, f=None, phi=None):
     return f, phi
 
 
+def make_lc_params(tau_f=0.8, A0=0.01, gamma=3.2, kappa=0.01, xi=0.7, Gamma=0.3) -> lb_lc_params:
+    """Defaults: DESIGN.md R44."""
+    return lb_lc_params(tau_f, A0, gamma, kappa, xi, Gamma)
+
+
+def lb_create_lc(nx: int, ny: int, nz: int, params: lb_lc_params):
+    h = _vp()
+    _check(_lb_create_lc(nx, ny, nz, C.byref(params), C.byref(h)), None)
+    return h.value
+
+
+def lb_set_state_lc(h, f, q, u) -> None:
+    n = lb_local_sites(h)
+    _check(_lb_set_state_lc(h, _ptr(f, Q * n), _ptr(q, 5 * n), _ptr(u, 3 * n)), h)
+
+
+def lb_get_state_lc(h, f=None, q=None, u=None):
+    n = lb_local_sites(h)
+    f = np.empty(Q * n) if f is None else f
+    q = np.empty(5 * n) if q is None else q
+    u = np.empty(3 * n) if u is None else u
+    _check(_lb_get_state_lc(h, _ptr(f, Q * n, True), _ptr(q, 5 * n, True), _ptr(u, 3 * n, True)), h)
+    return f, q, u
+
+
+def lb_init_lc(h, rho, u, n_dir) -> None:
+    n = lb_local_sites(h)
+    _check(_lb_init_lc(h, None if rho is None else _ptr(rho, n), None if u is None else _ptr(u, 3 * n),
+                       _ptr(n_dir, 3 * n)), h)
+
+
 def lb_debug_halo_mode(h, mode: int = -1) -> int:
     """-1: query (returns 0 exchange / 1 peer); 0 or 1: set (returns 0)."""
     rc = _lb_debug_halo_mode(h, mode)
@@ -346,3 +389,25 @@ class ChLattice(Lattice):
     def get_state(self):
         f, phi = lb_get_state_ch(self.h)
         return f.reshape((Q,) + self.shape), phi.reshape(self.shape)
+
+
+class LcLattice(Lattice):
+    """A liquid-crystal handle (lb_create_lc, NEXT-4): state (f, Q, u); arrays are
+    (19 | 5 | 3, nz, ny, nx)."""
+
+    def __init__(self, nx, ny, nz, params: lb_lc_params | None = None):
+        self.params = params or make_lc_params()
+        self.h = lb_create_lc(nx, ny, nz, self.params)
+        self.shape = (nz, ny, nx)
+
+    def set_state(self, f, q, u):
+        c = lambda a: np.ascontiguousarray(a, dtype=np.float64).reshape(-1)  # noqa: E731
+        lb_set_state_lc(self.h, c(f), c(q), c(u))
+
+    def init(self, n_dir, rho=None, u=None):
+        c = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64).reshape(-1)  # noqa: E731
+        lb_init_lc(self.h, c(rho), c(u), c(n_dir))
+
+    def get_state(self):
+        f, q, u = lb_get_state_lc(self.h)
+        return f.reshape((Q,) + self.shape), q.reshape((5,) + self.shape), u.reshape((3,) + self.shape)

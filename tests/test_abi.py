@@ -51,6 +51,24 @@ def test_create_rejects_bad_arguments(kw, msg):
     assert e.value.code == lb.LB_EINVAL and msg in str(e.value)
 
 
+@pytest.mark.parametrize(
+    "nx,kw,msg",
+    [
+        (15, {}, "nx even"),
+        (16, dict(tau_f=0.5), "tau_f"),
+        (16, dict(kappa=-0.1), "kappa"),
+        (16, dict(Gamma=-1.0), "Gamma"),
+        (16, dict(xi=float("nan")), "finite"),
+        (16, dict(A0=float("inf")), "finite"),
+    ],
+)
+def test_create_lc_rejects_bad_arguments(nx, kw, msg):
+    """The liquid-crystal handle validates before touching CUDA (no GPU here)."""
+    with pytest.raises(lb.LBError) as e:
+        lb.lb_create_lc(nx, 8, 8, lb.make_lc_params(**kw))
+    assert e.value.code == lb.LB_EINVAL and msg in str(e.value)
+
+
 def test_loopback_rejects_bad_slab_counts():
     with pytest.raises(lb.LBError) as e:
         lb.lb_create_loopback(8, 8, 9, lb.make_params(), 2)
