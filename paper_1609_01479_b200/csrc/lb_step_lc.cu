@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kLT, 1)
   // ---- f tile of plane zp -> buffer zp % 2 (three TMA boxes: the f slot runs)
   auto issue_f = [&](int zp) {
     if (tid == 0) {
-      const int b = cmod(zp, 2);
+      const int b = ((zp) & 1);
       fence_proxy_async();
       mbar_expect_tx(&sm.bar[b], Q * kLT * 8);
       const int cpl = (wz(zp) + GZ) * NSLOT;
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kLT, 1)
     }
   };
   auto wait_f = [&](int zp) {
-    const int b = cmod(zp, 2);
+    const int b = ((zp) & 1);
     mbar_wait(&sm.bar[b], (ph >> b) & 1);
     ph ^= 1u << b;
   };
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kLT, 1)
   auto issue_q = [&](int zp) {
     if (!has_q) return;
     const double* base = qA + (long long)wz(zp) * 5 * nxy + qsrc;
-    double(*ring)[NB] = sm.sQ[cmod(zp, 4)];
+    double(*ring)[NB] = sm.sQ[((zp) & 3)];
 #pragma unroll
     for (int c = 0; c < 5; ++c) cp_async_v<2>(&ring[c][bdst], base + c * nxy);
   };
@@ -237,12 +237,13 @@ __global__ void __launch_bounds__(kLT, 1)
   };
 
   // ---- H, sigma of plane zp at sigma-box site e; the in-plane stress columns go to sSig
+  // (ring slots: & 3 and & 1 are the non-negative residues also for zp < 0)
   auto fields_at = [&](int zp, int e, double (&q)[5], double (&H)[5], double (&sg)[3][3]) {
     const int ex = e % SX, ey = e / SX;
     const int c = (ey + 1) * BX + (ex + 1);
-    const double(*Q0)[NB] = sm.sQ[cmod(zp, 4)];
-    const double(*Qm)[NB] = sm.sQ[cmod(zp - 1, 4)];
-    const double(*Qp)[NB] = sm.sQ[cmod(zp + 1, 4)];
+    const double(*Q0)[NB] = sm.sQ[((zp) & 3)];
+    const double(*Qm)[NB] = sm.sQ[((zp - 1) & 3)];
+    const double(*Qp)[NB] = sm.sQ[((zp + 1) & 3)];
     double dq[3][5], lap[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {  // R37: central gradient, 7-point Laplacian
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(kLT, 1)
       lap[k] = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * v;
     }
     lc_fields(p, q, dq, lap, H, sg);
-    double(*s)[NS] = sm.sSig[cmod(zp, 2)];
+    double(*s)[NS] = sm.sSig[((zp) & 1)];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       s[a][e] = sg[a][0];
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kLT, 1)
     for (int a = 0; a < 3; ++a) up[a] = sm.sU[cmod(k + 1, 3)][a][cu];
     if (active) {
       // R39: F = div sigma (= -div P^th), the in-plane columns from sSig(k)
-      const double(*s)[NS] = sm.sSig[cmod(k, 2)];
+      const double(*s)[NS] = sm.sSig[((k) & 1)];
       double F[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kLT, 1)
       // R40: Guo BGK of f (A.7) and push (A.8); u' = (j + F/2) / rho
       double f[Q];
 #pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = sm.sF[cmod(k, 2)][frank(i)][tid];
+      for (int i = 0; i < Q; ++i) f[i] = sm.sF[((k) & 1)][frank(i)][tid];
       const long long zoff[3] = {(long long)wz(k - 1) + GZ, (long long)k + GZ, (long long)wz(k + 1) + GZ};
       const double g0[Q] = {};
       double un[3];
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(kLT, 1)
       double S5[5];
       corotation(p.lc_xi, W, q0, S5);
       // R42 (R31 per component): upwind fluxes through the six faces, then the update
-      const double(*Qk)[NB] = sm.sQ[cmod(k, 4)];
+      const double(*Qk)[NB] = sm.sQ[((k) & 3)];
       const double ufx_p = 0.5 * (uk[0][cu] + uk[0][cu + 1]), ufx_m = 0.5 * (uk[0][cu - 1] + uk[0][cu]);
       const double ufy_p = 0.5 * (uk[1][cu] + uk[1][cu + UX]), ufy_m = 0.5 * (uk[1][cu - UX] + uk[1][cu]);
       const double ufz_p = 0.5 * (uk[2][cu] + up[2]), ufz_m = 0.5 * (um[2] + uk[2][cu]);
