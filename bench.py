@@ -261,12 +261,12 @@ def run_ours(args):
     uid = None
     if world > 1:
         uid = D.broadcast_bytes(lb.lb_nccl_get_unique_id() if rank == 0 else None)
-    if args.collision in ("ch", "lc") and world > 1:
-        raise SystemExit(f"--collision {args.collision}: this variant is single-slab (one GPU)")
+    if args.collision == "ch" and world > 1:
+        raise SystemExit("--collision ch: the Cahn-Hilliard variant is single-slab (one GPU)")
     if args.collision == "ch":
         L = lb.ChLattice(nx, ny, nz, params, 0.8, 1.1, 1.0)
-    elif args.collision == "lc":
-        L = lb.LcLattice(nx, ny, nz, lb.make_lc_params())  # R44 defaults
+    elif args.collision == "lc":  # R44 defaults; z-slabs with NCCL halos under torchrun
+        L = lb.LcLattice(nx, ny, nz, lb.make_lc_params(), nranks=world, rank=rank, uid=uid)
     else:
         L = lb.Lattice(nx, ny, nz, params, nranks=world, rank=rank, uid=uid)
     bps = {"ch": BYTES_PER_SITE_CH, "lc": BYTES_PER_SITE_LC}.get(args.collision, BYTES_PER_SITE)
@@ -274,7 +274,7 @@ def run_ours(args):
         lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
     halo = ("peer (fused P2P stores)" if lb.lb_debug_halo_mode(L.h) == 1 else "NCCL send/recv") if world > 1 else None
     if args.collision == "lc":
-        L.init(synth.random_directors(nx, ny, nz, 0))  # R45: quench from random directors
+        L.init(synth.random_directors_slab(nx, ny, nz, z0, z1, 0))  # R45: quench from random directors
     else:
         L.init_equilibrium(synth.spinodal_phi_slab(nx, ny, nz, z0, z1, seed=0))
 

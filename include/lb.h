@@ -196,7 +196,7 @@ int lb_get_state_ch(lb_t* h, double* f, double* phi);
  *   Q <- Q - div J + S(W, Q) + Gamma H   (R41, R42: upwind J, W = grad u, stored u);
  * propagation of f.  State (R34): f canonical (19*nloc), Q by its five components
  * (xx, xy, xz, yy, yz) as q[c*nloc + s], and the stored velocity u[a*nloc + s].
- * One periodic lattice on the current GPU; nx even, else LB_EINVAL.  lb_step,
+ * A periodic lattice on the current GPU (or z-slabs, below); nx even, else LB_EINVAL.  lb_step,
  * lb_destroy, lb_last_error, lb_stream and the profiling calls work as for other
  * handles; lb_set_state, lb_get_state, lb_init_equilibrium, lb_get_phi and
  * lb_set_collision return LB_EINVAL. */
@@ -210,6 +210,15 @@ typedef struct {
 } lb_lc_params;
 
 int lb_create_lc(int nx, int ny, int nz, const lb_lc_params* params, lb_t** out);
+/* The same workload decomposed into z-slabs (nz % slabs == 0, nz/slabs >= 2): inside
+ * one handle on this GPU (loopback; host arrays = the whole lattice), or one rank
+ * per GPU (collective like lb_create_slab; host arrays = this rank's slab).  Before
+ * each step the Q planes z_lo, z_lo+1 / z_hi-1, z_hi and the u planes z_lo / z_hi go
+ * to the neighbours' ghost planes; after it, the f components that left the slab
+ * (device copies, or NCCL send/recv between ranks).  Bitwise equal to lb_create_lc. */
+int lb_create_lc_loopback(int nx, int ny, int nz, const lb_lc_params* params, int nslabs, lb_t** out);
+int lb_create_lc_slab(int nx, int ny, int nz, const lb_lc_params* params, int nranks, int rank, const void* id128,
+                      lb_t** out);
 /* Host arrays: f 19*nloc, q 5*nloc, u 3*nloc doubles (canonical layouts above);
  * set/get round trip bitwise. */
 int lb_set_state_lc(lb_t* h, const double* f, const double* q, const double* u);

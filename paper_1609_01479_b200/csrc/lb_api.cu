@@ -158,6 +158,14 @@ DevParams derive(const lb_params& p) {
 
 size_t dist_doubles(const Geom& G) { return (size_t)(G.nzl + 2 * GZ) * (size_t)G.plane; }
 size_t phi_doubles(const Geom& G) { return (size_t)(G.nzl + 2 * GP) * (size_t)G.nxy; }
+// liquid-crystal fields, plane-major [z][c][y][x] with ghost planes: Q (5 components,
+// 2 ghost planes each side: the stress at z +- 1 needs Q at z +- 2), u (3, one)
+constexpr int LC_GQ = 2, LC_GU = 1;
+size_t lc_q_doubles(const Geom& G) { return (size_t)(G.nzl + 2 * LC_GQ) * 5 * (size_t)G.nxy; }
+size_t lc_u_doubles(const Geom& G) { return (size_t)(G.nzl + 2 * LC_GU) * 3 * (size_t)G.nxy; }
+double* lc_q0(const Geom& G, double* q) { return q + (size_t)LC_GQ * 5 * G.nxy; }  // plane 0
+double* lc_u0(const Geom& G, double* u) { return u + (size_t)LC_GU * 3 * G.nxy; }
+int exchange_lc(lb_ctx* h);  // Q / u halos of the liquid-crystal slabs (defined with the LC calls)
 
 // ---- profiling -------------------------------------------------------------
 template <class Fn>
@@ -409,17 +417,22 @@ int one_step(lb_ctx* h, int mode) {
   const Geom& G = h->G;
   int rc;
   const bool peer = h->halo_mode == 1 && !G.zwrap;
-  if (h->lc && mode >= 0) {
-    Slab& s = h->slabs[0];
-    CK(h, timed(h, K_STEP, true, [&]() {
-         return launch_step_lc(G, h->dp, s.A, s.B, s.q, s.q2, s.u, s.u2, h->lczc, h->d_flag, &s.lcA, h->stream);
-       }));
-    std::swap(s.A, s.B);
-    std::swap(s.mapsA, s.mapsB);
-    std::swap(s.cmapsA, s.cmapsB);
-    std::swap(s.lcA, s.lcB);
-    std::swap(s.q, s.q2);
-    std::swap(s.u, s.u2);
+  if (h->lc && mode >= 0) {  // Q, u halos; the step; f halo (the components that left each slab)
+    if (!G.zwrap && (rc = exchange_lc(h))) return rc;
+    for (auto& s : h->slabs)
+      CK(h, timed(h, K_STEP, true, [&]() {
+           return launch_step_lc(G, h->dp, s.A, s.B, lc_q0(G, s.q), lc_q0(G, s.q2), lc_u0(G, s.u), lc_u0(G, s.u2),
+                                 h->lczc, h->d_flag, &s.lcA, h->stream);
+         }));
+    if (!G.zwrap && (rc = exchange_dist(h))) return rc;
+    for (auto& s : h->slabs) {
+      std::swap(s.A, s.B);
+      std::swap(s.mapsA, s.mapsB);
+      std::swap(s.cmapsA, s.cmapsB);
+      std::swap(s.lcA, s.lcB);
+      std::swap(s.q, s.q2);
+      std::swap(s.u, s.u2);
+    }
     return LB_OK;
   }
   if (h->ch && mode >= 0) {
@@ -1027,21 +1040,122 @@ lb_ctx* lc_handle(lb_t* h, int* rc) {
   return h;
 }
 
-// canonical host field a[c*nloc + s] (ncomp components) <-> device [z][c][y][x]
-int lc_field_h2d(lb_ctx* h, double* dev, const double* host, int ncomp) {
+// canonical host field a[c*N + s] (ncomp components, N = host sites, this slab's
+// sites starting at site0) <-> device plane-major [z][c][y][x] starting at plane 0
+int lc_field_h2d(lb_ctx* h, double* dev0, const double* host, int ncomp, size_t site0) {
   const Geom& G = h->G;
-  const size_t nxy = (size_t)G.nxy, nloc = nxy * G.nzl;
+  const size_t nxy = (size_t)G.nxy, N = host_nloc(h);
   for (int c = 0; c < ncomp; ++c)
-    CK(h, cudaMemcpy2DAsync(dev + c * nxy, ncomp * nxy * 8, host + c * nloc, nxy * 8, nxy * 8, G.nzl,
+    CK(h, cudaMemcpy2DAsync(dev0 + c * nxy, ncomp * nxy * 8, host + c * N + site0, nxy * 8, nxy * 8, G.nzl,
                             cudaMemcpyHostToDevice, h->stream));
   return LB_OK;
 }
-int lc_field_d2h(lb_ctx* h, double* host, const double* dev, int ncomp) {
+int lc_field_d2h(lb_ctx* h, double* host, const double* dev0, int ncomp, size_t site0) {
   const Geom& G = h->G;
-  const size_t nxy = (size_t)G.nxy, nloc = nxy * G.nzl;
+  const size_t nxy = (size_t)G.nxy, N = host_nloc(h);
   for (int c = 0; c < ncomp; ++c)
-    CK(h, cudaMemcpy2DAsync(host + c * nloc, nxy * 8, dev + c * nxy, ncomp * nxy * 8, nxy * 8, G.nzl,
+    CK(h, cudaMemcpy2DAsync(host + c * N + site0, nxy * 8, dev0 + c * nxy, ncomp * nxy * 8, nxy * 8, G.nzl,
                             cudaMemcpyDeviceToHost, h->stream));
+  return LB_OK;
+}
+
+// Q and u halos of z-slabs before a step: Q planes [nzl-2, nzl) -> ghost planes
+// [-2, 0) of the slab above, [0, 2) -> [nzl, nzl+2) of the slab below; u likewise
+// with one plane.  Each message is one contiguous run (plane-major layout).
+int exchange_lc(lb_ctx* h) {
+  const Geom& G = h->G;
+  const size_t qp = (size_t)5 * G.nxy, up_ = (size_t)3 * G.nxy;  // doubles per plane
+  auto qat = [&](Slab& s, int z) { return lc_q0(G, s.q) + (long long)z * qp; };
+  auto uat = [&](Slab& s, int z) { return lc_u0(G, s.u) + (long long)z * up_; };
+  if (h->nranks > 1) {
+    Slab& s = h->slabs[0];
+    const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
+    cudaError_t ce = timed(h, K_HALO_PHI, false, [&]() {
+      ncclGroupStart();
+      ncclSend(qat(s, G.nzl - LC_GQ), LC_GQ * qp, ncclDouble, up, h->comm, h->stream);
+      ncclRecv(qat(s, -LC_GQ), LC_GQ * qp, ncclDouble, dn, h->comm, h->stream);
+      ncclSend(qat(s, 0), LC_GQ * qp, ncclDouble, dn, h->comm, h->stream);
+      ncclRecv(qat(s, G.nzl), LC_GQ * qp, ncclDouble, up, h->comm, h->stream);
+      ncclSend(uat(s, G.nzl - 1), up_, ncclDouble, up, h->comm, h->stream);
+      ncclRecv(uat(s, -1), up_, ncclDouble, dn, h->comm, h->stream);
+      ncclSend(uat(s, 0), up_, ncclDouble, dn, h->comm, h->stream);
+      ncclRecv(uat(s, G.nzl), up_, ncclDouble, up, h->comm, h->stream);
+      return ncclGroupEnd() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+    });
+    if (ce != cudaSuccess) return set_err(h, LB_ENCCL, "NCCL Q / u halo exchange failed");
+    return LB_OK;
+  }
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    Slab& up = h->slabs[(r + 1) % h->nslabs];
+    Slab& dn = h->slabs[(r - 1 + h->nslabs) % h->nslabs];
+    CK(h, timed(h, K_HALO_PHI, false, [&]() {
+      const cudaMemcpyKind k = cudaMemcpyDeviceToDevice;
+      cudaError_t e = cudaMemcpyAsync(qat(up, -LC_GQ), qat(s, G.nzl - LC_GQ), LC_GQ * qp * 8, k, h->stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(qat(dn, G.nzl), qat(s, 0), LC_GQ * qp * 8, k, h->stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(uat(up, -1), uat(s, G.nzl - 1), up_ * 8, k, h->stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(uat(dn, G.nzl), uat(s, 0), up_ * 8, k, h->stream);
+      return e;
+    }));
+  }
+  return LB_OK;
+}
+
+int lc_create(int nx, int ny, int nz, const lb_lc_params* lp, int nranks, int rank, int nslabs, const void* id128,
+              lb_t** out) {
+  if (!out) return set_err(nullptr, LB_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!lp) return set_err(nullptr, LB_EINVAL, "params is NULL");
+  if (nx % 2 != 0) return set_err(nullptr, LB_EINVAL, "the liquid-crystal workload needs nx even (16-byte rows)");
+  if (!std::isfinite(lp->A0) || !std::isfinite(lp->gamma) || !std::isfinite(lp->xi))
+    return set_err(nullptr, LB_EINVAL, "A0, gamma and xi must be finite");
+  if (!std::isfinite(lp->Gamma) || lp->Gamma < 0) return set_err(nullptr, LB_EINVAL, "Gamma must be finite and >= 0");
+  if (nranks > 1 && !id128) return set_err(nullptr, LB_EINVAL, "id128 is NULL");
+  lb_params base{};
+  base.tau_f = lp->tau_f;
+  base.tau_g = 1.0;  // unused
+  base.kappa = lp->kappa;
+  int rc = create_common(nx, ny, nz, &base, nranks, rank, nslabs, out);
+  if (rc) return rc;
+  lb_ctx* h = *out;
+  h->lc = true;
+  h->halo_mode = 0;  // ghost planes + copies / NCCL send-recv
+  h->dp.lc_a0 = lp->A0;
+  h->dp.lc_gamma = lp->gamma;
+  h->dp.lc_xi = lp->xi;
+  h->dp.lc_Gamma = lp->Gamma;
+  h->lczc = lc_zchunk(h->G, h->num_sms);
+  const size_t nq = lc_q_doubles(h->G), nu = lc_u_doubles(h->G);
+  cudaError_t e = cudaSuccess;
+  bool maps_ok = true;
+  for (auto& s : h->slabs) {
+    for (double** b : {&s.q, &s.q2})
+      if (e == cudaSuccess && (e = cudaMalloc(b, nq * sizeof(double))) == cudaSuccess)
+        e = cudaMemsetAsync(*b, 0xff, nq * sizeof(double), h->stream);
+    for (double** b : {&s.u, &s.u2})
+      if (e == cudaSuccess && (e = cudaMalloc(b, nu * sizeof(double))) == cudaSuccess)
+        e = cudaMemsetAsync(*b, 0xff, nu * sizeof(double), h->stream);
+    maps_ok = maps_ok && make_step_maps(h->G, s.A, 8, &s.lcA) && make_step_maps(h->G, s.B, 8, &s.lcB);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess || !maps_ok) {
+    g_create_error = "liquid-crystal handle: allocation or TMA descriptor failed";
+    lb_destroy(h);
+    *out = nullptr;
+    return e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA;
+  }
+  if (nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      g_create_error = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      h->comm = nullptr;
+      lb_destroy(h);
+      *out = nullptr;
+      return LB_ENCCL;
+    }
+  }
   return LB_OK;
 }
 
@@ -1050,43 +1164,16 @@ int lc_field_d2h(lb_ctx* h, double* host, const double* dev, int ncomp) {
 extern "C" {
 
 int lb_create_lc(int nx, int ny, int nz, const lb_lc_params* lp, lb_t** out) {
-  if (!out) return set_err(nullptr, LB_EINVAL, "out is NULL");
-  *out = nullptr;
-  if (!lp) return set_err(nullptr, LB_EINVAL, "params is NULL");
-  if (nx % 2 != 0) return set_err(nullptr, LB_EINVAL, "the liquid-crystal workload needs nx even (16-byte rows)");
-  if (!std::isfinite(lp->A0) || !std::isfinite(lp->gamma) || !std::isfinite(lp->xi))
-    return set_err(nullptr, LB_EINVAL, "A0, gamma and xi must be finite");
-  if (!std::isfinite(lp->Gamma) || lp->Gamma < 0) return set_err(nullptr, LB_EINVAL, "Gamma must be finite and >= 0");
-  lb_params base{};
-  base.tau_f = lp->tau_f;
-  base.tau_g = 1.0;  // unused
-  base.kappa = lp->kappa;
-  int rc = create_common(nx, ny, nz, &base, 1, 0, 1, out);
-  if (rc) return rc;
-  lb_ctx* h = *out;
-  h->lc = true;
-  h->dp.lc_a0 = lp->A0;
-  h->dp.lc_gamma = lp->gamma;
-  h->dp.lc_xi = lp->xi;
-  h->dp.lc_Gamma = lp->Gamma;
-  h->lczc = lc_zchunk(h->G, h->num_sms);
-  Slab& s = h->slabs[0];
-  const size_t nloc = (size_t)h->G.nxy * h->G.nzl;
-  cudaError_t e = cudaSuccess;
-  for (double** b : {&s.q, &s.q2})
-    if (e == cudaSuccess && (e = cudaMalloc(b, 5 * nloc * sizeof(double))) == cudaSuccess)
-      e = cudaMemsetAsync(*b, 0xff, 5 * nloc * sizeof(double), h->stream);
-  for (double** b : {&s.u, &s.u2})
-    if (e == cudaSuccess && (e = cudaMalloc(b, 3 * nloc * sizeof(double))) == cudaSuccess)
-      e = cudaMemsetAsync(*b, 0xff, 3 * nloc * sizeof(double), h->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-  if (e != cudaSuccess || !make_step_maps(h->G, s.A, 8, &s.lcA) || !make_step_maps(h->G, s.B, 8, &s.lcB)) {
-    g_create_error = "liquid-crystal handle: allocation or TMA descriptor failed";
-    lb_destroy(h);
-    *out = nullptr;
-    return e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA;
-  }
-  return LB_OK;
+  return lc_create(nx, ny, nz, lp, 1, 0, 1, nullptr, out);
+}
+
+int lb_create_lc_loopback(int nx, int ny, int nz, const lb_lc_params* lp, int nslabs, lb_t** out) {
+  return lc_create(nx, ny, nz, lp, 1, 0, nslabs, nullptr, out);
+}
+
+int lb_create_lc_slab(int nx, int ny, int nz, const lb_lc_params* lp, int nranks, int rank, const void* id128,
+                      lb_t** out) {
+  return lc_create(nx, ny, nz, lp, nranks, rank, 1, id128, out);
 }
 
 int lb_set_state_lc(lb_t* h_, const double* f, const double* q, const double* u) {
@@ -1095,12 +1182,15 @@ int lb_set_state_lc(lb_t* h_, const double* f, const double* q, const double* u)
   if (!h) return rc;
   if (!f || !q || !u) return set_err(h, LB_EINVAL, "f, q or u is NULL");
   const Geom& G = h->G;
-  const size_t nloc = (size_t)G.nxy * G.nzl;
-  Slab& s = h->slabs[0];
-  CK(h, cudaMemcpyAsync(s.B, f, Q * nloc * 8, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemsetAsync(s.B + Q * nloc, 0, Q * nloc * 8, h->stream));  // the g slots are not used
-  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_canon_to_planes(G, s.B, s.A, h->stream); }));
-  if ((rc = lc_field_h2d(h, s.q, q, 5)) || (rc = lc_field_h2d(h, s.u, u, 3))) return rc;
+  const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    CK(h, cudaMemcpy2DAsync(s.B, nloc * 8, f + r * nloc, N * 8, nloc * 8, Q, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemsetAsync(s.B + Q * nloc, 0, Q * nloc * 8, h->stream));  // the g slots are not used
+    CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_canon_to_planes(G, s.B, s.A, h->stream); }));
+    if ((rc = lc_field_h2d(h, lc_q0(G, s.q), q, 5, r * nloc)) || (rc = lc_field_h2d(h, lc_u0(G, s.u), u, 3, r * nloc)))
+      return rc;
+  }
   CK(h, cudaStreamSynchronize(h->stream));
   resolve_pending(h);
   h->have_state = true;
@@ -1114,11 +1204,14 @@ int lb_get_state_lc(lb_t* h_, double* f, double* q, double* u) {
   if (!f || !q || !u) return set_err(h, LB_EINVAL, "f, q or u is NULL");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state_lc or lb_init_lc first");
   const Geom& G = h->G;
-  const size_t nloc = (size_t)G.nxy * G.nzl;
-  Slab& s = h->slabs[0];
-  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_planes_to_canon(G, s.A, s.B, h->stream); }));
-  CK(h, cudaMemcpyAsync(f, s.B, Q * nloc * 8, cudaMemcpyDeviceToHost, h->stream));
-  if ((rc = lc_field_d2h(h, q, s.q, 5)) || (rc = lc_field_d2h(h, u, s.u, 3))) return rc;
+  const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_planes_to_canon(G, s.A, s.B, h->stream); }));
+    CK(h, cudaMemcpy2DAsync(f + r * nloc, N * 8, s.B, nloc * 8, nloc * 8, Q, cudaMemcpyDeviceToHost, h->stream));
+    if ((rc = lc_field_d2h(h, q, lc_q0(G, s.q), 5, r * nloc)) || (rc = lc_field_d2h(h, u, lc_u0(G, s.u), 3, r * nloc)))
+      return rc;
+  }
   CK(h, cudaStreamSynchronize(h->stream));
   resolve_pending(h);
   return LB_OK;
@@ -1131,7 +1224,7 @@ int lb_init_lc(lb_t* h_, const double* rho, const double* u, const double* n) {
   if (!n) return set_err(h, LB_EINVAL, "n is NULL");
   const double gam = h->dp.lc_gamma;
   if (!(gam > 8.0 / 3.0)) return set_err(h, LB_EINVAL, "lb_init_lc needs gamma > 8/3 (a nematic bulk minimum)");
-  const size_t nloc = (size_t)h->G.nxy * h->G.nzl;
+  const size_t nloc = host_nloc(h);
   // R45: f = f^eq(rho, u) (R8), Q = S0 (n n - I/3), the stored velocity = u
   const double S0 = 0.25 + 0.75 * std::sqrt(1.0 - 8.0 / (3.0 * gam));
   std::vector<double> f(Q * nloc), q(5 * nloc), uu(3 * nloc, 0.0);

@@ -19,8 +19,11 @@
 // F(k) = div sigma at the site (in-plane columns from sSig, the z column from the
 // sigma_az the thread kept for planes k-1 and k+1: R39); collide f(k) (Guo BGK,
 // R40) and push (A.8); store u' = (j + F/2)/rho; LC update of Q(k) with the stored
-// u (co-rotation R41, upwind advection and Gamma H, R42) -> next Q buffer.  Single
-// periodic slab.
+// u (co-rotation R41, upwind advection and Gamma H, R42) -> next Q buffer.
+// A whole periodic lattice wraps in z; a z-slab reads Q on two ghost planes and u
+// on one at each end (filled by the exchange before the step) and pushes the f
+// components that leave it into the ghost planes of B (sent after the step), as
+// the binary-fluid step does.
 #include "lb_device.cuh"
 #include "lb_tma.cuh"
 
@@ -186,6 +189,9 @@ __global__ void __launch_bounds__(kLT, 1)
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
   auto wz = [&](int z) { return cmod(z, G.nzl); };
+  // plane of the Q and u fields: periodic within a whole-lattice slab, else the
+  // ghost planes (Q: -2 .. nzl+1, u: -1 .. nzl; qA, uA point at plane 0)
+  auto zf = [&](int z) { return G.zwrap ? cmod(z, G.nzl) : z; };
 
   if (tid == 0) {
     mbar_init(&sm.bar[0], 1);
@@ -223,14 +229,14 @@ __global__ void __launch_bounds__(kLT, 1)
   const int bdst = qrow * BX + 2 * qcu;  // same row pitch (36) in both boxes
   auto issue_q = [&](int zp) {
     if (!has_q) return;
-    const double* base = qA + (long long)wz(zp) * 5 * nxy + qsrc;
+    const double* base = qA + (long long)zf(zp) * 5 * nxy + qsrc;
     double(*ring)[NB] = sm.sQ[((zp) & 3)];
 #pragma unroll
     for (int c = 0; c < 5; ++c) cp_async_v<2>(&ring[c][bdst], base + c * nxy);
   };
   auto issue_u = [&](int zp) {
     if (!has_u) return;
-    const double* base = uA + (long long)wz(zp) * 3 * nxy + usrc;
+    const double* base = uA + (long long)zf(zp) * 3 * nxy + usrc;
     double(*ring)[NU] = sm.sU[cmod(zp, 3)];
 #pragma unroll
     for (int a = 0; a < 3; ++a) cp_async_v<2>(&ring[a][bdst], base + a * nxy);
@@ -344,7 +350,10 @@ __global__ void __launch_bounds__(kLT, 1)
       double f[Q];
 #pragma unroll
       for (int i = 0; i < Q; ++i) f[i] = sm.sF[((k) & 1)][frank(i)][tid];
-      const long long zoff[3] = {(long long)wz(k - 1) + GZ, (long long)k + GZ, (long long)wz(k + 1) + GZ};
+      // A.8 push targets: periodic in z for a whole lattice, else planes -1 / nzl are
+      // the ghost planes the exchange sends to the neighbouring slabs
+      double* const zb[3] = {push_plane(G, B, Peers{}, k - 1), push_plane(G, B, Peers{}, k),
+                             push_plane(G, B, Peers{}, k + 1)};
       const double g0[Q] = {};
       double un[3];
       const double rho = collide(
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(kLT, 1)
           [&](int i, double fs, double) {
             const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
             const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-            double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;
+            double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
             __stcs(d + (long long)slot(0, i) * nxy, fs);
           },
           un);
@@ -425,7 +434,7 @@ int lc_zchunk(const Geom& G, int num_sms) {
 cudaError_t launch_step_lc(const Geom& G, const DevParams& p, const double* A, double* B, const double* qA,
                            double* qB, const double* uA, double* uB, int zc, int* flag, const StepMaps* maps,
                            cudaStream_t st) {
-  if (!maps || !maps->ok || maps->ty != kLY || !G.zwrap || G.nx % 2 != 0) return cudaErrorInvalidValue;
+  if (!maps || !maps->ok || maps->ty != kLY || G.nx % 2 != 0) return cudaErrorInvalidValue;
   constexpr size_t smem = sizeof(LcSmem);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
   static bool attr = false;

@@ -88,6 +88,8 @@ class lb_lc_params(C.Structure):
 
 
 _lb_create_lc = _sig("lb_create_lc", _i, _i, _i, _i, C.POINTER(lb_lc_params), C.POINTER(_vp))
+_lb_create_lc_loopback = _sig("lb_create_lc_loopback", _i, _i, _i, _i, C.POINTER(lb_lc_params), _i, C.POINTER(_vp))
+_lb_create_lc_slab = _sig("lb_create_lc_slab", _i, _i, _i, _i, C.POINTER(lb_lc_params), _i, _i, _vp, C.POINTER(_vp))
 _lb_set_state_lc = _sig("lb_set_state_lc", _i, _vp, _vp, _vp, _vp)
 _lb_get_state_lc = _sig("lb_get_state_lc", _i, _vp, _vp, _vp, _vp)
 _lb_init_lc = _sig("lb_init_lc", _i, _vp, _vp, _vp, _vp)
@@ -98,7 +100,7 @@ EXPORTS = [
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
     "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_set_state_ch", "lb_get_state_ch",
-    "lb_create_lc", "lb_set_state_lc", "lb_get_state_lc", "lb_init_lc",
+    "lb_create_lc", "lb_create_lc_loopback", "lb_create_lc_slab", "lb_set_state_lc", "lb_get_state_lc", "lb_init_lc",
 ]
 
 
@@ -290,6 +292,19 @@ def lb_create_lc(nx: int, ny: int, nz: int, params: lb_lc_params):
     return h.value
 
 
+def lb_create_lc_loopback(nx: int, ny: int, nz: int, params: lb_lc_params, nslabs: int):
+    h = _vp()
+    _check(_lb_create_lc_loopback(nx, ny, nz, C.byref(params), nslabs, C.byref(h)), None)
+    return h.value
+
+
+def lb_create_lc_slab(nx: int, ny: int, nz: int, params: lb_lc_params, nranks: int, rank: int, uid: bytes):
+    h = _vp()
+    buf = C.create_string_buffer(uid, 128)
+    _check(_lb_create_lc_slab(nx, ny, nz, C.byref(params), nranks, rank, buf, C.byref(h)), None)
+    return h.value
+
+
 def lb_set_state_lc(h, f, q, u) -> None:
     n = lb_local_sites(h)
     _check(_lb_set_state_lc(h, _ptr(f, Q * n), _ptr(q, 5 * n), _ptr(u, 3 * n)), h)
@@ -395,10 +410,16 @@ class LcLattice(Lattice):
     """A liquid-crystal handle (lb_create_lc, NEXT-4): state (f, Q, u); arrays are
     (19 | 5 | 3, nz, ny, nx)."""
 
-    def __init__(self, nx, ny, nz, params: lb_lc_params | None = None):
+    def __init__(self, nx, ny, nz, params: lb_lc_params | None = None, nslabs: int = 1, nranks: int = 1,
+                 rank: int = 0, uid: bytes | None = None):
         self.params = params or make_lc_params()
-        self.h = lb_create_lc(nx, ny, nz, self.params)
-        self.shape = (nz, ny, nx)
+        if nranks > 1:
+            self.h = lb_create_lc_slab(nx, ny, nz, self.params, nranks, rank, uid)
+            self.shape = (nz // nranks, ny, nx)
+        else:
+            self.h = (lb_create_lc_loopback(nx, ny, nz, self.params, nslabs) if nslabs > 1
+                      else lb_create_lc(nx, ny, nz, self.params))
+            self.shape = (nz, ny, nx)
 
     def set_state(self, f, q, u):
         c = lambda a: np.ascontiguousarray(a, dtype=np.float64).reshape(-1)  # noqa: E731

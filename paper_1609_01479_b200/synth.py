@@ -73,12 +73,23 @@ def sample_sites(nx: int, ny: int, nz: int, n: int, seed: int = 7) -> list[tuple
 
 # ---- NEXT-4 liquid-crystal workload (R45) ------------------------
 def random_directors(nx: int, ny: int, nz: int, seed: int = 0) -> np.ndarray:
-    """Unit vectors n (3, nz, ny, nx), isotropically distributed: three standard
-    normals per site from PCG64 ``default_rng(seed)`` (site-major, canonical
-    site order), divided by their length."""
-    v = _rng(seed).standard_normal((nx * ny * nz, 3))
-    v = v / np.sqrt((v * v).sum(axis=1))[:, None]
-    return np.ascontiguousarray(v.T).reshape(3, nz, ny, nx)
+    """Unit vectors n (3, nz, ny, nx), uniform on the sphere: per site (canonical site
+    order) two uniforms U1, U2 of PCG64 ``default_rng(seed)``, cos(theta) = 2 U1 - 1,
+    phi = 2 pi U2."""
+    return random_directors_slab(nx, ny, nz, 0, nz, seed)
+
+
+def random_directors_slab(nx: int, ny: int, nz: int, z0: int, z1: int, seed: int = 0) -> np.ndarray:
+    """Planes [z0, z1) of ``random_directors(nx, ny, nz, seed)``, bitwise, without drawing
+    the rest (the stream is advanced past the 2 z0 nx ny earlier draws)."""
+    del nz
+    bg = np.random.PCG64(seed)
+    bg.advance(2 * z0 * nx * ny)
+    uv = np.random.Generator(bg).random(2 * nx * ny * (z1 - z0)).reshape(-1, 2)
+    c = 2.0 * uv[:, 0] - 1.0
+    s = np.sqrt(1.0 - c * c)
+    ph = 2.0 * np.pi * uv[:, 1]
+    return np.stack([s * np.cos(ph), s * np.sin(ph), c]).reshape(3, z1 - z0, ny, nx)
 
 
 def rough_lc_fields(nx: int, ny: int, nz: int, seed: int = 3):

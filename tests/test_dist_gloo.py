@@ -157,3 +157,74 @@ def test_slab_decomposed_oracle_equals_whole_lattice(world, shape, tmp_path):
     fs = np.concatenate([np.load(tmp_path / f"f{r}.npy") for r in range(world)], axis=1)
     gs = np.concatenate([np.load(tmp_path / f"g{r}.npy") for r in range(world)], axis=1)
     assert np.array_equal(fs, f) and np.array_equal(gs, g)
+
+
+# ---------------------------------------------------------------- liquid crystal (NEXT-4)
+from oracle import lb_lc as LC  # noqa: E402
+
+LP0 = LC.LcParams(A0=0.2, gamma=2.6, kappa=0.05, xi=-0.4, Gamma=0.5)
+
+
+def slab_step_lc(f, q5, u, p, plan, L):
+    """One LC oracle step on a z-slab with the exchanges of lb_api.cu (exchange_lc before
+    the step: Q planes [L-2, L) up / [0, 2) down, u planes L-1 up / 0 down; after it
+    the f components with c_z = +-1 that left the slab)."""
+    up, dn = plan["up"], plan["down"]
+    _, _, ny, nx = f.shape
+    qb = _sendrecv(q5[:, L - 2:], up, (5, 2, ny, nx), dn)
+    qa = _sendrecv(q5[:, :2], dn, (5, 2, ny, nx), up)
+    ub = _sendrecv(u[:, L - 1:], up, (3, 1, ny, nx), dn)
+    ua = _sendrecv(u[:, :1], dn, (3, 1, ny, nx), up)
+    qe = np.concatenate([qb, q5, qa], axis=1)  # Q planes -2 .. L+1
+    ue = np.concatenate([ub, u, ua], axis=1)  # u planes -1 .. L
+    rho, j = R.density(f), R.momentum(f)
+    LC.check_domain(f, q5, u, rho)
+    Q = LC.q_full(qe)
+    dQ, lapQ = LC.q_gradient(Q), LC.q_laplacian(Q)
+    H = LC.molecular_field(Q, lapQ, p)
+    P = LC.chemical_stress(Q, dQ, H, LC.free_energy_density(Q, dQ, p), p)
+    F = LC.force(P)[:, 2:L + 2]
+    u_new = R.velocity(rho, j, F)
+    fs = R.collide_f(f, rho, u_new, F, p.fluid)
+    q_next = LC.lc_update(Q[:, :, 1:L + 3], ue, H[:, :, 1:L + 3], p)[:, 1:L + 1]
+    o = np.zeros((19, L + 2, ny, nx))
+    for i in range(19):
+        sh = np.roll(fs[i], shift=(int(R.C[i, 1]), int(R.C[i, 0])), axis=(1, 2))
+        o[i, 1 + int(R.C[i, 2]):L + 1 + int(R.C[i, 2])] += sh
+    msg_up = np.stack([o[i, L + 1] for i in CZ_UP])
+    msg_dn = np.stack([o[i, 0] for i in CZ_DN])
+    from_dn = _sendrecv(msg_up, up, msg_up.shape, dn)
+    from_up = _sendrecv(msg_dn, dn, msg_dn.shape, up)
+    for k, i in enumerate(CZ_UP):
+        o[i, 1] = from_dn[k]
+    for k, i in enumerate(CZ_DN):
+        o[i, L] = from_up[k]
+    return o[:, 1:L + 1], q_next, u_new
+
+
+def _lc_rough(nx, ny, nz):
+    rho, u, q5, nf = synth.rough_lc_fields(nx, ny, nz, seed=5)
+    return R.f_equilibrium(rho, u) + nf, q5, u
+
+
+def _slab_body_lc(rank, world, shape, steps, out_dir):
+    nx, ny, nz = shape
+    plan = lb.lb_halo_plan(nx, ny, nz, world, rank)
+    z0, z1 = D.slab_range(nz, world, rank)
+    f, q5, u = (a[:, z0:z1].copy() for a in _lc_rough(nx, ny, nz))
+    for _ in range(steps):
+        f, q5, u = slab_step_lc(f, q5, u, LP0, plan, z1 - z0)
+    for name, a in (("f", f), ("q", q5), ("u", u)):
+        np.save(os.path.join(out_dir, f"{name}{rank}.npy"), a)
+
+
+@pytest.mark.parametrize("world,shape", [(2, (6, 5, 8)), (3, (4, 5, 9)), (4, (4, 4, 8))])
+def test_lc_slab_decomposed_oracle_equals_whole_lattice(world, shape, tmp_path):
+    """The liquid-crystal schedule of lb_create_lc_slab (Q on two halo planes, u on one,
+    f's crossing components), run on the oracle over gloo ranks: bitwise the whole lattice."""
+    steps = 3
+    _run(_slab_body_lc, world, shape, steps, str(tmp_path))
+    ref = LC.run(*_lc_rough(*shape), LP0, steps)
+    for name, a in zip("fqu", ref):
+        got = np.concatenate([np.load(tmp_path / f"{name}{r}.npy") for r in range(world)], axis=1)
+        assert np.array_equal(got, a), name

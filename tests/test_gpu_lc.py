@@ -179,3 +179,33 @@ def test_lc_errors():
         with pytest.raises(lb.LBError) as e:
             L.step(2)
         assert e.value.code == lb.LB_ENUMERIC
+
+
+def gpu_run_slabs(state, p, nsteps, nslabs):
+    f = state[0]
+    nz, ny, nx = f.shape[1:]
+    with lb.LcLattice(nx, ny, nz, cparams(p), nslabs=nslabs) as L:
+        L.set_state(*state)
+        got = L.get_state()
+        for a, b in zip(got, state):  # set/get through the slabs: bitwise
+            assert np.array_equal(a, b)
+        L.step(nsteps)
+        return L.get_state()
+
+
+@pytest.mark.parametrize("nslabs", [2, 4, 8])
+@pytest.mark.parametrize("p", [LP, LP2], ids=["default", "strong"])
+def test_lc_slabs_bitwise_equal_whole_lattice(nslabs, p):
+    """z-slabs on one GPU (loopback: the ghost-plane exchanges of Q, u and f that the
+    ranks do with NCCL) give the bits of the whole periodic lattice; 8 slabs = 2 planes
+    each, so the Q halo is a whole slab."""
+    st = rough(32, 12, 16, seed=63)
+    a = gpu_run(st, p, 3)
+    b = gpu_run_slabs(st, p, 3, nslabs)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_lc_slabs_parity_64cubed():
+    st = quench(64, 64, 64, seed=5)
+    assert_parity(gpu_run_slabs(st, LP, 10, 2), LC.run(*st, LP, 10))
