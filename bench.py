@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--lattice", default="", help="tuning only: NX,NY,NZ per GPU instead of the config's lattice")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -252,6 +253,9 @@ def run_ours(args):
     if world > 1:
         D.init("nccl")
     nx, ny, nzf, scaling, desc = CONFIGS[args.config]
+    if args.lattice:
+        nx, ny, nzl_ = (int(v) for v in args.lattice.split(","))
+        nzf, scaling, desc = (lambda n: nzl_ * n), "weak", f"tuning lattice {nx}x{ny}x{nzl_} per GPU"
     if args.collision == "lc":
         desc = desc.replace("binary fluid", "liquid crystal (Q tensor + D3Q19 fluid, NEXT-4)")
     nz = nzf(world)

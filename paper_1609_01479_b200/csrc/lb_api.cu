@@ -277,6 +277,15 @@ int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, i
   }
   h->ty = step_tile_rows(h->G, h->num_sms);
   h->zc = step_zchunk(h->G, h->num_sms, h->ty);
+  // tuning overrides (measurement only): tile rows 4 | 8, z-chunk planes
+  if (const char* e = std::getenv("LB_TILE_ROWS")) {
+    const int t = std::atoi(e);
+    if (t == 4 || t == 8) h->ty = t, h->zc = step_zchunk(h->G, h->num_sms, h->ty);
+  }
+  if (const char* e = std::getenv("LB_ZCHUNK")) {
+    const int z = std::atoi(e);
+    if (z >= 1) h->zc = z < h->nzl ? z : h->nzl;
+  }
   h->czc = cluster_zchunk(h->G, h->num_sms);
   rc = alloc_slabs(h);
   if (rc) {
@@ -1125,6 +1134,10 @@ int lc_create(int nx, int ny, int nz, const lb_lc_params* lp, int nranks, int ra
   h->dp.lc_xi = lp->xi;
   h->dp.lc_Gamma = lp->Gamma;
   h->lczc = lc_zchunk(h->G, h->num_sms);
+  if (const char* ev = std::getenv("LB_ZCHUNK")) {  // tuning override (measurement only)
+    const int z = std::atoi(ev);
+    if (z >= 1) h->lczc = z < h->nzl ? z : h->nzl;
+  }
   const size_t nq = lc_q_doubles(h->G), nu = lc_u_doubles(h->G);
   cudaError_t e = cudaSuccess;
   bool maps_ok = true;

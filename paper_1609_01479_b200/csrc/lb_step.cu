@@ -550,9 +550,17 @@ cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, doub
 // Tile rows: 8 (one CTA per SM, halo box 1.69x the tile) when the plane has enough
 // tiles to fill the GPU several times over; 4 (two CTAs per SM) for smaller planes,
 // where longer z-chunks matter more than the smaller halo.
+// Tile rows of the step kernel.  Even nx (TMA rows): 32 x 8 tiles and the
+// warp-specialised kernel for every plane size -- measured in round 1 against
+// 32 x 4 tiles of the tile kernel (two CTAs per SM): +12% at 128^3, +17% at 64^3,
+// +30% at 256^3, +7% at 256 x 256 x 32 (the 8-GPU slab of 256^3), equal at
+// 512 x 512 x 64.  Odd nx (per-thread copies): 32 x 4 tiles
+// unless the plane has >= 4 x SMs tiles of 32 x 8.
 int step_tile_rows(const Geom& G, int num_sms) {
+  if (LB_STEP_TY != 8) return 4;
+  if (G.nx % 2 == 0) return 8;
   const long long tiles8 = (long long)((G.nx + kTX - 1) / kTX) * ((G.ny + 7) / 8);
-  return (LB_STEP_TY == 8 && tiles8 >= 4LL * num_sms) ? 8 : 4;
+  return tiles8 >= 4LL * num_sms ? 8 : 4;
 }
 
 bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out) {
@@ -569,12 +577,30 @@ bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out) {
   return true;
 }
 
-// number of z-chunks: enough CTAs to fill the GPU several times, chunks >= 8 planes
+// Planes per z-chunk (one CTA = one tile x one z-chunk).
+// 32 x 8 tiles (one CTA per SM), from round-1 sweeps:
+//  * fewer tiles than SMs: one wave -- as many chunks as fit beside each other on
+//    the SMs (>= 8 planes each): 128^3 -> 2 x 64 planes, 64^3 -> 8 x 8;
+//  * otherwise chunks of 32 planes (best at 512 x 512 x 64 and 256^3: more planes
+//    per chunk lost up to 8%), or 16 when 32 leaves fewer than 4 waves of CTAs
+//    (256 x 256 x 64: +2%).
+// 32 x 4 tiles (odd nx): enough CTAs to fill the GPU several times, chunks >= 8.
 int step_zchunk(const Geom& G, int num_sms, int ty) {
   const long long tiles = (long long)((G.nx + kTX - 1) / kTX) * ((G.ny + ty - 1) / ty);
-  const long long target = (long long)LB_STEP_WAVES * num_sms;
-  long long nchunks = (target + tiles - 1) / tiles;
   const long long maxchunks = G.nzl >= 16 ? G.nzl / 8 : 1;
+  long long nchunks;
+  if (ty == 8) {
+    if (tiles < num_sms) {
+      nchunks = num_sms / tiles;
+    } else {
+      int zc = G.nzl < 32 ? G.nzl : 32;
+      if (zc == 32 && tiles * ((G.nzl + 31) / 32) < 4LL * num_sms) zc = 16;
+      nchunks = (G.nzl + zc - 1) / zc;
+    }
+  } else {
+    const long long target = (long long)LB_STEP_WAVES * num_sms;
+    nchunks = (target + tiles - 1) / tiles;
+  }
   if (nchunks > maxchunks) nchunks = maxchunks;
   if (nchunks < 1) nchunks = 1;
   return (int)((G.nzl + nchunks - 1) / nchunks);

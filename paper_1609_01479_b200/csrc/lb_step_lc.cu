@@ -423,8 +423,10 @@ __global__ void __launch_bounds__(kLT, 1)
 
 int lc_zchunk(const Geom& G, int num_sms) {
   const long long tiles = (long long)((G.nx + kLX - 1) / kLX) * ((G.ny + kLY - 1) / kLY);
-  // >= 3 waves of one CTA per SM; chunks of >= 16 planes (the prologue costs two planes)
-  long long nchunks = (3LL * num_sms + tiles - 1) / tiles;
+  // fewer tiles than SMs: one wave, as many chunks as fit beside each other (128^3:
+  // 2 x 64 planes, +11% over 3 waves of 19-plane chunks); otherwise >= 3 waves of one
+  // CTA per SM; chunks of >= 16 planes (the prologue costs two planes)
+  long long nchunks = tiles < num_sms ? num_sms / tiles : (3LL * num_sms + tiles - 1) / tiles;
   const long long maxchunks = G.nzl >= 32 ? G.nzl / 16 : 1;
   if (nchunks > maxchunks) nchunks = maxchunks;
   if (nchunks < 1) nchunks = 1;
