@@ -265,10 +265,8 @@ def run_ours(args):
     uid = None
     if world > 1:
         uid = D.broadcast_bytes(lb.lb_nccl_get_unique_id() if rank == 0 else None)
-    if args.collision == "ch" and world > 1:
-        raise SystemExit("--collision ch: the Cahn-Hilliard variant is single-slab (one GPU)")
-    if args.collision == "ch":
-        L = lb.ChLattice(nx, ny, nz, params, 0.8, 1.1, 1.0)
+    if args.collision == "ch":  # z-slabs with NCCL halos under torchrun
+        L = lb.ChLattice(nx, ny, nz, params, 0.8, 1.1, 1.0, nranks=world, rank=rank, uid=uid)
     elif args.collision == "lc":  # R44 defaults; z-slabs with NCCL halos under torchrun
         L = lb.LcLattice(nx, ny, nz, lb.make_lc_params(), nranks=world, rank=rank, uid=uid)
     else:

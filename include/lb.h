@@ -174,13 +174,23 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
  *   J = u_f * phi_upwind, u_f = (u(x) + u(x + e_a))/2, u = j/rho   (R30, R31)
  * instead of the g distribution, and f collides with the chemical stress in
  * its equilibrium and a three-rate MRT (model 1 of lb_set_collision, R32).
- * One periodic lattice on the current GPU (no slabs); nx even, else LB_EINVAL;
+ * A periodic lattice on the current GPU (or z-slabs, below); nx even, else LB_EINVAL;
  * tau_f and tau_g of params are unused, M enters the update directly.
  * lb_step, lb_get_phi, lb_init_equilibrium (f = f^eq(rho, u) of R8, phi as
  * given), lb_destroy work as for other handles; lb_set_state / lb_get_state
  * return LB_EINVAL (use the _ch pair: f canonical 19*nloc doubles, phi nloc). */
 int lb_create_ch(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk,
                  double tau_ghost, lb_t** out);
+/* The same variant on z-slabs (nz % slabs == 0, nz/slabs >= 2), in one handle on this
+ * GPU (loopback; host arrays = the whole lattice) or one rank per GPU (collective;
+ * host arrays = this rank's slab).  Before each step the f planes z_lo / z_hi (all
+ * 19 components: u = j/rho at z +- 1) go to the neighbours' ghost planes and phi
+ * two planes each way; after it, the f components that left the slab.  Bitwise
+ * equal to lb_create_ch. */
+int lb_create_ch_loopback(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk,
+                          double tau_ghost, int nslabs, lb_t** out);
+int lb_create_ch_slab(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk,
+                      double tau_ghost, int nranks, int rank, const void* id128, lb_t** out);
 int lb_set_state_ch(lb_t* h, const double* f, const double* phi);
 int lb_get_state_ch(lb_t* h, double* f, double* phi);
 

@@ -166,6 +166,7 @@ size_t lc_u_doubles(const Geom& G) { return (size_t)(G.nzl + 2 * LC_GU) * 3 * (s
 double* lc_q0(const Geom& G, double* q) { return q + (size_t)LC_GQ * 5 * G.nxy; }  // plane 0
 double* lc_u0(const Geom& G, double* u) { return u + (size_t)LC_GU * 3 * G.nxy; }
 int exchange_lc(lb_ctx* h);  // Q / u halos of the liquid-crystal slabs (defined with the LC calls)
+int exchange_fedge(lb_ctx* h);  // f edge planes of the Cahn-Hilliard slabs (defined with lb_create_ch)
 
 // ---- profiling -------------------------------------------------------------
 template <class Fn>
@@ -444,16 +445,20 @@ int one_step(lb_ctx* h, int mode) {
     }
     return LB_OK;
   }
-  if (h->ch && mode >= 0) {
-    Slab& s = h->slabs[0];
-    CK(h, timed(h, K_STEP, true, [&]() {
-         return launch_step_ch(G, h->dp, s.A, s.B, s.phi, s.phi2, h->zc, h->d_flag, &s.chA, h->stream);
-       }));
-    std::swap(s.A, s.B);
-    std::swap(s.mapsA, s.mapsB);
-    std::swap(s.cmapsA, s.cmapsB);
-    std::swap(s.chA, s.chB);
-    std::swap(s.phi, s.phi2);
+  if (h->ch && mode >= 0) {  // f edge planes and phi halos; the step; f halo
+    if (!G.zwrap && ((rc = exchange_fedge(h)) || (rc = exchange_phi(h)))) return rc;
+    for (auto& s : h->slabs)
+      CK(h, timed(h, K_STEP, true, [&]() {
+           return launch_step_ch(G, h->dp, s.A, s.B, s.phi, s.phi2, h->zc, h->d_flag, &s.chA, h->stream);
+         }));
+    if (!G.zwrap && (rc = exchange_dist(h))) return rc;
+    for (auto& s : h->slabs) {
+      std::swap(s.A, s.B);
+      std::swap(s.mapsA, s.mapsB);
+      std::swap(s.cmapsA, s.cmapsB);
+      std::swap(s.chA, s.chB);
+      std::swap(s.phi, s.phi2);
+    }
     return LB_OK;
   }
   if (mode < 0) {
@@ -601,6 +606,98 @@ int open_peers(lb_ctx* h) {
 
 // host (whole lattice for loopback, this rank's slab for NCCL) <-> canonical staging in B
 size_t host_nloc(const lb_ctx* h) { return (size_t)h->G.nxy * h->nzl * h->nslabs; }
+
+}  // namespace
+
+namespace {
+
+// Cahn-Hilliard slabs: f's edge planes (the 19 f slots of planes 0 and nzl-1 of the
+// current state A) to the neighbours' ghost planes nzl and -1 of A, where the
+// kernel's f box reads them for u = j / rho at z +- 1 (three slot runs each way).
+int exchange_fedge(lb_ctx* h) {
+  const Geom& G = h->G;
+  const int run0[3] = {0, 10, 28}, rlen[3] = {5, 9, 5};
+  if (h->nranks > 1) {
+    Slab& s = h->slabs[0];
+    const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
+    cudaError_t ce = timed(h, K_HALO_DIST, false, [&]() {
+      ncclGroupStart();
+      for (int r = 0; r < 3; ++r) {
+        const size_t cnt = (size_t)rlen[r] * G.nxy;
+        ncclSend(s.A + dist_index(G, G.nzl - 1, run0[r], 0), cnt, ncclDouble, up, h->comm, h->stream);
+        ncclRecv(s.A + dist_index(G, -1, run0[r], 0), cnt, ncclDouble, dn, h->comm, h->stream);
+        ncclSend(s.A + dist_index(G, 0, run0[r], 0), cnt, ncclDouble, dn, h->comm, h->stream);
+        ncclRecv(s.A + dist_index(G, G.nzl, run0[r], 0), cnt, ncclDouble, up, h->comm, h->stream);
+      }
+      return ncclGroupEnd() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+    });
+    if (ce != cudaSuccess) return set_err(h, LB_ENCCL, "NCCL f edge-plane exchange failed");
+    return LB_OK;
+  }
+  for (int i = 0; i < h->nslabs; ++i) {
+    Slab& s = h->slabs[i];
+    Slab& up = h->slabs[(i + 1) % h->nslabs];
+    Slab& dn = h->slabs[(i - 1 + h->nslabs) % h->nslabs];
+    CK(h, timed(h, K_HALO_DIST, false, [&]() {
+      cudaError_t e = cudaSuccess;
+      for (int r = 0; r < 3 && e == cudaSuccess; ++r) {
+        const size_t bytes = (size_t)rlen[r] * G.nxy * 8;
+        e = cudaMemcpyAsync(up.A + dist_index(G, -1, run0[r], 0), s.A + dist_index(G, G.nzl - 1, run0[r], 0), bytes,
+                            cudaMemcpyDeviceToDevice, h->stream);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(dn.A + dist_index(G, G.nzl, run0[r], 0), s.A + dist_index(G, 0, run0[r], 0), bytes,
+                              cudaMemcpyDeviceToDevice, h->stream);
+      }
+      return e;
+    }));
+  }
+  return LB_OK;
+}
+
+int ch_create(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk, double tau_ghost,
+              int nranks, int rank, int nslabs, const void* id128, lb_t** out) {
+  if (out) *out = nullptr;
+  if (nx % 2 != 0) return set_err(nullptr, LB_EINVAL, "the Cahn-Hilliard variant needs nx even (TMA rows)");
+  for (double t : {tau_shear, tau_bulk, tau_ghost})
+    if (!std::isfinite(t) || !(t > 0.5)) return set_err(nullptr, LB_EINVAL, "MRT relaxation times must be finite and > 0.5");
+  if (nranks > 1 && !id128) return set_err(nullptr, LB_EINVAL, "id128 is NULL");
+  int rc = create_common(nx, ny, nz, params, nranks, rank, nslabs, out);
+  if (rc) return rc;
+  lb_ctx* h = *out;
+  h->ch = true;
+  h->halo_mode = 0;  // ghost planes + copies / NCCL send-recv
+  h->dp.coll = 1;
+  h->dp.inv_tau_s = 1.0 / tau_shear;
+  h->dp.inv_tau_b = 1.0 / tau_bulk;
+  h->dp.inv_tau_ghost = 1.0 / tau_ghost;
+  cudaError_t e = cudaSuccess;
+  bool maps_ok = true;
+  for (auto& s : h->slabs) {
+    if (e == cudaSuccess) e = cudaMalloc(&s.phi2, phi_doubles(h->G) * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemsetAsync(s.phi2, 0xff, phi_doubles(h->G) * sizeof(double), h->stream);
+    maps_ok = maps_ok && make_ch_maps(h->G, s.A, h->ty, &s.chA) && make_ch_maps(h->G, s.B, h->ty, &s.chB);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess || !maps_ok) {
+    g_create_error = "Cahn-Hilliard handle: allocation or TMA descriptor failed";
+    lb_destroy(h);
+    *out = nullptr;
+    return e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA;
+  }
+  if (nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      g_create_error = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      h->comm = nullptr;
+      lb_destroy(h);
+      *out = nullptr;
+      return LB_ENCCL;
+    }
+  }
+  return LB_OK;
+}
 
 }  // namespace
 
@@ -889,28 +986,17 @@ int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out) {
 
 int lb_create_ch(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk, double tau_ghost,
                  lb_t** out) {
-  if (nx % 2 != 0) return set_err(nullptr, LB_EINVAL, "the Cahn-Hilliard variant needs nx even (TMA rows)");
-  for (double t : {tau_shear, tau_bulk, tau_ghost})
-    if (!std::isfinite(t) || !(t > 0.5)) return set_err(nullptr, LB_EINVAL, "MRT relaxation times must be finite and > 0.5");
-  int rc = create_common(nx, ny, nz, params, 1, 0, 1, out);
-  if (rc) return rc;
-  lb_ctx* h = *out;
-  h->ch = true;
-  h->dp.coll = 1;
-  h->dp.inv_tau_s = 1.0 / tau_shear;
-  h->dp.inv_tau_b = 1.0 / tau_bulk;
-  h->dp.inv_tau_ghost = 1.0 / tau_ghost;
-  Slab& s = h->slabs[0];
-  cudaError_t e = cudaMalloc(&s.phi2, phi_doubles(h->G) * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemsetAsync(s.phi2, 0xff, phi_doubles(h->G) * sizeof(double), h->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-  if (e != cudaSuccess || !make_ch_maps(h->G, s.A, h->ty, &s.chA) || !make_ch_maps(h->G, s.B, h->ty, &s.chB)) {
-    g_create_error = "Cahn-Hilliard handle: allocation or TMA descriptor failed";
-    lb_destroy(h);
-    *out = nullptr;
-    return e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA;
-  }
-  return LB_OK;
+  return ch_create(nx, ny, nz, params, tau_shear, tau_bulk, tau_ghost, 1, 0, 1, nullptr, out);
+}
+
+int lb_create_ch_loopback(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk,
+                          double tau_ghost, int nslabs, lb_t** out) {
+  return ch_create(nx, ny, nz, params, tau_shear, tau_bulk, tau_ghost, 1, 0, nslabs, nullptr, out);
+}
+
+int lb_create_ch_slab(int nx, int ny, int nz, const lb_params* params, double tau_shear, double tau_bulk,
+                      double tau_ghost, int nranks, int rank, const void* id128, lb_t** out) {
+  return ch_create(nx, ny, nz, params, tau_shear, tau_bulk, tau_ghost, nranks, rank, 1, id128, out);
 }
 
 int lb_set_state_ch(lb_t* h, const double* f, const double* phi) {
@@ -919,12 +1005,14 @@ int lb_set_state_ch(lb_t* h, const double* f, const double* phi) {
   if (!h->ch) return set_err(h, LB_EINVAL, "not a Cahn-Hilliard handle");
   if (!f || !phi) return set_err(h, LB_EINVAL, "f or phi is NULL");
   const Geom& G = h->G;
-  const size_t nloc = (size_t)G.nxy * G.nzl;
-  Slab& s = h->slabs[0];
-  CK(h, cudaMemcpyAsync(s.B, f, Q * nloc * 8, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaMemsetAsync(s.B + Q * nloc, 0, Q * nloc * 8, h->stream));  // the g slots are not used
-  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_canon_to_planes(G, s.B, s.A, h->stream); }));
-  CK(h, cudaMemcpyAsync(s.phi + phi_plane_index(G, 0), phi, nloc * 8, cudaMemcpyHostToDevice, h->stream));
+  const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    CK(h, cudaMemcpy2DAsync(s.B, nloc * 8, f + r * nloc, N * 8, nloc * 8, Q, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemsetAsync(s.B + Q * nloc, 0, Q * nloc * 8, h->stream));  // the g slots are not used
+    CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_canon_to_planes(G, s.B, s.A, h->stream); }));
+    CK(h, cudaMemcpyAsync(s.phi + phi_plane_index(G, 0), phi + r * nloc, nloc * 8, cudaMemcpyHostToDevice, h->stream));
+  }
   CK(h, cudaStreamSynchronize(h->stream));
   resolve_pending(h);
   h->have_state = true;
@@ -938,11 +1026,13 @@ int lb_get_state_ch(lb_t* h, double* f, double* phi) {
   if (!f || !phi) return set_err(h, LB_EINVAL, "f or phi is NULL");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state_ch or lb_init_equilibrium first");
   const Geom& G = h->G;
-  const size_t nloc = (size_t)G.nxy * G.nzl;
-  Slab& s = h->slabs[0];
-  CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_planes_to_canon(G, s.A, s.B, h->stream); }));
-  CK(h, cudaMemcpyAsync(f, s.B, Q * nloc * 8, cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaMemcpyAsync(phi, s.phi + phi_plane_index(G, 0), nloc * 8, cudaMemcpyDeviceToHost, h->stream));
+  const size_t nloc = (size_t)G.nxy * G.nzl, N = host_nloc(h);
+  for (int r = 0; r < h->nslabs; ++r) {
+    Slab& s = h->slabs[r];
+    CK(h, timed(h, K_PERMUTE, true, [&]() { return launch_planes_to_canon(G, s.A, s.B, h->stream); }));
+    CK(h, cudaMemcpy2DAsync(f + r * nloc, N * 8, s.B, nloc * 8, nloc * 8, Q, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(phi + r * nloc, s.phi + phi_plane_index(G, 0), nloc * 8, cudaMemcpyDeviceToHost, h->stream));
+  }
   CK(h, cudaStreamSynchronize(h->stream));
   resolve_pending(h);
   return LB_OK;

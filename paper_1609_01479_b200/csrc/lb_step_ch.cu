@@ -19,8 +19,9 @@
 // Iteration k: wait f(k+1), phi(k+2) -> u(k+1), mu(k+1) on the halo box; f(k)
 // to registers; issue f(k+2), phi(k+3); P(k) at the site (R4); collide f and
 // push (A.8); phi(k+1 step) = phi - div J + M lap mu (R30, R31) -> next phi
-// buffer.  Single periodic slab (the slab transport of this variant would also
-// have to carry f's edge planes for u at z +- 1: not built).
+// buffer.  A z-slab reads f's edge planes of its neighbours (for u at z +- 1) and
+// phi on two planes from ghost planes, and pushes the leaving f components into
+// the ghost planes of B, like the other step kernels.
 #include "lb_device.cuh"
 #include "lb_tma.cuh"
 
@@ -78,6 +79,9 @@ __global__ void __launch_bounds__(kCX* TY, 1)
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
   auto wz = [&](int z) { return cmod(z, G.nzl); };
+  // plane read at z: periodic within a whole-lattice slab, else the ghost planes
+  // (f: -1 and nzl, holding the neighbours' edge planes; phi: -2 .. nzl+1)
+  auto zf = [&](int z) { return G.zwrap ? wz(z) : z; };
 
   if (tid == 0) {
     for (int b = 0; b < NBUF; ++b) mbar_init(&sm.bar[b], 1);
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
   }
   auto issue_f = [&](int zp) {
     const int b = cmod(zp, NBUF);
-    const int zs = wz(zp);
+    const int zs = zf(zp);
     if (fbox_tma) {
       if (tid == 0) {
         fence_proxy_async();
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     pb_dst[r] = u < PBU ? row * BX + cu * 2 : -1;
   }
   auto issue_phi = [&](int zp) {
-    const double* base = phiA + phi_plane_index(G, wz(zp));
+    const double* base = phiA + phi_plane_index(G, zf(zp));
     double* ring = sm.sPhi[cmod(zp, 5)];
 #pragma unroll
     for (int r = 0; r < PBR; ++r)
@@ -249,12 +253,13 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     double P6[6];
     stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp - zm), lap, P6);
     // collide f (R23-R25) and push (A.8); g is not used in this variant
-    const long long zoff[3] = {(long long)wz(k - 1) + GZ, (long long)k + GZ, (long long)wz(k + 1) + GZ};
+    double* const zb[3] = {push_plane(G, B, Peers{}, k - 1), push_plane(G, B, Peers{}, k),
+                           push_plane(G, B, Peers{}, k + 1)};  // A.8; ghost planes for slabs
     const double g0[Q] = {};
     const double rho = collide_mrt(p, f, g0, 0.0, 0.0, P6, [&](int i, double fs, double) {
       const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
       const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-      double* d = B + zoff[cz(i) + 1] * G.plane + (long long)yd * G.nx + xd;
+      double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
       __stcs(d + (long long)slot(0, i) * nxy, fs);
     });
     // phi update (R30, R31): upwind fluxes through the six faces, M lap mu
@@ -310,7 +315,7 @@ bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out) {
 
 cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
                            double* phiB, int zc, int* flag, const ChMaps* maps, cudaStream_t st) {
-  if (!maps || !maps->ok || !G.zwrap) return cudaErrorInvalidValue;
+  if (!maps || !maps->ok) return cudaErrorInvalidValue;
   if (maps->ty == 8) return launch_ch_t<8>(G, p, A, B, phiA, phiB, zc, flag, maps, st);
   return launch_ch_t<4>(G, p, A, B, phiA, phiB, zc, flag, maps, st);
 }

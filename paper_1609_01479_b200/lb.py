@@ -78,6 +78,10 @@ _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
 _lb_set_collision = _sig("lb_set_collision", _i, _vp, _i, C.c_double, C.c_double, C.c_double)
 _lb_create_ch = _sig("lb_create_ch", _i, _i, _i, _i, C.POINTER(lb_params), C.c_double, C.c_double, C.c_double,
                      C.POINTER(_vp))
+_lb_create_ch_loopback = _sig("lb_create_ch_loopback", _i, _i, _i, _i, C.POINTER(lb_params), C.c_double, C.c_double,
+                              C.c_double, _i, C.POINTER(_vp))
+_lb_create_ch_slab = _sig("lb_create_ch_slab", _i, _i, _i, _i, C.POINTER(lb_params), C.c_double, C.c_double,
+                          C.c_double, _i, _i, _vp, C.POINTER(_vp))
 _lb_set_state_ch = _sig("lb_set_state_ch", _i, _vp, _vp, _vp)
 _lb_get_state_ch = _sig("lb_get_state_ch", _i, _vp, _vp, _vp)
 
@@ -99,7 +103,8 @@ EXPORTS = [
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
-    "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_set_state_ch", "lb_get_state_ch",
+    "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_create_ch_loopback", "lb_create_ch_slab", "lb_set_state_ch",
+    "lb_get_state_ch",
     "lb_create_lc", "lb_create_lc_loopback", "lb_create_lc_slab", "lb_set_state_lc", "lb_get_state_lc", "lb_init_lc",
 ]
 
@@ -268,6 +273,22 @@ def lb_create_ch(nx: int, ny: int, nz: int, params: lb_params, tau_shear=0.8, ta
     return h.value
 
 
+def lb_create_ch_loopback(nx: int, ny: int, nz: int, params: lb_params, tau_shear, tau_bulk, tau_ghost, nslabs: int):
+    h = _vp()
+    _check(_lb_create_ch_loopback(nx, ny, nz, C.byref(params), tau_shear, tau_bulk, tau_ghost, nslabs, C.byref(h)),
+           None)
+    return h.value
+
+
+def lb_create_ch_slab(nx: int, ny: int, nz: int, params: lb_params, tau_shear, tau_bulk, tau_ghost, nranks: int,
+                      rank: int, uid: bytes):
+    h = _vp()
+    buf = C.create_string_buffer(uid, 128)
+    _check(_lb_create_ch_slab(nx, ny, nz, C.byref(params), tau_shear, tau_bulk, tau_ghost, nranks, rank, buf,
+                              C.byref(h)), None)
+    return h.value
+
+
 def lb_set_state_ch(h, f, phi) -> None:
     n = lb_local_sites(h)
     _check(_lb_set_state_ch(h, _ptr(f, Q * n), _ptr(phi, n)), h)
@@ -392,10 +413,17 @@ class Lattice:
 class ChLattice(Lattice):
     """A finite-difference Cahn-Hilliard handle (lb_create_ch): state (f, phi)."""
 
-    def __init__(self, nx, ny, nz, params: lb_params | None = None, tau_shear=0.8, tau_bulk=1.1, tau_ghost=1.0):
+    def __init__(self, nx, ny, nz, params: lb_params | None = None, tau_shear=0.8, tau_bulk=1.1, tau_ghost=1.0,
+                 nslabs: int = 1, nranks: int = 1, rank: int = 0, uid: bytes | None = None):
         self.params = params or make_params()
-        self.h = lb_create_ch(nx, ny, nz, self.params, tau_shear, tau_bulk, tau_ghost)
-        self.shape = (nz, ny, nx)
+        t = (tau_shear, tau_bulk, tau_ghost)
+        if nranks > 1:
+            self.h = lb_create_ch_slab(nx, ny, nz, self.params, *t, nranks, rank, uid)
+            self.shape = (nz // nranks, ny, nx)
+        else:
+            self.h = (lb_create_ch_loopback(nx, ny, nz, self.params, *t, nslabs) if nslabs > 1
+                      else lb_create_ch(nx, ny, nz, self.params, *t))
+            self.shape = (nz, ny, nx)
 
     def set_state(self, f, phi):
         lb_set_state_ch(self.h, np.ascontiguousarray(f, dtype=np.float64).reshape(-1),

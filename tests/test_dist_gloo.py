@@ -228,3 +228,77 @@ def test_lc_slab_decomposed_oracle_equals_whole_lattice(world, shape, tmp_path):
     for name, a in zip("fqu", ref):
         got = np.concatenate([np.load(tmp_path / f"{name}{r}.npy") for r in range(world)], axis=1)
         assert np.array_equal(got, a), name
+
+
+# ---------------------------------------------------------------- Cahn-Hilliard (NEXT-2)
+from oracle import lb_ch as CH  # noqa: E402
+from oracle import lb_mrt as MRT  # noqa: E402
+
+CP0 = CH.ChParams(base=R.Params(mobility=0.2))
+
+
+def slab_step_ch(f, phi, p, plan, L):
+    """One Cahn-Hilliard oracle step on a z-slab with the exchanges of lb_api.cu
+    (exchange_fedge + exchange_phi before the step: f planes L-1 up / 0 down, all 19
+    components; phi planes [L-2, L) up / [0, 2) down; after it the leaving f
+    components)."""
+    up, dn = plan["up"], plan["down"]
+    _, _, ny, nx = f.shape
+    fb = _sendrecv(f[:, L - 1:], up, (19, 1, ny, nx), dn)
+    fa = _sendrecv(f[:, :1], dn, (19, 1, ny, nx), up)
+    pb = _sendrecv(phi[L - 2:], up, (2, ny, nx), dn)
+    pa = _sendrecv(phi[:2], dn, (2, ny, nx), up)
+    fe = np.concatenate([fb, f, fa], axis=1)  # f planes -1 .. L
+    pe = np.concatenate([pb, phi, pa])  # phi planes -2 .. L+1
+    b = p.base
+    rho_e, j_e = R.density(fe), R.momentum(fe)
+    u_e = MRT.velocity(rho_e, j_e)  # planes -1 .. L
+    grad_e, lap_e = R.gradient(pe), R.laplacian(pe)
+    mu_e = R.chemical_potential(pe, lap_e, b)
+    P = R.chemical_stress(pe, grad_e, lap_e, b)[:, :, 2:L + 2]
+    rho, u = rho_e[1:L + 1], u_e[:, 1:L + 1]
+    CH.check_domain(f, phi, rho)
+    fs = MRT.collide_f(f, rho, u, P, p.mrt)
+    phi_next = CH.phi_update(pe[1:L + 3], u_e, mu_e[1:L + 3], p)[1:L + 1]
+    o = np.zeros((19, L + 2, ny, nx))
+    for i in range(19):
+        sh = np.roll(fs[i], shift=(int(R.C[i, 1]), int(R.C[i, 0])), axis=(1, 2))
+        o[i, 1 + int(R.C[i, 2]):L + 1 + int(R.C[i, 2])] += sh
+    msg_up = np.stack([o[i, L + 1] for i in CZ_UP])
+    msg_dn = np.stack([o[i, 0] for i in CZ_DN])
+    from_dn = _sendrecv(msg_up, up, msg_up.shape, dn)
+    from_up = _sendrecv(msg_dn, dn, msg_dn.shape, up)
+    for k, i in enumerate(CZ_UP):
+        o[i, 1] = from_dn[k]
+    for k, i in enumerate(CZ_DN):
+        o[i, L] = from_up[k]
+    return o[:, 1:L + 1], phi_next
+
+
+def _ch_rough(nx, ny, nz):
+    rho, u, phi, nf, _ = synth.rough_fields(nx, ny, nz, seed=6)
+    return R.f_equilibrium(rho, u) + nf, phi
+
+
+def _slab_body_ch(rank, world, shape, steps, out_dir):
+    nx, ny, nz = shape
+    plan = lb.lb_halo_plan(nx, ny, nz, world, rank)
+    z0, z1 = D.slab_range(nz, world, rank)
+    f, phi = _ch_rough(nx, ny, nz)
+    f, phi = f[:, z0:z1].copy(), phi[z0:z1].copy()
+    for _ in range(steps):
+        f, phi = slab_step_ch(f, phi, CP0, plan, z1 - z0)
+    np.save(os.path.join(out_dir, f"f{rank}.npy"), f)
+    np.save(os.path.join(out_dir, f"p{rank}.npy"), phi)
+
+
+@pytest.mark.parametrize("world,shape", [(2, (6, 5, 8)), (3, (4, 5, 9)), (4, (4, 4, 8))])
+def test_ch_slab_decomposed_oracle_equals_whole_lattice(world, shape, tmp_path):
+    """The Cahn-Hilliard schedule of lb_create_ch_slab on the oracle over gloo ranks:
+    bitwise the whole lattice."""
+    steps = 3
+    _run(_slab_body_ch, world, shape, steps, str(tmp_path))
+    f, phi = CH.run(*_ch_rough(*shape), CP0, steps)
+    fs = np.concatenate([np.load(tmp_path / f"f{r}.npy") for r in range(world)], axis=1)
+    ps = np.concatenate([np.load(tmp_path / f"p{r}.npy") for r in range(world)], axis=0)
+    assert np.array_equal(fs, f) and np.array_equal(ps, phi)

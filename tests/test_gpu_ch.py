@@ -118,3 +118,29 @@ def test_ch_init_equilibrium_and_errors():
     with pytest.raises(lb.LBError) as e:
         lb.ChLattice(15, 8, 8)  # nx odd
     assert e.value.code == lb.LB_EINVAL
+
+
+def gpu_run_slabs(f, phi, cp, nsteps, nslabs):
+    nz, ny, nx = f.shape[1:]
+    with lb.ChLattice(nx, ny, nz, cparams(cp.base), cp.tau_s, cp.tau_b, cp.tau_ghost, nslabs=nslabs) as L:
+        L.set_state(f, phi)
+        f0, p0 = L.get_state()
+        assert np.array_equal(f0, f) and np.array_equal(p0, phi)  # set/get through the slabs: bitwise
+        L.step(nsteps)
+        return L.get_state()
+
+
+@pytest.mark.parametrize("nslabs", [2, 4, 8])
+def test_ch_slabs_bitwise_equal_whole_lattice(nslabs):
+    """z-slabs on one GPU (loopback: f edge planes and phi halos before the step, the
+    leaving f components after it -- the exchanges the ranks do with NCCL) give the
+    bits of the whole periodic lattice; 8 slabs = 2 planes each."""
+    f, phi = rough(32, 12, 16, seed=53)
+    f1, p1 = gpu_run(f, phi, CP, 3)
+    f2, p2 = gpu_run_slabs(f, phi, CP, 3, nslabs)
+    assert np.array_equal(f1, f2) and np.array_equal(p1, p2)
+
+
+def test_ch_slabs_parity_64cubed():
+    f, phi = spinodal(64, 64, 64, seed=6)
+    assert_parity(gpu_run_slabs(f, phi, CP, 10, 2), CH.run(f, phi, CP, 10))
