@@ -144,3 +144,26 @@ def test_ch_slabs_bitwise_equal_whole_lattice(nslabs):
 def test_ch_slabs_parity_64cubed():
     f, phi = spinodal(64, 64, 64, seed=6)
     assert_parity(gpu_run_slabs(f, phi, CP, 10, 2), CH.run(f, phi, CP, 10))
+
+
+def test_ch_parity_bench_launch_sampled():
+    """bench.py --collision ch: 512 x 512 x 64, lb_init_equilibrium (f = f^eq(1, 0),
+    phi as given), one step, sampled sites against the oracle on radius-4 windows."""
+    from sitewin import centre, window
+
+    nx, ny, nz = 512, 512, 64
+    phi = synth.spinodal_phi(nx, ny, nz, seed=0)
+    with lb.ChLattice(nx, ny, nz, cparams(R.Params()), 0.8, 1.1, 1.0) as L:
+        L.init_equilibrium(phi)
+        L.step(1)
+        f1, p1 = L.get_state()
+    cp = CH.ChParams(base=R.Params(), tau_s=0.8, tau_b=1.1, tau_ghost=1.0)
+    fs, ps, fr, pr = [], [], [], []
+    for (x, y, z) in synth.sample_sites(nx, ny, nz, 40, seed=14):
+        pw = window(phi, x, y, z, 4)
+        sh = pw.shape
+        fo, po = CH.step(R.f_equilibrium(np.ones(sh), np.zeros((3,) + sh)), pw, cp)
+        fr.append(centre(fo)), pr.append(centre(po))
+        fs.append(f1[:, z, y, x]), ps.append(p1[z, y, x])
+    assert rel(np.array(fs), np.array(fr)) <= TOL
+    assert rel(np.array(ps), np.array(pr)) <= TOL

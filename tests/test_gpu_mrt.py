@@ -147,3 +147,27 @@ def test_mrt_set_collision_errors_and_model_switch():
         lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
         with pytest.raises(lb.LBError):
             lb.lb_debug_step_kernel(L.h, 2)  # the cluster kernel is model 0 only
+
+
+def test_mrt_parity_bench_launch_sampled():
+    """bench.py --collision mrt: 512 x 512 x 64, lb_init_equilibrium on the spinodal
+    phi, one step, sampled sites against the oracle on windows."""
+    from sitewin import centre, crop, window
+
+    nx, ny, nz = 512, 512, 64
+    phi = synth.spinodal_phi(nx, ny, nz, seed=0)
+    with lb.Lattice(nx, ny, nz, cparams(P0)) as L:
+        lb.lb_set_collision(L.h, 1, MP.tau_s, MP.tau_b, MP.tau_ghost)
+        L.init_equilibrium(phi)
+        L.step(1)
+        f1, g1 = L.get_state()
+    fs, gs, fr, gr = [], [], [], []
+    for (x, y, z) in synth.sample_sites(nx, ny, nz, 40, seed=13):
+        pw = window(phi, x, y, z, 5)
+        sh = pw.shape
+        f0, g0 = R.equilibrium_state(np.ones(sh), np.zeros((3,) + sh), pw, P0)
+        fo, go = M.step(crop(f0), crop(g0), MP)
+        fr.append(centre(fo)), gr.append(centre(go))
+        fs.append(f1[:, z, y, x]), gs.append(g1[:, z, y, x])
+    assert rel(np.array(fs), np.array(fr)) <= TOL
+    assert rel(np.array(gs), np.array(gr)) <= TOL

@@ -389,3 +389,28 @@ def test_launch_count_and_profile():
         prof = lb.lb_profile(L.h)
         assert lb.lb_launch_count(L.h) > n0
         assert prof["k_step"][1] == 4 and prof["k_step"][0] > 0
+
+
+def test_parity_bench_launch_sampled():
+    """The bench's own launch: 512 x 512 x 64 (BASELINE config 5 per GPU),
+    lb_init_equilibrium on the R15 spinodal phi, one step in the default kernel and
+    z-chunking, against the oracle at sampled sites (corners included) on radius-4
+    windows (the initial state computed on radius-5 windows: g^eq needs lap phi)."""
+    from sitewin import centre, crop, window
+
+    nx, ny, nz = 512, 512, 64
+    phi = synth.spinodal_phi(nx, ny, nz, seed=0)
+    with lb.Lattice(nx, ny, nz, cparams(P0)) as L:
+        L.init_equilibrium(phi)
+        L.step(1)
+        f1, g1 = L.get_state()
+    fs, gs, fr, gr = [], [], [], []
+    for (x, y, z) in synth.sample_sites(nx, ny, nz, 40, seed=12):
+        pw = window(phi, x, y, z, 5)
+        sh = pw.shape
+        f0, g0 = R.equilibrium_state(np.ones(sh), np.zeros((3,) + sh), pw, P0)
+        fo, go = R.step(crop(f0), crop(g0), P0)
+        fr.append(centre(fo)), gr.append(centre(go))
+        fs.append(f1[:, z, y, x]), gs.append(g1[:, z, y, x])
+    assert rel(np.array(fs), np.array(fr)) <= TOL
+    assert rel(np.array(gs), np.array(gr)) <= TOL
