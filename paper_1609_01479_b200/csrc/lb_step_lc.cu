@@ -97,16 +97,18 @@ __device__ __forceinline__ void lc_fields(const DevParams& p, const double (&q)[
   H[2] = Hf[0][2];
   H[3] = Hf[1][1];
   H[4] = Hf[1][2];
-  double D[3][3][3];
+  // G_ab = d_a Q_cd d_b Q_cd over the symmetric pairs (cd): the diagonal and twice the
+  // three off-diagonal entries (Q_zz = -Q_xx - Q_yy); |grad Q|^2 = tr G
+  double dzz[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) full3(dq[c], D[c]);
-  double g2 = 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) g2 += D[c][a][b] * D[c][a][b];
+  for (int c = 0; c < 3; ++c) dzz[c] = -dq[c][0] - dq[c][3];
+  auto gab = [&](int a, int b) {
+    return (dq[a][0] * dq[b][0] + dq[a][3] * dq[b][3] + dzz[a] * dzz[b]) +
+           2.0 * (dq[a][1] * dq[b][1] + dq[a][2] * dq[b][2] + dq[a][4] * dq[b][4]);
+  };
+  const double Gxx = gab(0, 0), Gyy = gab(1, 1), Gzz = gab(2, 2), Gxy = gab(0, 1), Gxz = gab(0, 2), Gyz = gab(1, 2);
+  const double Gm[3][3] = {{Gxx, Gxy, Gxz}, {Gxy, Gyy, Gyz}, {Gxz, Gyz, Gzz}};
+  const double g2 = Gxx + Gyy + Gzz;
   const double bulk = 0.5 * p.lc_a0 * (1.0 - p.lc_gamma * (1.0 / 3.0)) * q2 - p.lc_a0 * p.lc_gamma * (1.0 / 3.0) * tr3 +
                       0.25 * p.lc_a0 * p.lc_gamma * q2 * q2;
   const double fed = bulk + 0.5 * p.kappa * g2;
@@ -122,11 +124,7 @@ __device__ __forceinline__ void lc_fields(const DevParams& p, const double (&q)[
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      double G = 0.0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) G += D[a][c][d] * D[b][c][d];
+      const double G = Gm[a][b];
       const double qt = Qm[a][b] + (a == b ? 1.0 / 3.0 : 0.0);
       sg[a][b] = ((a == b ? fed : 0.0) + 2.0 * xi * qt * qh) - xi * (M[a][b] + M[b][a]) - p.kappa * G +
                  (M[b][a] - M[a][b]);
