@@ -87,6 +87,15 @@ struct lb_ctx {
   double* d_token = nullptr;  // 4 doubles: NCCL barrier tokens
   bool have_state = false;
   bool broken = false;
+  // CUDA graphs of kGraphSteps steps (single process, no per-launch profiling): one
+  // per parity of the A/B buffers, keyed by the state buffer at capture; dropped by
+  // every call that changes what a step launches
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    const double* A = nullptr;
+    long long launches = 0;  // kernels per replay
+  } graphs[2];
+  bool stepped = false;  // one step ran outside a capture (first-launch attributes set)
   std::string err;
   long long launches = 0;
   // profiling
@@ -507,6 +516,72 @@ int one_step(lb_ctx* h, int mode) {
   return LB_OK;
 }
 
+// ---- CUDA graphs of the step loop ---------------------------------------------
+constexpr int kGraphSteps = 8;  // even: a replay returns the A/B buffers to their roles
+
+void drop_graphs(lb_ctx* h) {
+  for (auto& g : h->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = lb_ctx::StepGraph{};
+  }
+}
+
+bool graphs_usable(const lb_ctx* h) {
+  static const bool off = [] {
+    const char* e = std::getenv("LB_GRAPHS");
+    return e && !std::strcmp(e, "0");
+  }();
+  // ranks: the NCCL calls stay outside graphs; persistent kernel: host-side work counter
+  return !off && h->nranks == 1 && !h->prof_on && h->kernel_choice != 4 && h->stepped;
+}
+
+// Replay (capturing first if needed) kGraphSteps steps.  Returns LB_OK, or a
+// negative code; *done = false when no graph could be made (the caller steps plainly).
+int graph_steps(lb_ctx* h, bool* done) {
+  *done = false;
+  const double* A = h->slabs[0].A;
+  lb_ctx::StepGraph* g = nullptr;
+  for (auto& c : h->graphs)
+    if (c.exec && c.A == A) g = &c;
+  if (!g) {
+    lb_ctx::StepGraph* slot = !h->graphs[0].exec ? &h->graphs[0] : &h->graphs[1];
+    if (slot->exec) cudaGraphExecDestroy(slot->exec), *slot = lb_ctx::StepGraph{};
+    const long long n0 = h->launches;
+    if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      return LB_OK;
+    }
+    int rc = LB_OK;
+    for (int t = 0; t < kGraphSteps && !rc; ++t) rc = one_step(h, 0);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
+    const long long nk = h->launches - n0;
+    h->launches = n0;  // captured, not launched
+    if (rc || ec != cudaSuccess || !graph) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      h->broken = false;  // a failed capture is not a device failure: step plainly
+      h->err.clear();
+      return LB_OK;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+      cudaGetLastError();
+      return LB_OK;
+    }
+    slot->exec = exec;
+    slot->A = A;
+    slot->launches = nk;
+    g = slot;
+  }
+  CK(h, cudaGraphLaunch(g->exec, h->stream));
+  h->launches += g->launches;
+  *done = true;
+  return LB_OK;
+}
+
 int finish(lb_ctx* h) {
   CK(h, cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
@@ -824,7 +899,19 @@ int lb_step(lb_t* h, int nsteps) {
   if (rc) return rc;
   if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
-  for (int t = 0; t < nsteps; ++t)
+  int t = 0;
+  if (!h->stepped && nsteps > 0) {
+    if ((rc = one_step(h, 0))) return rc;
+    h->stepped = true;
+    ++t;
+  }
+  while (nsteps - t >= kGraphSteps && graphs_usable(h)) {
+    bool done = false;
+    if ((rc = graph_steps(h, &done))) return rc;
+    if (!done) break;
+    t += kGraphSteps;
+  }
+  for (; t < nsteps; ++t)
     if ((rc = one_step(h, 0))) return rc;
   return finish(h);
 }
@@ -853,6 +940,7 @@ int lb_debug_step_kernel(lb_t* h, int which) {
   if ((which == 3 || which == 4) && !h->slabs.empty() && !step_ws_fits(&h->slabs[0].mapsA))
     return set_err(h, LB_EINVAL, "the warp-specialised kernel needs nx even (TMA rows)");
   h->kernel_choice = which;
+  drop_graphs(h);
   return LB_OK;
 }
 
@@ -888,6 +976,7 @@ int lb_get_phi(lb_t* h, double* phi) {
 void lb_destroy(lb_t* h) {
   if (!h) return;
   if (h->stream) cudaStreamSynchronize(h->stream);
+  drop_graphs(h);
   close_peers(h);
   cudaFree(h->d_token);
   if (h->comm) ncclCommDestroy(h->comm);
@@ -921,7 +1010,7 @@ long long lb_launch_count(const lb_t* h) { return h ? h->launches : 0; }
 
 int lb_profile_enable(lb_t* h, int on) {
   if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
-  h->prof_on = on != 0;
+  h->prof_on = on != 0;  // (graphs are not used while per-launch events are on)
   return LB_OK;
 }
 
@@ -1043,6 +1132,7 @@ int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, doub
   if (rc) return rc;
   if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle's collision is fixed at lb_create_ch");
   if (h->lc) return set_err(h, LB_EINVAL, "a liquid-crystal handle's collision is fixed at lb_create_lc");
+  drop_graphs(h);
   if (model == 0) {
     h->dp.coll = 0;
     return LB_OK;
@@ -1065,6 +1155,7 @@ int lb_debug_halo_mode(lb_t* h, int mode) {
   if (mode == 1 && h->nranks > 1 && !h->peerB[0]) return set_err(h, LB_EINVAL, "no peer mapping on this handle");
   if (mode == 1 && h->G.zwrap) return set_err(h, LB_EINVAL, "a single periodic slab has no halo");
   h->halo_mode = mode;
+  drop_graphs(h);
   return LB_OK;
 }
 
