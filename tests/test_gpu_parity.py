@@ -414,3 +414,46 @@ def test_parity_bench_launch_sampled():
         fs.append(f1[:, z, y, x]), gs.append(g1[:, z, y, x])
     assert rel(np.array(fs), np.array(fr)) <= TOL
     assert rel(np.array(gs), np.array(gr)) <= TOL
+
+
+@pytest.mark.parametrize("nslabs,halo", [(1, None), (2, 0), (2, 1), (4, 1)])
+def test_graph_replay_bitwise_equal_plain_steps(nslabs, halo):
+    """lb_step(20) replays CUDA graphs of 8 steps (after one plain step); 20 calls of
+    lb_step(1) never do: the same bits and the same kernel count."""
+    f, g = rough(32, 12, 16, seed=9)
+    out = []
+    for mode in ("graph", "plain"):
+        with lb.Lattice(32, 12, 16, cparams(P0), nslabs=nslabs) as L:
+            if halo is not None:
+                lb.lb_debug_halo_mode(L.h, halo)
+            L.set_state(f, g)
+            n0 = lb.lb_launch_count(L.h)
+            if mode == "graph":
+                L.step(20)
+            else:
+                for _ in range(20):
+                    L.step(1)
+            out.append((L.get_state(), lb.lb_launch_count(L.h) - n0))
+    (a, na), (b, nb) = out
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert na == nb
+
+
+def test_graphs_dropped_on_collision_change():
+    """A cached graph of the BGK step must not survive lb_set_collision."""
+    f, g = rough(32, 12, 10, seed=10)
+    mp = (0.8, 1.1, 1.0)
+    with lb.Lattice(32, 12, 10, cparams(P0)) as L:
+        L.set_state(f, g)
+        L.step(17)  # captures graphs for both parities
+        lb.lb_set_collision(L.h, 1, *mp)
+        L.set_state(f, g)
+        L.step(17)
+        a = L.get_state()
+    with lb.Lattice(32, 12, 10, cparams(P0)) as L:
+        lb.lb_set_collision(L.h, 1, *mp)
+        L.set_state(f, g)
+        for _ in range(17):
+            L.step(1)
+        b = L.get_state()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
