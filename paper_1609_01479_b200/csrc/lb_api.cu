@@ -919,7 +919,7 @@ int lb_step(lb_t* h, int nsteps) {
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
   int rc = usable(h);
   if (rc) return rc;
-  if (nsteps < 0 || mode < 1 || mode > 4) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, 2, 3, 4} required");
+  if (nsteps < 0 || mode < 1 || mode > 5) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, ..., 5} required");
   if (h->ch || h->lc) return set_err(h, LB_EINVAL, "no memory probes for a Cahn-Hilliard or liquid-crystal handle");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
   for (int t = 0; t < nsteps; ++t)

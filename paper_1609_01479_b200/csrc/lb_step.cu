@@ -169,7 +169,9 @@ __global__ void __launch_bounds__(TX* TY, 1)
     k_step_async(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
                  const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
                  const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
-                 const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
+                 const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9,
+                 const __grid_constant__ CUtensorMap tm_rh5, const __grid_constant__ CUtensorMap tm_rh9,
+                 const __grid_constant__ CUtensorMap tm_rv5, const __grid_constant__ CUtensorMap tm_rv9) {
   using S = StepSmem<TX, TY>;
   constexpr int NT = TX * TY;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
@@ -227,7 +229,36 @@ __global__ void __launch_bounds__(TX* TY, 1)
     bool ghost;
     const int zs = zsrc(zp, ghost);
     if (ghost) return false;
-    if (USE_TMA && box_interior) {
+    if (MODE == 5 && USE_TMA && box_interior) {
+      // probe of a ring design: the g TILE of plane zp (kept, in the real design, for
+      // the collision two planes later) plus only the halo ring of the box (top and
+      // bottom 36 x 2, left and right 2 x TY), 4 TMA boxes per g slot run
+      if (tid == 0) {
+        const int cpl = (zs + GZ) * NSLOT;
+        constexpr int RH = BX * 2, RV = 2 * TY;  // sites per component of a ring box
+        double* base = &sm.sG[0][0];
+        fence_proxy_async();
+        mbar_expect_tx(&sm.bar_box, (unsigned)(Q * (2 * RH + 2 * RV) * 8 + TILE_BYTES));
+        int off = 0;  // doubles; every box starts 128-byte aligned
+        auto place = [&](int n) {
+          const int o = off;
+          off += (n + 15) / 16 * 16;
+          return base + o;
+        };
+        for (int r = 0; r < 3; ++r) {
+          const CUtensorMap* h = r == 1 ? &tm_rh9 : &tm_rh5;
+          const CUtensorMap* v = r == 1 ? &tm_rv9 : &tm_rv5;
+          const int c = cpl + (r == 0 ? 5 : (r == 1 ? 19 : 33)), len = r == 1 ? 9 : 5;
+          tma_load_3d(place(len * RH), h, x0 - 2, y0 - 2, c, &sm.bar_box, pol_last);
+          tma_load_3d(place(len * RH), h, x0 - 2, y0 + TY, c, &sm.bar_box, pol_last);
+          tma_load_3d(place(len * RV), v, x0 - 2, y0, c, &sm.bar_box, pol_last);
+          tma_load_3d(place(len * RV), v, x0 + TX, y0, c, &sm.bar_box, pol_last);
+        }
+        tma_load_3d(&sm.sTg[0][0], &tm_t5, x0, y0, cpl + 5, &sm.bar_box, pol_first);
+        tma_load_3d(&sm.sTg[5][0], &tm_t9, x0, y0, cpl + 19, &sm.bar_box, pol_first);
+        tma_load_3d(&sm.sTg[14][0], &tm_t5, x0, y0, cpl + 33, &sm.bar_box, pol_first);
+      }
+    } else if (USE_TMA && box_interior) {
       // three TMA boxes (g slots 5..9, 19..27, 33..37), one thread
       if (tid == 0) {
         const int cpl = (zs + GZ) * NSLOT;  // component-plane index of slot 0
@@ -390,7 +421,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     if (COLL == 1) own_P6(P6_cur);
   }
   bool box_issued = MODE != 3 ? issue_box(zA + 2) : false;
-  if (MODE != 4) issue_tile(zA, 1);
+  if (MODE != 4 && MODE != 5) issue_tile(zA, 1);
 
   // push targets: wrapped neighbour columns/rows of this thread's site
   const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
@@ -411,16 +442,19 @@ __global__ void __launch_bounds__(TX* TY, 1)
 #pragma unroll
       for (int i = 0; i < Q; ++i) g[i] = sm.sG[grank(i)][(ly + 2) * BX + (lx + 2)];
     }
-    if (MODE != 1 && MODE != 3 && MODE != 4) make_phi(k + 2);
+    if (MODE != 1 && MODE != 3 && MODE != 4 && MODE != 5) make_phi(k + 2);
     __syncthreads();  // sG consumed, ring written
     box_issued = (k + 1 < zB && MODE != 3) ? issue_box(k + 3) : false;
-    if (MODE != 1 && MODE != 3 && MODE != 4) {
+    if (MODE != 1 && MODE != 3 && MODE != 4 && MODE != 5) {
       compute_P(k + 1);
       __syncthreads();
       own_P(Pz_next, Fxy_next);
       if (COLL == 1) own_P6(P6_next);
     }
-    if (MODE != 4) {
+    if (MODE == 5) {  // probe: g from the tile the box barrier brought (two planes ahead)
+#pragma unroll
+      for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
+    } else if (MODE != 4) {
       wait_tile(1);  // g(k) tile landed
 #pragma unroll
       for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
@@ -527,7 +561,17 @@ cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double*
     resid = LB_RESID_OVERRIDE;
 #endif
   }
-  kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3]);
+  if constexpr (MODE == 5) {  // maps of the ring boxes of the probe, for this buffer
+    CUtensorMap rm[4];
+    if (!encode(&rm[0], G, A, kTX + 4, 2, 5) || !encode(&rm[1], G, A, kTX + 4, 2, 9) ||
+        !encode(&rm[2], G, A, 2, TY, 5) || !encode(&rm[3], G, A, 2, TY, 9))
+      return cudaErrorInvalidValue;
+    kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3], rm[0], rm[1],
+                                       rm[2], rm[3]);
+  } else {
+    kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3], m[0], m[1],
+                                       m[0], m[1]);
+  }
   return cudaGetLastError();
 }
 
@@ -539,6 +583,7 @@ cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, doub
     case 2: return launch_t<TY, USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st, pr);
     case 3: return launch_t<TY, USE_TMA, 3>(G, p, A, B, phig, zc, flag, maps, st, pr);
     case 4: return launch_t<TY, USE_TMA, 4>(G, p, A, B, phig, zc, flag, maps, st, pr);
+    case 5: return launch_t<TY, USE_TMA, 5>(G, p, A, B, phig, zc, flag, maps, st, pr);
     default:
       return p.coll == 1 ? launch_t<TY, USE_TMA, 0, 1>(G, p, A, B, phig, zc, flag, maps, st, pr)
                          : launch_t<TY, USE_TMA, 0, 0>(G, p, A, B, phig, zc, flag, maps, st, pr);

@@ -100,6 +100,7 @@ def main():
     out["probe2_plus_halo_phi_P"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 2), "probe2_plus_halo_phi_P")
     out["probe3_tile_only"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 3), "probe3_tile_only")
     out["probe4_box_no_gtile"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 4), "probe4_box_no_gtile")
+    out["probe5_gtile_ahead_ring"] = timed(lambda n: lb.lb_debug_step_probe(L.h, n, 5), "probe5_gtile_ahead_ring")
     out["k_stream_site_parallel"] = timed(lambda n: lb.lb_debug_stream(L.h, n), "k_stream_site_parallel")
     n = nx * ny * nz * 38
     x = torch.empty(n, dtype=torch.float64, device="cuda")
