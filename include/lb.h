@@ -164,7 +164,8 @@ int lb_debug_stream(lb_t* h, int nsteps);
  * stores but without the physics (mode 1: tile copies + halo box + propagation
  * stores; mode 2: also the phi / stress stencils; mode 3: tile copies and stores
  * only; mode 4: like mode 1, but g taken from the halo box instead of a second
- * tile copy).  The state afterwards is a propagated copy, not a solution.  Gives the
+ * tile copy; mode 5: f tile, the g tile two planes ahead and only the halo ring of
+ * the box, four TMA boxes per slot run).  The state afterwards is a propagated copy, not a solution.  Gives the
  * memory-side ceiling of the access pattern for the roofline analysis. */
 int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
 

@@ -592,9 +592,6 @@ cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, doub
 
 }  // namespace
 
-// Tile rows: 8 (one CTA per SM, halo box 1.69x the tile) when the plane has enough
-// tiles to fill the GPU several times over; 4 (two CTAs per SM) for smaller planes,
-// where longer z-chunks matter more than the smaller halo.
 // Tile rows of the step kernel.  Even nx (TMA rows): 32 x 8 tiles and the
 // warp-specialised kernel for every plane size -- measured in round 1 against
 // 32 x 4 tiles of the tile kernel (two CTAs per SM): +12% at 128^3, +17% at 64^3,
