@@ -209,3 +209,21 @@ def test_lc_slabs_bitwise_equal_whole_lattice(nslabs, p):
 def test_lc_slabs_parity_64cubed():
     st = quench(64, 64, 64, seed=5)
     assert_parity(gpu_run_slabs(st, LP, 10, 2), LC.run(*st, LP, 10))
+
+
+def test_lc_quench_long_run_stable_and_conserving():
+    """2000 steps of the R45 random-director quench at 64^3: the state stays finite,
+    Q stays in the physical range (|Q_ab| < 2/3), mass and momentum are conserved to
+    rounding, and the order relaxes (the mean Q:Q falls from 2 S0^2/3 as the random
+    texture anneals)."""
+    n = 64
+    st = quench(n, n, n, seed=8)
+    f0, q0 = st[0], st[1]
+    f1, q1, u1 = gpu_run(st, LP, 2000)
+    assert np.isfinite(f1).all() and np.isfinite(q1).all() and np.isfinite(u1).all()
+    assert np.abs(q1).max() < 2.0 / 3.0
+    assert abs(f1.sum() - f0.sum()) <= 1e-12 * f0.sum()
+    j0, j1 = R.momentum(f0).sum(axis=(1, 2, 3)), R.momentum(f1).sum(axis=(1, 2, 3))
+    assert np.abs(j1 - j0).max() <= 1e-12 * f0.sum()
+    Q0, Q1 = LC.q_full(q0), LC.q_full(q1)
+    assert (Q1 * Q1).sum(axis=(0, 1)).mean() < (Q0 * Q0).sum(axis=(0, 1)).mean()

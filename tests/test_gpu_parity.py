@@ -457,3 +457,30 @@ def test_graphs_dropped_on_collision_change():
             L.step(1)
         b = L.get_state()
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_spinodal_decomposition_long_run_128cubed():
+    """5000 steps of the R15 quench at 128^3 with the demo mobility (M = 0.45): the
+    mixture separates into the two bulk phases +-sqrt(-A/B) = +-1 (the free-energy
+    minima, R2), sum(phi) and mass stay at their initial values to 1e-12 of their
+    scale, and momentum stays zero to rounding (north_star conservation over a long
+    run, on the GPU alone)."""
+    n = 128
+    p = R.Params(mobility=0.45)
+    rho, u, phi = synth.spinodal_fields(n, n, n, seed=21)
+    with lb.Lattice(n, n, n, cparams(p)) as L:
+        L.init_equilibrium(phi)
+        f0, g0 = L.get_state()
+        L.step(5000)
+        f1, g1 = L.get_state()
+        ph = L.get_phi()
+    assert abs(g1.sum() - g0.sum()) <= 1e-12 * np.abs(g0).sum()
+    assert abs(f1.sum() - f0.sum()) <= 1e-12 * f0.sum()
+    j = R.momentum(f1).sum(axis=(1, 2, 3))
+    assert np.abs(j).max() <= 1e-11 * f0.sum()
+    # separated: most sites near a bulk value, both phases present, none far beyond it
+    # (small curved domains sit slightly above 1: the Laplace-pressure shift ~ kappa/R)
+    frac_bulk = float((np.abs(np.abs(ph) - 1.0) < 0.1).mean())
+    assert frac_bulk > 0.6, frac_bulk
+    assert (ph > 0.9).mean() > 0.2 and (ph < -0.9).mean() > 0.2
+    assert np.abs(ph).max() < 1.2
