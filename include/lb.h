@@ -260,8 +260,11 @@ int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, doub
  * distributed shared memory; needs nx % 64 == 0 and ny % 16 == 0, else
  * LB_EINVAL), 3 = the warp-specialised tile kernel (stencil and collision on
  * separate warps; needs nx even, else LB_EINVAL), 4 = the same with persistent
- * CTAs taking work items from a counter.  All give bitwise identical results.
- * Test / measurement support. */
+ * CTAs taking work items from a counter, 5 = the warp-specialised kernel with
+ * the phi exchange (neighbouring tiles' CTAs hand each other the phi halo through
+ * an L2-resident array and per-block flags instead of each loading the g halo
+ * box; one periodic slab, nx % 32 == 0, ny % 8 == 0, else LB_EINVAL).  All give
+ * bitwise identical results.  Test / measurement support. */
 int lb_debug_step_kernel(lb_t* h, int which);
 
 /* Halo transport of a slab handle.  mode -1: returns the current mode (0 or 1);

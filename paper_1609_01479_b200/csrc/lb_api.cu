@@ -70,7 +70,10 @@ struct lb_ctx {
   bool ch = false;        // NEXT-2 handle: state (f, phi), lb_create_ch
   bool lc = false;        // NEXT-4 handle: state (f, Q, u), lb_create_lc
   int lczc = 1;           // z-chunk of the liquid-crystal step kernel
-  int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised
+  int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised,
+                          // 5 warp-specialised with the phi exchange
+  double* xphi[2] = {nullptr, nullptr};  // phi exchange of the warp-specialised kernel (nx*ny*nzl), single slab
+  unsigned long long* xctr = nullptr;     // its in-order block counter
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
   WorkCounter wctr;       // work-item counter of the persistent step kernel
@@ -233,6 +236,14 @@ int alloc_slabs(lb_ctx* h) {
     if (!make_step_maps(h->G, s.A, h->ty, &s.mapsA) || !make_step_maps(h->G, s.B, h->ty, &s.mapsB) ||
         !make_cluster_maps(h->G, s.A, &s.cmapsA) || !make_cluster_maps(h->G, s.B, &s.cmapsB))
       return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed for the step kernel's TMA descriptors");
+  }
+  if (h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA)) {
+    const long long n = h->G.nxy * h->G.nzl;
+    for (int k = 0; k < 2; ++k) {
+      CK(h, cudaMalloc(&h->xphi[k], (size_t)n * sizeof(double)));
+      CK(h, fill_xch_empty(h->xphi[k], n, h->stream));
+    }
+    CK(h, cudaMalloc(&h->xctr, sizeof(unsigned long long)));
   }
   CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
   CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
@@ -498,7 +509,14 @@ int one_step(lb_ctx* h, int mode) {
            // default: the warp-specialised kernel for 32 x 8 tiles (large planes), the
            // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
            const bool ws = mode == 0 && step_ws_fits(&s.mapsA) &&
-                           (h->kernel_choice == 3 || h->kernel_choice == 4 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
+                           (h->kernel_choice >= 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
+           const bool xch = ws && h->xphi[0] && h->kernel_choice == 5 && step_xch_fits(G, &s.mapsA);
+           if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
+             const int k = s.A < s.B ? 0 : 1;
+             const XchArgs xa{h->xphi[k], h->xphi[1 - k], h->xctr};
+             return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
+                                   false, &xa);
+           }
            if (ws)
              return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
                                    h->kernel_choice == 4);
@@ -930,9 +948,12 @@ int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
 int lb_debug_step_kernel(lb_t* h, int which) {
   if (h && (h->ch || h->lc) && which != 0)
     return set_err(h, LB_EINVAL, "a Cahn-Hilliard or liquid-crystal handle has one step kernel");
-  if (!h || which < 0 || which > 4)
+  if (!h || which < 0 || which > 5)
     return set_err(h, LB_EINVAL,
-                   "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised) or 4 (persistent warp-specialised)");
+                   "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised), 4 (persistent warp-specialised) "
+                   "or 5 (warp-specialised with the phi exchange)");
+  if (which == 5 && !h->xphi[0])
+    return set_err(h, LB_EINVAL, "the phi exchange needs one periodic slab, nx %% 32 == 0 and ny %% 8 == 0 (TMA rows)");
   if (which == 2 && h->dp.coll != 0)
     return set_err(h, LB_EINVAL, "the cluster kernel implements only the BGK + force collision (model 0)");
   if (which == 2 && !h->slabs.empty() && !h->slabs[0].cmapsA.ok)
@@ -991,6 +1012,9 @@ void lb_destroy(lb_t* h) {
     cudaFree(s.u2);
   }
   cudaFree(h->d_flag);
+  cudaFree(h->xphi[0]);
+  cudaFree(h->xphi[1]);
+  cudaFree(h->xctr);
   cudaFree(h->wctr.dev);
   if (h->h_flag) cudaFreeHost(h->h_flag);
   for (auto& p : h->pending) {

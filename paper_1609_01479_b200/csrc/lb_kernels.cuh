@@ -83,6 +83,14 @@ __host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch
   const int t = grp * resid + (r - c * rg);
   return TileId{t % ntx, t / ntx, c};
 }
+// inverse of tile_of_block: the block of tile t (row-major) in chunk c
+__host__ __device__ inline int block_of_tile(int t, int c, int ntx, int nty, int nch, int resid) {
+  const int ntiles = ntx * nty;
+  if (resid > ntiles || resid < 1) resid = ntiles;
+  const int grp = t / resid;
+  const int rg = ntiles - grp * resid < resid ? ntiles - grp * resid : resid;
+  return grp * resid * nch + c * rg + (t - grp * resid);
+}
 
 // Fused halo ("peer" transport): the buffers of the
 // neighbouring slabs, on this GPU (loopback) or mapped from a peer GPU over
@@ -134,9 +142,22 @@ struct WorkCounter {
   unsigned long long base = 0;
 };
 bool step_ws_fits(const StepMaps* maps);
+// phi exchange (xch, single periodic slab): the stencil warps load only the g tile
+// and take the phi halo from the neighbouring tiles' CTAs through an L2-resident
+// phi array (nx*ny*nzl doubles) whose unwritten sites hold kXchEmpty: `cur` is
+// written (and polled) in this step, `old` (last step's) is reset to kXchEmpty for
+// the next; `ctr` hands out the blocks in order (zeroed before every launch).
+struct XchArgs {
+  double* cur = nullptr;
+  double* old = nullptr;
+  unsigned long long* ctr = nullptr;
+};
+constexpr unsigned long long kXchEmpty = 0xFFF4DEADBEEF0001ULL;  // a NaN no arithmetic produces
+bool step_xch_fits(const Geom& G, const StepMaps* maps);
+cudaError_t fill_xch_empty(double* buf, long long n, cudaStream_t st);
 cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                            int* flag, const StepMaps* mapsA, cudaStream_t st, const Peers& pr, WorkCounter* wc,
-                           bool persist);
+                           bool persist, const XchArgs* xch = nullptr);
 // the finite-difference Cahn-Hilliard variant (lb_step_ch.cu, NEXT-2): state f and
 // a phi field; one TMA map (f box of one component, (32+4) x (ty+2)); one slab
 struct alignas(64) ChMaps {

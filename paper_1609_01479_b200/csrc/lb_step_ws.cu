@@ -70,10 +70,12 @@ __host__ __device__ constexpr bool ws_split_regs(int ty) {
 #define LB_WS_CONT 1
 #endif
 
-__device__ __forceinline__ int wslot5(int z) {
-  const int s = z % 5;
-  return s < 0 ? s + 5 : s;
+template <int R>
+__device__ __forceinline__ int wslot(int z) {
+  const int s = z % R;
+  return s < 0 ? s + R : s;
 }
+__host__ __device__ constexpr int ws_threads(int ty, bool) { return kWTX * ty + ws_na(ty); }
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -81,8 +83,9 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int TY, int COLL>
+template <int TY, int COLL, bool XCH = false>
 struct alignas(128) WsSmem {
+  static constexpr int NPHI = XCH ? 6 : 5;  // phi ring planes (XCH: two planes of lag)
   static constexpr int NQ = COLL == 1 ? 8 : 5;  // hand-off values per site
   static constexpr int TX = kWTX, NT = TX * TY;
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
@@ -90,7 +93,7 @@ struct alignas(128) WsSmem {
   alignas(128) double sTf[Q][NT];  // f of the tile, f-slot order (TMA boxes TX x TY x 5|9|5)
   alignas(128) double sTg[Q][NT];  // g of the tile, g-slot order
   alignas(128) double sG[Q][NB];   // g on the box, g-slot order  (TMA boxes BX x BY x 5|9|5)
-  double sPhi[5][NB];              // ring of phi planes on the box
+  double sPhi[NPHI][NB];           // ring of phi planes on the box
   double sP[6][NP];                // chemical stress of one plane on the P box
   double sQ[2][NQ][NT];            // hand-off: phi, mu, then Fx, Fy, Fz (COLL 0) or P (COLL 1)
   unsigned long long bar_f, bar_g, bar_box, q_full[2], q_empty[2], item_full[4];
@@ -115,14 +118,28 @@ struct WsItem {
 // items.  When the next item continues the same tile in z, the stencil keeps its
 // phi ring and P state and skips the prologue.  Without PERSIST, one item per
 // CTA (L = blockIdx.x).
-template <int TY, bool PERSIST, int COLL>
-__global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
+//
+// XCH (phi exchange; one periodic slab, whole 32 x TY tiles): CTA i of a grid of
+// S <= resident CTAs takes blocks i, i + S, i + 2S, ... ("rounds" of S blocks).
+// The stencil warps load only the g TILE of plane j+2 (not the tile + 2-site halo
+// box), store phi of their tile to xphi and publish the plane in xflag[block]
+// (release); then they wait (acquire) for the 8 neighbouring tiles' blocks of the
+// same z-chunk to have published the plane and read the phi halo from xphi (L2).
+// Blocks wait only on blocks of the same or an earlier round: those have started
+// (a CTA takes its rounds in order) and publish before they wait, so the block
+// with the least progress never waits -- no deadlock.  A block with a neighbour in
+// a later round (the lower edge of a round's band of tiles) loads the full box
+// as in the plain kernel instead and waits for nobody.  phi is the same sum in the
+// same order either way, so the results are bit for bit those of the plain kernel.
+template <int TY, bool PERSIST, int COLL, bool XCH = false>
+__global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
               const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
-              unsigned long long* __restrict__ wctr, unsigned long long wbase,
+              unsigned long long* __restrict__ wctr, unsigned long long wbase, XchArgs xa,
               const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
               const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
-  using S = WsSmem<TY, COLL>;
+  using S = WsSmem<TY, COLL, XCH>;
+  static_assert(!XCH || (TY == 8 && COLL == 0 && !PERSIST), "phi exchange: 32 x 8 tiles, BGK, static rounds");
   constexpr int TX = kWTX, NT = S::NT;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
   constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
@@ -145,6 +162,19 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
     return it;
   };
 
+  // XCH: the block of neighbouring tile d = 0..7 ((dx, dy) row-major without
+  // (0, 0)) in the same z-chunk, and whether one of them is in a later round
+  auto xch_nb = [&](const WsItem& it, int d) {
+    const int e = d < 4 ? d : d + 1, dx = e % 3 - 1, dy = e / 3 - 1;
+    const int t = wrap_n(it.y0 / TY + dy, nty) * ntx + wrap_n(it.x0 / TX + dx, ntx);
+    return block_of_tile(t, it.zA / zc, ntx, nty, nch, resid);
+  };
+  auto xch_use_box = [&](const WsItem& it, int L) {
+    const int S = (int)gridDim.x, myr = L / S;
+    bool later = false;
+    for (int d = 0; d < 8; ++d) later |= xch_nb(it, d) / S > myr;
+    return later;
+  };
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
 
@@ -184,7 +214,10 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
     auto fetch_publish = [&](unsigned idx) {
       if (a == 0) {
         int L;
-        if (PERSIST) {
+        if (XCH) {  // in order: every block of a round is taken before any of the next
+          const unsigned long long v = atomicAdd(xa.ctr, 1ULL);
+          L = v < (unsigned long long)nitems ? (int)v : nitems;
+        } else if (PERSIST) {
           const unsigned long long v = atomicAdd(wctr, 1ULL) - wbase;
           L = v < (unsigned long long)nitems ? (int)v : nitems;
         } else {
@@ -204,6 +237,7 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
       const WsItem it = item_of(L);
       const int x0 = it.x0, y0 = it.y0, zA = it.zA, zB = it.zB;
       const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
+      const bool use_box = !XCH || xch_use_box(it, L);
       // per-thread copy plan of a wrapped halo box: 16-byte units
       long long box_src[BOXR];
       int box_dst[BOXR];
@@ -221,7 +255,16 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
         bool ghost;
         const int zs = zsrc(zp, ghost);
         if (ghost) return false;
-        if (box_interior) {
+        if (XCH && !use_box) {
+          if (a == 0) {  // the g tile only, in tile layout
+            const int cpl = (zs + GZ) * NSLOT;
+            fence_proxy_async();
+            mbar_expect_tx(&sm.bar_box, TILE_BYTES);
+            tma_load_3d(&sm.sG[0][0], &tm_t5, x0, y0, cpl + 5, &sm.bar_box, pol_last);
+            tma_load_3d(&sm.sG[0][0] + 5 * NT, &tm_t9, x0, y0, cpl + 19, &sm.bar_box, pol_last);
+            tma_load_3d(&sm.sG[0][0] + 14 * NT, &tm_t5, x0, y0, cpl + 33, &sm.bar_box, pol_last);
+          }
+        } else if (box_interior) {
           if (a == 0) {
             const int cpl = (zs + GZ) * NSLOT;
             fence_proxy_async();
@@ -246,7 +289,7 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
       // wait for the box, then make it visible to the whole role
       auto wait_box = [&](bool issued) {
         if (issued) {
-          if (box_interior) {
+          if (box_interior || (XCH && !use_box)) {
             mbar_wait(&sm.bar_box, ph_box);
             ph_box ^= 1;
           } else {
@@ -258,7 +301,24 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
       auto make_phi = [&](int zp) {
         bool ghost;
         const int zs = zsrc(zp, ghost);
-        double* ring = sm.sPhi[wslot5(zp)];
+        double* ring = sm.sPhi[wslot<S::NPHI>(zp)];
+        if (XCH && !ghost) {
+          double* xp = xa.cur + (long long)zs * nxy;
+          double* xo = xa.old + (long long)zs * nxy;
+          if (!use_box) {  // phi of the tile from the g tile
+            const double(*gt)[NT] = reinterpret_cast<const double(*)[NT]>(&sm.sG[0][0]);
+            for (int s = a; s < NT; s += kNA) {
+              double v = gt[grank(0)][s];  // A.3, canonical order (same as phi_sum)
+#pragma unroll
+              for (int i = 1; i < Q; ++i) v += gt[grank(i)][s];
+              ring[(s / TX + 2) * BX + s % TX + 2] = v;
+              const long long o = (long long)(y0 + s / TX) * G.nx + x0 + s % TX;
+              __stcg(xp + o, v);
+              __stcg(xo + o, __longlong_as_double((long long)kXchEmpty));
+            }
+            return;
+          }
+        }
         for (int b = a; b < NB; b += kNA) {
           double v;
           if (ghost) {
@@ -270,12 +330,21 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
             for (int i = 1; i < Q; ++i) v += sm.sG[grank(i)][b];
           }
           ring[b] = v;
+          if (XCH && !ghost) {
+            const int bx = b % BX - 2, by = b / BX - 2;
+            if (bx >= 0 && bx < TX && by >= 0 && by < TY)
+            {
+              const long long o = (long long)zs * nxy + (long long)(y0 + by) * G.nx + x0 + bx;
+              __stcg(xa.cur + o, v);
+              __stcg(xa.old + o, __longlong_as_double((long long)kXchEmpty));
+            }
+          }
         }
       };
       auto compute_P = [&](int zp) {
-        const double* f0 = sm.sPhi[wslot5(zp - 1)];
-        const double* f1 = sm.sPhi[wslot5(zp)];
-        const double* f2 = sm.sPhi[wslot5(zp + 1)];
+        const double* f0 = sm.sPhi[wslot<S::NPHI>(zp - 1)];
+        const double* f1 = sm.sPhi[wslot<S::NPHI>(zp)];
+        const double* f2 = sm.sPhi[wslot<S::NPHI>(zp + 1)];
         for (int e = a; e < NP; e += kNA) {
           const int c = (e / PX + 1) * BX + (e % PX + 1);
           const double ph = f1[c];
@@ -308,13 +377,52 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
       // the same tile continued in z: phi ring, P state and box stream carry on
       const bool cont = LB_WS_CONT && PERSIST && prev.x0 == x0 && prev.y0 == y0 && prev.zB == zA;
       const int n0 = cont ? 4 : 0;
+      // XCH lags two planes: iteration nn makes phi of the tile on box nn (stored
+      // to xa.cur); each halo thread loads its site of box nn-1 from the owner's
+      // store in xa.cur (L2) and uses it an iteration later -- if it still reads
+      // kXchEmpty the owner is behind and it polls again.  The value is its own
+      // flag: no fence, no separate flag word.
+      constexpr int lag = XCH ? 2 : 0;
+      constexpr int NH = 4 * BX + 4 * TY;  // halo: top and bottom 2 rows, left and right 2 columns
+      int h_ring = -1;
+      long long h_off = 0;
+      if (XCH && !use_box && a < NH) {
+        int bx, by;
+        if (a < 4 * BX) {
+          const int r = a / BX;
+          bx = a - r * BX;
+          by = r < 2 ? r : TY + r;  // rows 0, 1, TY + 2, TY + 3
+        } else {
+          const int q = a - 4 * BX, c = q / TY;
+          by = 2 + (q - c * TY);
+          bx = c < 2 ? c : TX + c;  // columns 0, 1, TX + 2, TX + 3
+        }
+        h_ring = by * BX + bx;
+        h_off = (long long)wrap_n(y0 - 2 + by, G.ny) * G.nx + wrap_n(x0 - 2 + bx, G.nx);
+      }
+      auto xsite = [&](int b) { return xa.cur + (long long)wrap_n(zA - 2 + b, G.nzl) * nxy + h_off; };
+      double pf = 0.0;  // the halo site of box nn-1, loaded an iteration ahead
       bool issued = issue_box(n0);
-      for (int n = n0; n <= nlast; ++n) {
-        const int zp = zA - 2 + n;
-        wait_box(issued);  // (also: everyone is past the previous hand-off)
-        make_phi(zp);
+      for (int nn = n0; nn <= nlast + lag; ++nn) {
+        double hv = 0.0;
+        const bool hw = XCH && h_ring >= 0 && nn - 2 >= 0 && nn - 2 <= nlast;
+        if (hw) {
+          hv = pf;
+          while (__double_as_longlong(hv) == (long long)kXchEmpty) hv = ld_relaxed_f64(xsite(nn - 2));
+        }
+        if (XCH && h_ring >= 0 && nn - 1 >= 0 && nn - 1 <= nlast) pf = ld_relaxed_f64(xsite(nn - 1));
+        if (nn <= nlast) {
+          wait_box(issued);  // (also: everyone is past the previous hand-off)
+          make_phi(zA - 2 + nn);
+        } else {
+          named_sync(2, kNA);
+        }
+        if (hw) sm.sPhi[wslot<S::NPHI>(zA - 4 + nn)][h_ring] = hv;
         named_sync(2, kNA);  // sG consumed, ring written
-        issued = n + 1 <= nlast ? issue_box(n + 1) : false;
+        if (nn <= nlast) {
+          issued = nn + 1 <= nlast ? issue_box(nn + 1) : false;
+        }
+        const int n = nn - lag, zp = zA - 2 + n;
         if (n < 2) continue;
         compute_P(zp - 1);  // needs phi(zp-2 .. zp)
         named_sync(2, kNA);
@@ -345,9 +453,9 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
         const int j = zp - 2;
         const int q = seq & 1, u = seq >> 1;
         if (u >= 1) mbar_wait(&sm.q_empty[q], (u - 1) & 1);
-        const double* r0 = sm.sPhi[wslot5(j)];
-        const double* rm = sm.sPhi[wslot5(j - 1)];
-        const double* rp = sm.sPhi[wslot5(j + 1)];
+        const double* r0 = sm.sPhi[wslot<S::NPHI>(j)];
+        const double* rm = sm.sPhi[wslot<S::NPHI>(j - 1)];
+        const double* rp = sm.sPhi[wslot<S::NPHI>(j + 1)];
 #pragma unroll
         for (int s = 0; s < SPT; ++s) {
           const int site = a + s * kNA;
@@ -488,12 +596,13 @@ __global__ void __launch_bounds__(kWTX* TY + ws_na(TY), 1)
 }
 
 
-template <int TY, bool PERSIST, int COLL>
+template <int TY, bool PERSIST, int COLL, bool XCH = false>
 cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc) {
-  constexpr size_t smem = sizeof(WsSmem<TY, COLL>);
+                        int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc,
+                        const XchArgs* xch = nullptr) {
+  constexpr size_t smem = sizeof(WsSmem<TY, COLL, XCH>);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
-  auto kern = k_step_ws<TY, PERSIST, COLL>;
+  auto kern = k_step_ws<TY, PERSIST, COLL, XCH>;
   static bool attr = false;
   static int resid = 0;  // CTAs resident at a time (tile_of_block; the persistent grid)
   if (!attr) {
@@ -503,7 +612,7 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWTX * TY + ws_na(TY), smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ws_threads(TY, XCH), smem);
     resid = sms * (per_sm > 0 ? per_sm : 1);
 #ifdef LB_RESID_OVERRIDE
     resid = LB_RESID_OVERRIDE;
@@ -512,9 +621,12 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   const int nitems = ((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc);
   if (PERSIST && (!wc || !wc->dev)) return cudaErrorInvalidValue;
-  const unsigned nblk = (unsigned)(PERSIST ? (nitems < resid ? nitems : resid) : nitems);
-  kern<<<nblk, kWTX * TY + ws_na(TY), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, wc ? wc->dev : nullptr,
-                                                  wc ? wc->base : 0ULL, m[0], m[1], m[2], m[3]);
+  if (XCH && (!xch || !xch->cur || !xch->old || !xch->ctr)) return cudaErrorInvalidValue;
+  const XchArgs xa = xch ? *xch : XchArgs{};
+  if (XCH && cudaMemsetAsync(xch->ctr, 0, sizeof(unsigned long long), st) != cudaSuccess) return cudaGetLastError();
+  const unsigned nblk = (unsigned)(PERSIST || XCH ? (nitems < resid ? nitems : resid) : nitems);
+  kern<<<nblk, ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, wc ? wc->dev : nullptr,
+                                                  wc ? wc->base : 0ULL, xa, m[0], m[1], m[2], m[3]);
   // every CTA takes one item past the end: the counter moved by nitems + grid
   if (PERSIST) wc->base += (unsigned long long)nitems + nblk;
   return cudaGetLastError();
@@ -524,11 +636,29 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
 
 bool step_ws_fits(const StepMaps* maps) { return maps && maps->ok && (maps->ty == 8 || maps->ty == 4); }
 
+bool step_xch_fits(const Geom& G, const StepMaps* maps) {
+  return step_ws_fits(maps) && maps->ty == 8 && G.zwrap && G.nx % kWTX == 0 && G.ny % 8 == 0;
+}
+namespace {
+__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+}  // namespace
+cudaError_t fill_xch_empty(double* buf, long long n, cudaStream_t st) {
+  k_fill_u64<<<592, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(buf), n, kXchEmpty);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                            int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc,
-                           bool persist) {
+                           bool persist, const XchArgs* xch) {
   if (!step_ws_fits(maps)) return cudaErrorInvalidValue;
   const bool t8 = maps->ty == 8;
+  if (xch && p.coll == 0) {  // (MRT: the plain kernel -- same bits)
+    if (!step_xch_fits(G, maps)) return cudaErrorInvalidValue;
+    return launch_ws_t<8, false, 0, true>(G, p, A, B, phig, zc, flag, maps, st, pr, wc, xch);
+  }
   if (p.coll == 1) {
     if (persist)
       return t8 ? launch_ws_t<8, true, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)

@@ -241,6 +241,68 @@ def test_ws_kernel_slabs_bitwise(nslabs):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+# ------------------------------------------------------------------ the phi exchange (kernel 5)
+def gpu_run_zc(f, g, p, nsteps, kernel, zchunk=None, coll=None):
+    """gpu_run with an optional z-chunk override (LB_ZCHUNK, read at lb_create) and
+    collision model (lb_set_collision)."""
+    import os
+
+    nz, ny, nx = f.shape[1:]
+    old = os.environ.get("LB_ZCHUNK")
+    if zchunk:
+        os.environ["LB_ZCHUNK"] = str(zchunk)
+    try:
+        L = lb.Lattice(nx, ny, nz, cparams(p))
+    finally:
+        if zchunk:
+            if old is None:
+                del os.environ["LB_ZCHUNK"]
+            else:
+                os.environ["LB_ZCHUNK"] = old
+    with L:
+        lb.lb_debug_step_kernel(L.h, kernel)
+        if coll is not None:
+            lb.lb_set_collision(L.h, 1, *coll)
+        L.set_state(f, g)
+        L.step(nsteps)
+        return L.get_state()
+
+
+@pytest.mark.parametrize("shape,zchunk", [((32, 8, 8), None), ((64, 16, 12), None), ((64, 64, 16), None),
+                                          ((96, 40, 9), 4), ((512, 304, 16), 8), ((512, 304, 16), None)])
+def test_xch_kernel_bitwise_equal_to_ws_kernel(shape, zchunk):
+    """The phi exchange (neighbouring tiles' CTAs hand each other the phi halo through
+    xphi + release/acquire flags; blocks with a neighbour in a later round load the
+    box) gives the bits of the warp-specialised kernel: one tile (every neighbour is
+    the tile itself), one round, several rounds with box fallbacks, two z-chunks; 20
+    steps, i.e. graph replays and the alternating flag tags of consecutive steps."""
+    nx, ny, nz = shape
+    steps = 20 if nx * ny * nz <= 200_000 else 3
+    f, g = rough(nx, ny, nz, seed=21)
+    a = gpu_run_zc(f, g, P0, steps, kernel=5, zchunk=zchunk)
+    b = gpu_run_zc(f, g, P0, steps, kernel=3)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    if nx * ny * nz <= 40_000:
+        assert_parity(a, R.run(f, g, P0, steps))
+
+
+def test_xch_kernel_mrt_bitwise():
+    f, g = rough(64, 32, 10, seed=22)
+    mp = (0.8, 1.1, 1.0)
+    a = gpu_run_zc(f, g, P0, 9, kernel=5, coll=mp)
+    b = gpu_run_zc(f, g, P0, 9, kernel=3, coll=mp)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("shape,nslabs", [((48, 16, 8), 1), ((64, 12, 8), 1), ((64, 16, 8), 2)])
+def test_xch_kernel_rejects_unfit_lattice(shape, nslabs):
+    nx, ny, nz = shape
+    with lb.Lattice(nx, ny, nz, nslabs=nslabs) as L:
+        with pytest.raises(lb.LBError) as e:
+            lb.lb_debug_step_kernel(L.h, 5)
+        assert e.value.code == lb.LB_EINVAL
+
+
 def test_ws_kernel_rejects_odd_nx():
     with lb.Lattice(7, 16, 8) as L:
         with pytest.raises(lb.LBError) as e:
