@@ -73,7 +73,7 @@ struct lb_ctx {
   int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised,
                           // 5 warp-specialised with the phi exchange
   double* xphi[2] = {nullptr, nullptr};  // phi exchange of the warp-specialised kernel (nx*ny*nzl), single slab
-  unsigned long long* xctr = nullptr;     // its in-order block counter
+  bool xch_default = false;               // kernel 0 uses it (one wave of blocks)
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
   WorkCounter wctr;       // work-item counter of the persistent step kernel
@@ -221,6 +221,17 @@ void resolve_pending(lb_ctx* h) {
 }
 
 // ---- allocation ------------------------------------------------------------
+// the two phi arrays of the phi-exchange kernel (kernel 5), filled with kXchEmpty
+int ensure_xch(lb_ctx* h) {
+  if (h->xphi[0]) return LB_OK;
+  const long long n = h->G.nxy * h->G.nzl;
+  for (int k = 0; k < 2; ++k) {
+    CK(h, cudaMalloc(&h->xphi[k], (size_t)n * sizeof(double)));
+    CK(h, fill_xch_empty(h->xphi[k], n, h->stream));
+  }
+  return LB_OK;
+}
+
 int alloc_slabs(lb_ctx* h) {
   h->slabs.resize(h->nslabs);
   for (int r = 0; r < h->nslabs; ++r) {
@@ -237,14 +248,9 @@ int alloc_slabs(lb_ctx* h) {
         !make_cluster_maps(h->G, s.A, &s.cmapsA) || !make_cluster_maps(h->G, s.B, &s.cmapsB))
       return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed for the step kernel's TMA descriptors");
   }
-  if (h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA)) {
-    const long long n = h->G.nxy * h->G.nzl;
-    for (int k = 0; k < 2; ++k) {
-      CK(h, cudaMalloc(&h->xphi[k], (size_t)n * sizeof(double)));
-      CK(h, fill_xch_empty(h->xphi[k], n, h->stream));
-    }
-    CK(h, cudaMalloc(&h->xctr, sizeof(unsigned long long)));
-  }
+  // the phi-exchange step kernel is the default where its blocks run in one wave
+  h->xch_default = h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) &&
+                   ws_xch_blocks(h->G, h->zc) <= h->num_sms && h->kernel_choice == 0;
   CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
   CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
   CK(h, cudaMalloc(&h->wctr.dev, sizeof(unsigned long long)));
@@ -510,10 +516,11 @@ int one_step(lb_ctx* h, int mode) {
            // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
            const bool ws = mode == 0 && step_ws_fits(&s.mapsA) &&
                            (h->kernel_choice >= 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
-           const bool xch = ws && h->xphi[0] && h->kernel_choice == 5 && step_xch_fits(G, &s.mapsA);
+           const bool xch = ws && h->xphi[0] && (h->kernel_choice == 5 || (h->kernel_choice == 0 && h->xch_default)) &&
+                            step_xch_fits(G, &s.mapsA);
            if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
              const int k = s.A < s.B ? 0 : 1;
-             const XchArgs xa{h->xphi[k], h->xphi[1 - k], h->xctr};
+             const XchArgs xa{h->xphi[k], h->xphi[1 - k]};
              return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
                                    false, &xa);
            }
@@ -917,6 +924,7 @@ int lb_step(lb_t* h, int nsteps) {
   if (rc) return rc;
   if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
+  if (nsteps > 0 && h->xch_default && !h->ch && !h->lc && (rc = ensure_xch(h))) return rc;  // (never inside a capture)
   int t = 0;
   if (!h->stepped && nsteps > 0) {
     if ((rc = one_step(h, 0))) return rc;
@@ -952,8 +960,12 @@ int lb_debug_step_kernel(lb_t* h, int which) {
     return set_err(h, LB_EINVAL,
                    "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised), 4 (persistent warp-specialised) "
                    "or 5 (warp-specialised with the phi exchange)");
-  if (which == 5 && !h->xphi[0])
+  if (which == 5 && (h->nslabs != 1 || h->slabs.empty() || !step_xch_fits(h->G, &h->slabs[0].mapsA)))
     return set_err(h, LB_EINVAL, "the phi exchange needs one periodic slab, nx %% 32 == 0 and ny %% 8 == 0 (TMA rows)");
+  if (which == 5) {
+    const int rc = ensure_xch(h);
+    if (rc) return rc;
+  }
   if (which == 2 && h->dp.coll != 0)
     return set_err(h, LB_EINVAL, "the cluster kernel implements only the BGK + force collision (model 0)");
   if (which == 2 && !h->slabs.empty() && !h->slabs[0].cmapsA.ok)
@@ -1014,7 +1026,6 @@ void lb_destroy(lb_t* h) {
   cudaFree(h->d_flag);
   cudaFree(h->xphi[0]);
   cudaFree(h->xphi[1]);
-  cudaFree(h->xctr);
   cudaFree(h->wctr.dev);
   if (h->h_flag) cudaFreeHost(h->h_flag);
   for (auto& p : h->pending) {

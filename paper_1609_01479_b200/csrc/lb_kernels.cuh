@@ -145,13 +145,13 @@ bool step_ws_fits(const StepMaps* maps);
 // phi exchange (xch, single periodic slab): the stencil warps load only the g tile
 // and take the phi halo from the neighbouring tiles' CTAs through an L2-resident
 // phi array (nx*ny*nzl doubles) whose unwritten sites hold kXchEmpty: `cur` is
-// written (and polled) in this step, `old` (last step's) is reset to kXchEmpty for
-// the next; `ctr` hands out the blocks in order (zeroed before every launch).
+// written (and read) in this step, `old` (last step's) is reset to kXchEmpty for
+// the next.
 struct XchArgs {
   double* cur = nullptr;
   double* old = nullptr;
-  unsigned long long* ctr = nullptr;
 };
+int ws_xch_blocks(const Geom& G, int zc);
 constexpr unsigned long long kXchEmpty = 0xFFF4DEADBEEF0001ULL;  // a NaN no arithmetic produces
 bool step_xch_fits(const Geom& G, const StepMaps* maps);
 cudaError_t fill_xch_empty(double* buf, long long n, cudaStream_t st);

@@ -62,6 +62,10 @@ __host__ __device__ constexpr bool ws_split_regs(int ty) {
 #define LB_WS_ST_POL (-1)
 #endif
 
+// XCH: planes the stencil's P / F / mu work trails its phi (the neighbours' slack)
+#ifndef LB_XCH_LAG
+#define LB_XCH_LAG 4
+#endif
 #ifndef LB_WS_FETCH_EARLY
 #define LB_WS_FETCH_EARLY 0
 #endif
@@ -85,7 +89,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
 
 template <int TY, int COLL, bool XCH = false>
 struct alignas(128) WsSmem {
-  static constexpr int NPHI = XCH ? 6 : 5;  // phi ring planes (XCH: two planes of lag)
+  static constexpr int NPHI = XCH ? LB_XCH_LAG + 4 : 5;  // phi ring planes (XCH: lag planes more)
   static constexpr int NQ = COLL == 1 ? 8 : 5;  // hand-off values per site
   static constexpr int TX = kWTX, NT = TX * TY;
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
@@ -119,18 +123,19 @@ struct WsItem {
 // phi ring and P state and skips the prologue.  Without PERSIST, one item per
 // CTA (L = blockIdx.x).
 //
-// XCH (phi exchange; one periodic slab, whole 32 x TY tiles): CTA i of a grid of
-// S <= resident CTAs takes blocks i, i + S, i + 2S, ... ("rounds" of S blocks).
-// The stencil warps load only the g TILE of plane j+2 (not the tile + 2-site halo
-// box), store phi of their tile to xphi and publish the plane in xflag[block]
-// (release); then they wait (acquire) for the 8 neighbouring tiles' blocks of the
-// same z-chunk to have published the plane and read the phi halo from xphi (L2).
-// Blocks wait only on blocks of the same or an earlier round: those have started
-// (a CTA takes its rounds in order) and publish before they wait, so the block
-// with the least progress never waits -- no deadlock.  A block with a neighbour in
-// a later round (the lower edge of a round's band of tiles) loads the full box
-// as in the plain kernel instead and waits for nobody.  phi is the same sum in the
-// same order either way, so the results are bit for bit those of the plain kernel.
+// XCH (phi exchange; one periodic slab, whole 32 x 8 tiles): the stencil warps
+// load only the g TILE of plane j+2, not the tile + 2-site halo box (-40% of the
+// box bytes), store phi of their tile to an L2-resident array (xa.cur) and take
+// the phi halo from the neighbouring tiles' stores there.  Empty sites hold the
+// NaN kXchEmpty, so a value is its own flag (no fences, no flag words); each
+// block resets its sites in last step's array (xa.old) for the next step.  A
+// halo site still empty when needed (its tile runs behind or has not started --
+// the next wave) is summed from g here: nobody waits, so no schedule can
+// deadlock, and phi is the same sum in the same order either way -- the results
+// are bit for bit those of the plain kernel.  Default where all blocks run in
+// one wave (the tiles' CTAs start together and stay within the lag of each
+// other: 128^3, 64^3); over several waves the neighbours drift apart and the
+// fallback sums cost more than the box.
 template <int TY, bool PERSIST, int COLL, bool XCH = false>
 __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
@@ -162,19 +167,6 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     return it;
   };
 
-  // XCH: the block of neighbouring tile d = 0..7 ((dx, dy) row-major without
-  // (0, 0)) in the same z-chunk, and whether one of them is in a later round
-  auto xch_nb = [&](const WsItem& it, int d) {
-    const int e = d < 4 ? d : d + 1, dx = e % 3 - 1, dy = e / 3 - 1;
-    const int t = wrap_n(it.y0 / TY + dy, nty) * ntx + wrap_n(it.x0 / TX + dx, ntx);
-    return block_of_tile(t, it.zA / zc, ntx, nty, nch, resid);
-  };
-  auto xch_use_box = [&](const WsItem& it, int L) {
-    const int S = (int)gridDim.x, myr = L / S;
-    bool later = false;
-    for (int d = 0; d < 8; ++d) later |= xch_nb(it, d) / S > myr;
-    return later;
-  };
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
 
@@ -214,10 +206,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     auto fetch_publish = [&](unsigned idx) {
       if (a == 0) {
         int L;
-        if (XCH) {  // in order: every block of a round is taken before any of the next
-          const unsigned long long v = atomicAdd(xa.ctr, 1ULL);
-          L = v < (unsigned long long)nitems ? (int)v : nitems;
-        } else if (PERSIST) {
+        if (PERSIST) {
           const unsigned long long v = atomicAdd(wctr, 1ULL) - wbase;
           L = v < (unsigned long long)nitems ? (int)v : nitems;
         } else {
@@ -237,7 +226,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       const WsItem it = item_of(L);
       const int x0 = it.x0, y0 = it.y0, zA = it.zA, zB = it.zB;
       const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
-      const bool use_box = !XCH || xch_use_box(it, L);
+      constexpr bool use_box = !XCH;
       // per-thread copy plan of a wrapped halo box: 16-byte units
       long long box_src[BOXR];
       int box_dst[BOXR];
@@ -377,12 +366,13 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       // the same tile continued in z: phi ring, P state and box stream carry on
       const bool cont = LB_WS_CONT && PERSIST && prev.x0 == x0 && prev.y0 == y0 && prev.zB == zA;
       const int n0 = cont ? 4 : 0;
-      // XCH lags two planes: iteration nn makes phi of the tile on box nn (stored
-      // to xa.cur); each halo thread loads its site of box nn-1 from the owner's
-      // store in xa.cur (L2) and uses it an iteration later -- if it still reads
-      // kXchEmpty the owner is behind and it polls again.  The value is its own
-      // flag: no fence, no separate flag word.
-      constexpr int lag = XCH ? 2 : 0;
+      // XCH lags LB_XCH_LAG planes: iteration nn makes phi of the tile on box nn
+      // (stored to xa.cur); each halo thread loads its site of box nn - lag + 1
+      // from the owner's store in xa.cur (L2) and uses it an iteration later -- if
+      // it still reads kXchEmpty the owner is behind (started later, runs slower)
+      // and the site's phi is summed from g here.  The value is its own flag: no
+      // fence, no flag word, no waiting.
+      constexpr int lag = XCH ? LB_XCH_LAG : 0;
       constexpr int NH = 4 * BX + 4 * TY;  // halo: top and bottom 2 rows, left and right 2 columns
       int h_ring = -1;
       long long h_off = 0;
@@ -401,23 +391,29 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         h_off = (long long)wrap_n(y0 - 2 + by, G.ny) * G.nx + wrap_n(x0 - 2 + bx, G.nx);
       }
       auto xsite = [&](int b) { return xa.cur + (long long)wrap_n(zA - 2 + b, G.nzl) * nxy + h_off; };
-      double pf = 0.0;  // the halo site of box nn-1, loaded an iteration ahead
+      // the owner has not stored it yet (a neighbouring tile that started later or
+      // runs behind): phi from g here instead, the same sum in the same order
+      auto phi_here = [&](int b) {
+        return phi_sum(A + (long long)(wrap_n(zA - 2 + b, G.nzl) + GZ) * G.plane + h_off, nxy);
+      };
+      double pf = 0.0;  // the halo site of box hb + 1, loaded an iteration ahead
       bool issued = issue_box(n0);
       for (int nn = n0; nn <= nlast + lag; ++nn) {
         double hv = 0.0;
-        const bool hw = XCH && h_ring >= 0 && nn - 2 >= 0 && nn - 2 <= nlast;
+        const int hb = nn - lag;  // the halo box completed in this iteration
+        const bool hw = XCH && h_ring >= 0 && hb >= 0 && hb <= nlast;
         if (hw) {
           hv = pf;
-          while (__double_as_longlong(hv) == (long long)kXchEmpty) hv = ld_relaxed_f64(xsite(nn - 2));
+          if (__double_as_longlong(hv) == (long long)kXchEmpty) hv = phi_here(hb);  // owner behind: sum it here
         }
-        if (XCH && h_ring >= 0 && nn - 1 >= 0 && nn - 1 <= nlast) pf = ld_relaxed_f64(xsite(nn - 1));
+        if (XCH && h_ring >= 0 && hb + 1 >= 0 && hb + 1 <= nlast) pf = ld_relaxed_f64(xsite(hb + 1));
         if (nn <= nlast) {
           wait_box(issued);  // (also: everyone is past the previous hand-off)
           make_phi(zA - 2 + nn);
         } else {
           named_sync(2, kNA);
         }
-        if (hw) sm.sPhi[wslot<S::NPHI>(zA - 4 + nn)][h_ring] = hv;
+        if (hw) sm.sPhi[wslot<S::NPHI>(zA - 2 + hb)][h_ring] = hv;
         named_sync(2, kNA);  // sG consumed, ring written
         if (nn <= nlast) {
           issued = nn + 1 <= nlast ? issue_box(nn + 1) : false;
@@ -621,10 +617,9 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   const int nitems = ((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc);
   if (PERSIST && (!wc || !wc->dev)) return cudaErrorInvalidValue;
-  if (XCH && (!xch || !xch->cur || !xch->old || !xch->ctr)) return cudaErrorInvalidValue;
+  if (XCH && (!xch || !xch->cur || !xch->old)) return cudaErrorInvalidValue;
   const XchArgs xa = xch ? *xch : XchArgs{};
-  if (XCH && cudaMemsetAsync(xch->ctr, 0, sizeof(unsigned long long), st) != cudaSuccess) return cudaGetLastError();
-  const unsigned nblk = (unsigned)(PERSIST || XCH ? (nitems < resid ? nitems : resid) : nitems);
+  const unsigned nblk = (unsigned)(PERSIST ? (nitems < resid ? nitems : resid) : nitems);
   kern<<<nblk, ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, wc ? wc->dev : nullptr,
                                                   wc ? wc->base : 0ULL, xa, m[0], m[1], m[2], m[3]);
   // every CTA takes one item past the end: the counter moved by nitems + grid
@@ -639,6 +634,7 @@ bool step_ws_fits(const StepMaps* maps) { return maps && maps->ok && (maps->ty =
 bool step_xch_fits(const Geom& G, const StepMaps* maps) {
   return step_ws_fits(maps) && maps->ty == 8 && G.zwrap && G.nx % kWTX == 0 && G.ny % 8 == 0;
 }
+int ws_xch_blocks(const Geom& G, int zc) { return (G.nx / kWTX) * ((G.ny + 7) / 8) * ((G.nzl + zc - 1) / zc); }
 namespace {
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

@@ -103,6 +103,9 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
   return v;
 }
 
+__device__ __forceinline__ void st_relaxed_u32(unsigned* a, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* a) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");

@@ -272,10 +272,11 @@ def gpu_run_zc(f, g, p, nsteps, kernel, zchunk=None, coll=None):
                                           ((96, 40, 9), 4), ((512, 304, 16), 8), ((512, 304, 16), None)])
 def test_xch_kernel_bitwise_equal_to_ws_kernel(shape, zchunk):
     """The phi exchange (neighbouring tiles' CTAs hand each other the phi halo through
-    xphi + release/acquire flags; blocks with a neighbour in a later round load the
-    box) gives the bits of the warp-specialised kernel: one tile (every neighbour is
-    the tile itself), one round, several rounds with box fallbacks, two z-chunks; 20
-    steps, i.e. graph replays and the alternating flag tags of consecutive steps."""
+    an L2-resident phi array whose empty sites hold a sentinel NaN; a site still
+    empty when needed is summed from g) gives the bits of the warp-specialised
+    kernel: one tile (every neighbour is the tile itself), one wave, several waves
+    (neighbours in the next wave: sums from g), two z-chunks; 20 steps, i.e. graph
+    replays and the two phi arrays swapping roles between steps."""
     nx, ny, nz = shape
     steps = 20 if nx * ny * nz <= 200_000 else 3
     f, g = rough(nx, ny, nz, seed=21)
@@ -284,6 +285,18 @@ def test_xch_kernel_bitwise_equal_to_ws_kernel(shape, zchunk):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     if nx * ny * nz <= 40_000:
         assert_parity(a, R.run(f, g, P0, steps))
+
+
+def test_xch_is_default_for_one_wave():
+    """Kernel 0 takes the phi exchange where all blocks fit in one wave (64^3: 16
+    tiles x 8 z-chunks) and the plain warp-specialised kernel otherwise: both
+    bitwise equal to kernel 3."""
+    for shape in [(64, 64, 64), (512, 304, 16)]:
+        nx, ny, nz = shape
+        f, g = rough(nx, ny, nz, seed=23)
+        a = gpu_run(f, g, P0, 2, kernel=0)
+        b = gpu_run(f, g, P0, 2, kernel=3)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
 def test_xch_kernel_mrt_bitwise():
