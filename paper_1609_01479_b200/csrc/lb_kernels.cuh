@@ -151,7 +151,7 @@ struct XchArgs {
   double* cur = nullptr;
   double* old = nullptr;
 };
-int ws_xch_blocks(const Geom& G, int zc);
+int ws_xch_blocks(const Geom& G, int zc);  // blocks of the step (tiles x z-chunks)
 constexpr unsigned long long kXchEmpty = 0xFFF4DEADBEEF0001ULL;  // a NaN no arithmetic produces
 bool step_xch_fits(const Geom& G, const StepMaps* maps);
 cudaError_t fill_xch_empty(double* buf, long long n, cudaStream_t st);

@@ -27,9 +27,12 @@ def main():
     ap.add_argument("--rounds", type=int, default=20)
     ap.add_argument("--mrt", action="store_true", help="collision model 1 (stress in f^eq, MRT)")
     ap.add_argument("--ch", action="store_true", help="the finite-difference Cahn-Hilliard variant (lb_create_ch)")
+    ap.add_argument("--lattice", default="", help="NX,NY,NZ instead of the config's lattice")
     a = ap.parse_args()
     nx, ny, nzf, _, desc = bench.CONFIGS[a.config]
     nz = nzf(1)
+    if a.lattice:
+        nx, ny, nz = (int(v) for v in a.lattice.split(","))
     if a.ch:
         L = lb.ChLattice(nx, ny, nz)
         L.init_equilibrium(synth.spinodal_phi(nx, ny, nz))
