@@ -74,6 +74,7 @@ struct lb_ctx {
                           // 5 warp-specialised with the phi exchange
   double* xphi[2] = {nullptr, nullptr};  // phi exchange of the warp-specialised kernel (nx*ny*nzl), single slab
   bool xch_default = false;               // kernel 0 uses it (one wave of blocks)
+  bool xch_dirty = false;                 // a step since the last one that used it: refill before the next
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
   WorkCounter wctr;       // work-item counter of the persistent step kernel
@@ -229,6 +230,17 @@ int ensure_xch(lb_ctx* h) {
     CK(h, cudaMalloc(&h->xphi[k], (size_t)n * sizeof(double)));
     CK(h, fill_xch_empty(h->xphi[k], n, h->stream));
   }
+  h->xch_dirty = false;
+  return LB_OK;
+}
+
+// A step without the phi exchange leaves the array of the next exchange step
+// unreset (stale phi would pass for fresh): refill both before it.
+int refresh_xch(lb_ctx* h) {
+  if (!h->xphi[0] || !h->xch_dirty) return LB_OK;
+  const long long n = h->G.nxy * h->G.nzl;
+  for (int k = 0; k < 2; ++k) CK(h, fill_xch_empty(h->xphi[k], n, h->stream));
+  h->xch_dirty = false;
   return LB_OK;
 }
 
@@ -452,6 +464,7 @@ int halo_barrier(lb_ctx* h, int kid) {
 int one_step(lb_ctx* h, int mode) {
   const Geom& G = h->G;
   int rc;
+  h->xch_dirty = true;  // until a phi-exchange launch below says otherwise
   const bool peer = h->halo_mode == 1 && !G.zwrap;
   if (h->lc && mode >= 0) {  // Q, u halos; the step; f halo (the components that left each slab)
     if (!G.zwrap && (rc = exchange_lc(h))) return rc;
@@ -518,6 +531,7 @@ int one_step(lb_ctx* h, int mode) {
                            (h->kernel_choice >= 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
            const bool xch = ws && h->xphi[0] && (h->kernel_choice == 5 || (h->kernel_choice == 0 && h->xch_default)) &&
                             step_xch_fits(G, &s.mapsA);
+           h->xch_dirty = !xch;
            if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
              const int k = s.A < s.B ? 0 : 1;
              const XchArgs xa{h->xphi[k], h->xphi[1 - k]};
@@ -925,6 +939,7 @@ int lb_step(lb_t* h, int nsteps) {
   if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
   if (nsteps > 0 && h->xch_default && !h->ch && !h->lc && (rc = ensure_xch(h))) return rc;  // (never inside a capture)
+  if (nsteps > 0 && (rc = refresh_xch(h))) return rc;
   int t = 0;
   if (!h->stepped && nsteps > 0) {
     if ((rc = one_step(h, 0))) return rc;

@@ -13,6 +13,9 @@ timeout 300 python bench.py --collision lc --steps 100 > gpurun_out/bench_lc.jso
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 50 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo ncu_launches=$?
 $CMD > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/prof_kstep_c5 $CMD > gpurun_out/ncu2.log 2>&1; echo ncu_full=$?
+CMD="python bench.py --config c3 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/plain_c3.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 50 --csv --log-file gpurun_out/launches_c3.csv $CMD > gpurun_out/ncu1_c3.log 2>&1; echo ncu_launches_c3=$?
+$CMD > gpurun_out/plain2_c3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/prof_kstep_c3 $CMD > gpurun_out/ncu2_c3.log 2>&1; echo ncu_full_c3=$?
 CMD="python bench.py --collision lc --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_lc.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 50 --csv --log-file gpurun_out/launches_lc.csv $CMD > gpurun_out/ncu1_lc.log 2>&1; echo ncu_launches_lc=$?
 $CMD > gpurun_out/plain2_lc.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_step_lc -s 3 -c 1 -o gpurun_out/prof_kstep_lc $CMD > gpurun_out/ncu2_lc.log 2>&1; echo ncu_full_lc=$?

@@ -17,15 +17,16 @@ import bench  # noqa: E402
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
-sites = 512 * 512 * 64
 UNITS = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
 traffic_path = os.path.join(P, "traffic.json")
 traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
 
-# (ncu report, launch list, profile suffix, traffic key)
-CAPTURES = [("prof_kstep_c5", "launches.csv", "c5", "k_step@c5"),
-            ("prof_kstep_lc", "launches_lc.csv", "lc", "k_step@c5-lc")]
-for rep_name, launch_csv, suffix, key in CAPTURES:
+# (ncu report, launch list, profile suffix, traffic key, sites, lattice)
+C5, C3 = 512 * 512 * 64, 128 ** 3
+CAPTURES = [("prof_kstep_c5", "launches.csv", "c5", "k_step@c5", C5, "512x512x64"),
+            ("prof_kstep_c3", "launches_c3.csv", "c3", "k_step@c3", C3, "128^3"),
+            ("prof_kstep_lc", "launches_lc.csv", "lc", "k_step@c5-lc", C5, "512x512x64")]
+for rep_name, launch_csv, suffix, key, sites, lat in CAPTURES:
     rep = os.path.join(G, rep_name + ".ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -55,7 +56,7 @@ for rep_name, launch_csv, suffix, key in CAPTURES:
         "dram_read_bytes_per_site": round(vals["dram__bytes_read.sum"] / sites, 1),
         "dram_write_bytes_per_site": round(vals["dram__bytes_write.sum"] / sites, 1),
         "src_hash": bench.src_hash(),
-        "source": f"profiles/{tag}_ncu_full_kstep_{suffix}.txt (ncu --set full, 512x512x64, 1 launch)"}
+        "source": f"profiles/{tag}_ncu_full_kstep_{suffix}.txt (ncu --set full, {lat}, 1 launch)"}
     print("traffic:", key, traffic[key])
 with open(traffic_path, "w") as fh:
     json.dump(traffic, fh, indent=1)

@@ -299,6 +299,37 @@ def test_xch_is_default_for_one_wave():
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+def test_xch_after_other_kernels_bitwise():
+    """Steps of the phi exchange interleaved with steps that do not use it (kernel 3,
+    the MRT collision, a probe) must not read stale phi from the exchange arrays:
+    the same bits as kernel 3 throughout."""
+    f, g = rough(64, 32, 16, seed=24)
+    mp = (0.8, 1.1, 1.0)
+    with lb.Lattice(64, 32, 16, cparams(P0)) as L:
+        L.set_state(f, g)
+        lb.lb_debug_step_kernel(L.h, 5)
+        L.step(10)
+        lb.lb_debug_step_kernel(L.h, 3)
+        L.step(1)
+        lb.lb_debug_step_kernel(L.h, 5)
+        L.step(3)
+        lb.lb_set_collision(L.h, 1, *mp)
+        L.step(1)
+        lb.lb_set_collision(L.h, 0)
+        L.step(9)
+        a = L.get_state()
+    with lb.Lattice(64, 32, 16, cparams(P0)) as L:
+        L.set_state(f, g)
+        lb.lb_debug_step_kernel(L.h, 3)
+        L.step(14)
+        lb.lb_set_collision(L.h, 1, *mp)
+        L.step(1)
+        lb.lb_set_collision(L.h, 0)
+        L.step(9)
+        b = L.get_state()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
 def test_xch_kernel_mrt_bitwise():
     f, g = rough(64, 32, 10, seed=22)
     mp = (0.8, 1.1, 1.0)
