@@ -3,7 +3,7 @@ mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo tests=$?; tail -2 gpurun_out/gpu_tests.log
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench=$?
-timeout 300 python bench.py --config c3 --no-cpu-baseline > gpurun_out/bench_c3.json 2>/dev/null; echo bench_c3=$?
+timeout 300 python bench.py --config c3 --steps 2000 --no-cpu-baseline > gpurun_out/bench_c3.json 2>/dev/null; echo bench_c3=$?
 timeout 300 python bench.py --config c2 --steps 1000 --no-cpu-baseline > gpurun_out/bench_c2.json 2>/dev/null; echo bench_c2=$?
 timeout 300 python bench.py --config c4 --steps 50 --no-cpu-baseline > gpurun_out/bench_c4.json 2>/dev/null; echo bench_c4=$?
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>/dev/null; echo ref=$?
