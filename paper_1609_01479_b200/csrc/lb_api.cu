@@ -534,7 +534,7 @@ int one_step(lb_ctx* h, int mode) {
            h->xch_dirty = !xch;
            if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
              const int k = s.A < s.B ? 0 : 1;
-             const XchArgs xa{h->xphi[k], h->xphi[1 - k]};
+             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1};
              return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
                                    false, &xa);
            }

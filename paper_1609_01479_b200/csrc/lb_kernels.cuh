@@ -147,9 +147,13 @@ bool step_ws_fits(const StepMaps* maps);
 // phi array (nx*ny*nzl doubles) whose unwritten sites hold kXchEmpty: `cur` is
 // written (and read) in this step, `old` (last step's) is reset to kXchEmpty for
 // the next.
+// depth: g tiles of the stencil in flight (1 or 2; 2 pays where the state is
+// about L2-sized and the step latency-bound, 64^3 +10%, and loses where it is
+// HBM-bound, 128^3 -6%: the earlier loads queue in front of the collision's).
 struct XchArgs {
   double* cur = nullptr;
   double* old = nullptr;
+  int depth = 1;
 };
 int ws_xch_blocks(const Geom& G, int zc);  // blocks of the step (tiles x z-chunks)
 constexpr unsigned long long kXchEmpty = 0xFFF4DEADBEEF0001ULL;  // a NaN no arithmetic produces

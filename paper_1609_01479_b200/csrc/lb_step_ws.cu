@@ -96,11 +96,12 @@ struct alignas(128) WsSmem {
   static constexpr int PX = TX + 2, PY = TY + 2, NP = PX * PY;  // P box: tile + 1 halo
   alignas(128) double sTf[Q][NT];  // f of the tile, f-slot order (TMA boxes TX x TY x 5|9|5)
   alignas(128) double sTg[Q][NT];  // g of the tile, g-slot order
-  alignas(128) double sG[Q][NB];   // g on the box, g-slot order  (TMA boxes BX x BY x 5|9|5)
+  // g on the box, g-slot order (TMA boxes BX x BY x 5|9|5); XCH: two g tiles [Q][NT]
+  alignas(128) double sG[Q][XCH ? 2 * NT : NB];
   double sPhi[NPHI][NB];           // ring of phi planes on the box
   double sP[6][NP];                // chemical stress of one plane on the P box
   double sQ[2][NQ][NT];            // hand-off: phi, mu, then Fx, Fy, Fz (COLL 0) or P (COLL 1)
-  unsigned long long bar_f, bar_g, bar_box, q_full[2], q_empty[2], item_full[4];
+  unsigned long long bar_f, bar_g, bar_box, bar_xb[2], q_full[2], q_empty[2], item_full[4];
   int sItem[4];                    // work items, fetched by the stencil warps
 };
 
@@ -174,6 +175,8 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     mbar_init(&sm.bar_f, 1);
     mbar_init(&sm.bar_g, 1);
     mbar_init(&sm.bar_box, 1);
+    mbar_init(&sm.bar_xb[0], 1);
+    mbar_init(&sm.bar_xb[1], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.q_full[s], kNA);
       mbar_init(&sm.q_empty[s], NT);
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     };
     constexpr int BROWU = BX / 2, BOXU = BY * BROWU, BOXR = (BOXU + kNA - 1) / kNA;
     unsigned ph_box = 0;
+    unsigned ph_xb = 0;  // XCH: parity bits of the two g tile buffers
     unsigned seq = 0;  // planes handed off so far: slot seq & 1, use seq >> 1
     double Pz_prev[SPT][3], Pz_cur[SPT][3], Fxy_cur[SPT][3];
     double P6_cur[SPT][COLL == 1 ? 6 : 1];  // COLL 1: P at the site, plane j
@@ -245,13 +249,15 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         const int zs = zsrc(zp, ghost);
         if (ghost) return false;
         if (XCH && !use_box) {
-          if (a == 0) {  // the g tile only, in tile layout
+          if (a == 0) {  // the g tile only, in tile layout, into buffer n & 1
             const int cpl = (zs + GZ) * NSLOT;
+            double* dst = &sm.sG[0][0] + (n & 1) * Q * NT;
+            unsigned long long* bar = &sm.bar_xb[n & 1];
             fence_proxy_async();
-            mbar_expect_tx(&sm.bar_box, TILE_BYTES);
-            tma_load_3d(&sm.sG[0][0], &tm_t5, x0, y0, cpl + 5, &sm.bar_box, pol_last);
-            tma_load_3d(&sm.sG[0][0] + 5 * NT, &tm_t9, x0, y0, cpl + 19, &sm.bar_box, pol_last);
-            tma_load_3d(&sm.sG[0][0] + 14 * NT, &tm_t5, x0, y0, cpl + 33, &sm.bar_box, pol_last);
+            mbar_expect_tx(bar, TILE_BYTES);
+            tma_load_3d(dst, &tm_t5, x0, y0, cpl + 5, bar, pol_last);
+            tma_load_3d(dst + 5 * NT, &tm_t9, x0, y0, cpl + 19, bar, pol_last);
+            tma_load_3d(dst + 14 * NT, &tm_t5, x0, y0, cpl + 33, bar, pol_last);
           }
         } else if (box_interior) {
           if (a == 0) {
@@ -276,9 +282,12 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         return true;
       };
       // wait for the box, then make it visible to the whole role
-      auto wait_box = [&](bool issued) {
-        if (issued) {
-          if (box_interior || (XCH && !use_box)) {
+      auto wait_box = [&](bool issued, int n) {
+        if (XCH && !use_box) {  // g tile n (always issued: one periodic slab)
+          mbar_wait(&sm.bar_xb[n & 1], (ph_xb >> (n & 1)) & 1);
+          ph_xb ^= 1u << (n & 1);
+        } else if (issued) {
+          if (box_interior) {
             mbar_wait(&sm.bar_box, ph_box);
             ph_box ^= 1;
           } else {
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         }
         named_sync(2, kNA);
       };
-      auto make_phi = [&](int zp) {
+      auto make_phi = [&](int zp, int n) {
         bool ghost;
         const int zs = zsrc(zp, ghost);
         double* ring = sm.sPhi[wslot<S::NPHI>(zp)];
@@ -295,7 +304,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           double* xp = xa.cur + (long long)zs * nxy;
           double* xo = xa.old + (long long)zs * nxy;
           if (!use_box) {  // phi of the tile from the g tile
-            const double(*gt)[NT] = reinterpret_cast<const double(*)[NT]>(&sm.sG[0][0]);
+            const double(*gt)[NT] = reinterpret_cast<const double(*)[NT]>(&sm.sG[0][0] + (n & 1) * Q * NT);
             for (int s = a; s < NT; s += kNA) {
               double v = gt[grank(0)][s];  // A.3, canonical order (same as phi_sum)
 #pragma unroll
@@ -398,6 +407,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       };
       double pf = 0.0;  // the halo site of box hb + 1, loaded an iteration ahead
       bool issued = issue_box(n0);
+      if (XCH && xa.depth == 2 && n0 + 1 <= nlast) issue_box(n0 + 1);  // two g tiles in flight
       for (int nn = n0; nn <= nlast + lag; ++nn) {
         double hv = 0.0;
         const int hb = nn - lag;  // the halo box completed in this iteration
@@ -408,15 +418,18 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         }
         if (XCH && h_ring >= 0 && hb + 1 >= 0 && hb + 1 <= nlast) pf = ld_relaxed_f64(xsite(hb + 1));
         if (nn <= nlast) {
-          wait_box(issued);  // (also: everyone is past the previous hand-off)
-          make_phi(zA - 2 + nn);
+          wait_box(issued, nn);  // (also: everyone is past the previous hand-off)
+          make_phi(zA - 2 + nn, nn);
         } else {
           named_sync(2, kNA);
         }
         if (hw) sm.sPhi[wslot<S::NPHI>(zA - 2 + hb)][h_ring] = hv;
         named_sync(2, kNA);  // sG consumed, ring written
         if (nn <= nlast) {
-          issued = nn + 1 <= nlast ? issue_box(nn + 1) : false;
+          if (XCH && xa.depth == 2)
+            issued = nn + 2 <= nlast ? issue_box(nn + 2) : false;
+          else
+            issued = nn + 1 <= nlast ? issue_box(nn + 1) : false;
         }
         const int n = nn - lag, zp = zA - 2 + n;
         if (n < 2) continue;
