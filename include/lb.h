@@ -253,18 +253,21 @@ int lb_init_lc(lb_t* h, const double* rho, const double* u, const double* n);
  * the next lb_step. */
 int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, double tau_ghost);
 
-/* Which step kernel lb_step uses: 0 = default (the warp-specialised kernel
- * when the plane is large enough for 32 x 8 tiles and nx is even, else the tile
- * kernel), 1 = the tile
+/* Which step kernel lb_step uses: 0 = default (the warp-specialised kernel for
+ * even nx, with the phi exchange of kernel 5 where the step's blocks -- 32 x 8
+ * tiles x z-chunks -- fit in one wave on the SMs, e.g. 64^3 and 128^3; else the
+ * tile kernel), 1 = the tile
  * kernel (halo box per CTA), 2 = the cluster kernel (phi halos shared through
  * distributed shared memory; needs nx % 64 == 0 and ny % 16 == 0, else
  * LB_EINVAL), 3 = the warp-specialised tile kernel (stencil and collision on
  * separate warps; needs nx even, else LB_EINVAL), 4 = the same with persistent
  * CTAs taking work items from a counter, 5 = the warp-specialised kernel with
- * the phi exchange (neighbouring tiles' CTAs hand each other the phi halo through
- * an L2-resident array and per-block flags instead of each loading the g halo
- * box; one periodic slab, nx % 32 == 0, ny % 8 == 0, else LB_EINVAL).  All give
- * bitwise identical results.  Test / measurement support. */
+ * the phi exchange (the stencil loads the g tile only and takes the phi halo from
+ * the neighbouring tiles' CTAs through an L2-resident phi array whose unwritten
+ * sites hold a sentinel NaN, summing it from g where the owner runs behind; one
+ * periodic slab, nx % 32 == 0, ny % 8 == 0, else LB_EINVAL; allocates two
+ * nx*ny*nz phi arrays).  All give bitwise identical results.  Test / measurement
+ * support. */
 int lb_debug_step_kernel(lb_t* h, int which);
 
 /* Halo transport of a slab handle.  mode -1: returns the current mode (0 or 1);
