@@ -83,14 +83,6 @@ __host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch
   const int t = grp * resid + (r - c * rg);
   return TileId{t % ntx, t / ntx, c};
 }
-// inverse of tile_of_block: the block of tile t (row-major) in chunk c
-__host__ __device__ inline int block_of_tile(int t, int c, int ntx, int nty, int nch, int resid) {
-  const int ntiles = ntx * nty;
-  if (resid > ntiles || resid < 1) resid = ntiles;
-  const int grp = t / resid;
-  const int rg = ntiles - grp * resid < resid ? ntiles - grp * resid : resid;
-  return grp * resid * nch + c * rg + (t - grp * resid);
-}
 
 // Fused halo ("peer" transport): the buffers of the
 // neighbouring slabs, on this GPU (loopback) or mapped from a peer GPU over
