@@ -73,7 +73,10 @@ struct lb_ctx {
   int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised,
                           // 5 warp-specialised with the phi exchange
   double* xphi[2] = {nullptr, nullptr};  // phi exchange of the warp-specialised kernel (nx*ny*nzl), single slab
-  bool xch_default = false;               // kernel 0 uses it (one wave of blocks)
+  bool xch_default = false;               // kernel 0 uses it (one wave of blocks, or bands of one wave)
+  int xch_band = 0;                       // tiles per launch of the banded exchange (0: one launch)
+  int* xch_pre = nullptr;                 // sites the bands take from later bands (ws_xch_pre_sites)
+  int xch_npre = 0;
   bool xch_dirty = false;                 // a step since the last one that used it: refill before the next
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
@@ -261,8 +264,24 @@ int alloc_slabs(lb_ctx* h) {
       return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed for the step kernel's TMA descriptors");
   }
   // the phi-exchange step kernel is the default where its blocks run in one wave
-  h->xch_default = h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) &&
-                   ws_xch_blocks(h->G, h->zc) <= h->num_sms && h->kernel_choice == 0;
+  // (LB_XCH_BAND: tuning override, tiles per band; 0 = no bands)
+  h->xch_band = ws_xch_band(h->G, h->zc, h->num_sms);
+  bool band_default = false;
+  if (const char* e = std::getenv("LB_XCH_BAND")) {
+    const int b = std::atoi(e);
+    if (b >= 0) h->xch_band = b;
+    band_default = b > 0;
+  }
+  h->xch_default = h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->kernel_choice == 0 &&
+                   (ws_xch_blocks(h->G, h->zc) <= h->num_sms || band_default);
+  if (h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->xch_band > 0) {
+    const std::vector<int> pre = ws_xch_pre_sites(h->G, h->xch_band);
+    h->xch_npre = (int)pre.size();
+    if (h->xch_npre > 0) {
+      CK(h, cudaMalloc(&h->xch_pre, pre.size() * sizeof(int)));
+      CK(h, cudaMemcpy(h->xch_pre, pre.data(), pre.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+  }
   CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
   CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
   CK(h, cudaMalloc(&h->wctr.dev, sizeof(unsigned long long)));
@@ -534,7 +553,12 @@ int one_step(lb_ctx* h, int mode) {
            h->xch_dirty = !xch;
            if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
              const int k = s.A < s.B ? 0 : 1;
-             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1};
+             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1, h->xch_band, 0,
+                              h->xch_pre, h->xch_npre};
+             if (h->xch_band > 0) {  // one launch per band (+ the pre-pass): counted beyond timed()'s one
+               const long long nt = (long long)(G.nx / 32) * (G.ny / 8);
+               h->launches += (nt + h->xch_band - 1) / h->xch_band - 1 + (h->xch_npre > 0);
+             }
              return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
                                    false, &xa);
            }
@@ -1041,6 +1065,7 @@ void lb_destroy(lb_t* h) {
   cudaFree(h->d_flag);
   cudaFree(h->xphi[0]);
   cudaFree(h->xphi[1]);
+  cudaFree(h->xch_pre);
   cudaFree(h->wctr.dev);
   if (h->h_flag) cudaFreeHost(h->h_flag);
   for (auto& p : h->pending) {

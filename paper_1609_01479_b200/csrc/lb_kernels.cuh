@@ -1,6 +1,7 @@
 // lb_kernels.cuh -- internal (C++) interface between the host runtime and the
 // sm_100a kernels.  Not part of the C ABI (include/lb.h is).
 #pragma once
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -142,11 +143,24 @@ bool step_ws_fits(const StepMaps* maps);
 // depth: g tiles of the stencil in flight (1 or 2; 2 pays where the state is
 // about L2-sized and the step latency-bound, 64^3 +10%, and loses where it is
 // HBM-bound, 128^3 -6%: the earlier loads queue in front of the collision's).
+// band: tiles per launch (0: all items in one launch).  Over several waves the
+// step is launched band by band, each band's tiles x z-chunks in one wave, so
+// the CTAs of neighbouring tiles start together again at every band (DESIGN.md
+// "phi exchange in bands"); l0 is the first work item of the launch (set by the
+// launcher).
 struct XchArgs {
   double* cur = nullptr;
   double* old = nullptr;
   int depth = 1;
+  int band = 0;
+  int l0 = 0;
+  const int* pre = nullptr;  // xy of the sites bands take from later bands (ws_xch_pre_sites), device
+  int npre = 0;
 };
+// tiles per band of the banded phi exchange: whole tile rows whose blocks (tiles
+// x z-chunks) fit in one wave of num_sms CTAs; 0 if the lattice fits one wave.
+int ws_xch_band(const Geom& G, int zc, int num_sms);
+std::vector<int> ws_xch_pre_sites(const Geom& G, int band);
 int ws_xch_blocks(const Geom& G, int zc);  // blocks of the step (tiles x z-chunks)
 constexpr unsigned long long kXchEmpty = 0xFFF4DEADBEEF0001ULL;  // a NaN no arithmetic produces
 bool step_xch_fits(const Geom& G, const StepMaps* maps);

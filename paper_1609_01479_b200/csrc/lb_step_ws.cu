@@ -20,6 +20,8 @@
 // The tile kernel is one CTA per SM at 32 x 8 tiles; there, every __syncthreads
 // between the phi/P phases and the collision phase stalled the store stream
 // (DESIGN.md "Tuning").  Needs 16-byte rows (nx even: TMA).
+#include <algorithm>
+
 #include "lb_device.cuh"
 #include "lb_tma.cuh"
 
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           const unsigned long long v = atomicAdd(wctr, 1ULL) - wbase;
           L = v < (unsigned long long)nitems ? (int)v : nitems;
         } else {
-          L = idx == 0 ? (int)blockIdx.x : nitems;
+          L = idx == 0 ? (int)blockIdx.x + xa.l0 : nitems;
         }
         sm.sItem[idx % 4] = L;
         mbar_arrive(&sm.item_full[idx % 4]);
@@ -605,6 +607,21 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
 }
 
 
+// Banded phi exchange: before the bands, phi of every site a band takes as halo
+// from a LATER band (xa.pre: the xy offsets, all planes), summed from g with
+// phi_sum and stored to xa.cur -- the edge tiles of a band would otherwise sum
+// them from g one site at a time on the stencil's path, and the launch waits for
+// its slowest block.  The owners store the same bits again when their band runs.
+__global__ void __launch_bounds__(256) k_xch_pre(Geom G, const double* __restrict__ A, double* __restrict__ cur,
+                                                 const int* __restrict__ pre, int npre) {
+  const long long n = (long long)G.nzl * npre;
+  for (long long t = blockIdx.x * 256LL + threadIdx.x; t < n; t += (long long)gridDim.x * 256) {
+    const int z = (int)(t / npre);
+    const long long xy = pre[t - (long long)z * npre];
+    __stcg(cur + (long long)z * G.nxy + xy, phi_sum(A + (long long)(z + GZ) * G.plane + xy, G.nxy));
+  }
+}
+
 template <int TY, bool PERSIST, int COLL, bool XCH = false>
 cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
                         int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc,
@@ -632,6 +649,24 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
   if (PERSIST && (!wc || !wc->dev)) return cudaErrorInvalidValue;
   if (XCH && (!xch || !xch->cur || !xch->old)) return cudaErrorInvalidValue;
   const XchArgs xa = xch ? *xch : XchArgs{};
+  if (XCH && xa.band > 0) {  // banded: one launch per band of tiles, each one wave
+    const int nch = (G.nzl + zc - 1) / zc, ntiles = nitems / nch;
+    if (xa.npre > 0) {  // the halo sites the bands take from later bands, first
+      k_xch_pre<<<148 * 4, 256, 0, st>>>(G, A, xa.cur, xa.pre, xa.npre);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    for (int t0 = 0; t0 < ntiles; t0 += xa.band) {
+      XchArgs xb = xa;
+      xb.l0 = t0 * nch;
+      const int rt = ntiles - t0 < xa.band ? ntiles - t0 : xa.band;
+      kern<<<(unsigned)(rt * nch), ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, xa.band, flag, pr, nullptr,
+                                                                    0ULL, xb, m[0], m[1], m[2], m[3]);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   const unsigned nblk = (unsigned)(PERSIST ? (nitems < resid ? nitems : resid) : nitems);
   kern<<<nblk, ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, wc ? wc->dev : nullptr,
                                                   wc ? wc->base : 0ULL, xa, m[0], m[1], m[2], m[3]);
@@ -648,6 +683,35 @@ bool step_xch_fits(const Geom& G, const StepMaps* maps) {
   return step_ws_fits(maps) && maps->ty == 8 && G.zwrap && G.nx % kWTX == 0 && G.ny % 8 == 0;
 }
 int ws_xch_blocks(const Geom& G, int zc) { return (G.nx / kWTX) * ((G.ny + 7) / 8) * ((G.nzl + zc - 1) / zc); }
+int ws_xch_band(const Geom& G, int zc, int num_sms) {
+  const int ntx = G.nx / kWTX, nty = (G.ny + 7) / 8, nch = (G.nzl + zc - 1) / zc;
+  const int ntiles = ntx * nty;
+  if ((long long)ntiles * nch <= num_sms) return 0;
+  const int per = num_sms / nch;  // tiles of one wave
+  if (per < 1) return 1;
+  const int nb = (ntiles + per - 1) / per;  // bands of about equal size
+  return (ntiles + nb - 1) / nb;
+}
+
+// xy offsets of the sites some band takes as phi halo from a later band: site s
+// lies in the 2-site ring of tile T iff T meets the 5 x 5 window around s, and
+// the tiles (32 x 8, both >= 5) met by the window are those of its 4 corners.
+std::vector<int> ws_xch_pre_sites(const Geom& G, int band) {
+  std::vector<int> out;
+  if (band <= 0) return out;
+  const int ntx = G.nx / kWTX;
+  auto w = [](int v, int n) { v %= n; return v < 0 ? v + n : v; };
+  auto band_of = [&](int x, int y) { return ((w(y, G.ny) / 8) * ntx + w(x, G.nx) / kWTX) / band; };
+  for (int y = 0; y < G.ny; ++y)
+    for (int x = 0; x < G.nx; ++x) {
+      const int b = band_of(x, y);
+      int m = b;
+      for (int dy = -2; dy <= 2; dy += 4)
+        for (int dx = -2; dx <= 2; dx += 4) m = std::min(m, band_of(x + dx, y + dy));
+      if (m < b) out.push_back(y * G.nx + x);
+    }
+  return out;
+}
 namespace {
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
