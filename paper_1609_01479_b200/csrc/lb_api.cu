@@ -553,7 +553,7 @@ int one_step(lb_ctx* h, int mode) {
            h->xch_dirty = !xch;
            if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
              const int k = s.A < s.B ? 0 : 1;
-             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1, h->xch_band, 0,
+             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1, h->xch_band, 0, 0,
                               h->xch_pre, h->xch_npre};
              if (h->xch_band > 0) {  // one launch per band (+ the pre-pass): counted beyond timed()'s one
                const long long nt = (long long)(G.nx / 32) * (G.ny / 8);

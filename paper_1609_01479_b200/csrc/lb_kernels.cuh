@@ -146,14 +146,13 @@ bool step_ws_fits(const StepMaps* maps);
 // band: tiles per launch (0: all items in one launch).  Over several waves the
 // step is launched band by band, each band's tiles x z-chunks in one wave, so
 // the CTAs of neighbouring tiles start together again at every band (DESIGN.md
-// "phi exchange in bands"); l0 is the first work item of the launch (set by the
-// launcher).
+// "phi exchange in bands").
 struct XchArgs {
   double* cur = nullptr;
   double* old = nullptr;
   int depth = 1;
   int band = 0;
-  int l0 = 0;
+  int t0 = 0, rt = 0;  // tiles [t0, t0 + rt) of one banded launch (set by the launcher)
   const int* pre = nullptr;  // xy of the sites bands take from later bands (ws_xch_pre_sites), device
   int npre = 0;
 };

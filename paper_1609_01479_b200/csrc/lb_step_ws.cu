@@ -161,7 +161,11 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
   const int nitems = ntx * nty * nch;
   const long long nxy = G.nxy;
   auto item_of = [&](int L) {
-    const TileId tb = tile_of_block(L, ntx, nty, nch, resid);
+    TileId tb = tile_of_block(L, ntx, nty, nch, resid);
+    if (XCH && xa.rt > 0) {  // banded: tiles [t0, t0 + rt) of this launch, chunk-major
+      const int t = xa.t0 + L % xa.rt;
+      tb = TileId{t % ntx, t / ntx, L / xa.rt};
+    }
     WsItem it;
     it.x0 = tb.bx * TX;
     it.y0 = tb.by * TY;
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           const unsigned long long v = atomicAdd(wctr, 1ULL) - wbase;
           L = v < (unsigned long long)nitems ? (int)v : nitems;
         } else {
-          L = idx == 0 ? (int)blockIdx.x + xa.l0 : nitems;
+          L = idx == 0 ? (int)blockIdx.x : nitems;
         }
         sm.sItem[idx % 4] = L;
         mbar_arrive(&sm.item_full[idx % 4]);
@@ -650,18 +654,28 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
   if (XCH && (!xch || !xch->cur || !xch->old)) return cudaErrorInvalidValue;
   const XchArgs xa = xch ? *xch : XchArgs{};
   if (XCH && xa.band > 0) {  // banded: one launch per band of tiles, each one wave
-    const int nch = (G.nzl + zc - 1) / zc, ntiles = nitems / nch;
+    const int ntiles = nitems / ((G.nzl + zc - 1) / zc);
     if (xa.npre > 0) {  // the halo sites the bands take from later bands, first
       k_xch_pre<<<148 * 4, 256, 0, st>>>(G, A, xa.cur, xa.pre, xa.npre);
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
+    // full bands: one chunk of the whole slab per tile; the last, partial band
+    // is cut into z-chunks (>= 8 planes) so that it fills the wave as well
     for (int t0 = 0; t0 < ntiles; t0 += xa.band) {
       XchArgs xb = xa;
-      xb.l0 = t0 * nch;
-      const int rt = ntiles - t0 < xa.band ? ntiles - t0 : xa.band;
-      kern<<<(unsigned)(rt * nch), ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, xa.band, flag, pr, nullptr,
-                                                                    0ULL, xb, m[0], m[1], m[2], m[3]);
+      xb.t0 = t0;
+      xb.rt = ntiles - t0 < xa.band ? ntiles - t0 : xa.band;
+      int nchb = 1;
+      if (xb.rt < xa.band) {
+        nchb = resid / xb.rt;
+        if (nchb > G.nzl / 8) nchb = G.nzl / 8;
+        if (nchb < 1) nchb = 1;
+      }
+      const int zcb = (G.nzl + nchb - 1) / nchb;
+      nchb = (G.nzl + zcb - 1) / zcb;
+      kern<<<(unsigned)(xb.rt * nchb), ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zcb, resid, flag, pr,
+                                                                       nullptr, 0ULL, xb, m[0], m[1], m[2], m[3]);
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
@@ -687,12 +701,14 @@ int ws_xch_band(const Geom& G, int zc, int num_sms) {
   const int ntx = G.nx / kWTX, nty = (G.ny + 7) / 8, nch = (G.nzl + zc - 1) / zc;
   const int ntiles = ntx * nty;
   if ((long long)ntiles * nch <= num_sms) return 0;
-  const int per = num_sms / nch;  // tiles of one wave
-  if (per < 1) return 1;
-  const int nb = (ntiles + per - 1) / per;  // bands of about equal size
-  return (ntiles + nb - 1) / nb;
+  if (ntiles <= num_sms) return ntiles;
+  if (num_sms < ntx) return num_sms;
+  // bands of whole tile rows, about equal (512 x 512 x 64: 8 bands of 8 rows, 128
+  // CTAs; partial-row bands of 147 tiles -6% -- more pre-pass sites, rows split
+  // between launches; 7 bands of 9 rows + one row cut in z -4%)
+  const int rows = num_sms / ntx, nb = (nty + rows - 1) / rows;
+  return (nty + nb - 1) / nb * ntx;
 }
-
 // xy offsets of the sites some band takes as phi halo from a later band: site s
 // lies in the 2-site ring of tile T iff T meets the 5 x 5 window around s, and
 // the tiles (32 x 8, both >= 5) met by the window are those of its 4 corners.

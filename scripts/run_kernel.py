@@ -16,9 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--steps", type=int, default=4)
+ap.add_argument("--lattice", default="", help="NX,NY,NZ instead of the config's lattice")
 a = ap.parse_args()
 nx, ny, nzf, _, _ = bench.CONFIGS[a.config]
 nz = nzf(1)
+if a.lattice:
+    nx, ny, nz = (int(v) for v in a.lattice.split(","))
 L = lb.Lattice(nx, ny, nz)
 L.init_equilibrium(synth.spinodal_phi(nx, ny, nz))
 lb.lb_debug_step_kernel(L.h, a.kernel)

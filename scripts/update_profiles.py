@@ -60,7 +60,24 @@ for rep_name, launch_csv, suffix, key, sites, lat in CAPTURES:
     print("traffic:", key, traffic[key])
 with open(traffic_path, "w") as fh:
     json.dump(traffic, fh, indent=1)
+# bench lines: roofline.traffic from the capture above when it was taken on the
+# same sources (bench.py reads traffic.json itself, but the bench runs before the
+# capture of the same call)
+TKEY = {"default": "k_step@c5", "c3": "k_step@c3", "c2": "k_step@c2", "c4": "k_step@c4", "mrt": "k_step@c5-mrt",
+        "ch": "k_step@c5-ch", "lc": "k_step@c5-lc"}
 for f in ("default", "c3", "c2", "c4", "ref", "mrt", "ch", "lc"):
     src = os.path.join(G, f"bench_{f}.json")
     if os.path.exists(src) and os.path.getsize(src) > 0:
-        shutil.copy(src, os.path.join(P, f"{tag}_bench_{f}.json"))
+        dst = os.path.join(P, f"{tag}_bench_{f}.json")
+        try:
+            line = json.loads(open(src).read().strip().splitlines()[-1])
+        except Exception:
+            shutil.copy(src, dst)
+            continue
+        e = traffic.get(TKEY.get(f, ""))
+        r = line.get("roofline")
+        if r is not None and r.get("traffic") is None and e and e.get("src_hash") == line.get("src_hash"):
+            r["traffic"] = e["dram_bytes_per_launch"]
+            r["traffic_source"] = e["source"]
+        with open(dst, "w") as fh:
+            fh.write(json.dumps(line) + "\n")

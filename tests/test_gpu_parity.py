@@ -287,19 +287,21 @@ def test_xch_kernel_bitwise_equal_to_ws_kernel(shape, zchunk):
         assert_parity(a, R.run(f, g, P0, steps))
 
 
-@pytest.mark.parametrize("shape,band,kernel", [((128, 48, 8), 5, 5), ((128, 48, 8), 1, 5), ((512, 304, 16), 37, 0),
-                                                ((512, 304, 16), 0, 5)])
+@pytest.mark.parametrize("shape,band,kernel", [((128, 48, 32), 5, 5), ((128, 48, 8), 1, 5), ((512, 304, 16), 37, 0),
+                                                ((512, 304, 16), 0, 5), ((512, 512, 24), None, 5)])
 def test_xch_bands_bitwise(shape, band, kernel, monkeypatch):
     """The banded phi exchange (one launch per band of tiles, each band one wave; a
     halo site of a later band is summed from g, one of an earlier band read from its
     store) gives the bits of kernel 3 for bands that are not whole tile rows, bands
     of one tile (every halo site summed from g), the default kernel taking the bands
-    (LB_XCH_BAND > 0) and LB_XCH_BAND = 0 (one launch over several waves)."""
+    (LB_XCH_BAND > 0), LB_XCH_BAND = 0 (one launch over several waves) and the
+    automatic bands (9 tile rows; the last band of one row cut into 3 z-chunks)."""
     nx, ny, nz = shape
     f, g = rough(nx, ny, nz, seed=29)
-    monkeypatch.setenv("LB_XCH_BAND", str(band))
+    if band is not None:
+        monkeypatch.setenv("LB_XCH_BAND", str(band))
     a = gpu_run(f, g, P0, 4, kernel=kernel)
-    monkeypatch.delenv("LB_XCH_BAND")
+    monkeypatch.delenv("LB_XCH_BAND", raising=False)
     b = gpu_run(f, g, P0, 4, kernel=3)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
