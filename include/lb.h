@@ -289,6 +289,17 @@ int lb_debug_halo_mode(lb_t* h, int mode);
  * planes, no halo plan).  Must equal lb_debug_propagation_map.  Host-only. */
 int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* out);
 
+/* Band plan of the banded phi exchange (kernel 5 over several waves, or kernel 0
+ * with LB_XCH_BAND > 0) for one periodic
+ * nx x ny x nz slab whose step uses z-chunks of zc planes on num_sms SMs.
+ * band >= 0 imposes the band (tiles of 32 x 8 per launch, 0 = no bands), band < 0
+ * asks for the automatic choice; *band_out receives it.  sites (capacity cap,
+ * may be NULL when cap == 0) receives, ascending, the xy offsets y*nx + x of the
+ * sites some band takes as phi halo (the 2-site ring of its tiles) from a LATER
+ * band -- those the pre-pass sums before the bands run.  Returns their number
+ * (which may exceed cap) or LB_EINVAL (nx % 32, ny % 8, sizes).  Host-only. */
+int lb_debug_xch_bands(int nx, int ny, int nz, int zc, int num_sms, int band, int* band_out, int* sites, int cap);
+
 /* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of
  * nranks, the ranks it sends its +z and -z halo to, and the number of doubles
  * per message: distributions (10 components x nx*ny) and phi (2 planes x nx*ny).

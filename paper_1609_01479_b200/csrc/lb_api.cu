@@ -1234,6 +1234,23 @@ int lb_debug_halo_mode(lb_t* h, int mode) {
   return LB_OK;
 }
 
+int lb_debug_xch_bands(int nx, int ny, int nz, int zc, int num_sms, int band, int* band_out, int* sites, int cap) {
+  if (!band_out || nx < 32 || ny < 8 || nz < 3 || nx % 32 || ny % 8 || zc < 1 || num_sms < 1 || cap < 0 ||
+      (cap > 0 && !sites))
+    return LB_EINVAL;
+  Geom G;
+  G.nx = nx;
+  G.ny = ny;
+  G.nzl = nz;
+  G.zwrap = true;
+  G.nxy = (long long)nx * ny;
+  G.plane = (long long)NSLOT * G.nxy;
+  *band_out = band >= 0 ? band : ws_xch_band(G, zc, num_sms);
+  const std::vector<int> pre = ws_xch_pre_sites(G, *band_out);
+  for (size_t k = 0; k < pre.size() && (long long)k < cap; ++k) sites[k] = pre[k];
+  return (int)pre.size();
+}
+
 int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* out) {
   if (!out || nx < 3 || ny < 3 || nz < 3 || nslabs < 1 || nz % nslabs || (nslabs > 1 && nz / nslabs < 2))
     return LB_EINVAL;

@@ -74,6 +74,7 @@ _lb_bytes_per_site = _sig("lb_bytes_per_site", C.c_double)
 _lb_debug_propagation_map = _sig("lb_debug_propagation_map", _i, _i, _i, _i, _i, _vp)
 _lb_debug_propagation_map_peers = _sig("lb_debug_propagation_map_peers", _i, _i, _i, _i, _i, _vp)
 _lb_debug_halo_mode = _sig("lb_debug_halo_mode", _i, _vp, _i)
+_lb_debug_xch_bands = _sig("lb_debug_xch_bands", _i, _i, _i, _i, _i, _i, _i, C.POINTER(_i), _vp, _i)
 _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
 _lb_set_collision = _sig("lb_set_collision", _i, _vp, _i, C.c_double, C.c_double, C.c_double)
 _lb_create_ch = _sig("lb_create_ch", _i, _i, _i, _i, C.POINTER(lb_params), C.c_double, C.c_double, C.c_double,
@@ -103,7 +104,7 @@ EXPORTS = [
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
-    "lb_debug_halo_mode", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_create_ch_loopback", "lb_create_ch_slab", "lb_set_state_ch",
+    "lb_debug_halo_mode", "lb_debug_xch_bands", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_create_ch_loopback", "lb_create_ch_slab", "lb_set_state_ch",
     "lb_get_state_ch",
     "lb_create_lc", "lb_create_lc_loopback", "lb_create_lc_slab", "lb_set_state_lc", "lb_get_state_lc", "lb_init_lc",
 ]
@@ -260,6 +261,17 @@ def lb_debug_propagation_map_peers(nx: int, ny: int, nz: int, nslabs: int = 1) -
     if rc != LB_OK:
         raise LBError(rc, "peer propagation map failed (bad sizes, a ghost-plane store or not a permutation)")
     return out.reshape(Q, nz, ny, nx)
+
+
+def lb_debug_xch_bands(nx: int, ny: int, nz: int, zc: int, num_sms: int, band: int = -1):
+    """(band, xy offsets the pre-pass of the banded phi exchange sums) -- host-only."""
+    b = C.c_int(0)
+    n = _lb_debug_xch_bands(nx, ny, nz, zc, num_sms, band, C.byref(b), None, 0)
+    if n < 0:
+        raise LBError(n, "lb_debug_xch_bands: bad sizes")
+    out = np.empty(max(n, 1), dtype=np.int32)
+    n = _lb_debug_xch_bands(nx, ny, nz, zc, num_sms, band, C.byref(b), out.ctypes.data, n)
+    return b.value, out[:n]
 
 
 def lb_set_collision(h, model: int, tau_shear: float = 0.8, tau_bulk: float = 1.0, tau_ghost: float = 1.0) -> None:
