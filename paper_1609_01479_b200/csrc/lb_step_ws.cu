@@ -21,6 +21,7 @@
 // between the phi/P phases and the collision phase stalled the store stream
 // (DESIGN.md "Tuning").  Needs 16-byte rows (nx even: TMA).
 #include <algorithm>
+#include <cstdlib>
 
 #include "lb_device.cuh"
 #include "lb_tma.cuh"
@@ -65,6 +66,9 @@ __host__ __device__ constexpr bool ws_split_regs(int ty) {
 #endif
 
 // XCH: planes the stencil's P / F / mu work trails its phi (the neighbours' slack)
+#ifndef LB_XCH_PF
+#define LB_XCH_PF 1  // iterations a halo site of the phi exchange is loaded ahead of its use (1 or 2)
+#endif
 #ifndef LB_XCH_LAG
 #define LB_XCH_LAG 4
 #endif
@@ -412,6 +416,9 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         return phi_sum(A + (long long)(wrap_n(zA - 2 + b, G.nzl) + GZ) * G.plane + h_off, nxy);
       };
       double pf = 0.0;  // the halo site of box hb + 1, loaded an iteration ahead
+      double pf2 = 0.0;  // (LB_XCH_PF 2: box hb + 2, two iterations ahead)
+      if (LB_XCH_PF == 2 && XCH && h_ring >= 0 && n0 - lag + 1 >= 0 && n0 - lag + 1 <= nlast)
+        pf2 = ld_relaxed_f64(xsite(n0 - lag + 1));
       bool issued = issue_box(n0);
       if (XCH && xa.depth == 2 && n0 + 1 <= nlast) issue_box(n0 + 1);  // two g tiles in flight
       for (int nn = n0; nn <= nlast + lag; ++nn) {
@@ -422,7 +429,12 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           hv = pf;
           if (__double_as_longlong(hv) == (long long)kXchEmpty) hv = phi_here(hb);  // owner behind: sum it here
         }
-        if (XCH && h_ring >= 0 && hb + 1 >= 0 && hb + 1 <= nlast) pf = ld_relaxed_f64(xsite(hb + 1));
+        if constexpr (LB_XCH_PF == 2) {
+          pf = pf2;
+          if (XCH && h_ring >= 0 && hb + 2 >= 0 && hb + 2 <= nlast) pf2 = ld_relaxed_f64(xsite(hb + 2));
+        } else {
+          if (XCH && h_ring >= 0 && hb + 1 >= 0 && hb + 1 <= nlast) pf = ld_relaxed_f64(xsite(hb + 1));
+        }
         if (nn <= nlast) {
           wait_box(issued, nn);  // (also: everyone is past the previous hand-off)
           make_phi(zA - 2 + nn, nn);
@@ -647,6 +659,10 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
 #ifdef LB_RESID_OVERRIDE
     resid = LB_RESID_OVERRIDE;
 #endif
+    if (const char* e = std::getenv("LB_RESID")) {  // tuning override (measurement only)
+      const int v = std::atoi(e);
+      if (v > 0) resid = v;
+    }
   }
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   const int nitems = ((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc);

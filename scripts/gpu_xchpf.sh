@@ -1,0 +1,10 @@
+# phi-exchange halo prefetch distance / lag variants: xch tests + A/B kernel 3 vs 5
+mkdir -p gpurun_out
+IFS=';' read -ra VS <<< "${VARIANTS:- }"
+for v in "${VS[@]}"; do
+  LB_NVCC_FLAGS="$v" python paper_1609_01479_b200/_build.py --force > /dev/null 2>&1 || echo build_fail "$v"
+  timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "xch" > gpurun_out/xchpf_tests.log 2>&1; echo "[$v] tests=$?"
+  for lat in 512,512,64 128,128,128 256,256,32; do
+    echo "[$v] lat=$lat $(timeout 300 python scripts/probe.py --lattice $lat --ab 3,5 --steps 20 --rounds 10 2>&1 | tail -1)"
+  done
+done
