@@ -274,7 +274,11 @@ int alloc_slabs(lb_ctx* h) {
   }
   h->xch_default = h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->kernel_choice == 0 &&
                    (ws_xch_blocks(h->G, h->zc) <= h->num_sms || band_default);
-  if (h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->xch_band > 0) {
+  // (LB_XCH_PRE=0: no pre-pass -- test support: later bands' halo sites are then
+  // read before their owners run, so stale exchange arrays show deterministically)
+  const char* pre_env = std::getenv("LB_XCH_PRE");
+  if (h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->xch_band > 0 &&
+      !(pre_env && !std::strcmp(pre_env, "0"))) {
     const std::vector<int> pre = ws_xch_pre_sites(h->G, h->xch_band);
     h->xch_npre = (int)pre.size();
     if (h->xch_npre > 0) {
@@ -548,7 +552,11 @@ int one_step(lb_ctx* h, int mode) {
            // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
            const bool ws = mode == 0 && step_ws_fits(&s.mapsA) &&
                            (h->kernel_choice >= 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
-           const bool xch = ws && h->xphi[0] && (h->kernel_choice == 5 || (h->kernel_choice == 0 && h->xch_default)) &&
+           // (MRT launches the plain kernel, which leaves the exchange arrays alone:
+           // the step must count as one without the exchange, or the next exchange
+           // step would read the phi of two steps ago where an owner runs behind)
+           const bool xch = ws && h->xphi[0] && h->dp.coll == 0 &&
+                            (h->kernel_choice == 5 || (h->kernel_choice == 0 && h->xch_default)) &&
                             step_xch_fits(G, &s.mapsA);
            h->xch_dirty = !xch;
            if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers

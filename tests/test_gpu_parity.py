@@ -349,6 +349,31 @@ def test_xch_after_other_kernels_bitwise():
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+def test_xch_after_mrt_bands_of_one_tile(monkeypatch):
+    """Deterministic form of the test above: with bands of one tile and no pre-pass
+    (LB_XCH_PRE=0) every tile reads the phi of the tiles after it BEFORE their
+    launch, so an exchange array still holding the phi of two steps ago (an MRT
+    step counted as an exchange step) is read, not overwritten in time.  The same
+    bits as kernel 3."""
+    f, g = rough(64, 32, 16, seed=25)
+    mp = (0.8, 1.1, 1.0)
+    monkeypatch.setenv("LB_XCH_BAND", "1")
+    monkeypatch.setenv("LB_XCH_PRE", "0")
+    states = []
+    for kernel in (5, 3):
+        with lb.Lattice(64, 32, 16, cparams(P0)) as L:
+            L.set_state(f, g)
+            lb.lb_debug_step_kernel(L.h, kernel)
+            L.step(3)
+            lb.lb_set_collision(L.h, 1, *mp)
+            L.step(1)
+            lb.lb_set_collision(L.h, 0)
+            L.step(4)
+            states.append(L.get_state())
+    (a, b) = states
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
 def test_xch_kernel_mrt_bitwise():
     f, g = rough(64, 32, 10, seed=22)
     mp = (0.8, 1.1, 1.0)
