@@ -25,7 +25,11 @@ traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
 C5, C3 = 512 * 512 * 64, 128 ** 3
 CAPTURES = [("prof_kstep_c5", "launches.csv", "c5", "k_step@c5", C5, "512x512x64"),
             ("prof_kstep_c3", "launches_c3.csv", "c3", "k_step@c3", C3, "128^3"),
-            ("prof_kstep_lc", "launches_lc.csv", "lc", "k_step@c5-lc", C5, "512x512x64")]
+            ("prof_kstep_lc", "launches_lc.csv", "lc", "k_step@c5-lc", C5, "512x512x64"),
+            ("prof_kstep_c2", "launches_c2.csv", "c2", "k_step@c2", 64 ** 3, "64^3"),
+            ("prof_kstep_c4", "launches_c4.csv", "c4", "k_step@c4", 256 ** 3, "256^3"),
+            ("prof_kstep_mrt", "launches_mrt.csv", "mrt", "k_step@c5-mrt", C5, "512x512x64"),
+            ("prof_kstep_ch", "launches_ch.csv", "ch", "k_step@c5-ch", C5, "512x512x64")]
 for rep_name, launch_csv, suffix, key, sites, lat in CAPTURES:
     rep = os.path.join(G, rep_name + ".ncu-rep")
     if not os.path.exists(rep):
