@@ -30,9 +30,15 @@ namespace {
 
 constexpr int kCX = 32;
 
-__device__ __forceinline__ int cmod(int z, int n) {
-  const int s = z % n;
-  return s < 0 ? s + n : s;
+// z wrapped into [0, n) for z in [-n, 2n): one compare and add, no division (the
+// kernel reaches planes zA - 2 .. zB + 1 of a periodic slab, nzl >= 3)
+__device__ __forceinline__ int zwrap1(int z, int n) { return z < 0 ? z + n : (z >= n ? z - n : z); }
+// ring slot of plane z >= -60: the floored z mod N (N divides 60), by an unsigned
+// modulo by a constant (multiply-high, no sign fix-up)
+template <int N>
+__device__ __forceinline__ int rslot(int z) {
+  static_assert(60 % N == 0, "ring size must divide 60");
+  return (int)((unsigned)(z + 60) % (unsigned)N);
 }
 
 // f box buffers: 3 (the box of plane k+2 goes out while plane k is collided: two
@@ -78,7 +84,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
 
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
-  auto wz = [&](int z) { return cmod(z, G.nzl); };
+  auto wz = [&](int z) { return zwrap1(z, G.nzl); };
   // plane read at z: periodic within a whole-lattice slab, else the ghost planes
   // (f: -1 and nzl, holding the neighbours' edge planes; phi: -2 .. nzl+1)
   auto zf = [&](int z) { return G.zwrap ? wz(z) : z; };
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     fb_dst[r] = u < FBU ? row * FX + cu * 2 : -1;
   }
   auto issue_f = [&](int zp) {
-    const int b = cmod(zp, NBUF);
+    const int b = rslot<NBUF>(zp);
     const int zs = zf(zp);
     if (fbox_tma) {
       if (tid == 0) {
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     }
   };
   auto wait_f = [&](int zp) {
-    const int b = cmod(zp, NBUF);
+    const int b = rslot<NBUF>(zp);
     if (fbox_tma) {
       mbar_wait(&sm.bar[b], (ph >> b) & 1);
       ph ^= 1u << b;
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
   }
   auto issue_phi = [&](int zp) {
     const double* base = phiA + phi_plane_index(G, zf(zp));
-    double* ring = sm.sPhi[cmod(zp, 5)];
+    double* ring = sm.sPhi[rslot<5>(zp)];
 #pragma unroll
     for (int r = 0; r < PBR; ++r)
       if (pb_dst[r] >= 0) cp_async_v<2>(&ring[pb_dst[r]], base + pb_src[r]);
@@ -153,12 +159,12 @@ __global__ void __launch_bounds__(kCX* TY, 1)
 
   // ---- u and mu of plane zp on the +-1 box (needs f box zp, phi zp-1 .. zp+1)
   auto make_u_mu_at = [&](int zp, int e) {
-    const double(*fb)[FS] = sm.sF[cmod(zp, NBUF)];
-    double(*u3)[NU] = sm.sU[cmod(zp, 3)];
-    double* mu = sm.sMu[cmod(zp, 3)];
-    const double* f0 = sm.sPhi[cmod(zp - 1, 5)];
-    const double* f1 = sm.sPhi[cmod(zp, 5)];
-    const double* f2 = sm.sPhi[cmod(zp + 1, 5)];
+    const double(*fb)[FS] = sm.sF[rslot<NBUF>(zp)];
+    double(*u3)[NU] = sm.sU[rslot<3>(zp)];
+    double* mu = sm.sMu[rslot<3>(zp)];
+    const double* f0 = sm.sPhi[rslot<5>(zp - 1)];
+    const double* f1 = sm.sPhi[rslot<5>(zp)];
+    const double* f2 = sm.sPhi[rslot<5>(zp + 1)];
     {
       const int ex = e % UX, ey = e / UX;
       const int fi = ey * FX + ex + 1;  // f box: x offset 2, y offset 1; u box: offsets 1, 1
@@ -232,11 +238,11 @@ __global__ void __launch_bounds__(kCX* TY, 1)
       make_u_mu_at(k + 1, cu);
       if (tid < NRING) make_u_mu_at(k + 1, ring_site(tid));
 #pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = sm.sF[cmod(k, NBUF)][frank(i)][cf];
+      for (int i = 0; i < Q; ++i) f[i] = sm.sF[rslot<NBUF>(k)][frank(i)][cf];
     } else {
       make_u_mu(k + 1);
 #pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = sm.sF[cmod(k, NBUF)][frank(i)][cf];
+      for (int i = 0; i < Q; ++i) f[i] = sm.sF[rslot<NBUF>(k)][frank(i)][cf];
       __syncthreads();  // f(k) consumed, u / mu (k+1) written
       if (k + 2 <= zB) issue_f(k + 2);
       if (k + 3 <= zB + 1) issue_phi(k + 3);
@@ -244,9 +250,9 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     }
     if (!active) continue;
     // P(k) at the site (R4, A.2)
-    const double* r0 = sm.sPhi[cmod(k, 5)];
-    const double* rm = sm.sPhi[cmod(k - 1, 5)];
-    const double* rp = sm.sPhi[cmod(k + 1, 5)];
+    const double* r0 = sm.sPhi[rslot<5>(k)];
+    const double* rm = sm.sPhi[rslot<5>(k - 1)];
+    const double* rp = sm.sPhi[rslot<5>(k + 1)];
     const double ph = r0[cb];
     const double xp = r0[cb + 1], xm = r0[cb - 1], yp = r0[cb + BX], ym = r0[cb - BX], zp = rp[cb], zm = rm[cb];
     const double lap = (xp + xm) + (yp + ym) + (zp + zm) - 6.0 * ph;
@@ -263,9 +269,9 @@ __global__ void __launch_bounds__(kCX* TY, 1)
       __stcs(d + (long long)slot(0, i) * nxy, fs);
     });
     // phi update (R30, R31): upwind fluxes through the six faces, M lap mu
-    const double* uk = &sm.sU[cmod(k, 3)][0][0];
-    const double* ukm = &sm.sU[cmod(k - 1, 3)][0][0];
-    const double* ukp = &sm.sU[cmod(k + 1, 3)][0][0];
+    const double* uk = &sm.sU[rslot<3>(k)][0][0];
+    const double* ukm = &sm.sU[rslot<3>(k - 1)][0][0];
+    const double* ukp = &sm.sU[rslot<3>(k + 1)][0][0];
     auto flux = [](double ua, double ub, double pa, double pb) {  // face between a and b = a + e
       const double uf = 0.5 * (ua + ub);
       return uf * (uf > 0.0 ? pa : pb);
@@ -274,9 +280,9 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     div = div + (flux(uk[cu], uk[cu + 1], ph, xp) - flux(uk[cu - 1], uk[cu], xm, ph));
     div = div + (flux(uk[NU + cu], uk[NU + cu + UX], ph, yp) - flux(uk[NU + cu - UX], uk[NU + cu], ym, ph));
     div = div + (flux(uk[2 * NU + cu], ukp[2 * NU + cu], ph, zp) - flux(ukm[2 * NU + cu], uk[2 * NU + cu], zm, ph));
-    const double* mk = sm.sMu[cmod(k, 3)];
+    const double* mk = sm.sMu[rslot<3>(k)];
     const double lapmu = (mk[cu + 1] + mk[cu - 1]) + (mk[cu + UX] + mk[cu - UX]) +
-                         (sm.sMu[cmod(k + 1, 3)][cu] + sm.sMu[cmod(k - 1, 3)][cu]) - 6.0 * mk[cu];
+                         (sm.sMu[rslot<3>(k + 1)][cu] + sm.sMu[rslot<3>(k - 1)][cu]) - 6.0 * mk[cu];
     const double phn = (ph - div) + p.mob * lapmu;
     phiB[phi_plane_index(G, k) + (long long)y * G.nx + x] = phn;
     if (!(rho > 0.0) || !isfinite(rho) || !isfinite(phn)) *flag = 1;  // R22

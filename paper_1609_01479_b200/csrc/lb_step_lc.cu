@@ -32,9 +32,15 @@ namespace {
 
 constexpr int kLX = 32, kLY = 8, kLT = kLX * kLY;
 
-__device__ __forceinline__ int cmod(int z, int n) {
-  const int s = z % n;
-  return s < 0 ? s + n : s;
+// z wrapped into [0, n) for z in [-n, 2n): one compare and add, no division (the
+// kernel reaches planes zA - 2 .. zB + 1 of a periodic slab, nzl >= 3)
+__device__ __forceinline__ int zwrap1(int z, int n) { return z < 0 ? z + n : (z >= n ? z - n : z); }
+// ring slot of plane z >= -60: the floored z mod N (N divides 60), by an unsigned
+// modulo by a constant (multiply-high, no sign fix-up)
+template <int N>
+__device__ __forceinline__ int rslot(int z) {
+  static_assert(60 % N == 0, "ring size must divide 60");
+  return (int)((unsigned)(z + 60) % (unsigned)N);
 }
 
 struct alignas(128) LcSmem {
@@ -186,10 +192,10 @@ __global__ void __launch_bounds__(kLT, 1)
 
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
-  auto wz = [&](int z) { return cmod(z, G.nzl); };
+  auto wz = [&](int z) { return zwrap1(z, G.nzl); };
   // plane of the Q and u fields: periodic within a whole-lattice slab, else the
   // ghost planes (Q: -2 .. nzl+1, u: -1 .. nzl; qA, uA point at plane 0)
-  auto zf = [&](int z) { return G.zwrap ? cmod(z, G.nzl) : z; };
+  auto zf = [&](int z) { return G.zwrap ? zwrap1(z, G.nzl) : z; };
 
   if (tid == 0) {
     mbar_init(&sm.bar[0], 1);
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(kLT, 1)
   auto issue_u = [&](int zp) {
     if (!has_u) return;
     const double* base = uA + (long long)zf(zp) * 3 * nxy + usrc;
-    double(*ring)[NU] = sm.sU[cmod(zp, 3)];
+    double(*ring)[NU] = sm.sU[rslot<3>(zp)];
 #pragma unroll
     for (int a = 0; a < 3; ++a) cp_async_v<2>(&ring[a][bdst], base + a * nxy);
   };
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(kLT, 1)
     box_plane(zA - 1, qm1, Hd, szm);
   }
 #pragma unroll
-  for (int a = 0; a < 3; ++a) um[a] = sm.sU[cmod(zA - 1, 3)][a][cu];
+  for (int a = 0; a < 3; ++a) um[a] = sm.sU[rslot<3>(zA - 1)][a][cu];
   __syncthreads();  // the slot of Q(zA-2) is free
   issue_q(zA + 2);
   cp_commit();
@@ -332,10 +338,10 @@ __global__ void __launch_bounds__(kLT, 1)
     cp_commit();
     double q1[5], H1[5], sz1[3];
     box_plane(k + 1, q1, H1, sz1);
-    const double(*uk)[NU] = sm.sU[cmod(k, 3)];
+    const double(*uk)[NU] = sm.sU[rslot<3>(k)];
     double up[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) up[a] = sm.sU[cmod(k + 1, 3)][a][cu];
+    for (int a = 0; a < 3; ++a) up[a] = sm.sU[rslot<3>(k + 1)][a][cu];
     if (active) {
       // R39: F = div sigma (= -div P^th), the in-plane columns from sSig(k)
       const double(*s)[NS] = sm.sSig[((k) & 1)];
