@@ -249,10 +249,13 @@ __global__ void __launch_bounds__(kCX* TY, 1)
       cp_commit();
     }
     if (!active) continue;
+    // ring slots of planes k - 1, k, k + 1 (one modulo each per plane)
+    const int p0 = rslot<5>(k), pm = p0 == 0 ? 4 : p0 - 1, pp = p0 == 4 ? 0 : p0 + 1;
+    const int u0 = rslot<3>(k), um = u0 == 0 ? 2 : u0 - 1, up = u0 == 2 ? 0 : u0 + 1;
     // P(k) at the site (R4, A.2)
-    const double* r0 = sm.sPhi[rslot<5>(k)];
-    const double* rm = sm.sPhi[rslot<5>(k - 1)];
-    const double* rp = sm.sPhi[rslot<5>(k + 1)];
+    const double* r0 = sm.sPhi[p0];
+    const double* rm = sm.sPhi[pm];
+    const double* rp = sm.sPhi[pp];
     const double ph = r0[cb];
     const double xp = r0[cb + 1], xm = r0[cb - 1], yp = r0[cb + BX], ym = r0[cb - BX], zp = rp[cb], zm = rm[cb];
     const double lap = (xp + xm) + (yp + ym) + (zp + zm) - 6.0 * ph;
@@ -269,9 +272,9 @@ __global__ void __launch_bounds__(kCX* TY, 1)
       __stcs(d + (long long)slot(0, i) * nxy, fs);
     });
     // phi update (R30, R31): upwind fluxes through the six faces, M lap mu
-    const double* uk = &sm.sU[rslot<3>(k)][0][0];
-    const double* ukm = &sm.sU[rslot<3>(k - 1)][0][0];
-    const double* ukp = &sm.sU[rslot<3>(k + 1)][0][0];
+    const double* uk = &sm.sU[u0][0][0];
+    const double* ukm = &sm.sU[um][0][0];
+    const double* ukp = &sm.sU[up][0][0];
     auto flux = [](double ua, double ub, double pa, double pb) {  // face between a and b = a + e
       const double uf = 0.5 * (ua + ub);
       return uf * (uf > 0.0 ? pa : pb);
@@ -280,9 +283,9 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     div = div + (flux(uk[cu], uk[cu + 1], ph, xp) - flux(uk[cu - 1], uk[cu], xm, ph));
     div = div + (flux(uk[NU + cu], uk[NU + cu + UX], ph, yp) - flux(uk[NU + cu - UX], uk[NU + cu], ym, ph));
     div = div + (flux(uk[2 * NU + cu], ukp[2 * NU + cu], ph, zp) - flux(ukm[2 * NU + cu], uk[2 * NU + cu], zm, ph));
-    const double* mk = sm.sMu[rslot<3>(k)];
+    const double* mk = sm.sMu[u0];
     const double lapmu = (mk[cu + 1] + mk[cu - 1]) + (mk[cu + UX] + mk[cu - UX]) +
-                         (sm.sMu[rslot<3>(k + 1)][cu] + sm.sMu[rslot<3>(k - 1)][cu]) - 6.0 * mk[cu];
+                         (sm.sMu[up][cu] + sm.sMu[um][cu]) - 6.0 * mk[cu];
     const double phn = (ph - div) + p.mob * lapmu;
     phiB[phi_plane_index(G, k) + (long long)y * G.nx + x] = phn;
     if (!(rho > 0.0) || !isfinite(rho) || !isfinite(phn)) *flag = 1;  // R22
