@@ -15,6 +15,7 @@ import pytest
 from oracle import lb_ch as CH
 from oracle import lb_ref as R
 from paper_1609_01479_b200 import synth
+from symmetry import CUBIC, cube_transform
 
 
 def _mode(field, axis, k_index):
@@ -145,3 +146,19 @@ def test_flat_interface_is_steady():
     assert np.abs(fl.u).max() < 1e-6
     phi_b = math.sqrt(-base.A / base.B)
     assert abs(ph[32 - 8] - phi_b) < 1e-3 and abs(ph[64 - 8] + phi_b) < 1e-3
+
+
+@pytest.mark.parametrize("Mc", CUBIC)
+def test_step_commutes_with_cubic_symmetry(Mc):
+    """The finite-difference Cahn-Hilliard + upwind advection step
+    uses the same stencil on every axis, with the upwind side chosen by the
+    sign of u along that axis, so it commutes with reflections and axis
+    permutations of the lattice (up to rounding)."""
+    p = CH.ChParams()
+    n = 5
+    f, phi = _rough(n, n, n, 14)
+    f1, p1 = CH.run(f, phi, p, 2)
+    T = lambda a: cube_transform(a, Mc, n)  # noqa: E731
+    f2, p2 = CH.run(T(f), T(phi), p, 2)
+    assert np.abs(f2 - T(f1)).max() <= 1e-13 * np.abs(f1).max()
+    assert np.abs(p2 - T(p1)).max() <= 1e-13 * np.abs(p1).max()

@@ -15,6 +15,7 @@ from oracle import lb_brute as BR
 from oracle import lb_mrt as M
 from oracle import lb_ref as R
 from paper_1609_01479_b200 import synth
+from symmetry import CUBIC, cube_transform
 
 P0 = R.Params()
 MP0 = M.MrtParams(base=P0, tau_s=0.8, tau_b=1.1, tau_ghost=1.0)
@@ -207,3 +208,20 @@ def test_flat_interface_is_steady_with_stress_in_equilibrium():
     assert np.abs(fl.u).max() < 1e-6
     phi_b = math.sqrt(-base.A / base.B)
     assert abs(ph[32 - 8] - phi_b) < 1e-3 and abs(ph[64 - 8] + phi_b) < 1e-3
+
+
+@pytest.mark.parametrize("Mc", CUBIC)
+def test_step_commutes_with_cubic_symmetry(Mc):
+    """Stress-in-equilibrium MRT keeps the cubic isotropy of the
+    BGK step: its moment projections split the second moment into trace and
+    traceless parts, both invariant under reflections and axis permutations.
+    A wrongly indexed stress component or projection row breaks this."""
+    n = 5
+    rho, u, phi, nf, ng = synth.rough_fields(n, n, n, 13)
+    f, g = R.equilibrium_state(rho, u, phi, P0)
+    f, g = f + nf, g + ng
+    f1, g1 = M.step(f, g, MP0)
+    T = lambda a: cube_transform(a, Mc, n)  # noqa: E731
+    f2, g2 = M.step(T(f), T(g), MP0)
+    assert np.abs(f2 - T(f1)).max() <= 1e-13 * np.abs(f1).max()
+    assert np.abs(g2 - T(g1)).max() <= 1e-13 * np.abs(g1).max()

@@ -16,6 +16,7 @@ import pytest
 from oracle import lb_brute as BR
 from oracle import lb_ref as R
 from paper_1609_01479_b200 import synth
+from symmetry import CUBIC, cube_transform
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "d3q19_appendix_b.txt")
 P0 = R.Params()  # R16 defaults
@@ -407,25 +408,7 @@ def test_flat_interface_profile():
     assert abs(ph[32 - 8] - phi_b) < 1e-3 and abs(ph[64 - 8] + phi_b) < 1e-3
 
 
-def _cube_transform(a, M, n):
-    """Apply the lattice point-group element M (3x3 signed permutation) to a
-    (19, n, n, n) field: b[j](M x) = a[i](x) with C[j] = M C[i]."""
-    perm = [int(np.flatnonzero((R.C == M @ R.C[i]).all(axis=1))[0]) for i in range(R.NVEL)]
-    z, y, x = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
-    X = np.stack([x.ravel(), y.ravel(), z.ravel()])
-    Xn = (M @ X) % n
-    b = np.empty_like(a)
-    for i in range(R.NVEL):
-        b[perm[i], Xn[2], Xn[1], Xn[0]] = a[i][X[2], X[1], X[0]]
-    return b
-
-
-@pytest.mark.parametrize("M", [
-    np.diag([-1, 1, 1]), np.diag([1, -1, 1]), np.diag([1, 1, -1]),
-    np.array([[0, 1, 0], [1, 0, 0], [0, 0, 1]]),
-    np.array([[0, 0, 1], [1, 0, 0], [0, 1, 0]]),
-    np.array([[0, -1, 0], [0, 0, 1], [-1, 0, 0]]),
-])
+@pytest.mark.parametrize("M", CUBIC)
 def test_step_commutes_with_cubic_symmetry(M):
     """The model is isotropic under the cubic group (D3Q19, the
     free energy and P_ab are built from rotation-invariant terms), so
@@ -436,7 +419,7 @@ def test_step_commutes_with_cubic_symmetry(M):
     n = 5
     f, g = _rough_state(n, n, n, seed=12)
     f1, g1 = R.step(f, g, P0)
-    T = lambda a: _cube_transform(a, M, n)
+    T = lambda a: cube_transform(a, M, n)  # noqa: E731
     f2, g2 = R.step(T(f), T(g), P0)
     assert np.abs(f2 - T(f1)).max() <= 1e-13 * np.abs(f1).max()
     assert np.abs(g2 - T(g1)).max() <= 1e-13 * np.abs(g1).max()
