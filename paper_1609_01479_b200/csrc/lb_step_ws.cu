@@ -204,7 +204,14 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     const unsigned long long pol_last = policy_of<LB_WS_BOX_POL>();
     auto zsrc = [&](int zp, bool& ghost) {
       ghost = false;
-      if (G.zwrap) { zp %= G.nzl; return zp < 0 ? zp + G.nzl : zp; }
+      if (G.zwrap) {  // one unsigned compare in the common case; a modulo only for slabs of < 3 planes
+        const int n = G.nzl;
+        if ((unsigned)zp >= (unsigned)n) {
+          zp += zp < 0 ? n : -n;
+          if ((unsigned)zp >= (unsigned)n) { zp %= n; zp += zp < 0 ? n : 0; }
+        }
+        return zp;
+      }
       ghost = zp < 0 || zp >= G.nzl;
       return zp;
     };
