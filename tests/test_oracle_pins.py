@@ -191,6 +191,73 @@ def test_force_converges_to_phi_grad_mu():
     assert 3.5 < errs[0] / errs[1] < 4.5
 
 
+def _mode3d(L, k_int, amp, th0):
+    """amp cos(2 pi (k_int . x) / L + th0) on an L^3 lattice, (z, y, x) array."""
+    z, y, x = np.meshgrid(np.arange(L), np.arange(L), np.arange(L), indexing="ij")
+    k = 2 * np.pi * np.asarray(k_int, dtype=np.float64) / L
+    th = k[0] * x + k[1] * y + k[2] * z + th0
+    return amp * np.cos(th), th, k
+
+
+def test_stress_single_mode_closed_form():
+    """R4 (A.4) on phi = eps cos(k.x + t): the discrete gradient is exactly
+    -eps sin(k.x + t) sin k_a (A.2), so every off-diagonal component is
+    P_ab = kappa eps^2 sin^2(k.x + t) sin k_a sin k_b (a != b), and the diagonal ones
+    add the isotropic part p0 - kappa phi lap phi - kappa/2 |grad phi|^2 with the
+    Laplacian eigenvalue -sum 2(1 - cos k_a).  A mode with k_x, k_y, k_z all non-zero
+    exercises every off-diagonal term."""
+    L, eps = 12, 0.3
+    phi, th, k = _mode3d(L, (1, 2, 3), eps, 0.4)
+    lam = -sum(2 * (1 - np.cos(k[a])) for a in range(3))
+    grad = R.gradient(phi)
+    lap = R.laplacian(phi)
+    P = R.chemical_stress(phi, grad, lap, P0)
+    s2 = np.sin(th) ** 2
+    g2 = eps * eps * s2 * sum(np.sin(k[a]) ** 2 for a in range(3))
+    iso = 0.5 * P0.A * phi ** 2 + 0.75 * P0.B * phi ** 4 - P0.kappa * lam * phi ** 2 - 0.5 * P0.kappa * g2
+    for a in range(3):
+        for b in range(3):
+            want = P0.kappa * eps * eps * s2 * np.sin(k[a]) * np.sin(k[b])
+            if a == b:
+                want = want + iso
+            assert np.abs(P[a, b] - want).max() < 2e-16, (a, b)
+            assert np.abs(P[a, b] - P[b, a]).max() < 1e-18  # symmetric
+
+
+@pytest.mark.parametrize("modes,sizes", [
+    # (k vector, amplitude, phase) triples summed into phi; every pair of axes coupled
+    ((((1, 1, 0), 0.5, 0.3), ((0, 1, 1), 0.3, 1.1), ((1, 0, 2), 0.2, 2.0)), (16, 32)),
+    ((((1, 2, 1), 0.6, 0.0), ((2, -1, 1), 0.25, 0.7)), (32, 64)),
+])
+def test_force_converges_to_phi_grad_mu_3d(modes, sizes):
+    """Gibbs-Duhem in 3-D: div P = phi grad mu holds identically in the continuum
+    for P_ab of R4 (A.4) -- the off-diagonal kappa d_a phi d_b phi and the
+    cross-derivatives d_b P_ab (a != b) of F (A.5) are what cancel the
+    kappa d_a(|grad phi|^2)/2 and kappa phi d_a lap phi terms.  So for a smooth
+    field varying along all three axes the discrete F = -div P approaches
+    -phi grad mu in EVERY component at second order: the error falls ~4x when
+    the lattice (and every wavelength) doubles.  A wrong factor or sign on the
+    off-diagonal stress, or a dropped cross-derivative, leaves an O(1) error."""
+    errs = []
+    for L in sizes:
+        phi = np.zeros((L, L, L))
+        for kv, amp, th0 in modes:
+            phi = phi + _mode3d(L, kv, amp, th0)[0]
+        lap = R.laplacian(phi)
+        F = R.force(R.chemical_stress(phi, R.gradient(phi), lap, P0))
+        mu = R.chemical_potential(phi, lap, P0)
+        gmu = R.gradient(mu)
+        e = []
+        for a in range(3):
+            want = -phi * gmu[a]
+            assert np.abs(want).max() > 1e-5  # every component is driven
+            e.append(np.abs(F[a] - want).max() / np.abs(want).max())
+        errs.append(e)
+    for a in range(3):
+        assert errs[0][a] < 0.3, errs
+        assert 3.5 < errs[0][a] / errs[1][a] < 4.5, errs
+
+
 def test_force_sums_to_zero():
     """R5: sum_x F = 0 (telescoping), so total momentum is conserved."""
     f, g = _rough_state(7, 6, 5)
