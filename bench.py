@@ -12,11 +12,13 @@ picks another BASELINE config (c1 16^3, c2 64^3, c3 128^3, c4 256^3 strong).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL halos)
 
-Timing: W >= 3 untimed steps, then exactly K steps bracketed by a barrier and a
-device synchronize, timed with CUDA events on the library's own stream, max over
-ranks (`value`); then K more steps with CUDA events around every kernel launch,
-from which the step kernel's average launch time (`roofline.achieved`).  Inputs
-are larger than L2 for c3-c5 (per-GPU state >= 1.3 GB).
+Timing: the step's CUDA graphs are captured first (lb_prepare), then W >= 3
+untimed steps, then exactly K steps bracketed by a barrier and a device
+synchronize, timed with CUDA events on the library's own stream, max over ranks
+(`value`); 5 more repetitions of the same K steps give `reps` (min, median,
+stddev); then K more steps with CUDA events around every kernel launch, from
+which the step kernel's average launch time (`roofline.achieved`).  Inputs are
+larger than L2 for c3-c5 (per-GPU state >= 1.3 GB).
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
 reference arm of this tier) on a bounded sample of the same workload.
 """
@@ -50,7 +52,11 @@ CONFIGS = {
     "c4": (256, 256, lambda n: 256, "strong", "256^3 binary fluid, strong scaling over z-slabs (BASELINE config 4)"),
     "c5": (512, 512, lambda n: 64 * n, "weak",
            "512x512x64 per GPU z-slab binary fluid, weak scaling, 512^3 at 8 GPUs (BASELINE config 5, reading R20)"),
+    "c5alt": (256, 256, lambda n: 512 * n, "weak",
+              "256x256x512 per GPU z-slab binary fluid, weak scaling (BASELINE config 5 as literally written, "
+              "the R20 alternative)"),
 }
+REPS = 5  # repetitions of the timed region after the first (min of >= 5, median, stddev)
 DEFAULT_CONFIG = "c5"
 
 
@@ -78,6 +84,18 @@ def peaks():
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def src_hash() -> str:
@@ -230,7 +248,8 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "sample": [sx, sy, sz]},
-        "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "host_cpus": os.cpu_count()},
         "e2e": {"value": v, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -282,31 +301,41 @@ def run_ours(args):
     else:
         L.init_equilibrium(synth.spinodal_phi_slab(nx, ny, nz, z0, z1, seed=0))
 
-    # warm-up: >= 3 steps, and >= 16 so that lb_step has captured its CUDA graph of
-    # the step loop (8 steps) before the timed region; the line reports the count
-    W = max(args.warmup, 3, 16)
+    # the CUDA graphs lb_step replays (single process) are captured here, outside
+    # the warm-up count and the timed regions; then W >= 3 untimed steps
+    W = max(args.warmup, 3)
     K = args.steps
     stream = torch.cuda.ExternalStream(lb.lb_stream(L.h))
+    lb.lb_prepare(L.h)
     L.step(W)
 
-    # timed region 1 -> `value`: K steps, no per-launch instrumentation (lb_step
-    # replays CUDA graphs of the step loop on a single process)
+    def timed_region():
+        """K steps bracketed by a barrier + device sync, CUDA events on the library's
+        stream; returns (max-over-ranks ms, kernel launches)."""
+        D.barrier()
+        torch.cuda.synchronize()
+        n0 = lb.lb_launch_count(L.h)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.step(K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        D.barrier()
+        return D.max_over_ranks(e0.elapsed_time(e1)), lb.lb_launch_count(L.h) - n0
+
+    # timed region 1 -> `value`: K steps, no per-launch instrumentation; then REPS
+    # more repetitions of it (min / median / stddev), clocks sampled throughout
     clocks = ClockSampler(local)
     time.sleep(0.25)
-    D.barrier()
-    torch.cuda.synchronize()
-    n0 = lb.lb_launch_count(L.h)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks.mark("start")
-    e0.record(stream)
-    L.step(K)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms, launches = timed_region()
+    rep_ms = [ms] + [timed_region()[0] for _ in range(REPS)]
     clocks.mark("end")
-    D.barrier()
-    launches = lb.lb_launch_count(L.h) - n0
-    ms = D.max_over_ranks(e0.elapsed_time(e1))
     clk = clocks.stop()
+    reps = {"n": len(rep_ms), "steps_each": K, "ms_per_step_min": min(rep_ms) / K,
+            "ms_per_step_median": statistics.median(rep_ms) / K, "ms_per_step_stddev": statistics.stdev(rep_ms) / K,
+            "mlups_max": nx * ny * nzf(world) * K / (min(rep_ms) * 1e-3) / 1e6,
+            "note": "value = the first region (exactly K steps); these are it and REPS more of the same K steps"}
     # timed region 2 -> `roofline`: the same K steps with CUDA events around every
     # kernel launch (per-kernel durations; the events cost ~8 us per step, which is
     # why region 1 runs without them)
@@ -364,7 +393,7 @@ def run_ours(args):
         cv, shp, dt = time_oracle(nx, ny, 20, collision=args.collision)
         cpu = {"value": cv / 1e6, "unit": "MLUPS", "cores": 1, "kind": "oracle",
                "sample": f"{oracle_stepper(args.collision)[0]}, 20 steps on a periodic {shp[0]}x{shp[1]}x{shp[2]} sub-lattice of the "
-                         f"workload, 1 thread ({dt:.1f} s of CPU)", "host_cpus": os.cpu_count()}
+                         f"workload, 1 thread ({dt:.1f} s of CPU)", "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
 
     L.close()
     if rank == 0:
@@ -393,7 +422,8 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_site": bps, "avg_launch_ms": ks_avg,
                          "step_frac": step_gbs / peak, "kernel_time_share": kernel_share},
-            "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "src_hash": src_hash(),
+            "reps": reps, "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+            "src_hash": src_hash(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

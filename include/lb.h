@@ -108,8 +108,18 @@ int lb_init_equilibrium(lb_t* h, const double* rho, const double* u, const doubl
 
 /* Advance nsteps >= 0 timesteps; returns after the device has finished.
  * LB_ENUMERIC if any site had rho <= 0 or a non-finite f/g/phi during these
- * steps (the flag is checked once, at the end).  Collective for slabs. */
+ * steps (R22): the kernels record the first offending (step, site)
+ * and lb_last_error names it -- global (x, y, z) and the step within this call;
+ * the flag is read once, at the end, so the state has advanced all nsteps.
+ * Collective for slabs. */
 int lb_step(lb_t* h, int nsteps);
+
+/* Optional: capture the CUDA graphs lb_step replays (8 steps each, one per
+ * buffer parity) now instead of at the first lb_step that can use them.  No
+ * device work and no change of state; a no-op where graphs are not used (ranks,
+ * per-launch profiling, LB_TUNE_GRAPHS 0).  Lets a caller keep graph capture out
+ * of a timed region (bench.py). */
+int lb_prepare(lb_t* h);
 
 /* Read the state back into host arrays of 19*nloc doubles each. */
 int lb_get_state(lb_t* h, double* f, double* g);
@@ -160,14 +170,18 @@ int lb_debug_propagation_map(int nx, int ny, int nz, int nslabs, int64_t* out);
  * the same kernel addressing and halo exchanges as lb_step.  Test support. */
 int lb_debug_stream(lb_t* h, int nsteps);
 
-/* Measurement probe: nsteps launches of the tile step kernel with its copies and
- * stores but without the physics (mode 1: tile copies + halo box + propagation
- * stores; mode 2: also the phi / stress stencils; mode 3: tile copies and stores
- * only; mode 4: like mode 1, but g taken from the halo box instead of a second
- * tile copy; mode 5: f tile, the g tile two planes ahead and only the halo ring of
- * the box, four TMA boxes per slot run).  The state afterwards is a propagated copy, not a solution.  Gives the
- * memory-side ceiling of the access pattern for the roofline analysis. */
-int lb_debug_step_probe(lb_t* h, int nsteps, int mode);
+/* Launch knobs of the step kernels, for measurement (the defaults are the tuned
+ * choice; nothing reads the environment).  Results are bitwise the same for any
+ * value.  Keys:
+ *   LB_TUNE_ZCHUNK    planes per z-chunk of a CTA (0: automatic, step_zchunk)
+ *   LB_TUNE_BAND_ROWS block order: tiles walked in bands of this many tile rows,
+ *                     column by column (1: row-major, the default)
+ *   LB_TUNE_RESID     CTAs assumed resident at a time by the block order (0: the
+ *                     kernel's occupancy on this device)
+ *   LB_TUNE_GRAPHS    0: step without CUDA graphs; 1 (default): graphs of 8 steps
+ * LB_EINVAL for an unknown key or a value out of range. */
+enum { LB_TUNE_ZCHUNK = 1, LB_TUNE_BAND_ROWS = 2, LB_TUNE_RESID = 3, LB_TUNE_GRAPHS = 4 };
+int lb_debug_tune(lb_t* h, int key, int value);
 
 /* ---- NEXT-2 variant: finite-difference Cahn-Hilliard (R29-R33) ----
  * A handle whose state is (f, phi): phi is a field updated each step by
@@ -248,26 +262,20 @@ int lb_init_lc(lb_t* h, const double* rho, const double* u, const double* n);
  *     relaxes with tau_shear (viscosity (tau_shear - 1/2)/3), its trace with
  *     tau_bulk, the ghost modes with tau_ghost; tau_f of lb_params is unused.
  *     g is unchanged (BGK with tau_g, R9/R10), with the force-free u.
- * Each tau finite and > 1/2, else LB_EINVAL; LB_EINVAL also for model 1 while
- * the cluster kernel is selected (it implements model 0 only).  Takes effect at
- * the next lb_step. */
+ * Each tau finite and > 1/2, else LB_EINVAL.  Takes effect at the next lb_step. */
 int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, double tau_ghost);
 
 /* Which step kernel lb_step uses: 0 = default (the warp-specialised kernel for
- * even nx, with the phi exchange of kernel 5 where the step's blocks -- 32 x 8
+ * even nx, with the phi exchange of kernel 3 where the step's blocks -- 32 x 8
  * tiles x z-chunks -- fit in one wave on the SMs, e.g. 64^3 and 128^3; else the
- * tile kernel), 1 = the tile
- * kernel (halo box per CTA), 2 = the cluster kernel (phi halos shared through
- * distributed shared memory; needs nx % 64 == 0 and ny % 16 == 0, else
- * LB_EINVAL), 3 = the warp-specialised tile kernel (stencil and collision on
- * separate warps; needs nx even, else LB_EINVAL), 4 = the same with persistent
- * CTAs taking work items from a counter, 5 = the warp-specialised kernel with
- * the phi exchange (the stencil loads the g tile only and takes the phi halo from
- * the neighbouring tiles' CTAs through an L2-resident phi array whose unwritten
- * sites hold a sentinel NaN, summing it from g where the owner runs behind; one
- * periodic slab, nx % 32 == 0, ny % 8 == 0, else LB_EINVAL; allocates two
- * nx*ny*nz phi arrays).  All give bitwise identical results.  Test / measurement
- * support. */
+ * tile kernel), 1 = the tile kernel (halo box per CTA), 2 = the warp-specialised
+ * tile kernel (stencil and collision on separate warps; needs nx even, else
+ * LB_EINVAL), 3 = the warp-specialised kernel with the phi exchange (the stencil
+ * loads the g tile only and takes the phi halo from the neighbouring tiles' CTAs
+ * through an L2-resident phi array whose unwritten sites hold a sentinel NaN,
+ * summing it from g where the owner runs behind; one periodic slab, nx % 32 == 0,
+ * ny % 8 == 0, else LB_EINVAL; allocates two nx*ny*nz phi arrays).  All give
+ * bitwise identical results.  Test / measurement support. */
 int lb_debug_step_kernel(lb_t* h, int which);
 
 /* Halo transport of a slab handle.  mode -1: returns the current mode (0 or 1);
@@ -279,8 +287,8 @@ int lb_debug_step_kernel(lb_t* h, int which);
  *    through CUDA IPC mappings between ranks); only a one-double NCCL send/recv
  *    per phase orders the ranks.
  * Default: 1 for loopback and for ranks whose neighbours' memory could be mapped
- * (checked end to end at lb_create_slab), else 0; environment LB_HALO=nccl (or
- * copy) forces 0.  Both give bitwise identical results.  LB_EINVAL for a single
+ * (checked end to end at lb_create_slab), else 0.  Both give bitwise identical
+ * results.  LB_EINVAL for a single
  * periodic slab or a rank handle without peer mappings. */
 int lb_debug_halo_mode(lb_t* h, int mode);
 
@@ -289,16 +297,12 @@ int lb_debug_halo_mode(lb_t* h, int mode);
  * planes, no halo plan).  Must equal lb_debug_propagation_map.  Host-only. */
 int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* out);
 
-/* Band plan of the banded phi exchange (kernel 5 over several waves, or kernel 0
- * with LB_XCH_BAND > 0) for one periodic
- * nx x ny x nz slab whose step uses z-chunks of zc planes on num_sms SMs.
- * band >= 0 imposes the band (tiles of 32 x 8 per launch, 0 = no bands), band < 0
- * asks for the automatic choice; *band_out receives it.  sites (capacity cap,
- * may be NULL when cap == 0) receives, ascending, the xy offsets y*nx + x of the
- * sites some band takes as phi halo (the 2-site ring of its tiles) from a LATER
- * band -- those the pre-pass sums before the bands run.  Returns their number
- * (which may exceed cap) or LB_EINVAL (nx % 32, ny % 8, sizes).  Host-only. */
-int lb_debug_xch_bands(int nx, int ny, int nz, int zc, int num_sms, int band, int* band_out, int* sites, int cap);
+/* Block order of the step kernels (host-only): for block L of a launch over ntx x
+ * nty tiles and nch z-chunks, out[3L .. 3L+2] = (tile column, tile row, chunk) as
+ * the kernels compute it with `resid` CTAs resident and bands of `band` tile rows
+ * (LB_TUNE_BAND_ROWS).  Every (tile, chunk) appears exactly once.  out holds
+ * 3 * ntx * nty * nch ints.  LB_EINVAL on bad arguments. */
+int lb_debug_tile_order(int ntx, int nty, int nch, int resid, int band, int* out);
 
 /* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of
  * nranks, the ranks it sends its +z and -z halo to, and the number of doubles

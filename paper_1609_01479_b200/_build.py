@@ -6,12 +6,13 @@ import os
 import subprocess
 import sys
 import sysconfig
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblb.so")
-SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_step_cluster.cu", "lb_step_ws.cu", "lb_step_ch.cu", "lb_step_lc.cu", "lb_api.cu"]
+SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_step_ws.cu", "lb_step_ch.cu", "lb_step_lc.cu", "lb_api.cu"]
 HEADERS = ["d3q19.cuh", "lb_kernels.cuh", "lb_device.cuh", "lb_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -36,23 +37,36 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel, then link liblb.so."""
     if not force and not _stale():
         return LIB
     inc, lib = nccl_dirs()
     nvcc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *os.environ.get("LB_NVCC_FLAGS", "").split(),
-           *[os.path.join(CSRC, s) for s in SOURCES],
-           "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}",
-           "-o", LIB + ".tmp"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+             "-Xptxas", "-v" if verbose else "-O3",
+             "-I", os.path.join(ROOT, "include"), "-I", inc,
+             *os.environ.get("LB_NVCC_FLAGS", "").split()]
+    objdir = os.path.join(PKG, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.splitext(s)[0] + ".o") for s in SOURCES]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
+        return subprocess.run([nvcc, *flags, "-c", os.path.join(CSRC, src), "-o", obj], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, zip(SOURCES, objs)))
+    for r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building liblb.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    r = subprocess.run([nvcc, *ARCH, "-shared", *objs, "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}",
+                        "-o", LIB + ".tmp"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building liblb.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking liblb.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

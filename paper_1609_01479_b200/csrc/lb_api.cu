@@ -42,7 +42,6 @@ struct Slab {
   double* u2 = nullptr;
   StepMaps lcA{}, lcB{};
   StepMaps mapsA{}, mapsB{};        // TMA descriptors of A and B (swapped with them)
-  ClusterMaps cmapsA{}, cmapsB{};  // same, for the cluster step kernel
 };
 
 struct Pending {
@@ -66,21 +65,21 @@ struct lb_ctx {
   int num_sms = 148;
   int zc = 1;             // z-chunk of the step kernel
   int ty = 8;             // tile rows of the step kernel
-  int czc = 1;            // z-chunk of the cluster step kernel
+  TileOrder order{0, 1};  // block order of the step kernels (0: the kernel's occupancy)
+  bool graphs_on = true;  // lb_debug_tune(LB_TUNE_GRAPHS)
   bool ch = false;        // NEXT-2 handle: state (f, phi), lb_create_ch
   bool lc = false;        // NEXT-4 handle: state (f, Q, u), lb_create_lc
   int lczc = 1;           // z-chunk of the liquid-crystal step kernel
-  int kernel_choice = 0;  // 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised,
-                          // 5 warp-specialised with the phi exchange
+  int kernel_choice = 0;  // 0 default, 1 tile, 2 warp-specialised, 3 warp-specialised with the phi exchange
   double* xphi[2] = {nullptr, nullptr};  // phi exchange of the warp-specialised kernel (nx*ny*nzl), single slab
-  bool xch_default = false;               // kernel 0 uses it (one wave of blocks, or bands of one wave)
-  int xch_band = 0;                       // tiles per launch of the banded exchange (0: one launch)
-  int* xch_pre = nullptr;                 // sites the bands take from later bands (ws_xch_pre_sites)
-  int xch_npre = 0;
+  bool xch_default = false;               // kernel 0 uses it (all blocks in one wave)
   bool xch_dirty = false;                 // a step since the last one that used it: refill before the next
-  int* d_flag = nullptr;
-  int* h_flag = nullptr;  // pinned
-  WorkCounter wctr;       // work-item counter of the persistent step kernel
+  // R22 health words (device): [0] first offending (step << 40 | site), ~0 = clean;
+  // [1] steps completed by the step kernels; d_done: CTAs finished in a launch
+  unsigned long long* d_health = nullptr;
+  unsigned* d_done = nullptr;
+  unsigned long long* h_health = nullptr;  // pinned copy of d_health[0]
+  long long steps_done = 0;                // host mirror of d_health[1]
   ncclComm_t comm = nullptr;
   // halo transport: 0 = exchange (ghost planes + copies / NCCL send-recv after the
   // kernels), 1 = peer (fused: the kernels store into the neighbours' buffers)
@@ -101,8 +100,9 @@ struct lb_ctx {
     cudaGraphExec_t exec = nullptr;
     const double* A = nullptr;
     long long launches = 0;  // kernels per replay
+    long long steps = 0;     // steps per replay
+    bool dirty_after = true;  // xch_dirty after a replay
   } graphs[2];
-  bool stepped = false;  // one step ran outside a capture (first-launch attributes set)
   std::string err;
   long long launches = 0;
   // profiling
@@ -247,6 +247,13 @@ int refresh_xch(lb_ctx* h) {
   return LB_OK;
 }
 
+// the phi-exchange step kernel is the default where its blocks run in one wave
+// (over several waves neighbouring tiles drift apart)
+void choose_xch(lb_ctx* h) {
+  h->xch_default = h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->kernel_choice == 0 &&
+                   ws_xch_blocks(h->G, h->zc) <= h->num_sms;
+}
+
 int alloc_slabs(lb_ctx* h) {
   h->slabs.resize(h->nslabs);
   for (int r = 0; r < h->nslabs; ++r) {
@@ -259,40 +266,35 @@ int alloc_slabs(lb_ctx* h) {
     CK(h, cudaMemsetAsync(s.A, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
     CK(h, cudaMemsetAsync(s.B, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
     CK(h, cudaMemsetAsync(s.phi, 0xff, phi_doubles(h->G) * sizeof(double), h->stream));
-    if (!make_step_maps(h->G, s.A, h->ty, &s.mapsA) || !make_step_maps(h->G, s.B, h->ty, &s.mapsB) ||
-        !make_cluster_maps(h->G, s.A, &s.cmapsA) || !make_cluster_maps(h->G, s.B, &s.cmapsB))
+    if (!make_step_maps(h->G, s.A, h->ty, &s.mapsA) || !make_step_maps(h->G, s.B, h->ty, &s.mapsB))
       return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed for the step kernel's TMA descriptors");
   }
-  // the phi-exchange step kernel is the default where its blocks run in one wave
-  // (LB_XCH_BAND: tuning override, tiles per band; 0 = no bands)
-  h->xch_band = ws_xch_band(h->G, h->zc, h->num_sms);
-  bool band_default = false;
-  if (const char* e = std::getenv("LB_XCH_BAND")) {
-    const int b = std::atoi(e);
-    if (b >= 0) h->xch_band = b;
-    band_default = b > 0;
-  }
-  h->xch_default = h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->kernel_choice == 0 &&
-                   (ws_xch_blocks(h->G, h->zc) <= h->num_sms || band_default);
-  // (LB_XCH_PRE=0: no pre-pass -- test support: later bands' halo sites are then
-  // read before their owners run, so stale exchange arrays show deterministically)
-  const char* pre_env = std::getenv("LB_XCH_PRE");
-  if (h->nslabs == 1 && step_xch_fits(h->G, &h->slabs[0].mapsA) && h->xch_band > 0 &&
-      !(pre_env && !std::strcmp(pre_env, "0"))) {
-    const std::vector<int> pre = ws_xch_pre_sites(h->G, h->xch_band);
-    h->xch_npre = (int)pre.size();
-    if (h->xch_npre > 0) {
-      CK(h, cudaMalloc(&h->xch_pre, pre.size() * sizeof(int)));
-      CK(h, cudaMemcpy(h->xch_pre, pre.data(), pre.size() * sizeof(int), cudaMemcpyHostToDevice));
-    }
-  }
-  CK(h, cudaMalloc(&h->d_flag, sizeof(int)));
-  CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
-  CK(h, cudaMalloc(&h->wctr.dev, sizeof(unsigned long long)));
-  CK(h, cudaMemsetAsync(h->wctr.dev, 0, sizeof(unsigned long long), h->stream));
-  CK(h, cudaMallocHost(&h->h_flag, sizeof(int)));
+  choose_xch(h);
+  CK(h, cudaMalloc(&h->d_health, 2 * sizeof(unsigned long long)));
+  CK(h, cudaMemsetAsync(h->d_health, 0xff, sizeof(unsigned long long), h->stream));
+  CK(h, cudaMemsetAsync(h->d_health + 1, 0, sizeof(unsigned long long), h->stream));
+  CK(h, cudaMalloc(&h->d_done, sizeof(unsigned)));
+  CK(h, cudaMemsetAsync(h->d_done, 0, sizeof(unsigned), h->stream));
+  CK(h, cudaMallocHost(&h->h_health, sizeof(unsigned long long)));
   CK(h, cudaStreamSynchronize(h->stream));
   return LB_OK;
+}
+
+// health words of slab r's launch in a step: only the last launch of a step ticks
+Health health_of(const lb_ctx* h, int r, bool tick) {
+  Health hl;
+  hl.flag = h->d_health;
+  hl.step = h->d_health + 1;
+  hl.done = tick ? h->d_done : nullptr;
+  hl.site0 = (long long)h->slabs[r].z0 * h->G.nxy;
+  return hl;
+}
+
+Launch launch_of(const lb_ctx* h) {
+  Launch ln;
+  ln.zc = h->zc;
+  ln.order = h->order;
+  return ln;
 }
 
 int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, int rank, int nslabs, lb_t** out) {
@@ -332,23 +334,20 @@ int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, i
     delete h;
     return LB_ECUDA;
   }
-  {
-    const char* env = std::getenv("LB_HALO");
-    const bool force_exchange = env && (!std::strcmp(env, "copy") || !std::strcmp(env, "nccl"));
-    h->halo_mode = (parts > 1 && nranks == 1 && !force_exchange) ? 1 : 0;  // ranks: after IPC setup
-  }
+  h->halo_mode = (parts > 1 && nranks == 1) ? 1 : 0;  // ranks: after the IPC setup
   h->ty = step_tile_rows(h->G, h->num_sms);
   h->zc = step_zchunk(h->G, h->num_sms, h->ty);
-  // tuning overrides (measurement only): tile rows 4 | 8, z-chunk planes
-  if (const char* e = std::getenv("LB_TILE_ROWS")) {
-    const int t = std::atoi(e);
-    if (t == 4 || t == 8) h->ty = t, h->zc = step_zchunk(h->G, h->num_sms, h->ty);
+  // every step kernel's per-device preparation now, never inside a graph capture
+  e = prepare_step_kernels();
+  if (e == cudaSuccess) e = prepare_ws_kernels();
+  if (e == cudaSuccess) e = prepare_ch_kernels();
+  if (e == cudaSuccess) e = prepare_lc_kernels();
+  if (e != cudaSuccess) {
+    set_err(nullptr, LB_ECUDA, "kernel preparation failed: %s", cudaGetErrorString(e));
+    cudaStreamDestroy(h->stream);
+    delete h;
+    return LB_ECUDA;
   }
-  if (const char* e = std::getenv("LB_ZCHUNK")) {
-    const int z = std::atoi(e);
-    if (z >= 1) h->zc = z < h->nzl ? z : h->nzl;
-  }
-  h->czc = cluster_zchunk(h->G, h->num_sms);
   rc = alloc_slabs(h);
   if (rc) {
     g_create_error = h->err;
@@ -480,50 +479,66 @@ int halo_barrier(lb_ctx* h, int kid) {
   return LB_OK;
 }
 
-// one timestep on every slab.  Single periodic slab: the fused step alone.
-// Slabs: phi on the two edge planes at each end (K_phi), phi halo exchange, the
-// fused step (A -> B), distribution halo exchange, swap.
-// mode: -1 propagation only (k_stream), 0 the step, 1/2 step-kernel memory probes
-int one_step(lb_ctx* h, int mode) {
-  const Geom& G = h->G;
-  int rc;
-  h->xch_dirty = true;  // until a phi-exchange launch below says otherwise
-  const bool peer = h->halo_mode == 1 && !G.zwrap;
-  if (h->lc && mode >= 0) {  // Q, u halos; the step; f halo (the components that left each slab)
-    if (!G.zwrap && (rc = exchange_lc(h))) return rc;
-    for (auto& s : h->slabs)
-      CK(h, timed(h, K_STEP, true, [&]() {
-           return launch_step_lc(G, h->dp, s.A, s.B, lc_q0(G, s.q), lc_q0(G, s.q2), lc_u0(G, s.u), lc_u0(G, s.u2),
-                                 h->lczc, h->d_flag, &s.lcA, h->stream);
-         }));
-    if (!G.zwrap && (rc = exchange_dist(h))) return rc;
-    for (auto& s : h->slabs) {
-      std::swap(s.A, s.B);
-      std::swap(s.mapsA, s.mapsB);
-      std::swap(s.cmapsA, s.cmapsB);
+// The host side of the end of a step: the next state becomes the current one (the
+// A/B buffers and their TMA maps; phi / Q / u fields of the Cahn-Hilliard and
+// liquid-crystal handles; the mapped neighbour buffers, which swap in lockstep).
+// fields = false: only the distributions (propagation only).
+void swap_roles(lb_ctx* h, bool fields = true) {
+  for (auto& s : h->slabs) {
+    std::swap(s.A, s.B);
+    std::swap(s.mapsA, s.mapsB);
+    if (h->lc && fields) {
       std::swap(s.lcA, s.lcB);
       std::swap(s.q, s.q2);
       std::swap(s.u, s.u2);
     }
-    return LB_OK;
-  }
-  if (h->ch && mode >= 0) {  // f edge planes and phi halos; the step; f halo
-    if (!G.zwrap && ((rc = exchange_fedge(h)) || (rc = exchange_phi(h)))) return rc;
-    for (auto& s : h->slabs)
-      CK(h, timed(h, K_STEP, true, [&]() {
-           return launch_step_ch(G, h->dp, s.A, s.B, s.phi, s.phi2, h->zc, h->d_flag, &s.chA, h->stream);
-         }));
-    if (!G.zwrap && (rc = exchange_dist(h))) return rc;
-    for (auto& s : h->slabs) {
-      std::swap(s.A, s.B);
-      std::swap(s.mapsA, s.mapsB);
-      std::swap(s.cmapsA, s.cmapsB);
+    if (h->ch && fields) {
       std::swap(s.chA, s.chB);
       std::swap(s.phi, s.phi2);
     }
+  }
+  for (int k = 0; k < 2; ++k) std::swap(h->peerA[k], h->peerB[k]);
+}
+
+// one timestep on every slab.  Single periodic slab: the fused step alone.
+// Slabs: phi on the two edge planes at each end (K_phi), phi halo exchange, the
+// fused step (A -> B), distribution halo exchange, swap.
+// stream_only: propagation only (k_stream, lb_debug_stream)
+int one_step(lb_ctx* h, bool stream_only = false) {
+  const Geom& G = h->G;
+  int rc;
+  h->xch_dirty = true;  // until a phi-exchange launch below says otherwise
+  const bool peer = h->halo_mode == 1 && !G.zwrap;
+  const int last = h->nslabs - 1;
+  if (h->lc && !stream_only) {  // Q, u halos; the step; f halo (the components that left each slab)
+    if (!G.zwrap && (rc = exchange_lc(h))) return rc;
+    for (int r = 0; r < h->nslabs; ++r) {
+      Slab& s = h->slabs[r];
+      CK(h, timed(h, K_STEP, true, [&]() {
+           return launch_step_lc(G, h->dp, s.A, s.B, lc_q0(G, s.q), lc_q0(G, s.q2), lc_u0(G, s.u), lc_u0(G, s.u2),
+                                 h->lczc, health_of(h, r, r == last), &s.lcA, h->stream);
+         }));
+    }
+    if (!G.zwrap && (rc = exchange_dist(h))) return rc;
+    swap_roles(h);
+    ++h->steps_done;
     return LB_OK;
   }
-  if (mode < 0) {
+  if (h->ch && !stream_only) {  // f edge planes and phi halos; the step; f halo
+    if (!G.zwrap && ((rc = exchange_fedge(h)) || (rc = exchange_phi(h)))) return rc;
+    for (int r = 0; r < h->nslabs; ++r) {
+      Slab& s = h->slabs[r];
+      CK(h, timed(h, K_STEP, true, [&]() {
+           return launch_step_ch(G, h->dp, s.A, s.B, s.phi, s.phi2, h->zc, health_of(h, r, r == last), &s.chA,
+                                 h->stream);
+         }));
+    }
+    if (!G.zwrap && (rc = exchange_dist(h))) return rc;
+    swap_roles(h);
+    ++h->steps_done;
+    return LB_OK;
+  }
+  if (stream_only) {
     for (int r = 0; r < h->nslabs; ++r) {
       Slab& s = h->slabs[r];
       const Peers pr = peers_of(h, r);
@@ -539,51 +554,36 @@ int one_step(lb_ctx* h, int mode) {
       }
       if ((rc = peer ? halo_barrier(h, K_HALO_PHI) : exchange_phi(h))) return rc;
     }
+    const Launch ln = launch_of(h);
     for (int r = 0; r < h->nslabs; ++r) {
       Slab& s = h->slabs[r];
       const Peers pr = peers_of(h, r);
+      const Health hl = health_of(h, r, r == last);
       CK(h, timed(h, K_STEP, true, [&]() {
-           // the cluster kernel is opt-in: measured slower than the tile kernel in round 1
-           // (cluster barrier per plane)
-           const bool cluster = mode == 0 && s.cmapsA.ok && h->kernel_choice == 2 && h->dp.coll == 0;
-           if (cluster)
-             return launch_step_cluster(G, h->dp, s.A, s.B, s.phi, h->czc, h->d_flag, &s.cmapsA, h->stream, pr);
            // default: the warp-specialised kernel for 32 x 8 tiles (large planes), the
            // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
-           const bool ws = mode == 0 && step_ws_fits(&s.mapsA) &&
-                           (h->kernel_choice >= 3 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
+           const bool ws = step_ws_fits(&s.mapsA) &&
+                           (h->kernel_choice >= 2 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
            // (MRT launches the plain kernel, which leaves the exchange arrays alone:
            // the step must count as one without the exchange, or the next exchange
            // step would read the phi of two steps ago where an owner runs behind)
            const bool xch = ws && h->xphi[0] && h->dp.coll == 0 &&
-                            (h->kernel_choice == 5 || (h->kernel_choice == 0 && h->xch_default)) &&
+                            (h->kernel_choice == 3 || (h->kernel_choice == 0 && h->xch_default)) &&
                             step_xch_fits(G, &s.mapsA);
            h->xch_dirty = !xch;
            if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
              const int k = s.A < s.B ? 0 : 1;
-             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1, h->xch_band, 0, 0,
-                              h->xch_pre, h->xch_npre};
-             if (h->xch_band > 0) {  // one launch per band (+ the pre-pass): counted beyond timed()'s one
-               const long long nt = (long long)(G.nx / 32) * (G.ny / 8);
-               h->launches += (nt + h->xch_band - 1) / h->xch_band - 1 + (h->xch_npre > 0);
-             }
-             return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
-                                   false, &xa);
+             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1};
+             return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr, &xa);
            }
-           if (ws)
-             return launch_step_ws(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, pr, &h->wctr,
-                                   h->kernel_choice == 4);
-           return launch_step(G, h->dp, s.A, s.B, s.phi, h->zc, h->d_flag, &s.mapsA, h->stream, mode, pr);
+           if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
+           return launch_step(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
          }));
     }
   }
   if ((rc = peer ? halo_barrier(h, K_HALO_DIST) : exchange_dist(h))) return rc;
-  for (auto& s : h->slabs) {
-    std::swap(s.A, s.B);
-    std::swap(s.mapsA, s.mapsB);
-    std::swap(s.cmapsA, s.cmapsB);
-  }
-  for (int k = 0; k < 2; ++k) std::swap(h->peerA[k], h->peerB[k]);  // the neighbours swapped too
+  swap_roles(h, !stream_only);
+  if (!stream_only) ++h->steps_done;
   return LB_OK;
 }
 
@@ -597,70 +597,114 @@ void drop_graphs(lb_ctx* h) {
   }
 }
 
+// Anything that changes what a step launches: the graphs go (every kernel was
+// prepared at lb_create, so a new one's first launch may be captured).
+void steps_changed(lb_ctx* h) { drop_graphs(h); }
+
 bool graphs_usable(const lb_ctx* h) {
-  static const bool off = [] {
-    const char* e = std::getenv("LB_GRAPHS");
-    return e && !std::strcmp(e, "0");
-  }();
-  // ranks: the NCCL calls stay outside graphs; persistent kernel: host-side work counter
-  return !off && h->nranks == 1 && !h->prof_on && h->kernel_choice != 4 && h->stepped;
+  // ranks: the NCCL calls stay outside graphs
+  return h->graphs_on && h->nranks == 1 && !h->prof_on;
+}
+
+// Everything one_step changes on the host: restored if a capture fails half way.
+struct HostStepState {
+  std::vector<Slab> slabs;
+  double* peerA[2];
+  double* peerB[2];
+  bool xch_dirty;
+  long long steps_done;
+};
+HostStepState save_state(const lb_ctx* h) {
+  HostStepState st{h->slabs, {h->peerA[0], h->peerA[1]}, {h->peerB[0], h->peerB[1]}, h->xch_dirty, h->steps_done};
+  return st;
+}
+void restore_state(lb_ctx* h, const HostStepState& st) {
+  h->slabs = st.slabs;
+  for (int k = 0; k < 2; ++k) h->peerA[k] = st.peerA[k], h->peerB[k] = st.peerB[k];
+  h->xch_dirty = st.xch_dirty;
+  h->steps_done = st.steps_done;
+}
+
+// Capture kGraphSteps steps from the current buffer roles into a graph slot (the
+// host state is restored afterwards: capturing runs nothing).  Returns the slot,
+// or nullptr when no graph could be made (the caller steps plainly).
+lb_ctx::StepGraph* capture_graph(lb_ctx* h) {
+  const double* A = h->slabs[0].A;
+  for (auto& c : h->graphs)
+    if (c.exec && c.A == A) return &c;
+  lb_ctx::StepGraph* slot = !h->graphs[0].exec ? &h->graphs[0] : &h->graphs[1];
+  if (slot->exec) cudaGraphExecDestroy(slot->exec), *slot = lb_ctx::StepGraph{};
+  const long long n0 = h->launches;
+  const HostStepState before = save_state(h);
+  if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  int rc = LB_OK;
+  for (int t = 0; t < kGraphSteps && !rc; ++t) rc = one_step(h);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
+  const long long nk = h->launches - n0;
+  h->launches = n0;  // captured, not launched
+  // a replay leaves the buffers where the capture left them: kGraphSteps is even,
+  // so that is where they started (checked, not assumed)
+  const bool same = h->slabs[0].A == before.slabs[0].A;
+  const long long nsteps = h->steps_done - before.steps_done;
+  const bool dirty_after = h->xch_dirty;
+  restore_state(h, before);
+  if (rc || ec != cudaSuccess || !graph || !same) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    h->broken = false;  // a failed capture is not a device failure: step plainly
+    h->err.clear();
+    return nullptr;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  slot->exec = exec;
+  slot->A = A;
+  slot->launches = nk;
+  slot->steps = nsteps;
+  slot->dirty_after = dirty_after;
+  return slot;
 }
 
 // Replay (capturing first if needed) kGraphSteps steps.  Returns LB_OK, or a
-// negative code; *done = false when no graph could be made (the caller steps plainly).
+// negative code; *done = false when no graph could be made (the caller steps
+// plainly, from the state as it was before the attempt).
 int graph_steps(lb_ctx* h, bool* done) {
   *done = false;
-  const double* A = h->slabs[0].A;
-  lb_ctx::StepGraph* g = nullptr;
-  for (auto& c : h->graphs)
-    if (c.exec && c.A == A) g = &c;
-  if (!g) {
-    lb_ctx::StepGraph* slot = !h->graphs[0].exec ? &h->graphs[0] : &h->graphs[1];
-    if (slot->exec) cudaGraphExecDestroy(slot->exec), *slot = lb_ctx::StepGraph{};
-    const long long n0 = h->launches;
-    if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-      cudaGetLastError();
-      return LB_OK;
-    }
-    int rc = LB_OK;
-    for (int t = 0; t < kGraphSteps && !rc; ++t) rc = one_step(h, 0);
-    cudaGraph_t graph = nullptr;
-    const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
-    const long long nk = h->launches - n0;
-    h->launches = n0;  // captured, not launched
-    if (rc || ec != cudaSuccess || !graph) {
-      if (graph) cudaGraphDestroy(graph);
-      cudaGetLastError();
-      h->broken = false;  // a failed capture is not a device failure: step plainly
-      h->err.clear();
-      return LB_OK;
-    }
-    cudaGraphExec_t exec = nullptr;
-    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ei != cudaSuccess) {
-      cudaGetLastError();
-      return LB_OK;
-    }
-    slot->exec = exec;
-    slot->A = A;
-    slot->launches = nk;
-    g = slot;
-  }
+  lb_ctx::StepGraph* g = capture_graph(h);
+  if (!g) return LB_OK;
   CK(h, cudaGraphLaunch(g->exec, h->stream));
   h->launches += g->launches;
+  h->steps_done += g->steps;
+  h->xch_dirty = g->dirty_after;
   *done = true;
   return LB_OK;
 }
 
-int finish(lb_ctx* h) {
-  CK(h, cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+// After a call's steps: wait, then the R22 report -- the first offending step and
+// site since the call began (the flag is reset for the next call).
+int finish(lb_ctx* h, long long step0 = -1) {
+  CK(h, cudaMemcpyAsync(h->h_health, h->d_health, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   resolve_pending(h);
-  if (*h->h_flag) {
-    CK(h, cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
+  const unsigned long long v = *h->h_health;
+  if (v != ~0ULL) {
+    CK(h, cudaMemsetAsync(h->d_health, 0xff, sizeof(unsigned long long), h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
-    return set_err(h, LB_ENUMERIC, "rho <= 0 or a non-finite value at some site (numerical-domain error)");
+    const long long step = (long long)(v >> 40), site = (long long)(v & ((1ULL << 40) - 1));
+    const long long x = site % h->nx, y = (site / h->nx) % h->ny, z = site / ((long long)h->nx * h->ny);
+    return set_err(h, LB_ENUMERIC,
+                   "numerical-domain error (R22): rho <= 0 or a non-finite value at site (x=%lld, y=%lld, z=%lld) "
+                   "in step %lld of this call (step %lld since the handle was created)",
+                   x, y, z, step0 >= 0 ? step - step0 : step, step);
   }
   return LB_OK;
 }
@@ -886,9 +930,7 @@ int lb_create_slab(int nx, int ny, int nz, const lb_params* params, int nranks, 
     *out = nullptr;
     return LB_ENCCL;
   }
-  const char* env = std::getenv("LB_HALO");
-  const bool force_exchange = env && (!std::strcmp(env, "nccl") || !std::strcmp(env, "copy"));
-  rc = force_exchange ? LB_OK : open_peers(h);
+  rc = open_peers(h);
   if (rc) {
     g_create_error = h->err;
     lb_destroy(h);
@@ -972,12 +1014,8 @@ int lb_step(lb_t* h, int nsteps) {
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state: call lb_set_state or lb_init_equilibrium first");
   if (nsteps > 0 && h->xch_default && !h->ch && !h->lc && (rc = ensure_xch(h))) return rc;  // (never inside a capture)
   if (nsteps > 0 && (rc = refresh_xch(h))) return rc;
+  const long long step0 = h->steps_done;
   int t = 0;
-  if (!h->stepped && nsteps > 0) {
-    if ((rc = one_step(h, 0))) return rc;
-    h->stepped = true;
-    ++t;
-  }
   while (nsteps - t >= kGraphSteps && graphs_usable(h)) {
     bool done = false;
     if ((rc = graph_steps(h, &done))) return rc;
@@ -985,42 +1023,72 @@ int lb_step(lb_t* h, int nsteps) {
     t += kGraphSteps;
   }
   for (; t < nsteps; ++t)
-    if ((rc = one_step(h, 0))) return rc;
-  return finish(h);
+    if ((rc = one_step(h))) return rc;
+  return finish(h, step0);
 }
 
-int lb_debug_step_probe(lb_t* h, int nsteps, int mode) {
+int lb_prepare(lb_t* h) {
   int rc = usable(h);
   if (rc) return rc;
-  if (nsteps < 0 || mode < 1 || mode > 5) return set_err(h, LB_EINVAL, "nsteps >= 0 and mode in {1, ..., 5} required");
-  if (h->ch || h->lc) return set_err(h, LB_EINVAL, "no memory probes for a Cahn-Hilliard or liquid-crystal handle");
-  if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
-  for (int t = 0; t < nsteps; ++t)
-    if ((rc = one_step(h, mode))) return rc;
-  return finish(h);
+  if (h->xch_default && !h->ch && !h->lc && (rc = ensure_xch(h))) return rc;
+  if ((rc = refresh_xch(h))) return rc;
+  if (!graphs_usable(h)) return LB_OK;
+  for (int parity = 0; parity < 2; ++parity) {  // the graphs of both buffer roles
+    capture_graph(h);
+    swap_roles(h);
+  }
+  CK(h, cudaStreamSynchronize(h->stream));
+  return LB_OK;
 }
 
 int lb_debug_step_kernel(lb_t* h, int which) {
   if (h && (h->ch || h->lc) && which != 0)
     return set_err(h, LB_EINVAL, "a Cahn-Hilliard or liquid-crystal handle has one step kernel");
-  if (!h || which < 0 || which > 5)
+  if (!h || which < 0 || which > 3)
     return set_err(h, LB_EINVAL,
-                   "which must be 0 (auto), 1 (tile), 2 (cluster), 3 (warp-specialised), 4 (persistent warp-specialised) "
-                   "or 5 (warp-specialised with the phi exchange)");
-  if (which == 5 && (h->nslabs != 1 || h->slabs.empty() || !step_xch_fits(h->G, &h->slabs[0].mapsA)))
+                   "which must be 0 (auto), 1 (tile), 2 (warp-specialised) or 3 (warp-specialised with the phi exchange)");
+  if (which == 3 && (h->nslabs != 1 || h->slabs.empty() || !step_xch_fits(h->G, &h->slabs[0].mapsA)))
     return set_err(h, LB_EINVAL, "the phi exchange needs one periodic slab, nx %% 32 == 0 and ny %% 8 == 0 (TMA rows)");
-  if (which == 5) {
+  if (which == 3) {
     const int rc = ensure_xch(h);
     if (rc) return rc;
   }
-  if (which == 2 && h->dp.coll != 0)
-    return set_err(h, LB_EINVAL, "the cluster kernel implements only the BGK + force collision (model 0)");
-  if (which == 2 && !h->slabs.empty() && !h->slabs[0].cmapsA.ok)
-    return set_err(h, LB_EINVAL, "the cluster kernel needs nx %% 64 == 0 and ny %% 16 == 0");
-  if ((which == 3 || which == 4) && !h->slabs.empty() && !step_ws_fits(&h->slabs[0].mapsA))
+  if (which == 2 && !h->slabs.empty() && !step_ws_fits(&h->slabs[0].mapsA))
     return set_err(h, LB_EINVAL, "the warp-specialised kernel needs nx even (TMA rows)");
   h->kernel_choice = which;
-  drop_graphs(h);
+  choose_xch(h);
+  steps_changed(h);
+  return LB_OK;
+}
+
+int lb_debug_tune(lb_t* h, int key, int value) {
+  if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
+  switch (key) {
+    case LB_TUNE_ZCHUNK:
+      if (value < 0) return set_err(h, LB_EINVAL, "z-chunk must be >= 0 (0: automatic)");
+      if (value == 0) {
+        h->zc = step_zchunk(h->G, h->num_sms, h->ty);
+        h->lczc = lc_zchunk(h->G, h->num_sms);
+      } else {
+        h->zc = h->lczc = value < h->nzl ? value : h->nzl;
+      }
+      if (!h->slabs.empty()) choose_xch(h);
+      break;
+    case LB_TUNE_BAND_ROWS:
+      if (value < 1) return set_err(h, LB_EINVAL, "band rows must be >= 1");
+      h->order.band = value;
+      break;
+    case LB_TUNE_RESID:
+      if (value < 0) return set_err(h, LB_EINVAL, "resident CTAs must be >= 0 (0: the kernel's occupancy)");
+      h->order.resid = value;
+      break;
+    case LB_TUNE_GRAPHS:
+      h->graphs_on = value != 0;
+      break;
+    default:
+      return set_err(h, LB_EINVAL, "unknown tuning key %d", key);
+  }
+  steps_changed(h);
   return LB_OK;
 }
 
@@ -1030,7 +1098,7 @@ int lb_debug_stream(lb_t* h, int nsteps) {
   if (nsteps < 0) return set_err(h, LB_EINVAL, "nsteps must be >= 0");
   if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
   for (int t = 0; t < nsteps; ++t)
-    if ((rc = one_step(h, -1))) return rc;
+    if ((rc = one_step(h, true))) return rc;
   return finish(h);
 }
 
@@ -1070,12 +1138,11 @@ void lb_destroy(lb_t* h) {
     cudaFree(s.u);
     cudaFree(s.u2);
   }
-  cudaFree(h->d_flag);
+  cudaFree(h->d_health);
+  cudaFree(h->d_done);
   cudaFree(h->xphi[0]);
   cudaFree(h->xphi[1]);
-  cudaFree(h->xch_pre);
-  cudaFree(h->wctr.dev);
-  if (h->h_flag) cudaFreeHost(h->h_flag);
+  if (h->h_health) cudaFreeHost(h->h_health);
   for (auto& p : h->pending) {
     cudaEventDestroy(p.e0);
     cudaEventDestroy(p.e1);
@@ -1215,7 +1282,7 @@ int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, doub
   if (rc) return rc;
   if (h->ch) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle's collision is fixed at lb_create_ch");
   if (h->lc) return set_err(h, LB_EINVAL, "a liquid-crystal handle's collision is fixed at lb_create_lc");
-  drop_graphs(h);
+  steps_changed(h);
   if (model == 0) {
     h->dp.coll = 0;
     return LB_OK;
@@ -1223,7 +1290,6 @@ int lb_set_collision(lb_t* h, int model, double tau_shear, double tau_bulk, doub
   if (model != 1) return set_err(h, LB_EINVAL, "model must be 0 (BGK + force) or 1 (stress in f^eq, MRT)");
   for (double t : {tau_shear, tau_bulk, tau_ghost})
     if (!std::isfinite(t) || !(t > 0.5)) return set_err(h, LB_EINVAL, "MRT relaxation times must be finite and > 0.5");
-  if (h->kernel_choice == 2) return set_err(h, LB_EINVAL, "the cluster kernel implements only model 0");
   h->dp.coll = 1;
   h->dp.inv_tau_s = 1.0 / tau_shear;
   h->dp.inv_tau_b = 1.0 / tau_bulk;
@@ -1238,25 +1304,8 @@ int lb_debug_halo_mode(lb_t* h, int mode) {
   if (mode == 1 && h->nranks > 1 && !h->peerB[0]) return set_err(h, LB_EINVAL, "no peer mapping on this handle");
   if (mode == 1 && h->G.zwrap) return set_err(h, LB_EINVAL, "a single periodic slab has no halo");
   h->halo_mode = mode;
-  drop_graphs(h);
+  steps_changed(h);
   return LB_OK;
-}
-
-int lb_debug_xch_bands(int nx, int ny, int nz, int zc, int num_sms, int band, int* band_out, int* sites, int cap) {
-  if (!band_out || nx < 32 || ny < 8 || nz < 3 || nx % 32 || ny % 8 || zc < 1 || num_sms < 1 || cap < 0 ||
-      (cap > 0 && !sites))
-    return LB_EINVAL;
-  Geom G;
-  G.nx = nx;
-  G.ny = ny;
-  G.nzl = nz;
-  G.zwrap = true;
-  G.nxy = (long long)nx * ny;
-  G.plane = (long long)NSLOT * G.nxy;
-  *band_out = band >= 0 ? band : ws_xch_band(G, zc, num_sms);
-  const std::vector<int> pre = ws_xch_pre_sites(G, *band_out);
-  for (size_t k = 0; k < pre.size() && (long long)k < cap; ++k) sites[k] = pre[k];
-  return (int)pre.size();
 }
 
 int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* out) {
@@ -1299,6 +1348,16 @@ int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* 
             if (out[(long long)i * N + sdst] != -1) return LB_EINVAL;  // not a permutation
             out[(long long)i * N + sdst] = ssrc;
           }
+  }
+  return LB_OK;
+}
+
+int lb_debug_tile_order(int ntx, int nty, int nch, int resid, int band, int* out) {
+  if (!out || ntx < 1 || nty < 1 || nch < 1 || resid < 1 || band < 1) return LB_EINVAL;
+  const int n = ntx * nty * nch;
+  for (int L = 0; L < n; ++L) {
+    const TileId t = tile_of_block(L, ntx, nty, nch, TileOrder{resid, band});
+    out[3 * L] = t.bx, out[3 * L + 1] = t.by, out[3 * L + 2] = t.bz;
   }
   return LB_OK;
 }
@@ -1415,10 +1474,6 @@ int lc_create(int nx, int ny, int nz, const lb_lc_params* lp, int nranks, int ra
   h->dp.lc_xi = lp->xi;
   h->dp.lc_Gamma = lp->Gamma;
   h->lczc = lc_zchunk(h->G, h->num_sms);
-  if (const char* ev = std::getenv("LB_ZCHUNK")) {  // tuning override (measurement only)
-    const int z = std::atoi(ev);
-    if (z >= 1) h->lczc = z < h->nzl ? z : h->nzl;
-  }
   const size_t nq = lc_q_doubles(h->G), nu = lc_u_doubles(h->G);
   cudaError_t e = cudaSuccess;
   bool maps_ok = true;

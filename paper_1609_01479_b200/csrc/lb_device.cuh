@@ -21,6 +21,26 @@ __device__ __forceinline__ double phi_sum(const double* __restrict__ a, long lon
   return s;
 }
 
+// R22: record site (x, y, local z) of this launch's slab as offending,
+// tagged with the step in progress; the smallest (step, site) of a call wins.
+__device__ __forceinline__ void health_report(const Health& h, const Geom& G, int x, int y, int z) {
+  const unsigned long long site =
+      (unsigned long long)(h.site0 + (long long)z * G.nxy + (long long)y * G.nx + x);
+  const unsigned long long step = *reinterpret_cast<volatile unsigned long long*>(h.step);
+  atomicMin(h.flag, (step << 40) | site);
+}
+// One thread per CTA, after the CTA's reports (a CTA barrier before): the last
+// CTA of the launch to finish advances the step counter -- every report of this
+// launch has read the step number by then.
+__device__ __forceinline__ void health_tick(const Health& h) {
+  if (!h.done) return;
+  __threadfence();
+  if (atomicAdd(h.done, 1u) == gridDim.x - 1) {
+    *h.done = 0;
+    atomicAdd(h.step, 1ULL);
+  }
+}
+
 // A.4 (R3): mu = A phi + B phi^3 - kappa lap phi
 __device__ __forceinline__ double chem_pot(const DevParams& p, double ph, double lap) {
   return p.A * ph + p.B * (ph * ph * ph) - p.kappa * lap;

@@ -1,7 +1,6 @@
 // lb_kernels.cuh -- internal (C++) interface between the host runtime and the
 // sm_100a kernels.  Not part of the C ABI (include/lb.h is).
 #pragma once
-#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -62,19 +61,27 @@ __host__ __device__ inline long long push_target(const Geom& G, int i, int x, in
 
 // Tile and z-chunk of a step-kernel block.  Blocks start in launch order, about
 // `resid` of them resident at a time, each taking about as long as the others.
-// The order is: groups of `resid` tiles (row-major); inside a group, all tiles of
-// chunk 0, then all of chunk 1, ...  So chunk c of a tile starts when chunk c-1
-// of the same tile ends, and its first planes (the box loads of planes zA-2 ..
-// zA+1, which the previous chunk loaded last) are still in L2 -- with chunks in
-// separate waves they were read from DRAM twice.  Row-major order inside a group
-// keeps the CTAs resident at one time on whole 4 KB rows (narrow strips, tried
+// The order is: groups of `resid` tiles; inside a group, all tiles of chunk 0,
+// then all of chunk 1, ...  So chunk c of a tile starts when chunk c-1 of the
+// same tile ends, and its first planes (the box loads of planes zA-2 .. zA+1,
+// which the previous chunk loaded last) are still in L2 -- with chunks in
+// separate waves they were read from DRAM twice.  Tiles are numbered row-major
+// (band = 1), or in bands of `band` tile rows walked column by column (tile t of
+// a band: column t / band, row t % band), which puts the y neighbours of a tile
+// next to it in launch order.  Whole rows (or bands of rows) keep the CTAs
+// resident at one time on whole 4 KB rows (narrow strips of tile columns, tried
 // to bring y neighbours closer in launch order, lost more in DRAM locality than
 // they gained in L2 reuse).
 struct TileId {
   int bx, by, bz;
 };
-__host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch, int resid) {
+struct TileOrder {
+  int resid = 148;  // CTAs resident at a time
+  int band = 1;     // tile rows per band
+};
+__host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch, TileOrder o) {
   const int ntiles = ntx * nty;
+  int resid = o.resid;
   if (resid > ntiles || resid < 1) resid = ntiles;
   const int per_group = resid * nch;
   const int grp = L / per_group;
@@ -82,8 +89,23 @@ __host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch
   const int rg = ntiles - grp * resid < resid ? ntiles - grp * resid : resid;
   const int c = r / rg;
   const int t = grp * resid + (r - c * rg);
-  return TileId{t % ntx, t / ntx, c};
+  if (o.band <= 1) return TileId{t % ntx, t / ntx, c};
+  const int per_band = o.band * ntx;  // tiles of a full band
+  const int b = t / per_band, u = t - b * per_band;
+  const int rows = nty - b * o.band < o.band ? nty - b * o.band : o.band;  // (last band may be partial)
+  return TileId{u / rows, b * o.band + u % rows, c};
 }
+
+// R22 numerical-domain report: the first offending site of a call.  The
+// step kernels fold (step << 40 | global site) into *flag with atomicMin (~0 =
+// clean); *step counts the steps the handle's step kernels completed (the last
+// CTA of the last launch of a step advances it, after every CTA's reports).
+struct Health {
+  unsigned long long* flag = nullptr;
+  unsigned long long* step = nullptr;
+  unsigned* done = nullptr;  // CTAs finished in this launch; nullptr: this launch does not tick
+  long long site0 = 0;       // global site index of local site 0 (slab z0 * nx * ny)
+};
 
 // Fused halo ("peer" transport): the buffers of the
 // neighbouring slabs, on this GPU (loopback) or mapped from a peer GPU over
@@ -112,6 +134,15 @@ __host__ __device__ inline double* push_plane(const Geom& G, double* B, const Pe
 // K_phi on local planes [z0, z1); with peers, edge planes also go to the neighbours' ghost planes
 cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st,
                        const Peers& pr = Peers{});
+// Per-device kernel preparation (dynamic shared memory attribute above 48 KB, and
+// the CTAs resident at a time): once per (kernel, device), thread-safe.
+cudaError_t prepare_kernel(const void* fn, size_t smem, int threads, int* resid);
+// every step kernel variant of lb_step.cu, lb_step_ws.cu, lb_step_ch.cu, lb_step_lc.cu
+// (at handle creation: no first-launch preparation ever happens inside a graph capture)
+cudaError_t prepare_step_kernels();
+cudaError_t prepare_ws_kernels();
+cudaError_t prepare_ch_kernels();
+cudaError_t prepare_lc_kernels();
 // the fused step (lb_step.cu): collide planes [0, nzl) of A into B; phig = phi
 // buffer whose ghost planes are read when !G.zwrap; zc = z-chunk per CTA
 int step_tile_rows(const Geom& G, int num_sms);  // 4 or 8
@@ -124,16 +155,16 @@ struct alignas(64) StepMaps {
   bool ok;
 };
 bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out);
-// mode 0 = the step; 1, 2 = memory probes (lb_debug_step_probe)
-cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* mapsA, cudaStream_t st, int mode = 0, const Peers& pr = Peers{});
-// the warp-specialised variant of the step (lb_step_ws.cu): same maps, nx even.
-// Persistent CTAs take work items from a device counter that only grows; `base`
-// is its value at the start of the next launch (advanced by every launch).
-struct WorkCounter {
-  unsigned long long* dev = nullptr;
-  unsigned long long base = 0;
+// Launch knobs of the step kernels: block order (tile_of_block; resid 0 = the
+// occupancy of the kernel on this device)
+struct Launch {
+  int zc = 1;
+  TileOrder order{0, 1};
 };
+cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                        const Launch& ln, const Health& hl, const StepMaps* mapsA, cudaStream_t st,
+                        const Peers& pr = Peers{});
+// the warp-specialised variant of the step (lb_step_ws.cu): same maps, nx even.
 bool step_ws_fits(const StepMaps* maps);
 // phi exchange (xch, single periodic slab): the stencil warps load only the g tile
 // and take the phi halo from the neighbouring tiles' CTAs through an L2-resident
@@ -143,30 +174,18 @@ bool step_ws_fits(const StepMaps* maps);
 // depth: g tiles of the stencil in flight (1 or 2; 2 pays where the state is
 // about L2-sized and the step latency-bound, 64^3 +10%, and loses where it is
 // HBM-bound, 128^3 -6%: the earlier loads queue in front of the collision's).
-// band: tiles per launch (0: all items in one launch).  Over several waves the
-// step is launched band by band, each band's tiles x z-chunks in one wave, so
-// the CTAs of neighbouring tiles start together again at every band (DESIGN.md
-// "phi exchange in bands").
 struct XchArgs {
   double* cur = nullptr;
   double* old = nullptr;
   int depth = 1;
-  int band = 0;
-  int t0 = 0, rt = 0;  // tiles [t0, t0 + rt) of one banded launch (set by the launcher)
-  const int* pre = nullptr;  // xy of the sites bands take from later bands (ws_xch_pre_sites), device
-  int npre = 0;
 };
-// tiles per band of the banded phi exchange: whole tile rows whose blocks (tiles
-// x z-chunks) fit in one wave of num_sms CTAs; 0 if the lattice fits one wave.
-int ws_xch_band(const Geom& G, int zc, int num_sms);
-std::vector<int> ws_xch_pre_sites(const Geom& G, int band);
 int ws_xch_blocks(const Geom& G, int zc);  // blocks of the step (tiles x z-chunks)
 constexpr unsigned long long kXchEmpty = 0xFFF4DEADBEEF0001ULL;  // a NaN no arithmetic produces
 bool step_xch_fits(const Geom& G, const StepMaps* maps);
 cudaError_t fill_xch_empty(double* buf, long long n, cudaStream_t st);
-cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                           int* flag, const StepMaps* mapsA, cudaStream_t st, const Peers& pr, WorkCounter* wc,
-                           bool persist, const XchArgs* xch = nullptr);
+cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                           const Launch& ln, const Health& hl, const StepMaps* mapsA, cudaStream_t st, const Peers& pr,
+                           const XchArgs* xch = nullptr);
 // the finite-difference Cahn-Hilliard variant (lb_step_ch.cu, NEXT-2): state f and
 // a phi field; one TMA map (f box of one component, (32+4) x (ty+2)); one slab
 struct alignas(64) ChMaps {
@@ -176,25 +195,14 @@ struct alignas(64) ChMaps {
 };
 bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out);
 cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
-                           double* phiB, int zc, int* flag, const ChMaps* mapsA, cudaStream_t st);
+                           double* phiB, int zc, const Health& hl, const ChMaps* mapsA, cudaStream_t st);
 // the liquid-crystal workload (lb_step_lc.cu, NEXT-4): state f (dist buffer, f slots),
 // Q (five components, q[z][c][y][x]) and u (q[z][a][y][x]); 32 x 8 tiles, the f tile
 // by TMA through maps m[0] (5 components) and m[1] (9) of make_step_maps(.., 8, ..)
 int lc_zchunk(const Geom& G, int num_sms);
 cudaError_t launch_step_lc(const Geom& G, const DevParams& p, const double* A, double* B, const double* qA,
-                           double* qB, const double* uA, double* uB, int zc, int* flag, const StepMaps* mapsA,
+                           double* qB, const double* uA, double* uB, int zc, const Health& hl, const StepMaps* mapsA,
                            cudaStream_t st);
-// the cluster variant of the step (lb_step_cluster.cu): phi halos shared through
-// distributed shared memory; for nx % 64 == 0 and ny % 16 == 0
-struct alignas(64) ClusterMaps {
-  unsigned char m[2][128];
-  bool ok;
-};
-bool cluster_step_fits(const Geom& G);
-bool make_cluster_maps(const Geom& G, const double* buf, ClusterMaps* out);
-int cluster_zchunk(const Geom& G, int num_sms);
-cudaError_t launch_step_cluster(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
-                                int zc, int* flag, const ClusterMaps* mapsA, cudaStream_t st, const Peers& pr = Peers{});
 cudaError_t launch_stream(const Geom& G, const double* A, double* B, cudaStream_t st, const Peers& pr = Peers{});
 cudaError_t launch_init_eq(const Geom& G, const DevParams& p, const double* phi, const double* rho,
                            const double* u, double* A, cudaStream_t st);

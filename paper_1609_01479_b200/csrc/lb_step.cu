@@ -33,112 +33,24 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "lb_device.cuh"
+#include "lb_tma.cuh"
 
 namespace lbk {
 namespace {
 
-// Tile 32 x 8 (256 threads, ~177 KB smem, one CTA per SM): the halo box is 1.69x
-// the tile (2.25x for 32 x 4); measured best at 512x512x64 with z-chunks giving
-// ~8 waves.
-#ifndef LB_STEP_TX
-#define LB_STEP_TX 32
-#endif
-#ifndef LB_STEP_TY
-#define LB_STEP_TY 8
-#endif
-// planes ahead of the asynchronous copies at which the same boxes are prefetched
-// into L2 (0: off)
-#ifndef LB_PF_DIST
-#define LB_PF_DIST 0
-#endif
-#ifndef LB_STEP_WAVES
-#define LB_STEP_WAVES 8
-#endif
-constexpr int kTX = LB_STEP_TX;
-// strip width of the block -> tile order (tile_of_block)
+// Tile 32 x 8 (256 threads, ~177 KB smem, one CTA per SM) or 32 x 4 (two CTAs per
+// SM, odd nx on small planes): the halo box is 1.69x the tile (2.25x for 32 x 4).
+constexpr int kTX = 32;
+constexpr int kStepWaves = 8;  // 32 x 4 tiles: z-chunks for ~8 waves of CTAs
 
 __device__ __forceinline__ int slot5(int z) {
   const int s = z % 5;
   return s < 0 ? s + 5 : s;
-}
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-// ---- mbarrier / TMA / bulk-copy primitives (PTX ISA 8.x, sm_90+) ------------
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  unsigned done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            unsigned long long* bar, unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const double* src, unsigned bytes, unsigned long long* bar,
-                                          unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
-               "r"(c2)
-               : "memory");
-}
-// L2 policies: the tile copy is the last use of f and g of a plane (evict first);
-// the g box is re-read two planes later by the tile copy (evict last).
-__device__ __forceinline__ unsigned long long policy_evict_first() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ unsigned long long policy_evict_last() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-// per-thread copies: wrapped halo boxes (16 B when rows are 16-byte aligned) and
-// everything for odd nx (8 B)
-template <int VEC>
-__device__ __forceinline__ void cp_async_v(void* dst, const double* src) {
-  if constexpr (VEC == 2)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// f components in slot order: rank j = 0..18 <-> slot 0..4 | 10..18 | 28..32
-__host__ __device__ constexpr int fslot_of_rank(int j) { return j < 5 ? j : (j < 14 ? 10 + (j - 5) : 28 + (j - 14)); }
-// g components in slot order: rank j = 0..18 <-> slot 5..9 | 19..27 | 33..37
-__host__ __device__ constexpr int gslot_of_rank(int j) { return j < 5 ? 5 + j : (j < 14 ? 19 + (j - 5) : 33 + (j - 14)); }
-__host__ __device__ constexpr int grank(int i) {  // canonical i -> rank
-  return slot(1, i) < 10 ? slot(1, i) - 5 : (slot(1, i) < 28 ? slot(1, i) - 19 + 5 : slot(1, i) - 33 + 14);
 }
 
 template <int TX, int TY>
@@ -154,24 +66,17 @@ struct alignas(128) StepSmem {
   unsigned long long bar_f, bar_g, bar_box;
 };
 
-// f components in slot order: rank j = 0..18 <-> slot 0..4 | 10..18 | 28..32
-__host__ __device__ constexpr int frank(int i) {  // canonical i -> rank
-  return slot(0, i) < 5 ? slot(0, i) : (slot(0, i) < 19 ? slot(0, i) - 10 + 5 : slot(0, i) - 28 + 14);
-}
-
 // USE_TMA: nx even (16-byte rows): TMA + bulk copies.  Otherwise 8-byte cp.async.
 // The tile's f and g are separate streams: f (from HBM) is consumed first and
 // re-issued for the next plane at the top of an iteration, so it has a whole
 // iteration of lead time; g (an L2 hit: the box brought it in two planes ago)
 // follows.
-template <int TX, int TY, bool USE_TMA, int MODE, int COLL>
+template <int TX, int TY, bool USE_TMA, int COLL>
 __global__ void __launch_bounds__(TX* TY, 1)
     k_step_async(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-                 const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
+                 const double* __restrict__ phig, int zc, TileOrder ord, Health hl, Peers pr,
                  const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
-                 const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9,
-                 const __grid_constant__ CUtensorMap tm_rh5, const __grid_constant__ CUtensorMap tm_rh9,
-                 const __grid_constant__ CUtensorMap tm_rv5, const __grid_constant__ CUtensorMap tm_rv9) {
+                 const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
   using S = StepSmem<TX, TY>;
   constexpr int NT = TX * TY;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
@@ -181,7 +86,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
 
   const int tid = threadIdx.x;
   const int lx = tid % TX, ly = tid / TX;
-  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc, resid);
+  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc, ord);
   const int x0 = tb.bx * TX, y0 = tb.by * TY;
   const int x = x0 + lx, y = y0 + ly;
   const bool active = (x < G.nx) && (y < G.ny);
@@ -208,7 +113,14 @@ __global__ void __launch_bounds__(TX* TY, 1)
   }
   auto zsrc = [&](int zp, bool& ghost) {
     ghost = false;
-    if (G.zwrap) { zp %= G.nzl; return zp < 0 ? zp + G.nzl : zp; }
+    if (G.zwrap) {  // one unsigned compare in the common case; a modulo only for slabs of < 3 planes
+      const int n = G.nzl;
+      if ((unsigned)zp >= (unsigned)n) {
+        zp += zp < 0 ? n : -n;
+        if ((unsigned)zp >= (unsigned)n) { zp %= n; zp += zp < 0 ? n : 0; }
+      }
+      return zp;
+    }
     ghost = zp < 0 || zp >= G.nzl;
     return zp;
   };
@@ -219,7 +131,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     mbar_init(&sm.bar_f, 1);
     mbar_init(&sm.bar_g, 1);
     mbar_init(&sm.bar_box, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_barrier_init();
   }
   __syncthreads();
   unsigned ph_f = 0, ph_g = 0, ph_box = 0;  // mbarrier parities
@@ -229,36 +141,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     bool ghost;
     const int zs = zsrc(zp, ghost);
     if (ghost) return false;
-    if (MODE == 5 && USE_TMA && box_interior) {
-      // probe of a ring design: the g TILE of plane zp (kept, in the real design, for
-      // the collision two planes later) plus only the halo ring of the box (top and
-      // bottom 36 x 2, left and right 2 x TY), 4 TMA boxes per g slot run
-      if (tid == 0) {
-        const int cpl = (zs + GZ) * NSLOT;
-        constexpr int RH = BX * 2, RV = 2 * TY;  // sites per component of a ring box
-        double* base = &sm.sG[0][0];
-        fence_proxy_async();
-        mbar_expect_tx(&sm.bar_box, (unsigned)(Q * (2 * RH + 2 * RV) * 8 + TILE_BYTES));
-        int off = 0;  // doubles; every box starts 128-byte aligned
-        auto place = [&](int n) {
-          const int o = off;
-          off += (n + 15) / 16 * 16;
-          return base + o;
-        };
-        for (int r = 0; r < 3; ++r) {
-          const CUtensorMap* h = r == 1 ? &tm_rh9 : &tm_rh5;
-          const CUtensorMap* v = r == 1 ? &tm_rv9 : &tm_rv5;
-          const int c = cpl + (r == 0 ? 5 : (r == 1 ? 19 : 33)), len = r == 1 ? 9 : 5;
-          tma_load_3d(place(len * RH), h, x0 - 2, y0 - 2, c, &sm.bar_box, pol_last);
-          tma_load_3d(place(len * RH), h, x0 - 2, y0 + TY, c, &sm.bar_box, pol_last);
-          tma_load_3d(place(len * RV), v, x0 - 2, y0, c, &sm.bar_box, pol_last);
-          tma_load_3d(place(len * RV), v, x0 + TX, y0, c, &sm.bar_box, pol_last);
-        }
-        tma_load_3d(&sm.sTg[0][0], &tm_t5, x0, y0, cpl + 5, &sm.bar_box, pol_first);
-        tma_load_3d(&sm.sTg[5][0], &tm_t9, x0, y0, cpl + 19, &sm.bar_box, pol_first);
-        tma_load_3d(&sm.sTg[14][0], &tm_t5, x0, y0, cpl + 33, &sm.bar_box, pol_first);
-      }
-    } else if (USE_TMA && box_interior) {
+    if (USE_TMA && box_interior) {
       // three TMA boxes (g slots 5..9, 19..27, 33..37), one thread
       if (tid == 0) {
         const int cpl = (zs + GZ) * NSLOT;  // component-plane index of slot 0
@@ -267,13 +150,6 @@ __global__ void __launch_bounds__(TX* TY, 1)
         tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
         tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
         tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
-        const int zq = G.zwrap ? wrap_n(zp + LB_PF_DIST, G.nzl) : zp + LB_PF_DIST;
-        if (LB_PF_DIST > 0 && zp + LB_PF_DIST <= zB + 1 && zq >= 0 && zq < G.nzl) {
-          const int cq = (zq + GZ) * NSLOT;
-          tma_prefetch_3d(&tm_g5, x0 - 2, y0 - 2, cq + 5);
-          tma_prefetch_3d(&tm_g9, x0 - 2, y0 - 2, cq + 19);
-          tma_prefetch_3d(&tm_g5, x0 - 2, y0 - 2, cq + 33);
-        }
       }
     } else {
       // the halo wraps the periodic edge (or odd nx): every thread copies its
@@ -312,12 +188,6 @@ __global__ void __launch_bounds__(TX* TY, 1)
         tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol_first);
         tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
         tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol_first);
-        if (LB_PF_DIST > 0 && dist == 0 && zp + LB_PF_DIST < zB) {
-          const int cq = (zp + LB_PF_DIST + GZ) * NSLOT;
-          tma_prefetch_3d(&tm_t5, x0, y0, cq);
-          tma_prefetch_3d(&tm_t9, x0, y0, cq + 10);
-          tma_prefetch_3d(&tm_t5, x0, y0, cq + 28);
-        }
       }
     } else {
       // odd nx: one 8-byte copy per (component, site), wrap only for partial tiles
@@ -401,7 +271,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
 
   // ---- prologue: phi on zA-2 .. zA+1; P on zA-1, zA; then prime the streams
   issue_tile(zA, 0);
-  for (int zp = zA - 2; zp <= zA + 1 && MODE != 3; ++zp) {
+  for (int zp = zA - 2; zp <= zA + 1; ++zp) {
     wait_box(issue_box(zp));
     __syncthreads();
     make_phi(zp);
@@ -409,7 +279,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
   }
   double Pz_prev[3] = {0, 0, 0}, Pz_cur[3] = {0, 0, 0}, Fxy_cur[3] = {0, 0, 0};
   double P6_cur[6] = {0, 0, 0, 0, 0, 0};  // COLL 1: P at this site, plane k
-  if (MODE == 0 || MODE == 2) {
+  {
     compute_P(zA - 1);
     __syncthreads();
     double unused[3];
@@ -420,8 +290,8 @@ __global__ void __launch_bounds__(TX* TY, 1)
     own_P(Pz_cur, Fxy_cur);
     if (COLL == 1) own_P6(P6_cur);
   }
-  bool box_issued = MODE != 3 ? issue_box(zA + 2) : false;
-  if (MODE != 4 && MODE != 5) issue_tile(zA, 1);
+  bool box_issued = issue_box(zA + 2);
+  issue_tile(zA, 1);
 
   // push targets: wrapped neighbour columns/rows of this thread's site
   const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
@@ -438,41 +308,20 @@ __global__ void __launch_bounds__(TX* TY, 1)
     issue_tile(k + 1, 0);
     double Pz_next[3] = {0, 0, 0}, Fxy_next[3] = {0, 0, 0};
     double P6_next[6] = {0, 0, 0, 0, 0, 0};
-    if (MODE == 4) {  // probe: g from the box interior instead of a second tile copy
-#pragma unroll
-      for (int i = 0; i < Q; ++i) g[i] = sm.sG[grank(i)][(ly + 2) * BX + (lx + 2)];
-    }
-    if (MODE != 1 && MODE != 3 && MODE != 4 && MODE != 5) make_phi(k + 2);
+    make_phi(k + 2);
     __syncthreads();  // sG consumed, ring written
-    box_issued = (k + 1 < zB && MODE != 3) ? issue_box(k + 3) : false;
-    if (MODE != 1 && MODE != 3 && MODE != 4 && MODE != 5) {
-      compute_P(k + 1);
-      __syncthreads();
-      own_P(Pz_next, Fxy_next);
-      if (COLL == 1) own_P6(P6_next);
-    }
-    if (MODE == 5) {  // probe: g from the tile the box barrier brought (two planes ahead)
+    box_issued = k + 1 < zB ? issue_box(k + 3) : false;
+    compute_P(k + 1);
+    __syncthreads();
+    own_P(Pz_next, Fxy_next);
+    if (COLL == 1) own_P6(P6_next);
+    wait_tile(1);  // g(k) tile landed
 #pragma unroll
-      for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
-    } else if (MODE != 4) {
-      wait_tile(1);  // g(k) tile landed
-#pragma unroll
-      for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
-      __syncthreads();  // sTg consumed
-      issue_tile(k + 1, 1);
-    }
+    for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
+    __syncthreads();  // sTg consumed
+    issue_tile(k + 1, 1);
     double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
-    if (MODE != 0 && active) {
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
-        const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
-        __stcs(d + (long long)slot(0, i) * nxy, f[i]);
-        __stcs(d + (long long)slot(1, i) * nxy, g[i]);
-      }
-    }
-    if (MODE == 0 && active) {
+    if (active) {
       const double* r0 = sm.sPhi[slot5(k)];
       const double ph = r0[cbox];
       const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) +
@@ -494,7 +343,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
         for (int a = 0; a < 3; ++a) F[a] = Fxy_cur[a] - 0.5 * (Pz_next[a] - Pz_prev[a]);
         rho = collide(p, f, g, ph, mu, F, push);
       }
-      if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
+      if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) health_report(hl, G, x, y, k);  // R22
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -507,24 +356,69 @@ __global__ void __launch_bounds__(TX* TY, 1)
   }
   cp_wait<0>();
   if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
+  __syncthreads();
+  if (tid == 0) health_tick(hl);
 }
 
-// ---- host: tensor maps ---------------------------------------------------------
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+template <int TY, bool USE_TMA, int COLL>
+cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                     const Launch& ln, const Health& hl, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
+  constexpr size_t smem = sizeof(StepSmem<kTX, TY>);
+  auto kern = k_step_async<kTX, TY, USE_TMA, COLL>;
+  int resid = 0;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), smem, kTX * TY, &resid);
+  if (e != cudaSuccess) return e;
+  TileOrder ord = ln.order;
+  if (ord.resid <= 0) ord.resid = resid;
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
+  const int zc = ln.zc;
+  const unsigned nblk = (unsigned)(((G.nx + kTX - 1) / kTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc));
+  kern<<<nblk, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, ord, hl, pr, m[0], m[1], m[2], m[3]);
+  return cudaGetLastError();
+}
+
+template <int TY, bool USE_TMA>
+cudaError_t launch_coll(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                        const Launch& ln, const Health& hl, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
+  return p.coll == 1 ? launch_t<TY, USE_TMA, 1>(G, p, A, B, phig, ln, hl, maps, st, pr)
+                     : launch_t<TY, USE_TMA, 0>(G, p, A, B, phig, ln, hl, maps, st, pr);
+}
+
+}  // namespace
+
+cudaError_t prepare_kernel(const void* fn, size_t smem, int threads, int* resid) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> CTAs resident at a time
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({fn, dev});
+  if (it != done.end()) {
+    *resid = it->second;
+    return cudaSuccess;
+  }
+  if (smem > 48 * 1024 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
+  int sms = 0, per_sm = 0;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem)) != cudaSuccess) return e;
+  *resid = sms * (per_sm > 0 ? per_sm : 1);
+  done[{fn, dev}] = *resid;
+  return cudaSuccess;
+}
+
+// buffer viewed as a 3-D fp64 tensor {x: nx, y: ny, component-plane: (nzl+2GZ)*38}
+bool encode_dist_map(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsigned by, unsigned bz) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
-// buffer viewed as a 3-D fp64 tensor {x: nx, y: ny, component-plane: (nzl+2GZ)*38}
-bool encode(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsigned by, unsigned bz) {
-  auto fn = encode_fn();
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   if (!fn) return false;
   cuuint64_t dims[3] = {(cuuint64_t)G.nx, (cuuint64_t)G.ny, (cuuint64_t)(G.nzl + 2 * GZ) * NSLOT};
   cuuint64_t strides[2] = {(cuuint64_t)G.nx * 8, (cuuint64_t)G.nxy * 8};
@@ -535,63 +429,6 @@ bool encode(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsig
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TY, bool USE_TMA, int MODE, int COLL = 0>
-cudaError_t launch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                     int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
-  constexpr size_t smem = sizeof(StepSmem<kTX, TY>);
-  auto kern = k_step_async<kTX, TY, USE_TMA, MODE, COLL>;
-  static bool attr = false;  // per-process, per-instantiation
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
-  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
-  const unsigned nblk = (unsigned)(((G.nx + kTX - 1) / kTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc));
-  dim3 grid(nblk);
-  static int resid = 0;  // CTAs resident at a time (tile_of_block)
-  if (!resid) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTX * TY, smem);
-    resid = sms * (per_sm > 0 ? per_sm : 1);
-#ifdef LB_RESID_OVERRIDE
-    resid = LB_RESID_OVERRIDE;
-#endif
-  }
-  if constexpr (MODE == 5) {  // maps of the ring boxes of the probe, for this buffer
-    CUtensorMap rm[4];
-    if (!encode(&rm[0], G, A, kTX + 4, 2, 5) || !encode(&rm[1], G, A, kTX + 4, 2, 9) ||
-        !encode(&rm[2], G, A, 2, TY, 5) || !encode(&rm[3], G, A, 2, TY, 9))
-      return cudaErrorInvalidValue;
-    kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3], rm[0], rm[1],
-                                       rm[2], rm[3]);
-  } else {
-    kern<<<grid, kTX * TY, smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, m[0], m[1], m[2], m[3], m[0], m[1],
-                                       m[0], m[1]);
-  }
-  return cudaGetLastError();
-}
-
-template <int TY, bool USE_TMA>
-cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st, int mode, const Peers& pr) {
-  switch (mode) {
-    case 1: return launch_t<TY, USE_TMA, 1>(G, p, A, B, phig, zc, flag, maps, st, pr);
-    case 2: return launch_t<TY, USE_TMA, 2>(G, p, A, B, phig, zc, flag, maps, st, pr);
-    case 3: return launch_t<TY, USE_TMA, 3>(G, p, A, B, phig, zc, flag, maps, st, pr);
-    case 4: return launch_t<TY, USE_TMA, 4>(G, p, A, B, phig, zc, flag, maps, st, pr);
-    case 5: return launch_t<TY, USE_TMA, 5>(G, p, A, B, phig, zc, flag, maps, st, pr);
-    default:
-      return p.coll == 1 ? launch_t<TY, USE_TMA, 0, 1>(G, p, A, B, phig, zc, flag, maps, st, pr)
-                         : launch_t<TY, USE_TMA, 0, 0>(G, p, A, B, phig, zc, flag, maps, st, pr);
-  }
-}
-
-}  // namespace
-
 // Tile rows of the step kernel.  Even nx (TMA rows): 32 x 8 tiles and the
 // warp-specialised kernel for every plane size -- measured in round 1 against
 // 32 x 4 tiles of the tile kernel (two CTAs per SM): +12% at 128^3, +17% at 64^3,
@@ -599,7 +436,6 @@ cudaError_t launch_mode(const Geom& G, const DevParams& p, const double* A, doub
 // 512 x 512 x 64.  Odd nx (per-thread copies): 32 x 4 tiles
 // unless the plane has >= 4 x SMs tiles of 32 x 8.
 int step_tile_rows(const Geom& G, int num_sms) {
-  if (LB_STEP_TY != 8) return 4;
   if (G.nx % 2 == 0) return 8;
   const long long tiles8 = (long long)((G.nx + kTX - 1) / kTX) * ((G.ny + 7) / 8);
   return tiles8 >= 4LL * num_sms ? 8 : 4;
@@ -611,10 +447,10 @@ bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out) {
   if (G.nx % 2 != 0) return true;  // odd rows: the cp.async path needs no maps
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out->m);
   const unsigned BX = kTX + 4, BY = ty + 4;
-  if (!encode(&m[0], G, buf, kTX, ty, 5)) return false;
-  if (!encode(&m[1], G, buf, kTX, ty, 9)) return false;
-  if (!encode(&m[2], G, buf, BX, BY, 5)) return false;
-  if (!encode(&m[3], G, buf, BX, BY, 9)) return false;
+  if (!encode_dist_map(&m[0], G, buf, kTX, ty, 5)) return false;
+  if (!encode_dist_map(&m[1], G, buf, kTX, ty, 9)) return false;
+  if (!encode_dist_map(&m[2], G, buf, BX, BY, 5)) return false;
+  if (!encode_dist_map(&m[3], G, buf, BX, BY, 9)) return false;
   out->ok = true;
   return true;
 }
@@ -640,7 +476,7 @@ int step_zchunk(const Geom& G, int num_sms, int ty) {
       nchunks = (G.nzl + zc - 1) / zc;
     }
   } else {
-    const long long target = (long long)LB_STEP_WAVES * num_sms;
+    const long long target = (long long)kStepWaves * num_sms;
     nchunks = (target + tiles - 1) / tiles;
   }
   if (nchunks > maxchunks) nchunks = maxchunks;
@@ -648,15 +484,32 @@ int step_zchunk(const Geom& G, int num_sms, int ty) {
   return (int)((G.nzl + nchunks - 1) / nchunks);
 }
 
-cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st, int mode, const Peers& pr) {
+cudaError_t prepare_step_kernels() {
+  int r = 0;
+  cudaError_t e = cudaSuccess;
+  auto prep = [&](const void* fn, size_t smem, int threads) {
+    if (e == cudaSuccess) e = prepare_kernel(fn, smem, threads, &r);
+  };
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 8, true, 0>), sizeof(StepSmem<kTX, 8>), kTX * 8);
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 8, true, 1>), sizeof(StepSmem<kTX, 8>), kTX * 8);
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 8, false, 0>), sizeof(StepSmem<kTX, 8>), kTX * 8);
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 8, false, 1>), sizeof(StepSmem<kTX, 8>), kTX * 8);
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 4, true, 0>), sizeof(StepSmem<kTX, 4>), kTX * 4);
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 4, true, 1>), sizeof(StepSmem<kTX, 4>), kTX * 4);
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 4, false, 0>), sizeof(StepSmem<kTX, 4>), kTX * 4);
+  prep(reinterpret_cast<const void*>(k_step_async<kTX, 4, false, 1>), sizeof(StepSmem<kTX, 4>), kTX * 4);
+  return e;
+}
+
+cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                        const Launch& ln, const Health& hl, const StepMaps* maps, cudaStream_t st, const Peers& pr) {
   if (!maps) return cudaErrorInvalidValue;
   const bool tma = maps->ok;
   if (maps->ty == 8)
-    return tma ? launch_mode<8, true>(G, p, A, B, phig, zc, flag, maps, st, mode, pr)
-               : launch_mode<8, false>(G, p, A, B, phig, zc, flag, maps, st, mode, pr);
-  return tma ? launch_mode<4, true>(G, p, A, B, phig, zc, flag, maps, st, mode, pr)
-             : launch_mode<4, false>(G, p, A, B, phig, zc, flag, maps, st, mode, pr);
+    return tma ? launch_coll<8, true>(G, p, A, B, phig, ln, hl, maps, st, pr)
+               : launch_coll<8, false>(G, p, A, B, phig, ln, hl, maps, st, pr);
+  return tma ? launch_coll<4, true>(G, p, A, B, phig, ln, hl, maps, st, pr)
+             : launch_coll<4, false>(G, p, A, B, phig, ln, hl, maps, st, pr);
 }
 
 }  // namespace lbk

@@ -61,7 +61,7 @@ struct alignas(128) ChSmem {
 template <int TY>
 __global__ void __launch_bounds__(kCX* TY, 1)
     k_step_ch(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-              const double* __restrict__ phiA, double* __restrict__ phiB, int zc, int* __restrict__ flag,
+              const double* __restrict__ phiA, double* __restrict__ phiB, int zc, Health hl,
               const __grid_constant__ CUtensorMap tm_f1) {
   using S = ChSmem<TY>;
   constexpr int TX = kCX, NT = S::NT;
@@ -288,30 +288,36 @@ __global__ void __launch_bounds__(kCX* TY, 1)
                          (sm.sMu[up][cu] + sm.sMu[um][cu]) - 6.0 * mk[cu];
     const double phn = (ph - div) + p.mob * lapmu;
     phiB[phi_plane_index(G, k) + (long long)y * G.nx + x] = phn;
-    if (!(rho > 0.0) || !isfinite(rho) || !isfinite(phn)) *flag = 1;  // R22
+    if (!(rho > 0.0) || !isfinite(rho) || !isfinite(phn)) health_report(hl, G, x, y, k);  // R22
   }
   cp_wait<0>();
+  __syncthreads();
+  if (tid == 0) health_tick(hl);
 }
 
 template <int TY>
 cudaError_t launch_ch_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
-                        double* phiB, int zc, int* flag, const ChMaps* maps, cudaStream_t st) {
+                        double* phiB, int zc, const Health& hl, const ChMaps* maps, cudaStream_t st) {
   constexpr size_t smem = sizeof(ChSmem<TY>);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
   auto kern = k_step_ch<TY>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  int resid = 0;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), smem, kCX * TY, &resid);
+  if (e != cudaSuccess) return e;
   const int tiles = ((G.nx + kCX - 1) / kCX) * ((G.ny + TY - 1) / TY);
   const int nblk = tiles * ((G.nzl + zc - 1) / zc);
-  kern<<<nblk, kCX * TY, smem, st>>>(G, p, A, B, phiA, phiB, zc, flag, *reinterpret_cast<const CUtensorMap*>(maps->m));
+  kern<<<nblk, kCX * TY, smem, st>>>(G, p, A, B, phiA, phiB, zc, hl, *reinterpret_cast<const CUtensorMap*>(maps->m));
   return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t prepare_ch_kernels() {
+  int r = 0;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(k_step_ch<8>), sizeof(ChSmem<8>), kCX * 8, &r);
+  if (e == cudaSuccess) e = prepare_kernel(reinterpret_cast<const void*>(k_step_ch<4>), sizeof(ChSmem<4>), kCX * 4, &r);
+  return e;
+}
 
 bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out) {
   out->ok = false;
@@ -323,10 +329,10 @@ bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out) {
 }
 
 cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
-                           double* phiB, int zc, int* flag, const ChMaps* maps, cudaStream_t st) {
+                           double* phiB, int zc, const Health& hl, const ChMaps* maps, cudaStream_t st) {
   if (!maps || !maps->ok) return cudaErrorInvalidValue;
-  if (maps->ty == 8) return launch_ch_t<8>(G, p, A, B, phiA, phiB, zc, flag, maps, st);
-  return launch_ch_t<4>(G, p, A, B, phiA, phiB, zc, flag, maps, st);
+  if (maps->ty == 8) return launch_ch_t<8>(G, p, A, B, phiA, phiB, zc, hl, maps, st);
+  return launch_ch_t<4>(G, p, A, B, phiA, phiB, zc, hl, maps, st);
 }
 
 }  // namespace lbk

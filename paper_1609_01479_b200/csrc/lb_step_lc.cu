@@ -173,7 +173,7 @@ __device__ __forceinline__ void corotation(double xi, const double (&W)[3][3], c
 __global__ void __launch_bounds__(kLT, 1)
     k_step_lc(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B, const double* __restrict__ qA,
               double* __restrict__ qB, const double* __restrict__ uA, double* __restrict__ uB, int zc,
-              int* __restrict__ flag, const __grid_constant__ CUtensorMap tm5, const __grid_constant__ CUtensorMap tm9) {
+              Health hl, const __grid_constant__ CUtensorMap tm5, const __grid_constant__ CUtensorMap tm9) {
   using S = LcSmem;
   constexpr int BX = S::BX, NB = S::NB, UX = S::UX, NU = S::NU, SX = S::SX, NS = S::NS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kLT, 1)
         __stcs(uB + zu + a * nxy, un[a]);
         chk += un[a];
       }
-      if (!(rho > 0.0) || !isfinite(chk)) *flag = 1;  // R22
+      if (!(rho > 0.0) || !isfinite(chk)) health_report(hl, G, x, y, k);  // R22
     }
     // rotate the per-thread planes
 #pragma unroll
@@ -421,9 +421,16 @@ __global__ void __launch_bounds__(kLT, 1)
     }
   }
   cp_wait<0>();
+  __syncthreads();
+  if (threadIdx.x == 0) health_tick(hl);
 }
 
 }  // namespace
+
+cudaError_t prepare_lc_kernels() {
+  int r = 0;
+  return prepare_kernel(reinterpret_cast<const void*>(k_step_lc), sizeof(LcSmem), kLT, &r);
+}
 
 int lc_zchunk(const Geom& G, int num_sms) {
   const long long tiles = (long long)((G.nx + kLX - 1) / kLX) * ((G.ny + kLY - 1) / kLY);
@@ -438,21 +445,18 @@ int lc_zchunk(const Geom& G, int num_sms) {
 }
 
 cudaError_t launch_step_lc(const Geom& G, const DevParams& p, const double* A, double* B, const double* qA,
-                           double* qB, const double* uA, double* uB, int zc, int* flag, const StepMaps* maps,
+                           double* qB, const double* uA, double* uB, int zc, const Health& hl, const StepMaps* maps,
                            cudaStream_t st) {
   if (!maps || !maps->ok || maps->ty != kLY || G.nx % 2 != 0) return cudaErrorInvalidValue;
   constexpr size_t smem = sizeof(LcSmem);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_step_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  int resid = 0;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(k_step_lc), smem, kLT, &resid);
+  if (e != cudaSuccess) return e;
   const int tiles = ((G.nx + kLX - 1) / kLX) * ((G.ny + kLY - 1) / kLY);
   const int nblk = tiles * ((G.nzl + zc - 1) / zc);
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
-  k_step_lc<<<nblk, kLT, smem, st>>>(G, p, A, B, qA, qB, uA, uB, zc, flag, m[0], m[1]);
+  k_step_lc<<<nblk, kLT, smem, st>>>(G, p, A, B, qA, qB, uA, uB, zc, hl, m[0], m[1]);
   return cudaGetLastError();
 }
 

@@ -20,9 +20,6 @@
 // The tile kernel is one CTA per SM at 32 x 8 tiles; there, every __syncthreads
 // between the phi/P phases and the collision phase stalled the store stream
 // (DESIGN.md "Tuning").  Needs 16-byte rows (nx even: TMA).
-#include <algorithm>
-#include <cstdlib>
-
 #include "lb_device.cuh"
 #include "lb_tma.cuh"
 
@@ -66,19 +63,7 @@ __host__ __device__ constexpr bool ws_split_regs(int ty) {
 #endif
 
 // XCH: planes the stencil's P / F / mu work trails its phi (the neighbours' slack)
-#ifndef LB_XCH_PF
-#define LB_XCH_PF 1  // iterations a halo site of the phi exchange is loaded ahead of its use (1 or 2)
-#endif
-#ifndef LB_XCH_LAG
-#define LB_XCH_LAG 4
-#endif
-#ifndef LB_WS_FETCH_EARLY
-#define LB_WS_FETCH_EARLY 0
-#endif
-// persistent CTAs: continue the same tile's next z-chunk without a prologue
-#ifndef LB_WS_CONT
-#define LB_WS_CONT 1
-#endif
+constexpr int kXchLag = 4;
 
 template <int R>
 __device__ __forceinline__ int wslot(int z) {
@@ -95,7 +80,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
 
 template <int TY, int COLL, bool XCH = false>
 struct alignas(128) WsSmem {
-  static constexpr int NPHI = XCH ? LB_XCH_LAG + 4 : 5;  // phi ring planes (XCH: lag planes more)
+  static constexpr int NPHI = XCH ? kXchLag + 4 : 5;  // phi ring planes (XCH: lag planes more)
   static constexpr int NQ = COLL == 1 ? 8 : 5;  // hand-off values per site
   static constexpr int TX = kWTX, NT = TX * TY;
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
@@ -107,29 +92,9 @@ struct alignas(128) WsSmem {
   double sPhi[NPHI][NB];           // ring of phi planes on the box
   double sP[6][NP];                // chemical stress of one plane on the P box
   double sQ[2][NQ][NT];            // hand-off: phi, mu, then Fx, Fy, Fz (COLL 0) or P (COLL 1)
-  unsigned long long bar_f, bar_g, bar_box, bar_xb[2], q_full[2], q_empty[2], item_full[4];
-  int sItem[4];                    // work items, fetched by the stencil warps
+  unsigned long long bar_f, bar_g, bar_box, bar_xb[2], q_full[2], q_empty[2];
 };
 
-// Work item L (tile x z-chunk) of the step, in tile_of_block order.
-struct WsItem {
-  int x0, y0, zA, zB;
-};
-
-// PERSIST: one CTA per SM takes work items (L = tile x z-chunk, tile_of_block
-// order) from a global counter until none are left -- the same order the block
-// scheduler would use, so the CTAs working at one time stay on neighbouring
-// tiles (a static L = blockIdx.x + i*gridDim.x split lets fast CTAs run ahead
-// into other bands of tiles: +185 B/site of DRAM reads).  The
-// stencil warps fetch the next item as they start the current one and publish it
-// to the collision warps (sItem ring, item_full mbarriers), so the collision warps
-// prefetch the next item's first f and g tiles while they finish the current
-// one, and the stencil warps fill the next item's pipeline (prologue) while the
-// collision warps drain the current one.  The hand-off counter runs on across
-// items.  When the next item continues the same tile in z, the stencil keeps its
-// phi ring and P state and skips the prologue.  Without PERSIST, one item per
-// CTA (L = blockIdx.x).
-//
 // XCH (phi exchange; one periodic slab, whole 32 x 8 tiles): the stencil warps
 // load only the g TILE of plane j+2, not the tile + 2-site halo box (-40% of the
 // box bytes), store phi of their tile to an L2-resident array (xa.cur) and take
@@ -143,15 +108,14 @@ struct WsItem {
 // one wave (the tiles' CTAs start together and stay within the lag of each
 // other: 128^3, 64^3); over several waves the neighbours drift apart and the
 // fallback sums cost more than the box.
-template <int TY, bool PERSIST, int COLL, bool XCH = false>
+template <int TY, int COLL, bool XCH = false>
 __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-              const double* __restrict__ phig, int zc, int resid, int* __restrict__ flag, Peers pr,
-              unsigned long long* __restrict__ wctr, unsigned long long wbase, XchArgs xa,
+              const double* __restrict__ phig, int zc, TileOrder ord, Health hl, Peers pr, XchArgs xa,
               const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
               const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
   using S = WsSmem<TY, COLL, XCH>;
-  static_assert(!XCH || (TY == 8 && COLL == 0 && !PERSIST), "phi exchange: 32 x 8 tiles, BGK, static rounds");
+  static_assert(!XCH || (TY == 8 && COLL == 0), "phi exchange: 32 x 8 tiles, BGK");
   constexpr int TX = kWTX, NT = S::NT;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
   constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
@@ -161,22 +125,10 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
   const int tid = threadIdx.x;
-  const int ntx = (G.nx + TX - 1) / TX, nty = (G.ny + TY - 1) / TY, nch = (G.nzl + zc - 1) / zc;
-  const int nitems = ntx * nty * nch;
+  const TileId tb = tile_of_block(blockIdx.x, (G.nx + TX - 1) / TX, (G.ny + TY - 1) / TY, (G.nzl + zc - 1) / zc, ord);
+  const int x0 = tb.bx * TX, y0 = tb.by * TY;
+  const int zA = tb.bz * zc, zB = min(zA + zc, G.nzl);
   const long long nxy = G.nxy;
-  auto item_of = [&](int L) {
-    TileId tb = tile_of_block(L, ntx, nty, nch, resid);
-    if (XCH && xa.rt > 0) {  // banded: tiles [t0, t0 + rt) of this launch, chunk-major
-      const int t = xa.t0 + L % xa.rt;
-      tb = TileId{t % ntx, t / ntx, L / xa.rt};
-    }
-    WsItem it;
-    it.x0 = tb.bx * TX;
-    it.y0 = tb.by * TY;
-    it.zA = tb.bz * zc;
-    it.zB = min(it.zA + zc, G.nzl);
-    return it;
-  };
 
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
@@ -191,7 +143,6 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       mbar_init(&sm.q_full[s], kNA);
       mbar_init(&sm.q_empty[s], NT);
     }
-    for (int s = 0; s < 4; ++s) mbar_init(&sm.item_full[s], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -221,314 +172,259 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     unsigned seq = 0;  // planes handed off so far: slot seq & 1, use seq >> 1
     double Pz_prev[SPT][3], Pz_cur[SPT][3], Fxy_cur[SPT][3];
     double P6_cur[SPT][COLL == 1 ? 6 : 1];  // COLL 1: P at the site, plane j
-    WsItem prev{-1, -1, -1, -1};
-    // item m goes to sItem[m % 4]; the value nitems ends the sequence
-    unsigned m = 0;
-    auto fetch_publish = [&](unsigned idx) {
-      if (a == 0) {
-        int L;
-        if (PERSIST) {
-          const unsigned long long v = atomicAdd(wctr, 1ULL) - wbase;
-          L = v < (unsigned long long)nitems ? (int)v : nitems;
-        } else {
-          L = idx == 0 ? (int)blockIdx.x : nitems;
+    const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
+    constexpr bool use_box = !XCH;
+    // per-thread copy plan of a wrapped halo box: 16-byte units
+    long long box_src[BOXR];
+    int box_dst[BOXR];
+#pragma unroll
+    for (int r = 0; r < BOXR; ++r) {
+      const int u = a + r * kNA;
+      const int row = u / BROWU, cu = u - row * BROWU;
+      box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
+      box_dst[r] = u < BOXU ? row * BX + cu * 2 : -1;
+    }
+    // box n (n = 0 .. nlast) is the g box of plane zA - 2 + n
+    const int nlast = zB - zA + 3;  // plane zB + 1
+    auto issue_box = [&](int n) -> bool {
+      const int zp = zA - 2 + n;
+      bool ghost;
+      const int zs = zsrc(zp, ghost);
+      if (ghost) return false;
+      if (XCH && !use_box) {
+        if (a == 0) {  // the g tile only, in tile layout, into buffer n & 1
+          const int cpl = (zs + GZ) * NSLOT;
+          double* dst = &sm.sG[0][0] + (n & 1) * Q * NT;
+          unsigned long long* bar = &sm.bar_xb[n & 1];
+          fence_proxy_async();
+          mbar_expect_tx(bar, TILE_BYTES);
+          tma_load_3d(dst, &tm_t5, x0, y0, cpl + 5, bar, pol_last);
+          tma_load_3d(dst + 5 * NT, &tm_t9, x0, y0, cpl + 19, bar, pol_last);
+          tma_load_3d(dst + 14 * NT, &tm_t5, x0, y0, cpl + 33, bar, pol_last);
         }
-        sm.sItem[idx % 4] = L;
-        mbar_arrive(&sm.item_full[idx % 4]);
+      } else if (box_interior) {
+        if (a == 0) {
+          const int cpl = (zs + GZ) * NSLOT;
+          fence_proxy_async();
+          mbar_expect_tx(&sm.bar_box, BOX_BYTES);
+          tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
+          tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
+          tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
+        }
+      } else {
+        const double* base = A + (long long)(zs + GZ) * G.plane;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          const double* bj = base + (long long)gslot_of_rank(j) * nxy;
+#pragma unroll
+          for (int r = 0; r < BOXR; ++r)
+            if (box_dst[r] >= 0) cp_async_v<2>(&sm.sG[j][box_dst[r]], bj + box_src[r]);
+        }
+        cp_commit();
+      }
+      return true;
+    };
+    // wait for the box, then make it visible to the whole role
+    auto wait_box = [&](bool issued, int n) {
+      if (XCH && !use_box) {  // g tile n (always issued: one periodic slab)
+        mbar_wait(&sm.bar_xb[n & 1], (ph_xb >> (n & 1)) & 1);
+        ph_xb ^= 1u << (n & 1);
+      } else if (issued) {
+        if (box_interior) {
+          mbar_wait(&sm.bar_box, ph_box);
+          ph_box ^= 1;
+        } else {
+          cp_wait<0>();
+        }
+      }
+      named_sync(2, kNA);
+    };
+    auto make_phi = [&](int zp, int n) {
+      bool ghost;
+      const int zs = zsrc(zp, ghost);
+      double* ring = sm.sPhi[wslot<S::NPHI>(zp)];
+      if (XCH && !ghost) {
+        double* xp = xa.cur + (long long)zs * nxy;
+        double* xo = xa.old + (long long)zs * nxy;
+        if (!use_box) {  // phi of the tile from the g tile
+          const double(*gt)[NT] = reinterpret_cast<const double(*)[NT]>(&sm.sG[0][0] + (n & 1) * Q * NT);
+          for (int s = a; s < NT; s += kNA) {
+            double v = gt[grank(0)][s];  // A.3, canonical order (same as phi_sum)
+#pragma unroll
+            for (int i = 1; i < Q; ++i) v += gt[grank(i)][s];
+            ring[(s / TX + 2) * BX + s % TX + 2] = v;
+            const long long o = (long long)(y0 + s / TX) * G.nx + x0 + s % TX;
+            st_relaxed_f64(xp + o, v);  // published to the neighbouring tiles' CTAs
+            st_relaxed_f64(xo + o, __longlong_as_double((long long)kXchEmpty));
+          }
+          return;
+        }
+      }
+      for (int b = a; b < NB; b += kNA) {
+        double v;
+        if (ghost) {
+          const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
+          v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
+        } else {
+          v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
+#pragma unroll
+          for (int i = 1; i < Q; ++i) v += sm.sG[grank(i)][b];
+        }
+        ring[b] = v;
       }
     };
-    fetch_publish(0);
-    named_sync(2, kNA);
-    int L = sm.sItem[0];
-    while (L < nitems) {
-#if LB_WS_FETCH_EARLY
-      fetch_publish(m + 1);  // early: the collision warps need it at this item's last plane
-#endif
-      const WsItem it = item_of(L);
-      const int x0 = it.x0, y0 = it.y0, zA = it.zA, zB = it.zB;
-      const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
-      constexpr bool use_box = !XCH;
-      // per-thread copy plan of a wrapped halo box: 16-byte units
-      long long box_src[BOXR];
-      int box_dst[BOXR];
+    auto compute_P = [&](int zp) {
+      const double* f0 = sm.sPhi[wslot<S::NPHI>(zp - 1)];
+      const double* f1 = sm.sPhi[wslot<S::NPHI>(zp)];
+      const double* f2 = sm.sPhi[wslot<S::NPHI>(zp + 1)];
+      for (int e = a; e < NP; e += kNA) {
+        const int c = (e / PX + 1) * BX + (e % PX + 1);
+        const double ph = f1[c];
+        const double xp = f1[c + 1], xm = f1[c - 1];
+        const double yp = f1[c + BX], ym = f1[c - BX];
+        const double zp_ = f2[c], zm = f0[c];
+        const double lap = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * ph;  // A.2
+        double P[6];
+        stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp_ - zm), lap, P);
 #pragma unroll
-      for (int r = 0; r < BOXR; ++r) {
-        const int u = a + r * kNA;
-        const int row = u / BROWU, cu = u - row * BROWU;
-        box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
-        box_dst[r] = u < BOXU ? row * BX + cu * 2 : -1;
+        for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
       }
-      // box n (n = 0 .. nlast) is the g box of plane zA - 2 + n
-      const int nlast = zB - zA + 3;  // plane zB + 1
-      auto issue_box = [&](int n) -> bool {
-        const int zp = zA - 2 + n;
-        bool ghost;
-        const int zs = zsrc(zp, ghost);
-        if (ghost) return false;
-        if (XCH && !use_box) {
-          if (a == 0) {  // the g tile only, in tile layout, into buffer n & 1
-            const int cpl = (zs + GZ) * NSLOT;
-            double* dst = &sm.sG[0][0] + (n & 1) * Q * NT;
-            unsigned long long* bar = &sm.bar_xb[n & 1];
-            fence_proxy_async();
-            mbar_expect_tx(bar, TILE_BYTES);
-            tma_load_3d(dst, &tm_t5, x0, y0, cpl + 5, bar, pol_last);
-            tma_load_3d(dst + 5 * NT, &tm_t9, x0, y0, cpl + 19, bar, pol_last);
-            tma_load_3d(dst + 14 * NT, &tm_t5, x0, y0, cpl + 33, bar, pol_last);
-          }
-        } else if (box_interior) {
-          if (a == 0) {
-            const int cpl = (zs + GZ) * NSLOT;
-            fence_proxy_async();
-            mbar_expect_tx(&sm.bar_box, BOX_BYTES);
-            tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
-            tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
-            tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
-          }
-        } else {
-          const double* base = A + (long long)(zs + GZ) * G.plane;
+    };
+    auto own_P6 = [&](int site, double* P6) {
+      const int e = (site / TX + 1) * PX + (site % TX + 1);
 #pragma unroll
-          for (int j = 0; j < Q; ++j) {
-            const double* bj = base + (long long)gslot_of_rank(j) * nxy;
-#pragma unroll
-            for (int r = 0; r < BOXR; ++r)
-              if (box_dst[r] >= 0) cp_async_v<2>(&sm.sG[j][box_dst[r]], bj + box_src[r]);
-          }
-          cp_commit();
-        }
-        return true;
-      };
-      // wait for the box, then make it visible to the whole role
-      auto wait_box = [&](bool issued, int n) {
-        if (XCH && !use_box) {  // g tile n (always issued: one periodic slab)
-          mbar_wait(&sm.bar_xb[n & 1], (ph_xb >> (n & 1)) & 1);
-          ph_xb ^= 1u << (n & 1);
-        } else if (issued) {
-          if (box_interior) {
-            mbar_wait(&sm.bar_box, ph_box);
-            ph_box ^= 1;
-          } else {
-            cp_wait<0>();
-          }
-        }
-        named_sync(2, kNA);
-      };
-      auto make_phi = [&](int zp, int n) {
-        bool ghost;
-        const int zs = zsrc(zp, ghost);
-        double* ring = sm.sPhi[wslot<S::NPHI>(zp)];
-        if (XCH && !ghost) {
-          double* xp = xa.cur + (long long)zs * nxy;
-          double* xo = xa.old + (long long)zs * nxy;
-          if (!use_box) {  // phi of the tile from the g tile
-            const double(*gt)[NT] = reinterpret_cast<const double(*)[NT]>(&sm.sG[0][0] + (n & 1) * Q * NT);
-            for (int s = a; s < NT; s += kNA) {
-              double v = gt[grank(0)][s];  // A.3, canonical order (same as phi_sum)
-#pragma unroll
-              for (int i = 1; i < Q; ++i) v += gt[grank(i)][s];
-              ring[(s / TX + 2) * BX + s % TX + 2] = v;
-              const long long o = (long long)(y0 + s / TX) * G.nx + x0 + s % TX;
-              __stcg(xp + o, v);
-              __stcg(xo + o, __longlong_as_double((long long)kXchEmpty));
-            }
-            return;
-          }
-        }
-        for (int b = a; b < NB; b += kNA) {
-          double v;
-          if (ghost) {
-            const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
-            v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
-          } else {
-            v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
-#pragma unroll
-            for (int i = 1; i < Q; ++i) v += sm.sG[grank(i)][b];
-          }
-          ring[b] = v;
-          if (XCH && !ghost) {
-            const int bx = b % BX - 2, by = b / BX - 2;
-            if (bx >= 0 && bx < TX && by >= 0 && by < TY)
-            {
-              const long long o = (long long)zs * nxy + (long long)(y0 + by) * G.nx + x0 + bx;
-              __stcg(xa.cur + o, v);
-              __stcg(xa.old + o, __longlong_as_double((long long)kXchEmpty));
-            }
-          }
-        }
-      };
-      auto compute_P = [&](int zp) {
-        const double* f0 = sm.sPhi[wslot<S::NPHI>(zp - 1)];
-        const double* f1 = sm.sPhi[wslot<S::NPHI>(zp)];
-        const double* f2 = sm.sPhi[wslot<S::NPHI>(zp + 1)];
-        for (int e = a; e < NP; e += kNA) {
-          const int c = (e / PX + 1) * BX + (e % PX + 1);
-          const double ph = f1[c];
-          const double xp = f1[c + 1], xm = f1[c - 1];
-          const double yp = f1[c + BX], ym = f1[c - BX];
-          const double zp_ = f2[c], zm = f0[c];
-          const double lap = (xp + xm) + (yp + ym) + (zp_ + zm) - 6.0 * ph;  // A.2
-          double P[6];
-          stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp_ - zm), lap, P);
-#pragma unroll
-          for (int q = 0; q < 6; ++q) sm.sP[q][e] = P[q];
-        }
-      };
-      auto own_P6 = [&](int site, double* P6) {
-        const int e = (site / TX + 1) * PX + (site % TX + 1);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) P6[q] = sm.sP[q][e];
-      };
-      auto own_P = [&](int site, double Pz[3], double Fxy[3]) {
-        const int e = (site / TX + 1) * PX + (site % TX + 1);
-        const auto& P = sm.sP;
-        Pz[0] = P[PXZ][e];
-        Pz[1] = P[PYZ][e];
-        Pz[2] = P[PZZ][e];
-        Fxy[0] = -0.5 * (P[PXX][e + 1] - P[PXX][e - 1]) - 0.5 * (P[PXY][e + PX] - P[PXY][e - PX]);
-        Fxy[1] = -0.5 * (P[PXY][e + 1] - P[PXY][e - 1]) - 0.5 * (P[PYY][e + PX] - P[PYY][e - PX]);
-        Fxy[2] = -0.5 * (P[PXZ][e + 1] - P[PXZ][e - 1]) - 0.5 * (P[PYZ][e + PX] - P[PYZ][e - PX]);
-      };
+      for (int q = 0; q < 6; ++q) P6[q] = sm.sP[q][e];
+    };
+    auto own_P = [&](int site, double Pz[3], double Fxy[3]) {
+      const int e = (site / TX + 1) * PX + (site % TX + 1);
+      const auto& P = sm.sP;
+      Pz[0] = P[PXZ][e];
+      Pz[1] = P[PYZ][e];
+      Pz[2] = P[PZZ][e];
+      Fxy[0] = -0.5 * (P[PXX][e + 1] - P[PXX][e - 1]) - 0.5 * (P[PXY][e + PX] - P[PXY][e - PX]);
+      Fxy[1] = -0.5 * (P[PXY][e + 1] - P[PXY][e - 1]) - 0.5 * (P[PYY][e + PX] - P[PYY][e - PX]);
+      Fxy[2] = -0.5 * (P[PXZ][e + 1] - P[PXZ][e - 1]) - 0.5 * (P[PYZ][e + PX] - P[PYZ][e - PX]);
+    };
 
-      // the same tile continued in z: phi ring, P state and box stream carry on
-      const bool cont = LB_WS_CONT && PERSIST && prev.x0 == x0 && prev.y0 == y0 && prev.zB == zA;
-      const int n0 = cont ? 4 : 0;
-      // XCH lags LB_XCH_LAG planes: iteration nn makes phi of the tile on box nn
-      // (stored to xa.cur); each halo thread loads its site of box nn - lag + 1
-      // from the owner's store in xa.cur (L2) and uses it an iteration later -- if
-      // it still reads kXchEmpty the owner is behind (started later, runs slower)
-      // and the site's phi is summed from g here.  The value is its own flag: no
-      // fence, no flag word, no waiting.
-      constexpr int lag = XCH ? LB_XCH_LAG : 0;
-      constexpr int NH = 4 * BX + 4 * TY;  // halo: top and bottom 2 rows, left and right 2 columns
-      int h_ring = -1;
-      long long h_off = 0;
-      if (XCH && !use_box && a < NH) {
-        int bx, by;
-        if (a < 4 * BX) {
-          const int r = a / BX;
-          bx = a - r * BX;
-          by = r < 2 ? r : TY + r;  // rows 0, 1, TY + 2, TY + 3
-        } else {
-          const int q = a - 4 * BX, c = q / TY;
-          by = 2 + (q - c * TY);
-          bx = c < 2 ? c : TX + c;  // columns 0, 1, TX + 2, TX + 3
-        }
-        h_ring = by * BX + bx;
-        h_off = (long long)wrap_n(y0 - 2 + by, G.ny) * G.nx + wrap_n(x0 - 2 + bx, G.nx);
+    // XCH lags kXchLag planes: iteration nn makes phi of the tile on box nn
+    // (stored to xa.cur); each halo thread loads its site of box nn - lag + 1
+    // from the owner's store in xa.cur (L2) and uses it an iteration later -- if
+    // it still reads kXchEmpty the owner is behind (started later, runs slower)
+    // and the site's phi is summed from g here.  The value is its own flag: no
+    // fence, no flag word, no waiting.
+    constexpr int lag = XCH ? kXchLag : 0;
+    constexpr int NH = 4 * BX + 4 * TY;  // halo: top and bottom 2 rows, left and right 2 columns
+    int h_ring = -1;
+    long long h_off = 0;
+    if (XCH && !use_box && a < NH) {
+      int bx, by;
+      if (a < 4 * BX) {
+        const int r = a / BX;
+        bx = a - r * BX;
+        by = r < 2 ? r : TY + r;  // rows 0, 1, TY + 2, TY + 3
+      } else {
+        const int q = a - 4 * BX, c = q / TY;
+        by = 2 + (q - c * TY);
+        bx = c < 2 ? c : TX + c;  // columns 0, 1, TX + 2, TX + 3
       }
-      auto xsite = [&](int b) { return xa.cur + (long long)wrap_n(zA - 2 + b, G.nzl) * nxy + h_off; };
-      // the owner has not stored it yet (a neighbouring tile that started later or
-      // runs behind): phi from g here instead, the same sum in the same order
-      auto phi_here = [&](int b) {
-        return phi_sum(A + (long long)(wrap_n(zA - 2 + b, G.nzl) + GZ) * G.plane + h_off, nxy);
-      };
-      double pf = 0.0;  // the halo site of box hb + 1, loaded an iteration ahead
-      double pf2 = 0.0;  // (LB_XCH_PF 2: box hb + 2, two iterations ahead)
-      if (LB_XCH_PF == 2 && XCH && h_ring >= 0 && n0 - lag + 1 >= 0 && n0 - lag + 1 <= nlast)
-        pf2 = ld_relaxed_f64(xsite(n0 - lag + 1));
-      bool issued = issue_box(n0);
-      if (XCH && xa.depth == 2 && n0 + 1 <= nlast) issue_box(n0 + 1);  // two g tiles in flight
-      for (int nn = n0; nn <= nlast + lag; ++nn) {
-        double hv = 0.0;
-        const int hb = nn - lag;  // the halo box completed in this iteration
-        const bool hw = XCH && h_ring >= 0 && hb >= 0 && hb <= nlast;
-        if (hw) {
-          hv = pf;
-          if (__double_as_longlong(hv) == (long long)kXchEmpty) hv = phi_here(hb);  // owner behind: sum it here
-        }
-        if constexpr (LB_XCH_PF == 2) {
-          pf = pf2;
-          if (XCH && h_ring >= 0 && hb + 2 >= 0 && hb + 2 <= nlast) pf2 = ld_relaxed_f64(xsite(hb + 2));
-        } else {
-          if (XCH && h_ring >= 0 && hb + 1 >= 0 && hb + 1 <= nlast) pf = ld_relaxed_f64(xsite(hb + 1));
-        }
-        if (nn <= nlast) {
-          wait_box(issued, nn);  // (also: everyone is past the previous hand-off)
-          make_phi(zA - 2 + nn, nn);
-        } else {
-          named_sync(2, kNA);
-        }
-        if (hw) sm.sPhi[wslot<S::NPHI>(zA - 2 + hb)][h_ring] = hv;
-        named_sync(2, kNA);  // sG consumed, ring written
-        if (nn <= nlast) {
-          if (XCH && xa.depth == 2)
-            issued = nn + 2 <= nlast ? issue_box(nn + 2) : false;
-          else
-            issued = nn + 1 <= nlast ? issue_box(nn + 1) : false;
-        }
-        const int n = nn - lag, zp = zA - 2 + n;
-        if (n < 2) continue;
-        compute_P(zp - 1);  // needs phi(zp-2 .. zp)
-        named_sync(2, kNA);
-        if (n == 2) {
-#pragma unroll
-          for (int s = 0; s < SPT; ++s) {
-            double unused[3];
-            own_P(a + s * kNA, Pz_prev[s], unused);
-          }
-          continue;
-        }
-        if (n == 3) {
-#pragma unroll
-          for (int s = 0; s < SPT; ++s) {
-            own_P(a + s * kNA, Pz_cur[s], Fxy_cur[s]);
-            if constexpr (COLL == 1) own_P6(a + s * kNA, P6_cur[s]);
-          }
-          continue;
-        }
-        double Pz_next[SPT][3], Fxy_next[SPT][3];
-        double P6_next[SPT][COLL == 1 ? 6 : 1];
-#pragma unroll
-        for (int s = 0; s < SPT; ++s) {
-          own_P(a + s * kNA, Pz_next[s], Fxy_next[s]);
-          if constexpr (COLL == 1) own_P6(a + s * kNA, P6_next[s]);
-        }
-        // hand phi, mu, F of plane j = zp - 2 to the collision warps
-        const int j = zp - 2;
-        const int q = seq & 1, u = seq >> 1;
-        if (u >= 1) mbar_wait(&sm.q_empty[q], (u - 1) & 1);
-        const double* r0 = sm.sPhi[wslot<S::NPHI>(j)];
-        const double* rm = sm.sPhi[wslot<S::NPHI>(j - 1)];
-        const double* rp = sm.sPhi[wslot<S::NPHI>(j + 1)];
-#pragma unroll
-        for (int s = 0; s < SPT; ++s) {
-          const int site = a + s * kNA;
-          const int cbox = (site / TX + 2) * BX + (site % TX + 2);
-          const double ph = r0[cbox];
-          const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) + (rp[cbox] + rm[cbox]) -
-                             6.0 * ph;
-          sm.sQ[q][0][site] = ph;
-          sm.sQ[q][1][site] = chem_pot(p, ph, lap);
-          if constexpr (COLL == 1) {
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-              sm.sQ[q][2 + c][site] = P6_cur[s][c];
-              P6_cur[s][c] = P6_next[s][c];
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              sm.sQ[q][2 + c][site] = Fxy_cur[s][c] - 0.5 * (Pz_next[s][c] - Pz_prev[s][c]);
-              Pz_prev[s][c] = Pz_cur[s][c];
-              Pz_cur[s][c] = Pz_next[s][c];
-              Fxy_cur[s][c] = Fxy_next[s][c];
-            }
-          }
-        }
-        mbar_arrive(&sm.q_full[q]);
-        ++seq;
-      }
-#if !LB_WS_FETCH_EARLY
-      // the next item, taken only now (after the last hand-off) so that the items in
-      // flight stay a window of about one per CTA
-      fetch_publish(m + 1);
-#endif
-      cp_wait<0>();
-      named_sync(2, kNA);  // ring / P of this item done before the next item's box lands; sItem visible
-      prev = it;
-      ++m;
-      L = sm.sItem[m % 4];
+      h_ring = by * BX + bx;
+      h_off = (long long)wrap_n(y0 - 2 + by, G.ny) * G.nx + wrap_n(x0 - 2 + bx, G.nx);
     }
+    auto xsite = [&](int b) { return xa.cur + (long long)wrap_n(zA - 2 + b, G.nzl) * nxy + h_off; };
+    // the owner has not stored it yet (a neighbouring tile that started later or
+    // runs behind): phi from g here instead, the same sum in the same order
+    auto phi_here = [&](int b) {
+      return phi_sum(A + (long long)(wrap_n(zA - 2 + b, G.nzl) + GZ) * G.plane + h_off, nxy);
+    };
+    double pf = 0.0;  // the halo site of box hb + 1, loaded an iteration ahead
+    bool issued = issue_box(0);
+    if (XCH && xa.depth == 2 && 1 <= nlast) issue_box(1);  // two g tiles in flight
+    for (int nn = 0; nn <= nlast + lag; ++nn) {
+      double hv = 0.0;
+      const int hb = nn - lag;  // the halo box completed in this iteration
+      const bool hw = XCH && h_ring >= 0 && hb >= 0 && hb <= nlast;
+      if (hw) {
+        hv = pf;
+        if (__double_as_longlong(hv) == (long long)kXchEmpty) hv = phi_here(hb);  // owner behind: sum it here
+      }
+      if (XCH && h_ring >= 0 && hb + 1 >= 0 && hb + 1 <= nlast) pf = ld_relaxed_f64(xsite(hb + 1));
+      if (nn <= nlast) {
+        wait_box(issued, nn);  // (also: everyone is past the previous hand-off)
+        make_phi(zA - 2 + nn, nn);
+      } else {
+        named_sync(2, kNA);
+      }
+      if (hw) sm.sPhi[wslot<S::NPHI>(zA - 2 + hb)][h_ring] = hv;
+      named_sync(2, kNA);  // sG consumed, ring written
+      if (nn <= nlast) {
+        if (XCH && xa.depth == 2)
+          issued = nn + 2 <= nlast ? issue_box(nn + 2) : false;
+        else
+          issued = nn + 1 <= nlast ? issue_box(nn + 1) : false;
+      }
+      const int n = nn - lag, zp = zA - 2 + n;
+      if (n < 2) continue;
+      compute_P(zp - 1);  // needs phi(zp-2 .. zp)
+      named_sync(2, kNA);
+      if (n == 2) {
+#pragma unroll
+        for (int s = 0; s < SPT; ++s) {
+          double unused[3];
+          own_P(a + s * kNA, Pz_prev[s], unused);
+        }
+        continue;
+      }
+      if (n == 3) {
+#pragma unroll
+        for (int s = 0; s < SPT; ++s) {
+          own_P(a + s * kNA, Pz_cur[s], Fxy_cur[s]);
+          if constexpr (COLL == 1) own_P6(a + s * kNA, P6_cur[s]);
+        }
+        continue;
+      }
+      double Pz_next[SPT][3], Fxy_next[SPT][3];
+      double P6_next[SPT][COLL == 1 ? 6 : 1];
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) {
+        own_P(a + s * kNA, Pz_next[s], Fxy_next[s]);
+        if constexpr (COLL == 1) own_P6(a + s * kNA, P6_next[s]);
+      }
+      // hand phi, mu, F of plane j = zp - 2 to the collision warps
+      const int j = zp - 2;
+      const int q = seq & 1, u = seq >> 1;
+      if (u >= 1) mbar_wait(&sm.q_empty[q], (u - 1) & 1);
+      const double* r0 = sm.sPhi[wslot<S::NPHI>(j)];
+      const double* rm = sm.sPhi[wslot<S::NPHI>(j - 1)];
+      const double* rp = sm.sPhi[wslot<S::NPHI>(j + 1)];
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) {
+        const int site = a + s * kNA;
+        const int cbox = (site / TX + 2) * BX + (site % TX + 2);
+        const double ph = r0[cbox];
+        const double lap = (r0[cbox + 1] + r0[cbox - 1]) + (r0[cbox + BX] + r0[cbox - BX]) + (rp[cbox] + rm[cbox]) -
+                           6.0 * ph;
+        sm.sQ[q][0][site] = ph;
+        sm.sQ[q][1][site] = chem_pot(p, ph, lap);
+        if constexpr (COLL == 1) {
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            sm.sQ[q][2 + c][site] = P6_cur[s][c];
+            P6_cur[s][c] = P6_next[s][c];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            sm.sQ[q][2 + c][site] = Fxy_cur[s][c] - 0.5 * (Pz_next[s][c] - Pz_prev[s][c]);
+            Pz_prev[s][c] = Pz_cur[s][c];
+            Pz_cur[s][c] = Pz_next[s][c];
+            Fxy_cur[s][c] = Fxy_next[s][c];
+          }
+        }
+      }
+      mbar_arrive(&sm.q_full[q]);
+      ++seq;
+    }
+    cp_wait<0>();
     return;
   }
 
@@ -538,177 +434,90 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
   const unsigned long long pol_first = policy_of<LB_WS_TILE_POL>();
   const unsigned long long pol_st = policy_of<(LB_WS_ST_POL < 0 ? 1 : LB_WS_ST_POL)>();
   unsigned ph_f = 0, ph_g = 0, seq = 0;
-  auto issue_tile = [&](const WsItem& it, int zp, int dist) {
+  auto issue_tile = [&](int zp, int dist) {
     if (tid == 0) {
       double(*dst)[NT] = dist == 0 ? sm.sTf : sm.sTg;
       unsigned long long* bar = dist == 0 ? &sm.bar_f : &sm.bar_g;
       const int cp0 = (zp + GZ) * NSLOT + (dist == 0 ? 0 : 5);
       fence_proxy_async();
       mbar_expect_tx(bar, TILE_BYTES);
-      tma_load_3d(&dst[0][0], &tm_t5, it.x0, it.y0, cp0, bar, pol_first);
-      tma_load_3d(&dst[5][0], &tm_t9, it.x0, it.y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
-      tma_load_3d(&dst[14][0], &tm_t5, it.x0, it.y0, cp0 + 28, bar, pol_first);
+      tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol_first);
+      tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
+      tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol_first);
     }
   };
-  unsigned m = 0;
-  mbar_wait(&sm.item_full[0], 0);
-  int L = sm.sItem[0];
-  if (L < nitems) {
-    const WsItem first = item_of(L);
-    issue_tile(first, first.zA, 0);
-    issue_tile(first, first.zA, 1);
-  }
-  while (L < nitems) {
-    const WsItem it = item_of(L);
-    const int lx = tid % TX, ly = tid / TX;
-    const int x = it.x0 + lx, y = it.y0 + ly;
-    const bool active = (x < G.nx) && (y < G.ny);
-    const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
-    int Ln = nitems;
-    WsItem nxt = it;
-    bool got_next = false;
-    // the tile after plane k: plane k+1 of this item, or the next item's first plane
-    auto issue_next = [&](int k, int dist) {
-      if (k + 1 < it.zB) {
-        issue_tile(it, k + 1, dist);
-        return;
-      }
-      if (!got_next) {
-        mbar_wait(&sm.item_full[(m + 1) % 4], ((m + 1) / 4) & 1);
-        Ln = sm.sItem[(m + 1) % 4];
-        if (Ln < nitems) nxt = item_of(Ln);
-        got_next = true;
-      }
-      if (Ln < nitems) issue_tile(nxt, nxt.zA, dist);
-    };
-    for (int k = it.zA; k < it.zB; ++k) {
-      double f[Q], g[Q];
-      mbar_wait(&sm.bar_f, ph_f);
-      ph_f ^= 1;
+  issue_tile(zA, 0);
+  issue_tile(zA, 1);
+  const int lx = tid % TX, ly = tid / TX;
+  const int x = x0 + lx, y = y0 + ly;
+  const bool active = (x < G.nx) && (y < G.ny);
+  const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
+  for (int k = zA; k < zB; ++k) {
+    double f[Q], g[Q];
+    mbar_wait(&sm.bar_f, ph_f);
+    ph_f ^= 1;
 #pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
-      named_sync(1, NT);  // sTf consumed
-      issue_next(k, 0);
-      const int q = seq & 1, u = seq >> 1;
-      mbar_wait(&sm.q_full[q], u & 1);
-      const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];
-      double V[S::NQ - 2];  // F (COLL 0) or P (COLL 1)
+    for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
+    named_sync(1, NT);  // sTf consumed
+    if (k + 1 < zB) issue_tile(k + 1, 0);
+    const int q = seq & 1, u = seq >> 1;
+    mbar_wait(&sm.q_full[q], u & 1);
+    const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];
+    double V[S::NQ - 2];  // F (COLL 0) or P (COLL 1)
 #pragma unroll
-      for (int c = 0; c < S::NQ - 2; ++c) V[c] = sm.sQ[q][2 + c][tid];
-      mbar_arrive(&sm.q_empty[q]);
-      ++seq;
-      mbar_wait(&sm.bar_g, ph_g);
-      ph_g ^= 1;
+    for (int c = 0; c < S::NQ - 2; ++c) V[c] = sm.sQ[q][2 + c][tid];
+    mbar_arrive(&sm.q_empty[q]);
+    ++seq;
+    mbar_wait(&sm.bar_g, ph_g);
+    ph_g ^= 1;
 #pragma unroll
-      for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
-      named_sync(1, NT);  // sTg consumed
-      issue_next(k, 1);
-      if (active) {
-        double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
-        auto push = [&](int i, double fs, double gs) {
-          const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
-          const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-          double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
-          if (LB_WS_ST_POL < 0) {
-            __stcs(d + (long long)slot(0, i) * nxy, fs);
-            __stcs(d + (long long)slot(1, i) * nxy, gs);
-          } else {
-            st_hint(d + (long long)slot(0, i) * nxy, fs, pol_st);
-            st_hint(d + (long long)slot(1, i) * nxy, gs, pol_st);
-          }
-        };
-        double rho;
-        if constexpr (COLL == 1) rho = collide_mrt(p, f, g, ph, mu, V, push);
-        else rho = collide(p, f, g, ph, mu, V, push);
-        if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) *flag = 1;  // R22
-      }
+    for (int i = 0; i < Q; ++i) g[i] = sm.sTg[grank(i)][tid];
+    named_sync(1, NT);  // sTg consumed
+    if (k + 1 < zB) issue_tile(k + 1, 1);
+    if (active) {
+      double* const zb[3] = {push_plane(G, B, pr, k - 1), push_plane(G, B, pr, k), push_plane(G, B, pr, k + 1)};
+      auto push = [&](int i, double fs, double gs) {
+        const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
+        const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
+        if (LB_WS_ST_POL < 0) {
+          __stcs(d + (long long)slot(0, i) * nxy, fs);
+          __stcs(d + (long long)slot(1, i) * nxy, gs);
+        } else {
+          st_hint(d + (long long)slot(0, i) * nxy, fs, pol_st);
+          st_hint(d + (long long)slot(1, i) * nxy, gs, pol_st);
+        }
+      };
+      double rho;
+      if constexpr (COLL == 1) rho = collide_mrt(p, f, g, ph, mu, V, push);
+      else rho = collide(p, f, g, ph, mu, V, push);
+      if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) health_report(hl, G, x, y, k);  // R22
     }
-    ++m;
-    L = Ln;
   }
   if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
+  named_sync(1, NT);
+  if (tid == 0) health_tick(hl);
 }
 
-
-// Banded phi exchange: before the bands, phi of every site a band takes as halo
-// from a LATER band (xa.pre: the xy offsets, all planes), summed from g with
-// phi_sum and stored to xa.cur -- the edge tiles of a band would otherwise sum
-// them from g one site at a time on the stencil's path, and the launch waits for
-// its slowest block.  The owners store the same bits again when their band runs.
-__global__ void __launch_bounds__(256) k_xch_pre(Geom G, const double* __restrict__ A, double* __restrict__ cur,
-                                                 const int* __restrict__ pre, int npre) {
-  const long long n = (long long)G.nzl * npre;
-  for (long long t = blockIdx.x * 256LL + threadIdx.x; t < n; t += (long long)gridDim.x * 256) {
-    const int z = (int)(t / npre);
-    const long long xy = pre[t - (long long)z * npre];
-    __stcg(cur + (long long)z * G.nxy + xy, phi_sum(A + (long long)(z + GZ) * G.plane + xy, G.nxy));
-  }
-}
-
-template <int TY, bool PERSIST, int COLL, bool XCH = false>
-cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                        int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc,
+template <int TY, int COLL, bool XCH = false>
+cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                        const Launch& ln, const Health& hl, const StepMaps* maps, cudaStream_t st, const Peers& pr,
                         const XchArgs* xch = nullptr) {
   constexpr size_t smem = sizeof(WsSmem<TY, COLL, XCH>);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
-  auto kern = k_step_ws<TY, PERSIST, COLL, XCH>;
-  static bool attr = false;
-  static int resid = 0;  // CTAs resident at a time (tile_of_block; the persistent grid)
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ws_threads(TY, XCH), smem);
-    resid = sms * (per_sm > 0 ? per_sm : 1);
-#ifdef LB_RESID_OVERRIDE
-    resid = LB_RESID_OVERRIDE;
-#endif
-    if (const char* e = std::getenv("LB_RESID")) {  // tuning override (measurement only)
-      const int v = std::atoi(e);
-      if (v > 0) resid = v;
-    }
-  }
+  auto kern = k_step_ws<TY, COLL, XCH>;
+  int resid = 0;
+  cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), smem, ws_threads(TY, XCH), &resid);
+  if (e != cudaSuccess) return e;
+  TileOrder ord = ln.order;
+  if (ord.resid <= 0) ord.resid = resid;
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
+  const int zc = ln.zc;
   const int nitems = ((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc);
-  if (PERSIST && (!wc || !wc->dev)) return cudaErrorInvalidValue;
   if (XCH && (!xch || !xch->cur || !xch->old)) return cudaErrorInvalidValue;
   const XchArgs xa = xch ? *xch : XchArgs{};
-  if (XCH && xa.band > 0) {  // banded: one launch per band of tiles, each one wave
-    const int ntiles = nitems / ((G.nzl + zc - 1) / zc);
-    if (xa.npre > 0) {  // the halo sites the bands take from later bands, first
-      k_xch_pre<<<148 * 4, 256, 0, st>>>(G, A, xa.cur, xa.pre, xa.npre);
-      const cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-    }
-    // full bands: one chunk of the whole slab per tile; the last, partial band
-    // is cut into z-chunks (>= 8 planes) so that it fills the wave as well
-    for (int t0 = 0; t0 < ntiles; t0 += xa.band) {
-      XchArgs xb = xa;
-      xb.t0 = t0;
-      xb.rt = ntiles - t0 < xa.band ? ntiles - t0 : xa.band;
-      int nchb = 1;
-      if (xb.rt < xa.band) {
-        nchb = resid / xb.rt;
-        if (nchb > G.nzl / 8) nchb = G.nzl / 8;
-        if (nchb < 1) nchb = 1;
-      }
-      const int zcb = (G.nzl + nchb - 1) / nchb;
-      nchb = (G.nzl + zcb - 1) / zcb;
-      kern<<<(unsigned)(xb.rt * nchb), ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zcb, resid, flag, pr,
-                                                                       nullptr, 0ULL, xb, m[0], m[1], m[2], m[3]);
-      const cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-  }
-  const unsigned nblk = (unsigned)(PERSIST ? (nitems < resid ? nitems : resid) : nitems);
-  kern<<<nblk, ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, resid, flag, pr, wc ? wc->dev : nullptr,
-                                                  wc ? wc->base : 0ULL, xa, m[0], m[1], m[2], m[3]);
-  // every CTA takes one item past the end: the counter moved by nitems + grid
-  if (PERSIST) wc->base += (unsigned long long)nitems + nblk;
+  kern<<<(unsigned)nitems, ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, ord, hl, pr, xa, m[0], m[1], m[2],
+                                                            m[3]);
   return cudaGetLastError();
 }
 
@@ -720,37 +529,6 @@ bool step_xch_fits(const Geom& G, const StepMaps* maps) {
   return step_ws_fits(maps) && maps->ty == 8 && G.zwrap && G.nx % kWTX == 0 && G.ny % 8 == 0;
 }
 int ws_xch_blocks(const Geom& G, int zc) { return (G.nx / kWTX) * ((G.ny + 7) / 8) * ((G.nzl + zc - 1) / zc); }
-int ws_xch_band(const Geom& G, int zc, int num_sms) {
-  const int ntx = G.nx / kWTX, nty = (G.ny + 7) / 8, nch = (G.nzl + zc - 1) / zc;
-  const int ntiles = ntx * nty;
-  if ((long long)ntiles * nch <= num_sms) return 0;
-  if (ntiles <= num_sms) return ntiles;
-  if (num_sms < ntx) return num_sms;
-  // bands of whole tile rows, about equal (512 x 512 x 64: 8 bands of 8 rows, 128
-  // CTAs; partial-row bands of 147 tiles -6% -- more pre-pass sites, rows split
-  // between launches; 7 bands of 9 rows + one row cut in z -4%)
-  const int rows = num_sms / ntx, nb = (nty + rows - 1) / rows;
-  return (nty + nb - 1) / nb * ntx;
-}
-// xy offsets of the sites some band takes as phi halo from a later band: site s
-// lies in the 2-site ring of tile T iff T meets the 5 x 5 window around s, and
-// the tiles (32 x 8, both >= 5) met by the window are those of its 4 corners.
-std::vector<int> ws_xch_pre_sites(const Geom& G, int band) {
-  std::vector<int> out;
-  if (band <= 0) return out;
-  const int ntx = G.nx / kWTX;
-  auto w = [](int v, int n) { v %= n; return v < 0 ? v + n : v; };
-  auto band_of = [&](int x, int y) { return ((w(y, G.ny) / 8) * ntx + w(x, G.nx) / kWTX) / band; };
-  for (int y = 0; y < G.ny; ++y)
-    for (int x = 0; x < G.nx; ++x) {
-      const int b = band_of(x, y);
-      int m = b;
-      for (int dy = -2; dy <= 2; dy += 4)
-        for (int dx = -2; dx <= 2; dx += 4) m = std::min(m, band_of(x + dx, y + dy));
-      if (m < b) out.push_back(y * G.nx + x);
-    }
-  return out;
-}
 namespace {
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -762,27 +540,34 @@ cudaError_t fill_xch_empty(double* buf, long long n, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig, int zc,
-                           int* flag, const StepMaps* maps, cudaStream_t st, const Peers& pr, WorkCounter* wc,
-                           bool persist, const XchArgs* xch) {
+cudaError_t prepare_ws_kernels() {
+  int r = 0;
+  cudaError_t e = cudaSuccess;
+  auto prep = [&](const void* fn, size_t smem, int threads) {
+    if (e == cudaSuccess) e = prepare_kernel(fn, smem, threads, &r);
+  };
+  prep(reinterpret_cast<const void*>(k_step_ws<8, 0, false>), sizeof(WsSmem<8, 0, false>), ws_threads(8, false));
+  prep(reinterpret_cast<const void*>(k_step_ws<8, 1, false>), sizeof(WsSmem<8, 1, false>), ws_threads(8, false));
+  prep(reinterpret_cast<const void*>(k_step_ws<8, 0, true>), sizeof(WsSmem<8, 0, true>), ws_threads(8, true));
+  prep(reinterpret_cast<const void*>(k_step_ws<4, 0, false>), sizeof(WsSmem<4, 0, false>), ws_threads(4, false));
+  prep(reinterpret_cast<const void*>(k_step_ws<4, 1, false>), sizeof(WsSmem<4, 1, false>), ws_threads(4, false));
+  return e;
+}
+
+cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
+                           const Launch& ln, const Health& hl, const StepMaps* maps, cudaStream_t st, const Peers& pr,
+                           const XchArgs* xch) {
   if (!step_ws_fits(maps)) return cudaErrorInvalidValue;
   const bool t8 = maps->ty == 8;
   if (xch && p.coll == 0) {  // (MRT: the plain kernel -- same bits)
     if (!step_xch_fits(G, maps)) return cudaErrorInvalidValue;
-    return launch_ws_t<8, false, 0, true>(G, p, A, B, phig, zc, flag, maps, st, pr, wc, xch);
+    return launch_ws_t<8, 0, true>(G, p, A, B, phig, ln, hl, maps, st, pr, xch);
   }
-  if (p.coll == 1) {
-    if (persist)
-      return t8 ? launch_ws_t<8, true, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
-                : launch_ws_t<4, true, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
-    return t8 ? launch_ws_t<8, false, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
-              : launch_ws_t<4, false, 1>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
-  }
-  if (persist)
-    return t8 ? launch_ws_t<8, true, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
-              : launch_ws_t<4, true, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
-  return t8 ? launch_ws_t<8, false, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc)
-            : launch_ws_t<4, false, 0>(G, p, A, B, phig, zc, flag, maps, st, pr, wc);
+  if (p.coll == 1)
+    return t8 ? launch_ws_t<8, 1>(G, p, A, B, phig, ln, hl, maps, st, pr)
+              : launch_ws_t<4, 1>(G, p, A, B, phig, ln, hl, maps, st, pr);
+  return t8 ? launch_ws_t<8, 0>(G, p, A, B, phig, ln, hl, maps, st, pr)
+            : launch_ws_t<4, 0>(G, p, A, B, phig, ln, hl, maps, st, pr);
 }
 
 }  // namespace lbk

@@ -1,6 +1,6 @@
 // lb_tma.cuh -- asynchronous-copy building blocks for the step kernels (sm_90+ PTX):
-// mbarriers, TMA tensor copies with L2 cache hints, cp.async, cluster barriers and
-// distributed shared memory, plus the host-side tensor-map encoder.
+// mbarriers, TMA tensor copies with L2 cache hints, cp.async, gpu-scope relaxed
+// accesses, plus the host-side tensor-map encoder.
 #pragma once
 
 #include <cuda.h>
@@ -45,14 +45,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// TMA 3-D prefetch of a box into L2 (no shared memory, no completion): brings a
-// later plane's data on chip while the current plane is being processed.
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
-               "r"(c2)
-               : "memory");
-}
-
 // L2 policies
 __device__ __forceinline__ unsigned long long policy_evict_first() {
   unsigned long long p;
@@ -93,39 +85,18 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// a strong (gpu-scope) load that bypasses L1: another CTA's store is seen once it
-// reaches L2 (the phi exchange)
+// The phi exchange between CTAs of one launch: relaxed gpu-scope (strong) loads and
+// stores, so a value one CTA publishes and another reads is not a data race under
+// the PTX memory model (an aligned 64-bit strong access is single-copy atomic: the
+// reader sees the old or the new value, never a mix).  No ordering is needed --
+// the value is its own flag (kXchEmpty).
 __device__ __forceinline__ double ld_relaxed_f64(const double* a) {
   double v;
   asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(a) : "memory");
   return v;
 }
-
-// thread-block clusters: rank, barrier, distributed shared memory
-__device__ __forceinline__ unsigned cluster_ctarank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Cluster barrier for shared-memory hand-offs only: the caller has already made
-// its shared-memory writes complete CTA-wide (bar.sync), so the arrive is relaxed
-// -- a release here would also wait for every outstanding global store.
-__device__ __forceinline__ void cluster_sync_smem() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// shared::cluster address of `local` (a shared-memory variable) in CTA `rank`
-__device__ __forceinline__ unsigned dsmem_addr(const void* local, unsigned rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ double ld_dsmem(unsigned addr) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-  return v;
+__device__ __forceinline__ void st_relaxed_f64(double* a, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
 }
 
 // f / g components in slot order (d3q19.cuh): three contiguous runs each

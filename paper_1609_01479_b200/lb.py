@@ -57,8 +57,9 @@ _lb_local_sites = _sig("lb_local_sites", C.c_size_t, _vp)
 _lb_set_state = _sig("lb_set_state", _i, _vp, _vp, _vp)
 _lb_init_equilibrium = _sig("lb_init_equilibrium", _i, _vp, _vp, _vp, _vp)
 _lb_step = _sig("lb_step", _i, _vp, _i)
+_lb_prepare = _sig("lb_prepare", _i, _vp)
 _lb_debug_stream = _sig("lb_debug_stream", _i, _vp, _i)
-_lb_debug_step_probe = _sig("lb_debug_step_probe", _i, _vp, _i, _i)
+_lb_debug_tune = _sig("lb_debug_tune", _i, _vp, _i, _i)
 _lb_debug_step_kernel = _sig("lb_debug_step_kernel", _i, _vp, _i)
 _lb_get_state = _sig("lb_get_state", _i, _vp, _vp, _vp)
 _lb_get_phi = _sig("lb_get_phi", _i, _vp, _vp)
@@ -74,7 +75,7 @@ _lb_bytes_per_site = _sig("lb_bytes_per_site", C.c_double)
 _lb_debug_propagation_map = _sig("lb_debug_propagation_map", _i, _i, _i, _i, _i, _vp)
 _lb_debug_propagation_map_peers = _sig("lb_debug_propagation_map_peers", _i, _i, _i, _i, _i, _vp)
 _lb_debug_halo_mode = _sig("lb_debug_halo_mode", _i, _vp, _i)
-_lb_debug_xch_bands = _sig("lb_debug_xch_bands", _i, _i, _i, _i, _i, _i, _i, C.POINTER(_i), _vp, _i)
+_lb_debug_tile_order = _sig("lb_debug_tile_order", _i, _i, _i, _i, _i, _i, _vp)
 _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
 _lb_set_collision = _sig("lb_set_collision", _i, _vp, _i, C.c_double, C.c_double, C.c_double)
 _lb_create_ch = _sig("lb_create_ch", _i, _i, _i, _i, C.POINTER(lb_params), C.c_double, C.c_double, C.c_double,
@@ -101,10 +102,10 @@ _lb_init_lc = _sig("lb_init_lc", _i, _vp, _vp, _vp, _vp)
 
 EXPORTS = [
     "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
-    "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_debug_stream", "lb_debug_step_probe", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
+    "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_prepare", "lb_debug_stream", "lb_debug_tune", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
-    "lb_debug_halo_mode", "lb_debug_xch_bands", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_create_ch_loopback", "lb_create_ch_slab", "lb_set_state_ch",
+    "lb_debug_halo_mode", "lb_debug_tile_order", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_create_ch_loopback", "lb_create_ch_slab", "lb_set_state_ch",
     "lb_get_state_ch",
     "lb_create_lc", "lb_create_lc_loopback", "lb_create_lc_slab", "lb_set_state_lc", "lb_get_state_lc", "lb_init_lc",
 ]
@@ -182,6 +183,10 @@ def lb_step(h, nsteps: int) -> None:
     _check(_lb_step(h, nsteps), h)
 
 
+def lb_prepare(h) -> None:
+    _check(_lb_prepare(h), h)
+
+
 def lb_debug_stream(h, nsteps: int) -> None:
     _check(_lb_debug_stream(h, nsteps), h)
 
@@ -190,8 +195,12 @@ def lb_debug_step_kernel(h, which: int) -> None:
     _check(_lb_debug_step_kernel(h, which), h)
 
 
-def lb_debug_step_probe(h, nsteps: int, mode: int) -> None:
-    _check(_lb_debug_step_probe(h, nsteps, mode), h)
+# lb_debug_tune keys (include/lb.h)
+LB_TUNE_ZCHUNK, LB_TUNE_BAND_ROWS, LB_TUNE_RESID, LB_TUNE_GRAPHS = 1, 2, 3, 4
+
+
+def lb_debug_tune(h, key: int, value: int) -> None:
+    _check(_lb_debug_tune(h, key, value), h)
 
 
 def lb_get_state(h, f=None, g=None):
@@ -263,15 +272,12 @@ def lb_debug_propagation_map_peers(nx: int, ny: int, nz: int, nslabs: int = 1) -
     return out.reshape(Q, nz, ny, nx)
 
 
-def lb_debug_xch_bands(nx: int, ny: int, nz: int, zc: int, num_sms: int, band: int = -1):
-    """(band, xy offsets the pre-pass of the banded phi exchange sums) -- host-only."""
-    b = C.c_int(0)
-    n = _lb_debug_xch_bands(nx, ny, nz, zc, num_sms, band, C.byref(b), None, 0)
-    if n < 0:
-        raise LBError(n, "lb_debug_xch_bands: bad sizes")
-    out = np.empty(max(n, 1), dtype=np.int32)
-    n = _lb_debug_xch_bands(nx, ny, nz, zc, num_sms, band, C.byref(b), out.ctypes.data, n)
-    return b.value, out[:n]
+def lb_debug_tile_order(ntx: int, nty: int, nch: int, resid: int, band: int = 1) -> np.ndarray:
+    out = np.empty((ntx * nty * nch, 3), dtype=np.int32)
+    rc = _lb_debug_tile_order(ntx, nty, nch, resid, band, out.ctypes.data)
+    if rc != LB_OK:
+        raise LBError(rc, "lb_debug_tile_order: bad arguments")
+    return out
 
 
 def lb_set_collision(h, model: int, tau_shear: float = 0.8, tau_bulk: float = 1.0, tau_ghost: float = 1.0) -> None:

@@ -14,7 +14,7 @@ int main(int argc, char** argv) {
     const int n = ntx * nty * nch;
     std::vector<int> seen(n, 0), pos(n, -1);
     for (int L = 0; L < n; ++L) {
-      const lbk::TileId t = lbk::tile_of_block(L, ntx, nty, nch, resid);
+      const lbk::TileId t = lbk::tile_of_block(L, ntx, nty, nch, lbk::TileOrder{resid, 1});
       if (t.bx < 0 || t.bx >= ntx || t.by < 0 || t.by >= nty || t.bz < 0 || t.bz >= nch) {
         printf("out of range: L=%d -> (%d,%d,%d) for %d %d %d %d\n", L, t.bx, t.by, t.bz, ntx, nty, nch, resid);
         return 1;

@@ -113,41 +113,25 @@ def test_halo_plan_ring(nranks):
         lb.lb_halo_plan(16, 12, 33, 2, 0)
 
 
-def _brute_xch_pre(nx, ny, band):
-    """Sites some band takes as phi halo from a later band, by the definition: walk
-    every tile (32 x 8, row-major, band = tile // band) and its 2-site ring."""
-    ntx = nx // 32
-    owner = lambda x, y: ((y % ny) // 8 * ntx + (x % nx) // 32) // band  # noqa: E731
-    need = set()
-    for t in range(ntx * (ny // 8)):
-        x0, y0, b = (t % ntx) * 32, (t // ntx) * 8, t // band
-        for y in range(y0 - 2, y0 + 10):
-            for x in range(x0 - 2, x0 + 34):
-                if owner(x, y) > b:
-                    need.add((y % ny) * nx + x % nx)
-    return sorted(need)
 
 
-@pytest.mark.parametrize("nx,ny,band", [(128, 48, 5), (128, 48, 1), (128, 48, 4), (96, 40, 7), (512, 64, 16),
-                                        (64, 32, 3), (32, 16, 1)])
-def test_xch_prepass_sites_brute_force(nx, ny, band):
-    """The pre-pass of the banded phi exchange (host-built site list, lb_step_ws.cu
-    ws_xch_pre_sites: the 4 corners of the 5 x 5 window) covers exactly the halo
-    sites a band takes from later bands -- brute force over every tile's 2-ring,
-    including the periodic wrap in x and y and bands that split tile rows."""
-    b, sites = lb.lb_debug_xch_bands(nx, ny, 8, 8, 148, band)
-    assert b == band
-    assert sites.tolist() == _brute_xch_pre(nx, ny, band)
-
-
-def test_xch_automatic_bands():
-    """Automatic bands: none where tiles x z-chunks fit one wave, else equal bands of
-    whole tile rows that fit 148 CTAs (512 x 512 x 64: 8 bands of 8 rows = 128)."""
-    assert lb.lb_debug_xch_bands(128, 128, 128, 64, 148)[0] == 0
-    assert lb.lb_debug_xch_bands(512, 512, 64, 32, 148)[0] == 128
-    assert lb.lb_debug_xch_bands(512, 304, 16, 16, 148)[0] == 128
-    assert lb.lb_debug_xch_bands(256, 256, 32, 32, 148)[0] == 128
-    b, sites = lb.lb_debug_xch_bands(512, 512, 64, 32, 148)
-    assert len(sites) == 8 * 2 * 512  # two rows below each band boundary, and above band 0
-    with pytest.raises(lb.LBError):
-        lb.lb_debug_xch_bands(100, 64, 8, 8, 148)
+@pytest.mark.parametrize("ntx,nty,nch,resid,band", [(16, 64, 2, 148, 1), (16, 64, 2, 148, 4), (16, 19, 3, 40, 4),
+                                                    (5, 7, 1, 148, 3), (16, 64, 2, 148, 64), (3, 2, 4, 1, 2)])
+def test_tile_order_is_a_permutation(ntx, nty, nch, resid, band):
+    """lb_debug_tile_order (the kernels' tile_of_block): every (tile, z-chunk) once;
+    chunk c of a tile after chunk c-1; with bands, consecutive blocks of a band
+    walk its rows column by column (y neighbours adjacent in launch order)."""
+    o = lb.lb_debug_tile_order(ntx, nty, nch, resid, band)
+    keys = {tuple(r) for r in o.tolist()}
+    assert len(keys) == ntx * nty * nch == len(o)
+    assert all(0 <= bx < ntx and 0 <= by < nty and 0 <= bz < nch for bx, by, bz in keys)
+    pos = {tuple(r): i for i, r in enumerate(o.tolist())}
+    for (bx, by, bz), i in pos.items():
+        if bz > 0:
+            assert pos[(bx, by, bz - 1)] < i
+    if band > 1 and nty % band == 0 and resid >= ntx * nty:
+        # first group, chunk 0: rows of a band interleave
+        assert o[0].tolist() == [0, 0, 0] and o[1].tolist() == [0, 1, 0]
+        assert o[band].tolist() == [1, 0, 0]
+    if band == 1 and resid >= ntx:
+        assert o[1].tolist() == [1 % ntx, 1 // ntx, 0]

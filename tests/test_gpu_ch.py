@@ -111,7 +111,7 @@ def test_ch_init_equilibrium_and_errors():
         assert np.array_equal(p1, phi)
         assert rel(f1, R.f_equilibrium(np.ones_like(phi), np.zeros((3,) + phi.shape))) <= 1e-15
         for call in (lambda: lb.lb_get_state(L.h), lambda: lb.lb_set_collision(L.h, 1),
-                     lambda: lb.lb_debug_step_kernel(L.h, 3), lambda: lb.lb_debug_step_probe(L.h, 1, 1)):
+                     lambda: lb.lb_debug_step_kernel(L.h, 2)):
             with pytest.raises(lb.LBError) as e:
                 call()
             assert e.value.code == lb.LB_EINVAL

@@ -163,7 +163,7 @@ def test_lc_errors():
             assert e.value.code == lb.LB_ESTATE
         L.set_state(*rough(16, 8, 8))
         for call in (lambda: lb.lb_get_state(L.h), lambda: lb.lb_get_phi(L.h), lambda: lb.lb_set_collision(L.h, 1),
-                     lambda: lb.lb_debug_step_kernel(L.h, 3), lambda: lb.lb_debug_step_probe(L.h, 1, 1),
+                     lambda: lb.lb_debug_step_kernel(L.h, 2),
                      lambda: lb.lb_init_equilibrium(L.h, None, None, np.zeros(16 * 8 * 8))):
             with pytest.raises(lb.LBError) as e:
                 call()

@@ -84,10 +84,10 @@ def test_mrt_parity_64cubed_10_steps():
 
 @pytest.mark.parametrize("shape", [(16, 16, 16), (34, 10, 7), (64, 64, 16)])
 def test_mrt_kernels_bitwise_equal(shape):
-    """Tile, warp-specialised and persistent kernels share collide_mrt: same bits."""
+    """Tile and warp-specialised kernels share collide_mrt: same bits."""
     f, g = rough(*shape, seed=33)
     a = gpu_run(f, g, MP, 3, kernel=1)
-    for k in (3, 4):
+    for k in (2,):
         b = gpu_run(f, g, MP, 3, kernel=k)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
@@ -95,7 +95,7 @@ def test_mrt_kernels_bitwise_equal(shape):
 def test_mrt_32x8_tiles_bitwise_and_parity():
     """The bench's 32 x 8 tile shape (plane with >= 4 x 148 tiles), two z-chunks."""
     f, g = spinodal(512, 304, 16, seed=34)
-    a = gpu_run(f, g, MP, 1, kernel=3)
+    a = gpu_run(f, g, MP, 1, kernel=2)
     b = gpu_run(f, g, MP, 1, kernel=1)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
@@ -104,7 +104,7 @@ def test_mrt_32x8_tiles_bitwise_and_parity():
 def test_mrt_slabs_bitwise(nslabs, halo):
     f, g = rough(32, 16, 16, seed=35)
     a = gpu_run(f, g, MP, 4, nslabs=1, kernel=1)
-    b = gpu_run(f, g, MP, 4, nslabs=nslabs, kernel=3, halo=halo)
+    b = gpu_run(f, g, MP, 4, nslabs=nslabs, kernel=2, halo=halo)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
@@ -143,10 +143,6 @@ def test_mrt_set_collision_errors_and_model_switch():
         f1, g1 = L.get_state()
     f0, g0 = R.run(f, g, P0, 2)
     assert rel(f1, f0) <= TOL and rel(g1, g0) <= TOL
-    with lb.Lattice(64, 16, 8) as L:
-        lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
-        with pytest.raises(lb.LBError):
-            lb.lb_debug_step_kernel(L.h, 2)  # the cluster kernel is model 0 only
 
 
 def test_mrt_parity_bench_launch_sampled():

@@ -36,14 +36,17 @@ def rough(nx, ny, nz, seed=1, p=P0):
     return f + nf, g + ng
 
 
-def gpu_run(f, g, p, nsteps, nslabs=1, kernel=0, halo=None):
-    """kernel: 0 default, 1 tile, 2 cluster, 3 warp-specialised, 4 persistent warp-specialised (lb_debug_step_kernel);
-    halo: None default, 0 exchange, 1 peer (fused) transport between slabs (lb_debug_halo_mode)."""
+def gpu_run(f, g, p, nsteps, nslabs=1, kernel=0, halo=None, tune=None):
+    """kernel: 0 default, 1 tile, 2 warp-specialised, 3 warp-specialised with the phi exchange
+    (lb_debug_step_kernel); halo: None default, 0 exchange, 1 peer (fused) transport between
+    slabs (lb_debug_halo_mode); tune: {key: value} of lb_debug_tune."""
     nz, ny, nx = f.shape[1:]
     with lb.Lattice(nx, ny, nz, cparams(p), nslabs=nslabs) as L:
         lb.lb_debug_step_kernel(L.h, kernel)
         if halo is not None:
             lb.lb_debug_halo_mode(L.h, halo)
+        for k, v in (tune or {}).items():
+            lb.lb_debug_tune(L.h, k, v)
         L.set_state(f, g)
         L.step(nsteps)
         return L.get_state()
@@ -165,36 +168,6 @@ def test_parity_full_size_sampled(nx, ny, nz):
     assert rel(np.array(gs), np.array(gr)) <= TOL
 
 
-# ------------------------------------------------------------------ the cluster step kernel
-@pytest.mark.parametrize("shape", [(64, 16, 8), (128, 32, 12), (64, 48, 5), (192, 16, 3)])
-def test_cluster_kernel_parity_and_bitwise_equal_to_tile_kernel(shape):
-    """lb_step_cluster.cu (phi halos through distributed shared memory) gives the same
-    bits as the tile kernel and meets the parity tolerance against the oracle."""
-    nx, ny, nz = shape
-    f, g = rough(nx, ny, nz, seed=12)
-    a = gpu_run(f, g, P0, 4, kernel=2)
-    b = gpu_run(f, g, P0, 4, kernel=1)
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-    assert_parity(a, R.run(f, g, P0, 4))
-
-
-@pytest.mark.parametrize("nslabs", [2, 4])
-def test_cluster_kernel_slabs_bitwise(nslabs):
-    f, g = rough(64, 16, 16, seed=13)
-    a = gpu_run(f, g, P0, 5, nslabs=1, kernel=2)
-    b = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=2)
-    c = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=1)
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-    assert np.array_equal(a[0], c[0]) and np.array_equal(a[1], c[1])
-
-
-def test_cluster_kernel_rejects_unfit_lattice():
-    with lb.Lattice(24, 16, 8) as L:
-        with pytest.raises(lb.LBError) as e:
-            lb.lb_debug_step_kernel(L.h, 2)
-        assert e.value.code == lb.LB_EINVAL
-
-
 # ------------------------------------------------------------------ the warp-specialised step kernel
 @pytest.mark.parametrize("shape", [(16, 16, 16), (24, 20, 18), (34, 10, 7), (64, 64, 16), (4, 31, 6)])
 def test_ws_kernel_parity_and_bitwise_equal_to_tile_kernel(shape):
@@ -203,9 +176,9 @@ def test_ws_kernel_parity_and_bitwise_equal_to_tile_kernel(shape):
     tolerance against the oracle."""
     nx, ny, nz = shape
     f, g = rough(nx, ny, nz, seed=14)
-    a = gpu_run(f, g, P0, 4, kernel=3)
+    a = gpu_run(f, g, P0, 4, kernel=2)
     b = gpu_run(f, g, P0, 4, kernel=1)
-    c = gpu_run(f, g, P0, 4, kernel=4)  # persistent CTAs
+    c = gpu_run(f, g, P0, 4, kernel=2, tune={lb.LB_TUNE_BAND_ROWS: 3})  # another block order
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert np.array_equal(c[0], b[0]) and np.array_equal(c[1], b[1])
     assert_parity(a, R.run(f, g, P0, 4))
@@ -217,10 +190,10 @@ def test_ws_kernel_32x8_tiles_and_z_chunks():
     brute-force oracle."""
     nx, ny, nz = 512, 304, 16
     f, g = spinodal(nx, ny, nz, seed=15)
-    a = gpu_run(f, g, P0, 1, kernel=3)
+    a = gpu_run(f, g, P0, 1, kernel=2)
     b = gpu_run(f, g, P0, 1, kernel=1)
-    c = gpu_run(f, g, P0, 2, kernel=4)
-    d = gpu_run(f, g, P0, 2, kernel=3)
+    c = gpu_run(f, g, P0, 2, kernel=2, tune={lb.LB_TUNE_BAND_ROWS: 4, lb.LB_TUNE_ZCHUNK: 5})
+    d = gpu_run(f, g, P0, 2, kernel=2)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert np.array_equal(c[0], d[0]) and np.array_equal(c[1], d[1])
     smp = BR.SiteSampler(f, g, P0)
@@ -237,29 +210,44 @@ def test_ws_kernel_32x8_tiles_and_z_chunks():
 def test_ws_kernel_slabs_bitwise(nslabs):
     f, g = rough(32, 16, 16, seed=16)
     a = gpu_run(f, g, P0, 5, nslabs=1, kernel=1)
-    b = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=3)
+    b = gpu_run(f, g, P0, 5, nslabs=nslabs, kernel=2)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-# ------------------------------------------------------------------ the phi exchange (kernel 5)
-def gpu_run_zc(f, g, p, nsteps, kernel, zchunk=None, coll=None):
-    """gpu_run with an optional z-chunk override (LB_ZCHUNK, read at lb_create) and
-    collision model (lb_set_collision)."""
-    import os
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("band", [2, 4, 7])
+def test_block_order_bands_bitwise(kernel, band):
+    """The block order (tiles walked in bands of tile rows, column by column;
+    lb_debug_tune LB_TUNE_BAND_ROWS) changes only when a tile runs, not what it
+    computes: bitwise equal to row-major order, including a partial last band
+    (ny / 8 = 19 tile rows) and several z-chunks."""
+    nx, ny, nz = 128, 152, 12
+    f, g = rough(nx, ny, nz, seed=26)
+    a = gpu_run(f, g, P0, 3, kernel=kernel, tune={lb.LB_TUNE_BAND_ROWS: band, lb.LB_TUNE_ZCHUNK: 4,
+                                                  lb.LB_TUNE_RESID: 40})
+    b = gpu_run(f, g, P0, 3, kernel=kernel)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
+
+def test_tune_errors_and_graphs_off():
+    f, g = rough(32, 12, 10, seed=27)
+    a = gpu_run(f, g, P0, 17, tune={lb.LB_TUNE_GRAPHS: 0})
+    b = gpu_run(f, g, P0, 17)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    with lb.Lattice(8, 8, 8) as L:
+        for key, val in [(99, 1), (lb.LB_TUNE_ZCHUNK, -1), (lb.LB_TUNE_BAND_ROWS, 0), (lb.LB_TUNE_RESID, -2)]:
+            with pytest.raises(lb.LBError) as e:
+                lb.lb_debug_tune(L.h, key, val)
+            assert e.value.code == lb.LB_EINVAL
+
+
+# ------------------------------------------------------------------ the phi exchange (kernel 3)
+def gpu_run_zc(f, g, p, nsteps, kernel, zchunk=None, coll=None):
+    """gpu_run with an optional z-chunk (lb_debug_tune) and collision model (lb_set_collision)."""
     nz, ny, nx = f.shape[1:]
-    old = os.environ.get("LB_ZCHUNK")
-    if zchunk:
-        os.environ["LB_ZCHUNK"] = str(zchunk)
-    try:
-        L = lb.Lattice(nx, ny, nz, cparams(p))
-    finally:
+    with lb.Lattice(nx, ny, nz, cparams(p)) as L:
         if zchunk:
-            if old is None:
-                del os.environ["LB_ZCHUNK"]
-            else:
-                os.environ["LB_ZCHUNK"] = old
-    with L:
+            lb.lb_debug_tune(L.h, lb.LB_TUNE_ZCHUNK, zchunk)
         lb.lb_debug_step_kernel(L.h, kernel)
         if coll is not None:
             lb.lb_set_collision(L.h, 1, *coll)
@@ -280,30 +268,11 @@ def test_xch_kernel_bitwise_equal_to_ws_kernel(shape, zchunk):
     nx, ny, nz = shape
     steps = 20 if nx * ny * nz <= 200_000 else 3
     f, g = rough(nx, ny, nz, seed=21)
-    a = gpu_run_zc(f, g, P0, steps, kernel=5, zchunk=zchunk)
-    b = gpu_run_zc(f, g, P0, steps, kernel=3)
+    a = gpu_run_zc(f, g, P0, steps, kernel=3, zchunk=zchunk)
+    b = gpu_run_zc(f, g, P0, steps, kernel=2)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     if nx * ny * nz <= 40_000:
         assert_parity(a, R.run(f, g, P0, steps))
-
-
-@pytest.mark.parametrize("shape,band,kernel", [((128, 48, 32), 5, 5), ((128, 48, 8), 1, 5), ((512, 304, 16), 37, 0),
-                                                ((512, 304, 16), 0, 5), ((512, 512, 24), None, 5)])
-def test_xch_bands_bitwise(shape, band, kernel, monkeypatch):
-    """The banded phi exchange (one launch per band of tiles, each band one wave; a
-    halo site of a later band is summed from g, one of an earlier band read from its
-    store) gives the bits of kernel 3 for bands that are not whole tile rows, bands
-    of one tile (every halo site summed from g), the default kernel taking the bands
-    (LB_XCH_BAND > 0), LB_XCH_BAND = 0 (one launch over several waves) and the
-    automatic bands (9 tile rows; the last band of one row cut into 3 z-chunks)."""
-    nx, ny, nz = shape
-    f, g = rough(nx, ny, nz, seed=29)
-    if band is not None:
-        monkeypatch.setenv("LB_XCH_BAND", str(band))
-    a = gpu_run(f, g, P0, 4, kernel=kernel)
-    monkeypatch.delenv("LB_XCH_BAND", raising=False)
-    b = gpu_run(f, g, P0, 4, kernel=3)
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
 def test_xch_is_default_for_one_wave():
@@ -314,23 +283,23 @@ def test_xch_is_default_for_one_wave():
         nx, ny, nz = shape
         f, g = rough(nx, ny, nz, seed=23)
         a = gpu_run(f, g, P0, 2, kernel=0)
-        b = gpu_run(f, g, P0, 2, kernel=3)
+        b = gpu_run(f, g, P0, 2, kernel=2)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
 def test_xch_after_other_kernels_bitwise():
-    """Steps of the phi exchange interleaved with steps that do not use it (kernel 3,
-    the MRT collision, a probe) must not read stale phi from the exchange arrays:
-    the same bits as kernel 3 throughout."""
+    """Steps of the phi exchange interleaved with steps that do not use it (kernel 2,
+    the MRT collision) must not read stale phi from the exchange arrays: the same
+    bits as kernel 2 throughout."""
     f, g = rough(64, 32, 16, seed=24)
     mp = (0.8, 1.1, 1.0)
     with lb.Lattice(64, 32, 16, cparams(P0)) as L:
         L.set_state(f, g)
-        lb.lb_debug_step_kernel(L.h, 5)
-        L.step(10)
         lb.lb_debug_step_kernel(L.h, 3)
+        L.step(10)
+        lb.lb_debug_step_kernel(L.h, 2)
         L.step(1)
-        lb.lb_debug_step_kernel(L.h, 5)
+        lb.lb_debug_step_kernel(L.h, 3)
         L.step(3)
         lb.lb_set_collision(L.h, 1, *mp)
         L.step(1)
@@ -339,7 +308,7 @@ def test_xch_after_other_kernels_bitwise():
         a = L.get_state()
     with lb.Lattice(64, 32, 16, cparams(P0)) as L:
         L.set_state(f, g)
-        lb.lb_debug_step_kernel(L.h, 3)
+        lb.lb_debug_step_kernel(L.h, 2)
         L.step(14)
         lb.lb_set_collision(L.h, 1, *mp)
         L.step(1)
@@ -349,36 +318,11 @@ def test_xch_after_other_kernels_bitwise():
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-def test_xch_after_mrt_bands_of_one_tile(monkeypatch):
-    """Deterministic form of the test above: with bands of one tile and no pre-pass
-    (LB_XCH_PRE=0) every tile reads the phi of the tiles after it BEFORE their
-    launch, so an exchange array still holding the phi of two steps ago (an MRT
-    step counted as an exchange step) is read, not overwritten in time.  The same
-    bits as kernel 3."""
-    f, g = rough(64, 32, 16, seed=25)
-    mp = (0.8, 1.1, 1.0)
-    monkeypatch.setenv("LB_XCH_BAND", "1")
-    monkeypatch.setenv("LB_XCH_PRE", "0")
-    states = []
-    for kernel in (5, 3):
-        with lb.Lattice(64, 32, 16, cparams(P0)) as L:
-            L.set_state(f, g)
-            lb.lb_debug_step_kernel(L.h, kernel)
-            L.step(3)
-            lb.lb_set_collision(L.h, 1, *mp)
-            L.step(1)
-            lb.lb_set_collision(L.h, 0)
-            L.step(4)
-            states.append(L.get_state())
-    (a, b) = states
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-
-
 def test_xch_kernel_mrt_bitwise():
     f, g = rough(64, 32, 10, seed=22)
     mp = (0.8, 1.1, 1.0)
-    a = gpu_run_zc(f, g, P0, 9, kernel=5, coll=mp)
-    b = gpu_run_zc(f, g, P0, 9, kernel=3, coll=mp)
+    a = gpu_run_zc(f, g, P0, 9, kernel=3, coll=mp)
+    b = gpu_run_zc(f, g, P0, 9, kernel=2, coll=mp)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
@@ -387,15 +331,19 @@ def test_xch_kernel_rejects_unfit_lattice(shape, nslabs):
     nx, ny, nz = shape
     with lb.Lattice(nx, ny, nz, nslabs=nslabs) as L:
         with pytest.raises(lb.LBError) as e:
-            lb.lb_debug_step_kernel(L.h, 5)
+            lb.lb_debug_step_kernel(L.h, 3)
         assert e.value.code == lb.LB_EINVAL
 
 
 def test_ws_kernel_rejects_odd_nx():
     with lb.Lattice(7, 16, 8) as L:
         with pytest.raises(lb.LBError) as e:
-            lb.lb_debug_step_kernel(L.h, 3)
+            lb.lb_debug_step_kernel(L.h, 2)
         assert e.value.code == lb.LB_EINVAL
+        for bad in (4, 5, -1):  # (removed kernels)
+            with pytest.raises(lb.LBError) as e:
+                lb.lb_debug_step_kernel(L.h, bad)
+            assert e.value.code == lb.LB_EINVAL
 
 
 # ------------------------------------------------------------------ fused (peer) halo transport
@@ -407,14 +355,14 @@ def test_loopback_defaults_to_fused_halo():
             lb.lb_debug_halo_mode(L.h, 1)  # one periodic slab has no halo
 
 
-@pytest.mark.parametrize("kernel", [1, 3, 4])
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("shape,nslabs", [((12, 10, 16), 2), ((32, 16, 16), 4), ((34, 9, 12), 3), ((7, 5, 8), 4)])
 def test_fused_halo_bitwise_equal_to_exchange_and_one_slab(kernel, shape, nslabs):
     """The step kernel storing the leaving components straight into the neighbour
     slab's buffer (and K_phi into its phi ghost planes) gives the same bits as the
     ghost-plane + exchange transport and as the undecomposed lattice."""
     nx, ny, nz = shape
-    if kernel in (3, 4) and nx % 2:
+    if kernel == 2 and nx % 2:
         pytest.skip("warp-specialised kernel needs nx even")
     f, g = rough(nx, ny, nz, seed=17)
     ref = gpu_run(f, g, P0, 5, nslabs=1, kernel=1)
@@ -424,7 +372,7 @@ def test_fused_halo_bitwise_equal_to_exchange_and_one_slab(kernel, shape, nslabs
         assert np.array_equal(a[0], ref[0]) and np.array_equal(a[1], ref[1])
 
 
-def test_fused_halo_cluster_kernel_and_stream_only():
+def test_fused_halo_ws_kernel_and_stream_only():
     f, g = rough(64, 16, 16, seed=18)
     a = gpu_run(f, g, P0, 3, nslabs=2, kernel=2, halo=1)
     b = gpu_run(f, g, P0, 3, nslabs=1, kernel=1)
@@ -494,21 +442,70 @@ def test_conservation_64cubed_1000_steps():
 
 
 # ------------------------------------------------------------------ errors
-def test_numeric_error_flag():
+@pytest.mark.parametrize("kernel,nslabs", [(0, 1), (1, 1), (2, 1), (0, 2)])
+def test_numeric_error_flag(kernel, nslabs):
+    """R22: rho <= 0 or a non-finite value -> LB_ENUMERIC naming the global
+    site and the step (the first offending one of the call)."""
     f, g = rough(8, 8, 8)
-    f[:, 3, 2, 1] = 0.0  # rho = 0 at one site
-    with lb.Lattice(8, 8, 8) as L:
+    f[:, 6, 2, 1] = 0.0  # rho = 0 at (x=1, y=2, z=6): in the second slab of two
+    with lb.Lattice(8, 8, 8, nslabs=nslabs) as L:
+        lb.lb_debug_step_kernel(L.h, kernel)
         L.set_state(f, g)
         with pytest.raises(lb.LBError) as e:
             L.step(1)
         assert e.value.code == lb.LB_ENUMERIC
-    g[5, 1, 1, 1] = np.nan
-    f[:, 3, 2, 1] = 1.0 / 19
-    with lb.Lattice(8, 8, 8) as L:
+        assert "(x=1, y=2, z=6)" in str(e.value) and "step 0 of this call" in str(e.value), str(e.value)
+    f, g = rough(8, 8, 8)
+    g[5, 1, 1, 1] = np.nan  # NaN in a moving g: pushed on to (x+cx, y+cy, z+cz) and spreading
+    with lb.Lattice(8, 8, 8, nslabs=nslabs) as L:
+        lb.lb_debug_step_kernel(L.h, kernel)
+        L.set_state(f, g)
+        L.step(0)
+        with pytest.raises(lb.LBError) as e:
+            L.step(12)  # (graph replays)
+        assert e.value.code == lb.LB_ENUMERIC
+        assert "(x=1, y=1, z=1)" in str(e.value) and "step 0 of this call" in str(e.value), str(e.value)
+
+
+@pytest.mark.parametrize("pre", [0, 2])
+def test_numeric_error_names_later_step(pre):
+    """A state that goes bad only in step 1: tau_f = 1 and no force (A = B = kappa
+    = 0), rest everywhere except one dense, fast site (rho = 1000, u = (0.3, 0.7, 0))
+    whose equilibrium components with c.u = -0.3 or -0.4 are negative (e.g. c =
+    (-1, 0, 0): w rho (1 - 0.9 + 0.405 - 0.87) < 0); pushed to the neighbours they
+    make rho < 0 there in the next step.  The report names the smallest such site,
+    (x0-1, y0, z0-1) -- the site the oracle's R22 error names for the same state --
+    and step 1, counted from the call's first step (after `pre` clean steps)."""
+    p = R.Params(tau_f=1.0, A=0.0, B=0.0, kappa=0.0)
+    n = 10
+    rho = np.ones((n, n, n))
+    u = np.zeros((3, n, n, n))
+    x0, y0, z0 = 5, 4, 6
+    f, g = R.equilibrium_state(rho, u, np.zeros((n, n, n)), p)
+    rho[z0, y0, x0] = 1000.0
+    u[0, z0, y0, x0] = 0.3
+    u[1, z0, y0, x0] = 0.7
+    fd, _ = R.equilibrium_state(rho, u, np.zeros((n, n, n)), p)
+    f[:, z0, y0, x0] = fd[:, z0, y0, x0]
+    for kernel in (0, 1):
+        with lb.Lattice(n, n, n, cparams(p)) as L:
+            lb.lb_debug_step_kernel(L.h, kernel)
+            L.set_state(f, g)
+            with pytest.raises(lb.LBError) as e:
+                L.step(3)
+            msg = str(e.value)
+            assert e.value.code == lb.LB_ENUMERIC
+            assert f"(x={x0 - 1}, y={y0}, z={z0 - 1})" in msg and "step 1 of this call" in msg, msg
+    # after `pre` clean rest steps elsewhere: the count is per call
+    with lb.Lattice(n, n, n, cparams(p)) as L:
+        L.set_state(*R.equilibrium_state(np.ones((n, n, n)), np.zeros((3, n, n, n)), np.zeros((n, n, n)), p))
+        L.step(pre)
         L.set_state(f, g)
         with pytest.raises(lb.LBError) as e:
             L.step(2)
-        assert e.value.code == lb.LB_ENUMERIC
+        assert "step 1 of this call" in str(e.value) and f"(step {pre + 1} since" in str(e.value), str(e.value)
+        L.set_state(*R.equilibrium_state(np.ones((n, n, n)), np.zeros((3, n, n, n)), np.zeros((n, n, n)), p))
+        L.step(9)  # clean again: the flag was reset
 
 
 def test_state_errors_and_zero_steps():
