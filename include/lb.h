@@ -95,6 +95,19 @@ int lb_create_slab(int nx, int ny, int nz, const lb_params* params, int nranks, 
 /* Number of sites this handle's host arrays hold (nloc).  Returns 0 for NULL. */
 size_t lb_local_sites(const lb_t* h);
 
+/* One rank of a z-slab decomposition, bootstrapped by the caller instead of NCCL
+ * (collective over all ranks, like lb_create_slab).  allgather(ctx, send, recv,
+ * bytes) must gather `bytes` host bytes from every rank into recv (nranks * bytes,
+ * rank order) and return 0; it is called during this call, by lb_init_equilibrium
+ * and by lb_step on propagation-only steps, until lb_destroy (the library keeps
+ * fn and ctx).  The halo transport is the peer one (CUDA IPC mappings of the
+ * neighbours' buffers, device-side ordering): if the neighbours' memory cannot be
+ * mapped, LB_ENCCL.  Ranks may share a GPU here (tests), since nothing of this
+ * path needs one communicator rank per device. */
+typedef int (*lb_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
+int lb_create_slab_ext(int nx, int ny, int nz, const lb_params* params, int nranks, int rank,
+                       lb_allgather_fn allgather, void* ctx, lb_t** out);
+
 /* Load the state: f, g are host arrays of 19*nloc doubles each, canonical
  * layout.  Bitwise: lb_get_state right after returns exactly these bits. */
 int lb_set_state(lb_t* h, const double* f, const double* g);
@@ -179,8 +192,20 @@ int lb_debug_stream(lb_t* h, int nsteps);
  *   LB_TUNE_RESID     CTAs assumed resident at a time by the block order (0: the
  *                     kernel's occupancy on this device)
  *   LB_TUNE_GRAPHS    0: step without CUDA graphs; 1 (default): graphs of 8 steps
+ *   LB_TUNE_L2_BOX, LB_TUNE_L2_FTILE, LB_TUNE_L2_GTILE
+ *                     L2 eviction policy of the warp-specialised kernel's copies of
+ *                     the g halo box, the f tile and the g tile: 0 evict_normal,
+ *                     1 evict_first, 2 evict_last, 3 evict_unchanged
  * LB_EINVAL for an unknown key or a value out of range. */
-enum { LB_TUNE_ZCHUNK = 1, LB_TUNE_BAND_ROWS = 2, LB_TUNE_RESID = 3, LB_TUNE_GRAPHS = 4 };
+enum {
+  LB_TUNE_ZCHUNK = 1,
+  LB_TUNE_BAND_ROWS = 2,
+  LB_TUNE_RESID = 3,
+  LB_TUNE_GRAPHS = 4,
+  LB_TUNE_L2_BOX = 5,
+  LB_TUNE_L2_FTILE = 6,
+  LB_TUNE_L2_GTILE = 7
+};
 int lb_debug_tune(lb_t* h, int key, int value);
 
 /* ---- NEXT-2 variant: finite-difference Cahn-Hilliard (R29-R33) ----
@@ -291,6 +316,16 @@ int lb_debug_step_kernel(lb_t* h, int which);
  * results.  LB_EINVAL for a single
  * periodic slab or a rank handle without peer mappings. */
 int lb_debug_halo_mode(lb_t* h, int mode);
+
+/* One step in three host-visible phases (test support; peer transport of a slab
+ * handle of the binary fluid): phase 0 = K_phi of the slab edges into the
+ * neighbours' ghost planes, phase 1 = the step kernel, its pushes into the
+ * neighbours and the end-of-step role swap, phase 2 = the lb_step epilogue (wait
+ * for the neighbours' pushes, numerical-domain and timeout report).  Each phase
+ * returns after the device has finished it, so ranks that put a barrier between
+ * phases never have a kernel waiting on another rank's: the device-side waits of
+ * the next phase are already satisfied.  LB_EINVAL for other handles. */
+int lb_debug_step_phase(lb_t* h, int phase);
 
 /* lb_debug_propagation_map for the peer transport: the destinations come from the
  * kernels' own address arithmetic with the neighbouring slabs' buffers (no ghost

@@ -42,6 +42,7 @@ struct Slab {
   double* u2 = nullptr;
   StepMaps lcA{}, lcB{};
   StepMaps mapsA{}, mapsB{};        // TMA descriptors of A and B (swapped with them)
+  unsigned long long* sync = nullptr;  // SW_WORDS sync words of the peer transport (slabs only)
 };
 
 struct Pending {
@@ -66,6 +67,7 @@ struct lb_ctx {
   int zc = 1;             // z-chunk of the step kernel
   int ty = 8;             // tile rows of the step kernel
   TileOrder order{0, 1};  // block order of the step kernels (0: the kernel's occupancy)
+  L2Pol l2{};             // L2 policies of the warp-specialised kernel's copies
   bool graphs_on = true;  // lb_debug_tune(LB_TUNE_GRAPHS)
   bool ch = false;        // NEXT-2 handle: state (f, phi), lb_create_ch
   bool lc = false;        // NEXT-4 handle: state (f, Q, u), lb_create_lc
@@ -89,8 +91,13 @@ struct lb_ctx {
   double* peerA[2] = {nullptr, nullptr};
   double* peerB[2] = {nullptr, nullptr};
   double* peerPhi[2] = {nullptr, nullptr};
+  unsigned long long* peerSync[2] = {nullptr, nullptr};  // the neighbours' sync words
   std::vector<void*> ipc_opened;
   double* d_token = nullptr;  // 4 doubles: NCCL barrier tokens
+  // external bootstrap (lb_create_slab_ext): the caller's all-gather, no NCCL
+  lb_allgather_fn allgather = nullptr;
+  void* allgather_ctx = nullptr;
+  unsigned long long* h_sync = nullptr;  // pinned: SW_ERR of each slab, read by finish()
   bool have_state = false;
   bool broken = false;
   // CUDA graphs of kGraphSteps steps (single process, no per-launch profiling): one
@@ -270,6 +277,13 @@ int alloc_slabs(lb_ctx* h) {
       return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed for the step kernel's TMA descriptors");
   }
   choose_xch(h);
+  if (!h->G.zwrap) {  // sync words of the peer transport, one set per slab
+    for (auto& s : h->slabs) {
+      CK(h, cudaMalloc(&s.sync, SW_WORDS * sizeof(unsigned long long)));
+      CK(h, cudaMemsetAsync(s.sync, 0, SW_WORDS * sizeof(unsigned long long), h->stream));
+    }
+    CK(h, cudaMallocHost(&h->h_sync, h->nslabs * sizeof(unsigned long long)));
+  }
   CK(h, cudaMalloc(&h->d_health, 2 * sizeof(unsigned long long)));
   CK(h, cudaMemsetAsync(h->d_health, 0xff, sizeof(unsigned long long), h->stream));
   CK(h, cudaMemsetAsync(h->d_health + 1, 0, sizeof(unsigned long long), h->stream));
@@ -294,6 +308,7 @@ Launch launch_of(const lb_ctx* h) {
   Launch ln;
   ln.zc = h->zc;
   ln.order = h->order;
+  ln.l2 = h->l2;
   return ln;
 }
 
@@ -404,9 +419,22 @@ int exchange_dist(lb_ctx* h) {
   return LB_OK;
 }
 
+int halo_barrier(lb_ctx* h, int kid);
+
 int exchange_phi(lb_ctx* h) {
   const Geom& G = h->G;
   const size_t cnt = (size_t)2 * G.nxy;
+  if (h->nranks > 1 && !h->comm) {  // external bootstrap: copies into the mapped neighbours' ghost planes
+    if (!h->peerPhi[0] || !h->peerPhi[1]) return set_err(h, LB_EINVAL, "no halo transport on this handle");
+    Slab& s = h->slabs[0];
+    int rc = halo_barrier(h, K_HALO_PHI);  // every rank's phi planes are in place
+    if (rc) return rc;
+    CK(h, cudaMemcpyAsync(h->peerPhi[1] + phi_plane_index(G, -2), s.phi + phi_plane_index(G, G.nzl - 2),
+                          cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->peerPhi[0] + phi_plane_index(G, G.nzl), s.phi + phi_plane_index(G, 0),
+                          cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    return halo_barrier(h, K_HALO_PHI);  // (stream synchronised first) every rank's copies have landed
+  }
   if (h->nranks > 1) {
     Slab& s = h->slabs[0];
     const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
@@ -448,6 +476,9 @@ Peers peers_of(const lb_ctx* h, int r) {
     P.up = h->peerB[1];
     P.phi_dn = h->peerPhi[0];
     P.phi_up = h->peerPhi[1];
+    P.sync = h->slabs[0].sync;
+    P.sync_dn = h->peerSync[0];
+    P.sync_up = h->peerSync[1];
   } else {
     const Slab& dn = h->slabs[(r - 1 + h->nslabs) % h->nslabs];
     const Slab& up = h->slabs[(r + 1) % h->nslabs];
@@ -455,6 +486,9 @@ Peers peers_of(const lb_ctx* h, int r) {
     P.up = up.B;
     P.phi_dn = dn.phi;
     P.phi_up = up.phi;
+    P.sync = h->slabs[r].sync;
+    P.sync_dn = dn.sync;
+    P.sync_up = up.sync;
   }
   return P;
 }
@@ -466,6 +500,13 @@ Peers peers_of(const lb_ctx* h, int r) {
 // visible to the kernels that follow.  Loopback slabs share one stream: no-op.
 int halo_barrier(lb_ctx* h, int kid) {
   if (h->nranks == 1) return LB_OK;
+  if (h->allgather) {  // external bootstrap: the device work so far, then the caller's all-gather as a barrier
+    CK(h, cudaStreamSynchronize(h->stream));
+    const char mine = 1;
+    std::vector<char> all(h->nranks);
+    if (h->allgather(h->allgather_ctx, &mine, all.data(), 1) != 0) return set_err(h, LB_ENCCL, "the caller's all-gather failed");
+    return LB_OK;
+  }
   const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
   cudaError_t ce = timed(h, kid, false, [&]() {
     ncclGroupStart();
@@ -498,6 +539,28 @@ void swap_roles(lb_ctx* h, bool fields = true) {
     }
   }
   for (int k = 0; k < 2; ++k) std::swap(h->peerA[k], h->peerB[k]);
+}
+
+// The step kernel of the binary fluid on one slab.  Default: the warp-specialised
+// kernel for 32 x 8 tiles (large planes), the tile kernel for 32 x 4 tiles (two
+// CTAs per SM) and odd nx; the phi exchange where all blocks
+// run in one wave.
+cudaError_t launch_bgk_step(lb_ctx* h, Slab& s, const Launch& ln, const Health& hl, const Peers& pr) {
+  const Geom& G = h->G;
+  const bool ws = step_ws_fits(&s.mapsA) && (h->kernel_choice >= 2 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
+  // (MRT launches the plain kernel, which leaves the exchange arrays alone: the
+  // step must count as one without the exchange, or the next exchange step would
+  // read the phi of two steps ago where an owner runs behind)
+  const bool xch = ws && h->xphi[0] && h->dp.coll == 0 &&
+                   (h->kernel_choice == 3 || (h->kernel_choice == 0 && h->xch_default)) && step_xch_fits(G, &s.mapsA);
+  h->xch_dirty = !xch;
+  if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
+    const int k = s.A < s.B ? 0 : 1;
+    const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1};
+    return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr, &xa);
+  }
+  if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
+  return launch_step(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
 }
 
 // one timestep on every slab.  Single periodic slab: the fused step alone.
@@ -549,39 +612,26 @@ int one_step(lb_ctx* h, bool stream_only = false) {
       for (int r = 0; r < h->nslabs; ++r) {
         Slab& s = h->slabs[r];
         const Peers pr = peers_of(h, r);
-        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, 2, h->stream, pr); }));
-        CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, G.nzl - 2, G.nzl, h->stream, pr); }));
+        if (peer) {  // edge phi into the neighbours' ghost planes, ordered by the sync words (NEXT-1)
+          CK(h, timed(h, K_PHI, true, [&]() { return launch_phi_edges(G, s.A, s.phi, h->stream, pr, h->num_sms); }));
+        } else {
+          CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, 2, h->stream); }));
+          CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, G.nzl - 2, G.nzl, h->stream); }));
+        }
       }
-      if ((rc = peer ? halo_barrier(h, K_HALO_PHI) : exchange_phi(h))) return rc;
+      if (!peer && (rc = exchange_phi(h))) return rc;
     }
     const Launch ln = launch_of(h);
     for (int r = 0; r < h->nslabs; ++r) {
       Slab& s = h->slabs[r];
       const Peers pr = peers_of(h, r);
       const Health hl = health_of(h, r, r == last);
-      CK(h, timed(h, K_STEP, true, [&]() {
-           // default: the warp-specialised kernel for 32 x 8 tiles (large planes), the
-           // tile kernel for 32 x 4 tiles (two CTAs per SM) and odd nx
-           const bool ws = step_ws_fits(&s.mapsA) &&
-                           (h->kernel_choice >= 2 || (h->kernel_choice == 0 && s.mapsA.ty == 8));
-           // (MRT launches the plain kernel, which leaves the exchange arrays alone:
-           // the step must count as one without the exchange, or the next exchange
-           // step would read the phi of two steps ago where an owner runs behind)
-           const bool xch = ws && h->xphi[0] && h->dp.coll == 0 &&
-                            (h->kernel_choice == 3 || (h->kernel_choice == 0 && h->xch_default)) &&
-                            step_xch_fits(G, &s.mapsA);
-           h->xch_dirty = !xch;
-           if (xch) {  // the two phi buffers alternate with the A/B roles of the state buffers
-             const int k = s.A < s.B ? 0 : 1;
-             const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1};
-             return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr, &xa);
-           }
-           if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
-           return launch_step(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
-         }));
+      CK(h, timed(h, K_STEP, true, [&]() { return launch_bgk_step(h, s, ln, hl, pr); }));
     }
   }
-  if ((rc = peer ? halo_barrier(h, K_HALO_DIST) : exchange_dist(h))) return rc;
+  // peer transport: the step kernels published their pushes (device-side); only
+  // propagation-only steps between ranks (test support) order by a host barrier
+  if ((rc = peer ? (stream_only ? halo_barrier(h, K_HALO_DIST) : LB_OK) : exchange_dist(h))) return rc;
   swap_roles(h, !stream_only);
   if (!stream_only) ++h->steps_done;
   return LB_OK;
@@ -602,8 +652,9 @@ void drop_graphs(lb_ctx* h) {
 void steps_changed(lb_ctx* h) { drop_graphs(h); }
 
 bool graphs_usable(const lb_ctx* h) {
-  // ranks: the NCCL calls stay outside graphs
-  return h->graphs_on && h->nranks == 1 && !h->prof_on;
+  // ranks: with the peer transport a step is kernels only (device-side ordering);
+  // the NCCL exchange transport stays outside graphs
+  return h->graphs_on && (h->nranks == 1 || h->halo_mode == 1) && !h->prof_on;
 }
 
 // Everything one_step changes on the host: restored if a capture fails half way.
@@ -692,9 +743,22 @@ int graph_steps(lb_ctx* h, bool* done) {
 // After a call's steps: wait, then the R22 report -- the first offending step and
 // site since the call began (the flag is reset for the next call).
 int finish(lb_ctx* h, long long step0 = -1) {
+  const bool peer = h->halo_mode == 1 && !h->G.zwrap;
+  // ranks: the neighbours' stores into this slab have landed before lb_step returns
+  if (peer && h->nranks > 1) CK(h, launch_wait_inbound(peers_of(h, 0), h->stream));
   CK(h, cudaMemcpyAsync(h->h_health, h->d_health, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+  if (peer)
+    for (int r = 0; r < h->nslabs; ++r)
+      CK(h, cudaMemcpyAsync(h->h_sync + r, h->slabs[r].sync + SW_ERR, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   resolve_pending(h);
+  if (peer)
+    for (int r = 0; r < h->nslabs; ++r)
+      if (h->h_sync[r]) {
+        h->broken = true;
+        return set_err(h, LB_ECUDA, "peer transport: a wait for a neighbour's epoch timed out (slab %d)", r);
+      }
   const unsigned long long v = *h->h_health;
   if (v != ~0ULL) {
     CK(h, cudaMemsetAsync(h->d_health, 0xff, sizeof(unsigned long long), h->stream));
@@ -717,53 +781,70 @@ __global__ void k_poke(double* p, double v) {
 void close_peers(lb_ctx* h) {
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   h->ipc_opened.clear();
-  for (int k = 0; k < 2; ++k) h->peerA[k] = h->peerB[k] = h->peerPhi[k] = nullptr;
+  for (int k = 0; k < 2; ++k) h->peerA[k] = h->peerB[k] = h->peerPhi[k] = nullptr, h->peerSync[k] = nullptr;
 }
 
-// Peer transport between ranks (collective): exchange CUDA IPC handles of A, B and
-// phi over NCCL, map the neighbours' buffers, and check the mapping end to end --
-// each rank stores a token into both neighbours' phi ghost planes with a kernel
-// and reads back what its neighbours stored.  On success halo_mode = 1; if the
-// neighbours' memory cannot be mapped (no peer access) or the check fails on any
-// rank, every rank keeps the NCCL exchange (the decision is agreed by an
-// all-reduce).  Only a NCCL/CUDA error on the way is an error.
+// All-gather of `bytes` host bytes per rank (rank order) over the handle's
+// bootstrap: NCCL (lb_create_slab) or the caller's callback (lb_create_slab_ext).
+int allgather_host(lb_ctx* h, const void* mine, void* all, size_t bytes) {
+  if (h->allgather) {
+    if (h->allgather(h->allgather_ctx, mine, all, bytes) != 0)
+      return set_err(h, LB_ENCCL, "the caller's all-gather failed");
+    return LB_OK;
+  }
+  char* d_all = nullptr;
+  CK(h, cudaMalloc(&d_all, bytes * h->nranks));
+  CK(h, cudaMemcpyAsync(d_all + bytes * h->rank, mine, bytes, cudaMemcpyHostToDevice, h->stream));
+  NK(h, ncclAllGather(d_all + bytes * h->rank, d_all, bytes, ncclChar, h->comm, h->stream));
+  CK(h, cudaMemcpyAsync(all, d_all, bytes * h->nranks, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(d_all);
+  return LB_OK;
+}
+
+// Peer transport between ranks (collective): exchange CUDA IPC handles of A, B,
+// phi and the sync words over the bootstrap, map the neighbours' buffers, and
+// check the mapping end to end -- each rank stores a token into both neighbours'
+// phi ghost planes with a kernel and reads back what its neighbours stored.  On
+// success halo_mode = 1; if the neighbours' memory cannot be mapped (no peer
+// access) or the check fails on any rank, every rank keeps the NCCL exchange (the
+// decision is agreed by an all-gather; an external bootstrap has no exchange
+// transport, so there it is an error).  Only a NCCL/CUDA error on the way is an
+// error otherwise.
 int open_peers(lb_ctx* h) {
   const Geom& G = h->G;
   Slab& s = h->slabs[0];
   CK(h, cudaMalloc(&h->d_token, 4 * sizeof(double)));
   CK(h, cudaMemsetAsync(h->d_token, 0, 4 * sizeof(double), h->stream));
   struct Handles {
-    cudaIpcMemHandle_t a, b, phi;
+    cudaIpcMemHandle_t a, b, phi, sync;
   } mine{};
   int ok = 1;
   if (cudaIpcGetMemHandle(&mine.a, s.A) != cudaSuccess || cudaIpcGetMemHandle(&mine.b, s.B) != cudaSuccess ||
-      cudaIpcGetMemHandle(&mine.phi, s.phi) != cudaSuccess)
+      cudaIpcGetMemHandle(&mine.phi, s.phi) != cudaSuccess || cudaIpcGetMemHandle(&mine.sync, s.sync) != cudaSuccess)
     ok = 0;
   cudaGetLastError();
   std::vector<Handles> all(h->nranks);
-  char* d_all = nullptr;
-  CK(h, cudaMalloc(&d_all, sizeof(Handles) * h->nranks));
-  CK(h, cudaMemcpyAsync(d_all + sizeof(Handles) * h->rank, &mine, sizeof mine, cudaMemcpyHostToDevice, h->stream));
-  NK(h, ncclAllGather(d_all + sizeof(Handles) * h->rank, d_all, sizeof(Handles), ncclChar, h->comm, h->stream));
-  CK(h, cudaMemcpyAsync(all.data(), d_all, sizeof(Handles) * h->nranks, cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
-  cudaFree(d_all);
+  int rc = allgather_host(h, &mine, all.data(), sizeof(Handles));
+  if (rc) return rc;
   const int nb[2] = {(h->rank - 1 + h->nranks) % h->nranks, (h->rank + 1) % h->nranks};
   for (int k = 0; k < 2 && ok; ++k) {
     if (k == 1 && nb[1] == nb[0]) {
       h->peerA[1] = h->peerA[0], h->peerB[1] = h->peerB[0], h->peerPhi[1] = h->peerPhi[0];
+      h->peerSync[1] = h->peerSync[0];
       break;
     }
-    const cudaIpcMemHandle_t* hs[3] = {&all[nb[k]].a, &all[nb[k]].b, &all[nb[k]].phi};
-    double** dst[3] = {&h->peerA[k], &h->peerB[k], &h->peerPhi[k]};
-    for (int j = 0; j < 3 && ok; ++j) {
+    const cudaIpcMemHandle_t* hs[4] = {&all[nb[k]].a, &all[nb[k]].b, &all[nb[k]].phi, &all[nb[k]].sync};
+    void** dst[4] = {reinterpret_cast<void**>(&h->peerA[k]), reinterpret_cast<void**>(&h->peerB[k]),
+                     reinterpret_cast<void**>(&h->peerPhi[k]), reinterpret_cast<void**>(&h->peerSync[k])};
+    for (int j = 0; j < 4 && ok; ++j) {
       void* p = nullptr;
       if (cudaIpcOpenMemHandle(&p, *hs[j], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
         ok = 0;
         cudaGetLastError();
       } else {
         h->ipc_opened.push_back(p);
-        *dst[j] = static_cast<double*>(p);
+        *dst[j] = p;
       }
     }
   }
@@ -774,22 +855,18 @@ int open_peers(lb_ctx* h) {
     k_poke<<<1, 1, 0, h->stream>>>(h->peerPhi[0] + phi_plane_index(G, G.nzl) + 1, 2000.0 + h->rank);
     CK(h, cudaGetLastError());
   }
-  int rc = halo_barrier(h, K_HALO_PHI);
-  if (rc) return rc;
+  if ((rc = halo_barrier(h, K_HALO_PHI))) return rc;
   double got[2] = {0, 0};
   CK(h, cudaMemcpyAsync(&got[0], s.phi + phi_plane_index(G, -GP), 8, cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaMemcpyAsync(&got[1], s.phi + phi_plane_index(G, G.nzl) + 1, 8, cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   ok = ok && got[0] == 1000.0 + nb[0] && got[1] == 2000.0 + nb[1];
   // every rank must agree (a neighbour that could not map falls back with us)
-  int* d_ok = nullptr;
-  CK(h, cudaMalloc(&d_ok, sizeof(int)));
-  CK(h, cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-  NK(h, ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
-  CK(h, cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
-  cudaFree(d_ok);
+  std::vector<int> oks(h->nranks);
+  if ((rc = allgather_host(h, &ok, oks.data(), sizeof(int)))) return rc;
+  for (int v : oks) ok = ok && v;
   if (!ok) close_peers(h);
+  if (!ok && h->allgather) return set_err(h, LB_ENCCL, "peer mapping failed and an external bootstrap has no exchange transport");
   h->halo_mode = ok ? 1 : 0;
   return LB_OK;
 }
@@ -940,6 +1017,55 @@ int lb_create_slab(int nx, int ny, int nz, const lb_params* params, int nranks, 
   return LB_OK;
 }
 
+int lb_create_slab_ext(int nx, int ny, int nz, const lb_params* params, int nranks, int rank,
+                       lb_allgather_fn allgather, void* ctx, lb_t** out) {
+  if (!allgather) return set_err(nullptr, LB_EINVAL, "allgather is NULL");
+  if (nranks < 2) return set_err(nullptr, LB_EINVAL, "an external bootstrap needs nranks >= 2");
+  int rc = create_common(nx, ny, nz, params, nranks, rank, 1, out);
+  if (rc) return rc;
+  lb_ctx* h = *out;
+  h->allgather = allgather;
+  h->allgather_ctx = ctx;
+  if ((rc = open_peers(h))) {
+    g_create_error = h->err;
+    lb_destroy(h);
+    *out = nullptr;
+    return rc;
+  }
+  return LB_OK;
+}
+
+int lb_debug_step_phase(lb_t* h, int phase) {
+  int rc = usable(h);
+  if (rc) return rc;
+  if (phase < 0 || phase > 2) return set_err(h, LB_EINVAL, "phase must be 0 (K_phi), 1 (step) or 2 (finish)");
+  if (h->ch || h->lc || h->G.zwrap || h->halo_mode != 1)
+    return set_err(h, LB_EINVAL, "step phases exist for slab handles of the binary fluid with the peer transport");
+  if (!h->have_state) return set_err(h, LB_ESTATE, "no state");
+  const Geom& G = h->G;
+  if (phase == 0) {
+    for (int r = 0; r < h->nslabs; ++r)
+      CK(h, launch_phi_edges(G, h->slabs[r].A, h->slabs[r].phi, h->stream, peers_of(h, r), h->num_sms));
+    ++h->launches;
+    CK(h, cudaStreamSynchronize(h->stream));
+    return LB_OK;
+  }
+  if (phase == 1) {
+    const Launch ln = launch_of(h);
+    for (int r = 0; r < h->nslabs; ++r) {
+      Slab& s = h->slabs[r];
+      const Health hl = health_of(h, r, r == h->nslabs - 1);
+      CK(h, launch_bgk_step(h, s, ln, hl, peers_of(h, r)));
+      ++h->launches;
+    }
+    swap_roles(h);
+    ++h->steps_done;
+    CK(h, cudaStreamSynchronize(h->stream));
+    return LB_OK;
+  }
+  return finish(h);
+}
+
 size_t lb_local_sites(const lb_t* h) { return h ? host_nloc(h) : 0; }
 
 int lb_set_state(lb_t* h, const double* f, const double* g) {
@@ -1085,6 +1211,12 @@ int lb_debug_tune(lb_t* h, int key, int value) {
     case LB_TUNE_GRAPHS:
       h->graphs_on = value != 0;
       break;
+    case LB_TUNE_L2_BOX:
+    case LB_TUNE_L2_FTILE:
+    case LB_TUNE_L2_GTILE:
+      if (value < 0 || value > 3) return set_err(h, LB_EINVAL, "L2 policy must be 0 (normal), 1 (first), 2 (last) or 3 (unchanged)");
+      (key == LB_TUNE_L2_BOX ? h->l2.box : key == LB_TUNE_L2_FTILE ? h->l2.ftile : h->l2.gtile) = value;
+      break;
     default:
       return set_err(h, LB_EINVAL, "unknown tuning key %d", key);
   }
@@ -1140,6 +1272,8 @@ void lb_destroy(lb_t* h) {
   }
   cudaFree(h->d_health);
   cudaFree(h->d_done);
+  for (auto& s : h->slabs) cudaFree(s.sync);
+  if (h->h_sync) cudaFreeHost(h->h_sync);
   cudaFree(h->xphi[0]);
   cudaFree(h->xphi[1]);
   if (h->h_health) cudaFreeHost(h->h_health);

@@ -41,6 +41,61 @@ __device__ __forceinline__ void health_tick(const Health& h) {
   }
 }
 
+// ---- device-side ordering of the peer transport (lb_kernels.cuh "SyncWord") ----
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* a, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait (one thread) until local sync word w >= target; bounded: after
+// kSyncTimeoutNs, or once any wait of this slab has timed out, give up and leave
+// SW_ERR set (lb_step reports it) -- a broken peer never hangs the GPU.
+__device__ __forceinline__ void sync_wait_ge(unsigned long long* sync, int w, unsigned long long target) {
+  if (ld_acquire_sys_u64(sync + w) >= target) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys_u64(sync + w) < target) {
+    if (*reinterpret_cast<volatile unsigned long long*>(sync + SW_ERR)) return;
+    if (globaltimer_ns() - t0 > kSyncTimeoutNs) {
+      atomicExch(sync + SW_ERR, 1ULL);
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+// End of a launch, one thread per CTA after a CTA barrier (every thread's stores
+// into the neighbours done and fenced at system scope): the last CTA of the
+// launch advances this slab's epoch `ew` and publishes it to the neighbours'
+// words `to_dn` (in the slab below) and `to_up` (in the slab above).
+__device__ __forceinline__ void sync_publish(const Peers& pr, int done_w, int ew, int to_dn, int to_up) {
+  if (!pr.sync) return;
+  __threadfence_system();
+  if (atomicAdd(pr.sync + done_w, 1ULL) == gridDim.x - 1) {
+    pr.sync[done_w] = 0;
+    __threadfence_system();
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + ew) + 1;
+    pr.sync[ew] = e;
+    st_release_sys_u64(pr.sync_dn + to_dn, e);
+    st_release_sys_u64(pr.sync_up + to_up, e);
+  }
+}
+// Step kernels: a CTA whose planes need the ghost phi planes of the slab below
+// (zA - 2 < 0) or above (zB + 1 >= nzl) waits for that neighbour's K_phi of this
+// step (this slab's own K_phi ran just before, so its phi epoch is the target).
+__device__ __forceinline__ void sync_wait_ghost_phi(const Geom& G, const Peers& pr, int zA, int zB) {
+  if (!pr.sync || G.zwrap) return;
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + SW_PHI_EPOCH);
+  if (zA - 2 < 0) sync_wait_ge(pr.sync, SW_PHI_FROM_DN, e);
+  if (zB + 1 >= G.nzl) sync_wait_ge(pr.sync, SW_PHI_FROM_UP, e);
+}
+
 // A.4 (R3): mu = A phi + B phi^3 - kappa lap phi
 __device__ __forceinline__ double chem_pot(const DevParams& p, double ph, double lap) {
   return p.A * ph + p.B * (ph * ph * ph) - p.kappa * lap;

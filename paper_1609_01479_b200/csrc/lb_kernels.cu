@@ -42,6 +42,43 @@ __global__ void __launch_bounds__(TPB) k_phi(Geom G, const double* __restrict__ 
   if (pr.phi_dn || pr.phi_up) __threadfence_system();
 }
 
+// K_phi of the peer transport (NEXT-1): phi of planes 0, 1, nzl-2, nzl-1 (A.3),
+// stored here and into the neighbours' ghost planes; ordered by the sync words
+// (lb_kernels.cuh "SyncWord"): every CTA first waits for both neighbours' step of
+// the previous timestep (their stores into planes 0 / nzl-1 of this slab's state,
+// and their reads of their ghost planes, are then complete); the last CTA
+// publishes this slab's phi epoch.  Grid-stride over the 4 planes.
+__global__ void __launch_bounds__(TPB) k_phi_edges(Geom G, const double* __restrict__ A, double* __restrict__ phi,
+                                                   Peers pr) {
+  if (threadIdx.x == 0) {
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + SW_PUSH_EPOCH);
+    sync_wait_ge(pr.sync, SW_PUSH_FROM_DN, e);
+    sync_wait_ge(pr.sync, SW_PUSH_FROM_UP, e);
+  }
+  __syncthreads();
+  const long long n = 4 * G.nxy;
+  for (long long t = (long long)blockIdx.x * TPB + threadIdx.x; t < n; t += (long long)gridDim.x * TPB) {
+    const int k = (int)(t / G.nxy);
+    const int z = k < 2 ? k : G.nzl - 4 + k;
+    const long long xy = t - (long long)k * G.nxy;
+    const double v = phi_sum(A + dist_index(G, z, 0, xy), G.nxy);
+    phi[phi_plane_index(G, z) + xy] = v;
+    if (z < GP) pr.phi_dn[phi_plane_index(G, G.nzl + z) + xy] = v;
+    if (z >= G.nzl - GP) pr.phi_up[phi_plane_index(G, z - G.nzl) + xy] = v;
+  }
+  __threadfence_system();  // this thread's stores into the neighbours, before the CTA's publication
+  __syncthreads();
+  if (threadIdx.x == 0) sync_publish(pr, SW_DONE_PHI, SW_PHI_EPOCH, SW_PHI_FROM_UP, SW_PHI_FROM_DN);
+}
+
+// End of lb_step on a rank: the neighbours' step launches up to this slab's push
+// epoch have completed, so their stores into this slab's state have landed.
+__global__ void k_wait_inbound(Peers pr) {
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + SW_PUSH_EPOCH);
+  sync_wait_ge(pr.sync, SW_PUSH_FROM_DN, e);
+  sync_wait_ge(pr.sync, SW_PUSH_FROM_UP, e);
+}
+
 // Propagation only (test support, lb_debug_stream): the push of A.8 with the
 // same addressing (push_target) and slot map as the step kernel.
 __global__ void __launch_bounds__(TPB) k_stream(Geom G, const double* __restrict__ A, double* __restrict__ B, Peers pr) {
@@ -129,6 +166,23 @@ cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int 
   const long long n = G.nxy * (z1 - z0);
   if (n <= 0) return cudaSuccess;
   k_phi<<<blocks_for(n), TPB, 0, st>>>(G, A, phi, z0, z1, pr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_phi_edges(const Geom& G, const double* A, double* phi, cudaStream_t st, const Peers& pr,
+                             int num_sms) {
+  if (!pr.sync || !pr.sync_dn || !pr.sync_up || !pr.phi_dn || !pr.phi_up || G.zwrap || G.nzl < 2)
+    return cudaErrorInvalidValue;
+  // nzl = 2 or 3: the edge pairs overlap; each plane is summed once per occurrence (same bits)
+  const long long blocks = blocks_for(4 * G.nxy);
+  const unsigned grid = (unsigned)(blocks < 4LL * num_sms ? blocks : 4LL * num_sms);
+  k_phi_edges<<<grid, TPB, 0, st>>>(G, A, phi, pr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_inbound(const Peers& pr, cudaStream_t st) {
+  if (!pr.sync) return cudaSuccess;
+  k_wait_inbound<<<1, 1, 0, st>>>(pr);
   return cudaGetLastError();
 }
 

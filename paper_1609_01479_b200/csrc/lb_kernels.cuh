@@ -113,11 +113,39 @@ struct Health {
 // out of the slab straight into the neighbour's next state, and K_phi its edge
 // planes straight into the neighbour's phi ghost planes -- no separate exchange.
 // nullptr: ghost planes here + a copy / NCCL exchange afterwards.
+//
+// Ordering is device-side (NEXT-1): each slab owns a few 64-bit sync words; a
+// neighbour WRITES its epochs into them (st.release.sys, remote) and the owner
+// POLLS them (ld.acquire.sys, local).  Per step t, with epochs counted per slab:
+//   K_phi(t)  waits for push(dn), push(up) >= its own push epoch (the neighbours'
+//             step t-1 has stored into this slab's state and stopped reading its
+//             phi ghost planes), stores its edge phi planes, and its last CTA
+//             publishes phi epoch t+1 to both neighbours;
+//   step(t)   CTAs whose z-chunk reads a ghost phi plane wait for phi(dn) or
+//             phi(up) >= its own phi epoch; interior chunks never wait; its last
+//             CTA publishes push epoch t+1 to both neighbours.
+// Waits are bounded (kSyncTimeoutNs): a timeout sets SW_ERR and lb_step fails.
+enum SyncWord {
+  SW_PHI_FROM_DN = 0,   // phi epoch of the slab below (it wrote our ghost planes -2, -1)
+  SW_PHI_FROM_UP = 1,   // phi epoch of the slab above (ghost planes nzl, nzl+1)
+  SW_PUSH_FROM_DN = 2,  // push epoch of the slab below (its step stored into our plane 0)
+  SW_PUSH_FROM_UP = 3,  // push epoch of the slab above (our plane nzl-1)
+  SW_PHI_EPOCH = 4,     // own K_phi launches completed
+  SW_PUSH_EPOCH = 5,    // own step launches completed
+  SW_DONE_PHI = 6,      // CTAs of the current K_phi launch finished
+  SW_DONE_STEP = 7,     // CTAs of the current step launch finished
+  SW_ERR = 8,           // a wait timed out
+  SW_WORDS = 16
+};
+constexpr unsigned long long kSyncTimeoutNs = 20ULL * 1000 * 1000 * 1000;
 struct Peers {
   double* dn = nullptr;      // next-state buffer (B) of the slab below
   double* up = nullptr;      // next-state buffer (B) of the slab above
   double* phi_dn = nullptr;  // phi buffer of the slab below
   double* phi_up = nullptr;  // phi buffer of the slab above
+  unsigned long long* sync = nullptr;     // this slab's sync words (nullptr: no device-side ordering)
+  unsigned long long* sync_dn = nullptr;  // the neighbours' sync words
+  unsigned long long* sync_up = nullptr;
 };
 // Base of the distribution plane that local plane zd in [-1, nzl] is pushed to:
 // this slab's plane (wrapping when G.zwrap, else its ghost planes -1 / nzl), or,
@@ -131,9 +159,16 @@ __host__ __device__ inline double* push_plane(const Geom& G, double* B, const Pe
 
 // ---- launchers (lb_kernels.cu) -------------------------------------------
 // All launch on `st`, return cudaGetLastError().
-// K_phi on local planes [z0, z1); with peers, edge planes also go to the neighbours' ghost planes
+// K_phi on local planes [z0, z1) (lb_get_phi; the exchange transport's edges)
 cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st,
                        const Peers& pr = Peers{});
+// K_phi of the peer transport: the two edge planes at each end, stored here and
+// into the neighbours' ghost planes, ordered by the sync words (pr.sync required)
+cudaError_t launch_phi_edges(const Geom& G, const double* A, double* phi, cudaStream_t st, const Peers& pr,
+                             int num_sms);
+// one thread: wait until both neighbours' step launches up to this slab's push
+// epoch have completed (all their stores into this slab have landed)
+cudaError_t launch_wait_inbound(const Peers& pr, cudaStream_t st);
 // Per-device kernel preparation (dynamic shared memory attribute above 48 KB, and
 // the CTAs resident at a time): once per (kernel, device), thread-safe.
 cudaError_t prepare_kernel(const void* fn, size_t smem, int threads, int* resid);
@@ -157,9 +192,16 @@ struct alignas(64) StepMaps {
 bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out);
 // Launch knobs of the step kernels: block order (tile_of_block; resid 0 = the
 // occupancy of the kernel on this device)
+// L2 eviction policy of a copy: 0 evict_normal, 1 evict_first, 2 evict_last, 3 evict_unchanged
+struct L2Pol {
+  int box = 2;    // g box (tile + 2-site halo) of plane j+2: re-read as the g tile two planes later
+  int ftile = 1;  // f tile of plane j: its last use
+  int gtile = 1;  // g tile of plane j
+};
 struct Launch {
   int zc = 1;
   TileOrder order{0, 1};
+  L2Pol l2{};  // warp-specialised kernel
 };
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
                         const Launch& ln, const Health& hl, const StepMaps* mapsA, cudaStream_t st,

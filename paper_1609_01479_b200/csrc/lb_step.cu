@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     mbar_init(&sm.bar_box, 1);
     fence_barrier_init();
   }
+  if (tid == 0) sync_wait_ghost_phi(G, pr, zA, zB);  // peer transport: slab-edge chunks wait for the neighbours' K_phi
   __syncthreads();
   unsigned ph_f = 0, ph_g = 0, ph_box = 0;  // mbarrier parities
 
@@ -355,9 +356,12 @@ __global__ void __launch_bounds__(TX* TY, 1)
     for (int q = 0; q < 6; ++q) P6_cur[q] = P6_next[q];
   }
   cp_wait<0>();
-  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
+  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the publication below
   __syncthreads();
-  if (tid == 0) health_tick(hl);
+  if (tid == 0) {
+    health_tick(hl);
+    sync_publish(pr, SW_DONE_STEP, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN);
+  }
 }
 
 template <int TY, bool USE_TMA, int COLL>

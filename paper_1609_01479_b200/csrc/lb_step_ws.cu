@@ -50,14 +50,7 @@ __host__ __device__ constexpr int ws_na(int ty) { return LB_WS_NA < kWTX * ty ? 
 __host__ __device__ constexpr bool ws_split_regs(int ty) {
   return LB_WS_REGS_STENCIL > 0 && kWTX * ty == 256 && ws_na(ty) == 256;
 }
-// L2 policies (policy_of): g box (re-read by the g tile two planes later), f and g
-// tiles (last use), stores (-1: st.global.cs)
-#ifndef LB_WS_BOX_POL
-#define LB_WS_BOX_POL 2
-#endif
-#ifndef LB_WS_TILE_POL
-#define LB_WS_TILE_POL 1
-#endif
+// pushes: st.global.cs (LB_WS_ST_POL < 0) or an L2 policy (policy_of kind)
 #ifndef LB_WS_ST_POL
 #define LB_WS_ST_POL (-1)
 #endif
@@ -111,7 +104,7 @@ struct alignas(128) WsSmem {
 template <int TY, int COLL, bool XCH = false>
 __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
-              const double* __restrict__ phig, int zc, TileOrder ord, Health hl, Peers pr, XchArgs xa,
+              const double* __restrict__ phig, int zc, TileOrder ord, L2Pol l2, Health hl, Peers pr, XchArgs xa,
               const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
               const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
   using S = WsSmem<TY, COLL, XCH>;
@@ -152,7 +145,11 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     if constexpr (ws_split_regs(TY))
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(COLL == 1 ? LB_WS_REGS_STENCIL_MRT : LB_WS_REGS_STENCIL));
     const int a = tid - NT;
-    const unsigned long long pol_last = policy_of<LB_WS_BOX_POL>();
+    const unsigned long long pol_last = policy_rt(l2.box);
+    if (pr.sync && !G.zwrap && (zA - 2 < 0 || zB + 1 >= G.nzl)) {  // peer transport: a slab-edge chunk
+      if (a == 0) sync_wait_ghost_phi(G, pr, zA, zB);                 // waits for the neighbours' K_phi
+      named_sync(2, kNA);
+    }
     auto zsrc = [&](int zp, bool& ghost) {
       ghost = false;
       if (G.zwrap) {  // one unsigned compare in the common case; a modulo only for slabs of < 3 planes
@@ -431,19 +428,20 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
   // ============================== collision warps ==============================
   if constexpr (ws_split_regs(TY))
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(COLL == 1 ? LB_WS_REGS_COLL_MRT : LB_WS_REGS_COLL));
-  const unsigned long long pol_first = policy_of<LB_WS_TILE_POL>();
+  const unsigned long long pol_f = policy_rt(l2.ftile), pol_g = policy_rt(l2.gtile);
   const unsigned long long pol_st = policy_of<(LB_WS_ST_POL < 0 ? 1 : LB_WS_ST_POL)>();
   unsigned ph_f = 0, ph_g = 0, seq = 0;
   auto issue_tile = [&](int zp, int dist) {
     if (tid == 0) {
       double(*dst)[NT] = dist == 0 ? sm.sTf : sm.sTg;
       unsigned long long* bar = dist == 0 ? &sm.bar_f : &sm.bar_g;
+      const unsigned long long pol = dist == 0 ? pol_f : pol_g;
       const int cp0 = (zp + GZ) * NSLOT + (dist == 0 ? 0 : 5);
       fence_proxy_async();
       mbar_expect_tx(bar, TILE_BYTES);
-      tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol_first);
-      tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol_first);
-      tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol_first);
+      tma_load_3d(&dst[0][0], &tm_t5, x0, y0, cp0, bar, pol);
+      tma_load_3d(&dst[5][0], &tm_t9, x0, y0, cp0 + (dist == 0 ? 10 : 14), bar, pol);
+      tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol);
     }
   };
   issue_tile(zA, 0);
@@ -494,9 +492,12 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) health_report(hl, G, x, y, k);  // R22
     }
   }
-  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the halo barrier
+  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the publication below
   named_sync(1, NT);
-  if (tid == 0) health_tick(hl);
+  if (tid == 0) {
+    health_tick(hl);
+    sync_publish(pr, SW_DONE_STEP, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN);
+  }
 }
 
 template <int TY, int COLL, bool XCH = false>
@@ -516,8 +517,8 @@ cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, doub
   const int nitems = ((G.nx + kWTX - 1) / kWTX) * ((G.ny + TY - 1) / TY) * ((G.nzl + zc - 1) / zc);
   if (XCH && (!xch || !xch->cur || !xch->old)) return cudaErrorInvalidValue;
   const XchArgs xa = xch ? *xch : XchArgs{};
-  kern<<<(unsigned)nitems, ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, ord, hl, pr, xa, m[0], m[1], m[2],
-                                                            m[3]);
+  kern<<<(unsigned)nitems, ws_threads(TY, XCH), smem, st>>>(G, p, A, B, phig, zc, ord, ln.l2, hl, pr, xa, m[0], m[1],
+                                                            m[2], m[3]);
   return cudaGetLastError();
 }
 

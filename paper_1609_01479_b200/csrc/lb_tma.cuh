@@ -61,6 +61,9 @@ __device__ __forceinline__ unsigned long long policy_of() {
   else asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ unsigned long long policy_rt(int kind) {
+  return kind == 0 ? policy_of<0>() : (kind == 1 ? policy_of<1>() : (kind == 2 ? policy_of<2>() : policy_of<3>()));
+}
 // store with an L2 policy
 __device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");

@@ -43,6 +43,17 @@ def broadcast_bytes(payload: bytes | None, nbytes: int = 128, src: int = 0) -> b
     return bytes(t.cpu().numpy().tobytes())
 
 
+def allgather_bytes(payload: bytes) -> bytes:
+    """Every rank's `payload` (all the same length), concatenated in rank order: the
+    bootstrap all-gather of lb_create_slab_ext (CUDA IPC handles, agreement flags,
+    barriers) over whatever process group is initialised (gloo or NCCL)."""
+    n = len(payload)
+    t = torch.frombuffer(bytearray(payload), dtype=torch.uint8).to(_device()) if n else torch.zeros(0, dtype=torch.uint8, device=_device())
+    out = [torch.zeros(n, dtype=torch.uint8, device=_device()) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return b"".join(bytes(o.cpu().numpy().tobytes()) for o in out)
+
+
 def max_over_ranks(v: float) -> float:
     """Max of a float over all ranks (the timing rule: max over ranks)."""
     if not dist.is_initialized() or dist.get_world_size() == 1:

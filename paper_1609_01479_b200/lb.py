@@ -53,6 +53,10 @@ _lb_create = _sig("lb_create", _i, _i, _i, _i, C.POINTER(lb_params), C.POINTER(_
 _lb_create_loopback = _sig("lb_create_loopback", _i, _i, _i, _i, C.POINTER(lb_params), _i, C.POINTER(_vp))
 _lb_nccl_get_unique_id = _sig("lb_nccl_get_unique_id", _i, _vp)
 _lb_create_slab = _sig("lb_create_slab", _i, _i, _i, _i, C.POINTER(lb_params), _i, _i, _vp, C.POINTER(_vp))
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+_lb_create_slab_ext = _sig("lb_create_slab_ext", _i, _i, _i, _i, C.POINTER(lb_params), _i, _i, ALLGATHER_FN, _vp,
+                           C.POINTER(_vp))
+_lb_debug_step_phase = _sig("lb_debug_step_phase", _i, _vp, _i)
 _lb_local_sites = _sig("lb_local_sites", C.c_size_t, _vp)
 _lb_set_state = _sig("lb_set_state", _i, _vp, _vp, _vp)
 _lb_init_equilibrium = _sig("lb_init_equilibrium", _i, _vp, _vp, _vp, _vp)
@@ -101,7 +105,7 @@ _lb_get_state_lc = _sig("lb_get_state_lc", _i, _vp, _vp, _vp, _vp)
 _lb_init_lc = _sig("lb_init_lc", _i, _vp, _vp, _vp, _vp)
 
 EXPORTS = [
-    "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_local_sites",
+    "lb_version", "lb_create", "lb_create_loopback", "lb_nccl_get_unique_id", "lb_create_slab", "lb_create_slab_ext", "lb_debug_step_phase", "lb_local_sites",
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_prepare", "lb_debug_stream", "lb_debug_tune", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
@@ -164,6 +168,31 @@ def lb_create_slab(nx: int, ny: int, nz: int, params: lb_params, nranks: int, ra
     return h
 
 
+def lb_create_slab_ext(nx: int, ny: int, nz: int, params: lb_params, nranks: int, rank: int, allgather):
+    """lb_create_slab bootstrapped by `allgather(mine: bytes) -> bytes` (nranks * len(mine),
+    rank order; e.g. dist.allgather_bytes).  Returns (handle, callback); keep the
+    callback alive as long as the handle (the library calls it until lb_destroy)."""
+
+    def cb(_ctx, send, recv, nbytes):
+        try:
+            out = allgather(C.string_at(send, nbytes))
+            if len(out) != nranks * nbytes:
+                return -1
+            C.memmove(recv, out, len(out))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed all-gather
+            return -1
+
+    fn = ALLGATHER_FN(cb)
+    h = _vp()
+    _check(_lb_create_slab_ext(nx, ny, nz, C.byref(params), nranks, rank, fn, None, C.byref(h)), None)
+    return h, fn
+
+
+def lb_debug_step_phase(h, phase: int) -> None:
+    _check(_lb_debug_step_phase(h, phase), h)
+
+
 def lb_local_sites(h) -> int:
     return int(_lb_local_sites(h))
 
@@ -197,6 +226,7 @@ def lb_debug_step_kernel(h, which: int) -> None:
 
 # lb_debug_tune keys (include/lb.h)
 LB_TUNE_ZCHUNK, LB_TUNE_BAND_ROWS, LB_TUNE_RESID, LB_TUNE_GRAPHS = 1, 2, 3, 4
+LB_TUNE_L2_BOX, LB_TUNE_L2_FTILE, LB_TUNE_L2_GTILE = 5, 6, 7
 
 
 def lb_debug_tune(h, key: int, value: int) -> None:
@@ -383,9 +413,15 @@ class Lattice:
     """A handle plus its shape.  Arrays at this level are (19, nz, ny, nx)."""
 
     def __init__(self, nx, ny, nz, params: lb_params | None = None, nslabs: int = 1, nranks: int = 1, rank: int = 0,
-                 uid: bytes | None = None):
+                 uid: bytes | None = None, allgather=None):
+        """nranks > 1: one rank of a z-slab decomposition, bootstrapped by NCCL (uid from
+        lb_nccl_get_unique_id) or, with `allgather` (bytes -> bytes), by the caller."""
         self.params = params or make_params()
-        if nranks > 1:
+        self._cb = None
+        if nranks > 1 and allgather is not None:
+            self.h, self._cb = lb_create_slab_ext(nx, ny, nz, self.params, nranks, rank, allgather)
+            self.shape = (nz // nranks, ny, nx)
+        elif nranks > 1:
             self.h = lb_create_slab(nx, ny, nz, self.params, nranks, rank, uid)
             self.shape = (nz // nranks, ny, nx)
         else:

@@ -16,7 +16,9 @@ import torch  # noqa: E402
 
 from paper_1609_01479_b200 import lb, synth  # noqa: E402
 
-KEYS = {"zc": lb.LB_TUNE_ZCHUNK, "band": lb.LB_TUNE_BAND_ROWS, "resid": lb.LB_TUNE_RESID, "graphs": lb.LB_TUNE_GRAPHS}
+KEYS = {"zc": lb.LB_TUNE_ZCHUNK, "band": lb.LB_TUNE_BAND_ROWS, "resid": lb.LB_TUNE_RESID, "graphs": lb.LB_TUNE_GRAPHS,
+        "box": lb.LB_TUNE_L2_BOX, "ft": lb.LB_TUNE_L2_FTILE, "gt": lb.LB_TUNE_L2_GTILE}
+DEFAULTS = {"zc": 0, "band": 1, "resid": 0, "graphs": 1, "box": 2, "ft": 1, "gt": 1}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("nx", type=int)
@@ -53,5 +55,5 @@ with lb.Lattice(a.nx, a.ny, a.nz) as L:
             out[s].append(round(a.nx * a.ny * a.nz * a.steps / (e0.elapsed_time(e1) * 1e-3) / 1e6, 1))
             for kv in s.split(","):  # back to the defaults
                 k, _ = kv.split("=")
-                lb.lb_debug_tune(L.h, KEYS[k], {"zc": 0, "band": 1, "resid": 0, "graphs": 1}[k])
+                lb.lb_debug_tune(L.h, KEYS[k], DEFAULTS[k])
 print(json.dumps({"lattice": [a.nx, a.ny, a.nz], "kernel": a.kernel, "mlups": out}))

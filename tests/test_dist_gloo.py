@@ -73,6 +73,10 @@ def _helpers_body(rank, world):
     assert D.sum_over_ranks(1.0) == float(world)
     z0, z1 = D.slab_range(8 * world, world, rank)
     assert (z0, z1) == (8 * rank, 8 * rank + 8)
+    # the all-gather of lb_create_slab_ext's bootstrap (IPC handles, agreement flags)
+    mine = bytes([rank, 255 - rank]) * 3
+    assert D.allgather_bytes(mine) == b"".join(bytes([r, 255 - r]) * 3 for r in range(world))
+    assert D.allgather_bytes(b"") == b""
     D.barrier()
 
 

@@ -388,6 +388,20 @@ def test_fused_halo_ws_kernel_and_stream_only():
     assert np.array_equal(f1, f0) and np.array_equal(g1, g0)
 
 
+@pytest.mark.parametrize("kernel,shape,nslabs", [(0, (32, 16, 16), 2), (0, (32, 16, 16), 4), (0, (24, 10, 16), 8),
+                                                 (2, (64, 24, 12), 3), (1, (33, 9, 12), 2), (1, (17, 19, 12), 4)])
+@pytest.mark.parametrize("halo", [0, 1])
+def test_slabs_parity_against_oracle(kernel, shape, nslabs, halo):
+    """Loopback z-slabs of the BGK path (both halo transports; the peer one with the
+    device-side epochs of NEXT-1) against the oracle directly at R18's 1e-12 --
+    not only against the GPU's own one-slab run -- including odd-nx tile-kernel
+    slabs and 8 slabs of 2 planes."""
+    nx, ny, nz = shape
+    f, g = rough(nx, ny, nz, seed=41)
+    a = gpu_run(f, g, P0, 6, nslabs=nslabs, kernel=kernel, halo=halo)
+    assert_parity(a, R.run(f, g, P0, 6))
+
+
 # ------------------------------------------------------------------ bitwise properties of the GPU path
 @pytest.mark.parametrize("nslabs", [2, 4, 8])
 def test_slab_decomposition_is_bitwise_identical(nslabs):
