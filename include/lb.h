@@ -332,6 +332,21 @@ int lb_debug_step_phase(lb_t* h, int phase);
  * planes, no halo plan).  Must equal lb_debug_propagation_map.  Host-only. */
 int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* out);
 
+/* Memory-safety check (test support; this pool has no compute-sanitizer): every
+ * field buffer (f/g A and B, phi, Q, u, the phi-exchange arrays) is allocated with
+ * 64 KB guard zones on both sides holding a fixed byte pattern.  Returns the
+ * number of guard bytes that no longer hold it -- 0 unless some kernel or copy
+ * stored outside its buffer -- or a negative LB_* code. */
+long long lb_debug_guards(lb_t* h);
+
+/* Built with -DLB_CHECKED (liblb_checked.so, _build.build(checked=True))?  1 or 0.
+ * In that build the kernels check their computed indices (wrapped halo boxes,
+ * ghost phi planes, exchange sites, push targets); lb_debug_check returns the
+ * source line (in the kernel files) of the first check that failed, 0 if none,
+ * or a negative LB_* code.  Always 0 in the product build. */
+int lb_debug_checked(void);
+int lb_debug_check(lb_t* h);
+
 /* Block order of the step kernels (host-only): for block L of a launch over ntx x
  * nty tiles and nch z-chunks, out[3L .. 3L+2] = (tile column, tile row, chunk) as
  * the kernels compute it with `resid` CTAs resident and bands of `band` tile rows

@@ -12,6 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblb.so")
+LIB_CHECKED = os.path.join(PKG, "liblb_checked.so")  # -DLB_CHECKED: device bounds checks (test support)
 SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_step_ws.cu", "lb_step_ch.cu", "lb_step_lc.cu", "lb_api.cu"]
 HEADERS = ["d3q19.cuh", "lb_kernels.cuh", "lb_device.cuh", "lb_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -28,25 +29,28 @@ def nccl_dirs() -> tuple[str, str]:
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "lb.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every source to an object in parallel, then link liblb.so."""
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Compile every source to an object in parallel, then link liblb.so (checked:
+    liblb_checked.so, the same sources with -DLB_CHECKED)."""
+    out = LIB_CHECKED if checked else LIB
+    if not force and not _stale(out):
+        return out
     inc, lib = nccl_dirs()
     nvcc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
              "-Xptxas", "-v" if verbose else "-O3",
              "-I", os.path.join(ROOT, "include"), "-I", inc,
+             *(["-DLB_CHECKED"] if checked else []),
              *os.environ.get("LB_NVCC_FLAGS", "").split()]
-    objdir = os.path.join(PKG, "build_obj")
+    objdir = os.path.join(PKG, "build_obj_checked" if checked else "build_obj")
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, os.path.splitext(s)[0] + ".o") for s in SOURCES]
 
@@ -63,13 +67,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
     r = subprocess.run([nvcc, *ARCH, "-shared", *objs, "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}",
-                        "-o", LIB + ".tmp"], capture_output=True, text=True)
+                        "-o", out + ".tmp"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed linking liblb.so")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

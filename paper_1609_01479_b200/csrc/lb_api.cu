@@ -80,6 +80,7 @@ struct lb_ctx {
   // [1] steps completed by the step kernels; d_done: CTAs finished in a launch
   unsigned long long* d_health = nullptr;
   unsigned* d_done = nullptr;
+  int* d_check = nullptr;  // LB_CHECKED builds: first failed device bounds check
   unsigned long long* h_health = nullptr;  // pinned copy of d_health[0]
   long long steps_done = 0;                // host mirror of d_health[1]
   ncclComm_t comm = nullptr;
@@ -98,6 +99,7 @@ struct lb_ctx {
   lb_allgather_fn allgather = nullptr;
   void* allgather_ctx = nullptr;
   unsigned long long* h_sync = nullptr;  // pinned: SW_ERR of each slab, read by finish()
+  std::vector<std::pair<double*, size_t>> guarded;  // buffers with guard zones (dev_alloc)
   bool have_state = false;
   bool broken = false;
   // CUDA graphs of kGraphSteps steps (single process, no per-launch profiling): one
@@ -232,12 +234,33 @@ void resolve_pending(lb_ctx* h) {
 }
 
 // ---- allocation ------------------------------------------------------------
+// Every field buffer carries guard zones of kGuardBytes on both sides, filled
+// with kGuardByte: lb_debug_guards finds any store that left its buffer (the
+// out-of-bounds half of a memory checker, which this pool has no tool for).
+constexpr size_t kGuardBytes = 64 * 1024;
+constexpr unsigned char kGuardByte = 0xA5;
+
+cudaError_t dev_alloc(lb_ctx* h, double** p, size_t bytes) {
+  unsigned char* raw = nullptr;
+  cudaError_t e = cudaMalloc(&raw, bytes + 2 * kGuardBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(raw, kGuardByte, kGuardBytes, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(raw + kGuardBytes + bytes, kGuardByte, kGuardBytes, h->stream);
+  *p = reinterpret_cast<double*>(raw + kGuardBytes);
+  h->guarded.push_back({*p, bytes});
+  return e;
+}
+void* raw_of(const void* p) { return p ? (void*)(static_cast<const unsigned char*>(p) - kGuardBytes) : nullptr; }
+void dev_free(double* p) {
+  if (p) cudaFree(raw_of(p));
+}
+
 // the two phi arrays of the phi-exchange kernel (kernel 5), filled with kXchEmpty
 int ensure_xch(lb_ctx* h) {
   if (h->xphi[0]) return LB_OK;
   const long long n = h->G.nxy * h->G.nzl;
   for (int k = 0; k < 2; ++k) {
-    CK(h, cudaMalloc(&h->xphi[k], (size_t)n * sizeof(double)));
+    CK(h, dev_alloc(h, &h->xphi[k], (size_t)n * sizeof(double)));
     CK(h, fill_xch_empty(h->xphi[k], n, h->stream));
   }
   h->xch_dirty = false;
@@ -266,9 +289,9 @@ int alloc_slabs(lb_ctx* h) {
   for (int r = 0; r < h->nslabs; ++r) {
     Slab& s = h->slabs[r];
     s.z0 = (h->rank * h->nslabs + r) * h->nzl;
-    CK(h, cudaMalloc(&s.A, dist_doubles(h->G) * sizeof(double)));
-    CK(h, cudaMalloc(&s.B, dist_doubles(h->G) * sizeof(double)));
-    CK(h, cudaMalloc(&s.phi, phi_doubles(h->G) * sizeof(double)));
+    CK(h, dev_alloc(h, &s.A, dist_doubles(h->G) * sizeof(double)));
+    CK(h, dev_alloc(h, &s.B, dist_doubles(h->G) * sizeof(double)));
+    CK(h, dev_alloc(h, &s.phi, phi_doubles(h->G) * sizeof(double)));
     // NaN-fill: a read of a plane nobody wrote shows up as a parity failure
     CK(h, cudaMemsetAsync(s.A, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
     CK(h, cudaMemsetAsync(s.B, 0xff, dist_doubles(h->G) * sizeof(double), h->stream));
@@ -289,6 +312,8 @@ int alloc_slabs(lb_ctx* h) {
   CK(h, cudaMemsetAsync(h->d_health + 1, 0, sizeof(unsigned long long), h->stream));
   CK(h, cudaMalloc(&h->d_done, sizeof(unsigned)));
   CK(h, cudaMemsetAsync(h->d_done, 0, sizeof(unsigned), h->stream));
+  CK(h, cudaMalloc(&h->d_check, sizeof(int)));
+  CK(h, cudaMemsetAsync(h->d_check, 0, sizeof(int), h->stream));
   CK(h, cudaMallocHost(&h->h_health, sizeof(unsigned long long)));
   CK(h, cudaStreamSynchronize(h->stream));
   return LB_OK;
@@ -301,6 +326,7 @@ Health health_of(const lb_ctx* h, int r, bool tick) {
   hl.step = h->d_health + 1;
   hl.done = tick ? h->d_done : nullptr;
   hl.site0 = (long long)h->slabs[r].z0 * h->G.nxy;
+  hl.check = h->d_check;
   return hl;
 }
 
@@ -820,8 +846,9 @@ int open_peers(lb_ctx* h) {
     cudaIpcMemHandle_t a, b, phi, sync;
   } mine{};
   int ok = 1;
-  if (cudaIpcGetMemHandle(&mine.a, s.A) != cudaSuccess || cudaIpcGetMemHandle(&mine.b, s.B) != cudaSuccess ||
-      cudaIpcGetMemHandle(&mine.phi, s.phi) != cudaSuccess || cudaIpcGetMemHandle(&mine.sync, s.sync) != cudaSuccess)
+  // (handles of whole allocations: the field buffers start kGuardBytes into theirs)
+  if (cudaIpcGetMemHandle(&mine.a, raw_of(s.A)) != cudaSuccess || cudaIpcGetMemHandle(&mine.b, raw_of(s.B)) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine.phi, raw_of(s.phi)) != cudaSuccess || cudaIpcGetMemHandle(&mine.sync, s.sync) != cudaSuccess)
     ok = 0;
   cudaGetLastError();
   std::vector<Handles> all(h->nranks);
@@ -844,7 +871,7 @@ int open_peers(lb_ctx* h) {
         cudaGetLastError();
       } else {
         h->ipc_opened.push_back(p);
-        *dst[j] = p;
+        *dst[j] = j < 3 ? static_cast<unsigned char*>(p) + kGuardBytes : p;
       }
     }
   }
@@ -940,7 +967,7 @@ int ch_create(int nx, int ny, int nz, const lb_params* params, double tau_shear,
   cudaError_t e = cudaSuccess;
   bool maps_ok = true;
   for (auto& s : h->slabs) {
-    if (e == cudaSuccess) e = cudaMalloc(&s.phi2, phi_doubles(h->G) * sizeof(double));
+    if (e == cudaSuccess) e = dev_alloc(h, &s.phi2, phi_doubles(h->G) * sizeof(double));
     if (e == cudaSuccess) e = cudaMemsetAsync(s.phi2, 0xff, phi_doubles(h->G) * sizeof(double), h->stream);
     maps_ok = maps_ok && make_ch_maps(h->G, s.A, h->ty, &s.chA) && make_ch_maps(h->G, s.B, h->ty, &s.chB);
   }
@@ -1261,21 +1288,15 @@ void lb_destroy(lb_t* h) {
   cudaFree(h->d_token);
   if (h->comm) ncclCommDestroy(h->comm);
   for (auto& s : h->slabs) {
-    cudaFree(s.A);
-    cudaFree(s.B);
-    cudaFree(s.phi);
-    cudaFree(s.phi2);
-    cudaFree(s.q);
-    cudaFree(s.q2);
-    cudaFree(s.u);
-    cudaFree(s.u2);
+    for (double* b : {s.A, s.B, s.phi, s.phi2, s.q, s.q2, s.u, s.u2}) dev_free(b);
   }
   cudaFree(h->d_health);
   cudaFree(h->d_done);
+  cudaFree(h->d_check);
   for (auto& s : h->slabs) cudaFree(s.sync);
   if (h->h_sync) cudaFreeHost(h->h_sync);
-  cudaFree(h->xphi[0]);
-  cudaFree(h->xphi[1]);
+  dev_free(h->xphi[0]);
+  dev_free(h->xphi[1]);
   if (h->h_health) cudaFreeHost(h->h_health);
   for (auto& p : h->pending) {
     cudaEventDestroy(p.e0);
@@ -1486,6 +1507,38 @@ int lb_debug_propagation_map_peers(int nx, int ny, int nz, int nslabs, int64_t* 
   return LB_OK;
 }
 
+int lb_debug_check(lb_t* h) {
+  if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
+  int line = 0;
+  if (cudaMemcpy(&line, h->d_check, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_err(h, LB_ECUDA, "check word read-back failed");
+  return line;
+}
+
+int lb_debug_checked(void) {
+#ifdef LB_CHECKED
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+long long lb_debug_guards(lb_t* h) {
+  if (!h) return set_err(nullptr, LB_EINVAL, "handle is NULL");
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return set_err(h, LB_ECUDA, "stream synchronisation failed");
+  std::vector<unsigned char> g(kGuardBytes);
+  long long bad = 0;
+  for (const auto& b : h->guarded) {
+    const unsigned char* raw = static_cast<const unsigned char*>(raw_of(b.first));
+    for (const unsigned char* z : {raw, raw + kGuardBytes + b.second}) {
+      if (cudaMemcpy(g.data(), z, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return set_err(h, LB_ECUDA, "guard read-back failed");
+      for (unsigned char c : g) bad += c != kGuardByte;
+    }
+  }
+  return bad;
+}
+
 int lb_debug_tile_order(int ntx, int nty, int nch, int resid, int band, int* out) {
   if (!out || ntx < 1 || nty < 1 || nch < 1 || resid < 1 || band < 1) return LB_EINVAL;
   const int n = ntx * nty * nch;
@@ -1613,10 +1666,10 @@ int lc_create(int nx, int ny, int nz, const lb_lc_params* lp, int nranks, int ra
   bool maps_ok = true;
   for (auto& s : h->slabs) {
     for (double** b : {&s.q, &s.q2})
-      if (e == cudaSuccess && (e = cudaMalloc(b, nq * sizeof(double))) == cudaSuccess)
+      if (e == cudaSuccess && (e = dev_alloc(h, b, nq * sizeof(double))) == cudaSuccess)
         e = cudaMemsetAsync(*b, 0xff, nq * sizeof(double), h->stream);
     for (double** b : {&s.u, &s.u2})
-      if (e == cudaSuccess && (e = cudaMalloc(b, nu * sizeof(double))) == cudaSuccess)
+      if (e == cudaSuccess && (e = dev_alloc(h, b, nu * sizeof(double))) == cudaSuccess)
         e = cudaMemsetAsync(*b, 0xff, nu * sizeof(double), h->stream);
     maps_ok = maps_ok && make_step_maps(h->G, s.A, 8, &s.lcA) && make_step_maps(h->G, s.B, 8, &s.lcB);
   }

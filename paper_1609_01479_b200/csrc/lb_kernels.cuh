@@ -10,6 +10,21 @@
 
 namespace lbk {
 
+// LB_CHECKED builds (liblb_checked.so, test support): device-side bounds checks of
+// the kernels' computed indices.  A failed check records its source line in the
+// handle's check word (Health::check, read by lb_debug_check) and execution goes
+// on -- no trap, no fault; in the product build the checks compile to nothing.
+#ifdef LB_CHECKED
+#define LB_CHECK(hl, cond)                                  \
+  do {                                                      \
+    if (!(cond) && (hl).check) atomicCAS((hl).check, 0, __LINE__); \
+  } while (0)
+#else
+#define LB_CHECK(hl, cond) \
+  do {                     \
+  } while (0)
+#endif
+
 // Constants of the step derived once on the host from lb_params (R2, R7-R10).
 struct DevParams {
   double A, B, kappa;
@@ -105,6 +120,7 @@ struct Health {
   unsigned long long* step = nullptr;
   unsigned* done = nullptr;  // CTAs finished in this launch; nullptr: this launch does not tick
   long long site0 = 0;       // global site index of local site 0 (slab z0 * nx * ny)
+  int* check = nullptr;      // LB_CHECKED builds: first failed bounds check (source line)
 };
 
 // Fused halo ("peer" transport): the buffers of the

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
     const int row = u / BROWU, cu = u - row * BROWU;
     box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * VEC);
     box_dst[r] = u < BOXU ? row * BX + cu * VEC : -1;
+    LB_CHECK(hl, box_dst[r] < 0 || (box_dst[r] + VEC - 1 < NB && box_src[r] >= 0 && box_src[r] + VEC - 1 < nxy));
   }
   auto zsrc = [&](int zp, bool& ghost) {
     ghost = false;
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
       double v;
       if (ghost) {
         const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
+        LB_CHECK(hl, zs >= -GP && zs < G.nzl + GP && gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny);
         v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
       } else {
         v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
@@ -331,6 +333,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
       auto push = [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+        LB_CHECK(hl, xd >= 0 && xd < G.nx && yd >= 0 && yd < G.ny);
         double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
         __stcs(d + (long long)slot(0, i) * nxy, fs);
         __stcs(d + (long long)slot(1, i) * nxy, gs);

@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     const double rho = collide_mrt(p, f, g0, 0.0, 0.0, P6, [&](int i, double fs, double) {
       const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
       const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+      LB_CHECK(hl, xd >= 0 && xd < G.nx && yd >= 0 && yd < G.ny);
       double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
       __stcs(d + (long long)slot(0, i) * nxy, fs);
     });

@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       const int row = u / BROWU, cu = u - row * BROWU;
       box_src[r] = (long long)wrapy(y0 - 2 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
       box_dst[r] = u < BOXU ? row * BX + cu * 2 : -1;
+      LB_CHECK(hl, box_dst[r] < 0 || (box_dst[r] + 1 < NB && box_src[r] >= 0 && box_src[r] + 1 < nxy));
     }
     // box n (n = 0 .. nlast) is the g box of plane zA - 2 + n
     const int nlast = zB - zA + 3;  // plane zB + 1
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         double v;
         if (ghost) {
           const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
+          LB_CHECK(hl, zs >= -GP && zs < G.nzl + GP && gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny);
           v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
         } else {
           v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
@@ -326,6 +328,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       }
       h_ring = by * BX + bx;
       h_off = (long long)wrap_n(y0 - 2 + by, G.ny) * G.nx + wrap_n(x0 - 2 + bx, G.nx);
+      LB_CHECK(hl, h_ring >= 0 && h_ring < NB && h_off >= 0 && h_off < nxy);
     }
     auto xsite = [&](int b) { return xa.cur + (long long)wrap_n(zA - 2 + b, G.nzl) * nxy + h_off; };
     // the owner has not stored it yet (a neighbouring tile that started later or
@@ -477,6 +480,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       auto push = [&](int i, double fs, double gs) {
         const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
         const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+        LB_CHECK(hl, xd >= 0 && xd < G.nx && yd >= 0 && yd < G.ny);
         double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;  // A.8 push
         if (LB_WS_ST_POL < 0) {
           __stcs(d + (long long)slot(0, i) * nxy, fs);

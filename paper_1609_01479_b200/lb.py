@@ -14,7 +14,10 @@ import os
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblb.so")
+# LB_VARIANT=checked loads the bounds-checked test build (liblb_checked.so: device
+# index checks, lb_debug_check) -- the same kernels and results; test support only
+_LIB_NAME = "liblb_checked.so" if os.environ.get("LB_VARIANT") == "checked" else "liblb.so"
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), _LIB_NAME)
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
         f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -79,6 +82,9 @@ _lb_bytes_per_site = _sig("lb_bytes_per_site", C.c_double)
 _lb_debug_propagation_map = _sig("lb_debug_propagation_map", _i, _i, _i, _i, _i, _vp)
 _lb_debug_propagation_map_peers = _sig("lb_debug_propagation_map_peers", _i, _i, _i, _i, _i, _vp)
 _lb_debug_halo_mode = _sig("lb_debug_halo_mode", _i, _vp, _i)
+_lb_debug_guards = _sig("lb_debug_guards", _ll, _vp)
+_lb_debug_check = _sig("lb_debug_check", _i, _vp)
+_lb_debug_checked = _sig("lb_debug_checked", _i)
 _lb_debug_tile_order = _sig("lb_debug_tile_order", _i, _i, _i, _i, _i, _i, _vp)
 _lb_halo_plan = _sig("lb_halo_plan", _i, _i, _i, _i, _i, _i, _vp)
 _lb_set_collision = _sig("lb_set_collision", _i, _vp, _i, C.c_double, C.c_double, C.c_double)
@@ -109,7 +115,7 @@ EXPORTS = [
     "lb_set_state", "lb_init_equilibrium", "lb_step", "lb_prepare", "lb_debug_stream", "lb_debug_tune", "lb_debug_step_kernel", "lb_get_state", "lb_get_phi", "lb_destroy",
     "lb_last_error", "lb_stream", "lb_launch_count", "lb_profile_enable", "lb_profile_reset", "lb_profile_count",
     "lb_profile_entry", "lb_bytes_per_site", "lb_debug_propagation_map", "lb_debug_propagation_map_peers",
-    "lb_debug_halo_mode", "lb_debug_tile_order", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_create_ch_loopback", "lb_create_ch_slab", "lb_set_state_ch",
+    "lb_debug_halo_mode", "lb_debug_tile_order", "lb_debug_guards", "lb_debug_check", "lb_debug_checked", "lb_halo_plan", "lb_set_collision", "lb_create_ch", "lb_create_ch_loopback", "lb_create_ch_slab", "lb_set_state_ch",
     "lb_get_state_ch",
     "lb_create_lc", "lb_create_lc_loopback", "lb_create_lc_slab", "lb_set_state_lc", "lb_get_state_lc", "lb_init_lc",
 ]
@@ -300,6 +306,26 @@ def lb_debug_propagation_map_peers(nx: int, ny: int, nz: int, nslabs: int = 1) -
     if rc != LB_OK:
         raise LBError(rc, "peer propagation map failed (bad sizes, a ghost-plane store or not a permutation)")
     return out.reshape(Q, nz, ny, nx)
+
+
+def lb_debug_guards(h) -> int:
+    """Guard-zone bytes no longer holding their pattern (0 = no store left its buffer)."""
+    n = int(_lb_debug_guards(h))
+    if n < 0:
+        raise LBError(n, lb_last_error(h))
+    return n
+
+
+def lb_debug_check(h) -> int:
+    """LB_CHECKED builds: source line of the first failed device bounds check (0: none)."""
+    n = int(_lb_debug_check(h))
+    if n < 0:
+        raise LBError(n, lb_last_error(h))
+    return n
+
+
+def lb_debug_checked() -> bool:
+    return bool(_lb_debug_checked())
 
 
 def lb_debug_tile_order(ntx: int, nty: int, nch: int, resid: int, band: int = 1) -> np.ndarray:

@@ -1,11 +1,17 @@
-"""Small cases of every step kernel for compute-sanitizer (one tool per run):
+"""Small cases of every step kernel, checked for memory safety without
+compute-sanitizer (closed on this pool): after each run the guard zones around
+every field buffer must be intact (lb_debug_guards == 0) and, with the
+bounds-checked build (LB_VARIANT=checked), no device index check may have failed
+(lb_debug_check == 0); buffers start NaN-filled, so a read of memory nobody wrote
+shows up as an oracle mismatch.  Cases:
 the warp-specialised kernel with the phi exchange (16^3 default), the plain
 warp-specialised and tile kernels, 32 x 8 tiles over several waves with a
 wrapped box, two loopback slabs with the peer transport (K_phi edges, P2P
 pushes, device-side epochs), the MRT collision, the Cahn-Hilliard and the
-liquid-crystal kernels.  Exits non-zero if any result misses the oracle.
+liquid-crystal kernels.  Exits non-zero if any result misses the oracle or any
+check fails.
 
-  compute-sanitizer --tool memcheck python scripts/sanitize_cases.py
+  LB_VARIANT=checked python scripts/sanitize_cases.py
 """
 import os
 import sys
@@ -35,6 +41,17 @@ def rough(nx, ny, nz, seed=1):
 
 
 bad = []
+
+
+def memsafe(L, name):
+    guards = lb.lb_debug_guards(L.h)
+    line = lb.lb_debug_check(L.h)
+    print(f"  {name}: guard bytes changed {guards}, failed device check at line {line}", flush=True)
+    if guards or line:
+        bad.append(name + " (memory)")
+
+
+print("bounds-checked build:", lb.lb_debug_checked(), flush=True)
 for (shape, kernel, nslabs, halo, steps) in [((16, 16, 16), 0, 1, None, 3), ((16, 16, 16), 2, 1, None, 2),
                                              ((17, 12, 8), 1, 1, None, 2), ((64, 24, 6), 2, 1, None, 1),
                                              ((32, 16, 8), 0, 2, 1, 2), ((32, 16, 8), 1, 2, 1, 2),
@@ -48,6 +65,7 @@ for (shape, kernel, nslabs, halo, steps) in [((16, 16, 16), 0, 1, None, 3), ((16
         L.set_state(f, g)
         L.step(steps)
         f1, g1 = L.get_state()
+        memsafe(L, f"{shape} kernel {kernel} slabs {nslabs}")
     f0, g0 = R.run(f, g, P, steps)
     e = max(rel(f1, f0), rel(g1, g0))
     print(f"case {shape} kernel {kernel} slabs {nslabs} halo {halo}: rel err {e:.2e}", flush=True)
@@ -62,6 +80,7 @@ with lb.Lattice(16, 8, 8, CP) as L:
     L.set_state(f, g)
     L.step(2)
     f1, g1 = L.get_state()
+    memsafe(L, "mrt")
 f0, g0 = M.run(f, g, mp, 2)
 e = max(rel(f1, f0), rel(g1, g0))
 print(f"case mrt: rel err {e:.2e}", flush=True)
@@ -74,6 +93,7 @@ with lb.ChLattice(16, 8, 8, CP, 0.8, 1.1, 1.0) as L:
     L.set_state(fch, phi)
     L.step(2)
     f1, p1 = L.get_state()
+    memsafe(L, "ch")
 f0, p0 = CH.run(fch, phi, CH.ChParams(base=P, tau_s=0.8, tau_b=1.1, tau_ghost=1.0), 2)
 e = max(rel(f1, f0), rel(p1, p0))
 print(f"case ch: rel err {e:.2e}", flush=True)
@@ -86,6 +106,7 @@ with lb.LcLattice(16, 8, 8, lb.make_lc_params(lp.tau_f, lp.A0, lp.gamma, lp.kapp
     L.set_state(*st)
     L.step(2)
     got = L.get_state()
+    memsafe(L, "lc")
 ref = LC.run(*st, lp, 2)
 e = max(rel(got[0], ref[0]), rel(got[1], ref[1]))
 print(f"case lc: rel err {e:.2e}", flush=True)
