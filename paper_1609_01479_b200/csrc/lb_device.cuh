@@ -31,10 +31,11 @@ __device__ __forceinline__ void health_report(const Health& h, const Geom& G, in
 }
 // One thread per CTA, after the CTA's reports (a CTA barrier before): the last
 // CTA of the launch to finish advances the step counter -- every report of this
-// launch has read the step number by then.
+// launch has read the step number by then (its value, not its visibility, is
+// what matters: the reports are atomics the host reads after a stream sync, so
+// no fence -- a gpu-scope fence here held every CTA until its pushes drained).
 __device__ __forceinline__ void health_tick(const Health& h) {
   if (!h.done) return;
-  __threadfence();
   if (atomicAdd(h.done, 1u) == gridDim.x - 1) {
     *h.done = 0;
     atomicAdd(h.step, 1ULL);
