@@ -63,14 +63,20 @@ def u_scale(f, rho):
     return float((np.abs(f) * cabs).sum(axis=0).__truediv__(rho).max())
 
 
-def assert_parity(fg_gpu, fg_ref, tol=TOL):
+def assert_parity(fg_gpu, fg_ref, tol=TOL, u_strict_tol=None):
+    """R18.  Also reports the strict ||du||_inf / ||u||_inf (no cancellation scale);
+    u_strict_tol, if given, bounds it too."""
     (f1, g1), (f0, g0) = fg_gpu, fg_ref
     r1, j1, p1 = R.macroscopic(f1, g1)
     r0, j0, p0 = R.macroscopic(f0, g0)
     u1, u0 = j1 / r1, j0 / r0
     u_err = float(np.abs(u1 - u0).max() / max(np.abs(u0).max(), u_scale(f0, r0)))
-    errs = {"f": rel(f1, f0), "g": rel(g1, g0), "phi": rel(p1, p0), "rho": rel(r1, r0), "u": u_err}
-    bad = {k: v for k, v in errs.items() if not v <= tol}
+    errs = {"f": rel(f1, f0), "g": rel(g1, g0), "phi": rel(p1, p0), "rho": rel(r1, r0), "u": u_err,
+            "u_strict": rel(u1, u0)}
+    print("parity (R18; u_strict = max|du| / max|u|):", {k: f"{v:.2e}" for k, v in errs.items()})
+    bad = {k: v for k, v in errs.items() if k != "u_strict" and not v <= tol}
+    if u_strict_tol is not None and not errs["u_strict"] <= u_strict_tol:
+        bad["u_strict"] = errs["u_strict"]
     assert not bad, f"parity errors above {tol}: {bad} (all: {errs})"
     return errs
 
@@ -122,9 +128,22 @@ def test_init_equilibrium_matches_oracle(kind, nslabs):
 
 # ------------------------------------------------------------------ parity
 def test_parity_16cubed_10_steps_spinodal():
-    """BASELINE config 1: 16^3, spinodal random phi +- 0.01, 10 steps, fp64."""
+    """BASELINE config 1: 16^3, spinodal random phi +- 0.01, 10 steps, fp64.  The
+    velocity is also held to the strict norm-wise 1e-12 (max|du| / max|u|, no
+    cancellation scale)."""
     f, g = spinodal(16, 16, 16)
-    assert_parity(gpu_run(f, g, P0, 10), R.run(f, g, P0, 10))
+    assert_parity(gpu_run(f, g, P0, 10), R.run(f, g, P0, 10), u_strict_tol=1e-12)
+
+
+@pytest.mark.parametrize("shape,steps", [((16, 16, 16), 100), ((24, 20, 18), 5), ((64, 64, 64), 10)])
+def test_parity_u_strict(shape, steps):
+    """The strict velocity error max|du| / max|u| on the spinodal quench (u builds up
+    from rest, so it is small and cancels in j = sum c f) and on the rough state:
+    reported, and bounded at 1e-11 (R18 bounds the cancellation-scaled form)."""
+    nx, ny, nz = shape
+    f, g = spinodal(nx, ny, nz, seed=3) if steps != 5 else rough(nx, ny, nz, seed=3)
+    errs = assert_parity(gpu_run(f, g, P0, steps), R.run(f, g, P0, steps), u_strict_tol=1e-11)
+    assert errs["u_strict"] >= 0
 
 
 @pytest.mark.parametrize("shape", [(16, 16, 16), (17, 19, 13), (3, 3, 3), (24, 20, 18), (33, 5, 4), (4, 31, 6)])
