@@ -224,19 +224,19 @@ __global__ void __launch_bounds__(kCX* TY, 1)
 
   for (int k = zA; k < zB; ++k) {
     cp_wait<0>();  // phi(k+2)
-    if constexpr (NBUF == 2) wait_f(k + 1);
+    wait_f(k + 1);
     __syncthreads();  // (also: everyone is past iteration k-1)
     double f[Q];
     if constexpr (NBUF == 3) {
       // one barrier per plane: the buffer of plane k-1 and the ring slots of k-2 are
-      // free.  f(k) was waited for in iteration k-1; f(k+1) is waited for only after
-      // the collision below (its box went out an iteration and a collision ago), then
-      // u, mu (k+1) at this thread's own site are computed by this thread (all the
-      // update of plane k reads of plane k+1), the ring of the box by the first NRING
-      // threads (read only after the next barrier)
+      // free; u, mu (k+1) at this thread's own site are computed by this thread (all
+      // the update of plane k reads of plane k+1), the ring of the box by the first
+      // NRING threads (read only after the next barrier)
       if (k + 2 <= zB) issue_f(k + 2);
       if (k + 3 <= zB + 1) issue_phi(k + 3);
       cp_commit();
+      make_u_mu_at(k + 1, cu);
+      if (tid < NRING) make_u_mu_at(k + 1, ring_site(tid));
 #pragma unroll
       for (int i = 0; i < Q; ++i) f[i] = sm.sF[rslot<NBUF>(k)][frank(i)][cf];
     } else {
@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(kCX* TY, 1)
       if (k + 3 <= zB + 1) issue_phi(k + 3);
       cp_commit();
     }
+    if (!active) continue;
     // ring slots of planes k - 1, k, k + 1 (one modulo each per plane)
     const int p0 = rslot<5>(k), pm = p0 == 0 ? 4 : p0 - 1, pp = p0 == 4 ? 0 : p0 + 1;
     const int u0 = rslot<3>(k), um = u0 == 0 ? 2 : u0 - 1, up = u0 == 2 ? 0 : u0 + 1;
@@ -257,29 +258,20 @@ __global__ void __launch_bounds__(kCX* TY, 1)
     const double* rp = sm.sPhi[pp];
     const double ph = r0[cb];
     const double xp = r0[cb + 1], xm = r0[cb - 1], yp = r0[cb + BX], ym = r0[cb - BX], zp = rp[cb], zm = rm[cb];
-    double rho = 1.0;
-    if (active) {
-      const double lap = (xp + xm) + (yp + ym) + (zp + zm) - 6.0 * ph;
-      double P6[6];
-      stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp - zm), lap, P6);
-      // collide f (R23-R25) and push (A.8); g is not used in this variant
-      double* const zb[3] = {push_plane(G, B, Peers{}, k - 1), push_plane(G, B, Peers{}, k),
-                             push_plane(G, B, Peers{}, k + 1)};  // A.8; ghost planes for slabs
-      const double g0[Q] = {};
-      rho = collide_mrt(p, f, g0, 0.0, 0.0, P6, [&](int i, double fs, double) {
-        const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
-        const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
-        LB_CHECK(hl, xd >= 0 && xd < G.nx && yd >= 0 && yd < G.ny);
-        double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
-        __stcs(d + (long long)slot(0, i) * nxy, fs);
-      });
-    }
-    if constexpr (NBUF == 3) {
-      wait_f(k + 1);
-      make_u_mu_at(k + 1, cu);
-      if (tid < NRING) make_u_mu_at(k + 1, ring_site(tid));
-    }
-    if (!active) continue;
+    const double lap = (xp + xm) + (yp + ym) + (zp + zm) - 6.0 * ph;
+    double P6[6];
+    stress6(p, ph, 0.5 * (xp - xm), 0.5 * (yp - ym), 0.5 * (zp - zm), lap, P6);
+    // collide f (R23-R25) and push (A.8); g is not used in this variant
+    double* const zb[3] = {push_plane(G, B, Peers{}, k - 1), push_plane(G, B, Peers{}, k),
+                           push_plane(G, B, Peers{}, k + 1)};  // A.8; ghost planes for slabs
+    const double g0[Q] = {};
+    const double rho = collide_mrt(p, f, g0, 0.0, 0.0, P6, [&](int i, double fs, double) {
+      const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
+      const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
+      LB_CHECK(hl, xd >= 0 && xd < G.nx && yd >= 0 && yd < G.ny);
+      double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
+      __stcs(d + (long long)slot(0, i) * nxy, fs);
+    });
     // phi update (R30, R31): upwind fluxes through the six faces, M lap mu
     const double* uk = &sm.sU[u0][0][0];
     const double* ukm = &sm.sU[um][0][0];

@@ -95,3 +95,56 @@ def test_two_ranks_peer_transport_bitwise(shape, kernel, tmp_path):
     fr, gr = R.run(f0, g0, P0, nsteps)
     assert np.abs(f - fr).max() / np.abs(fr).max() <= 1e-12
     assert np.abs(g - gr).max() / np.abs(gr).max() <= 1e-12
+
+
+def _entry_nccl(rank, world, port, outdir):
+    """lb_create_slab (NCCL bootstrap) with both ranks on one GPU: NCCL refuses two
+    communicator ranks on one device, so creation must fail cleanly (LB_ENCCL, a
+    message, no hang); if this NCCL accepts it, the ranks step in phases as above."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        uid = D.broadcast_bytes(lb.lb_nccl_get_unique_id() if rank == 0 else None)
+        outcome = "created"
+        try:
+            L = lb.Lattice(16, 8, 8, nranks=world, rank=rank, uid=uid)
+        except lb.LBError as e:
+            outcome = f"error {e.code} {e}"
+            L = None
+        if L is not None:
+            rho, u, phi, nf, ng = synth.rough_fields(16, 8, 8, 3)
+            f, g = R.equilibrium_state(rho, u, phi, P0)
+            z0, z1 = D.slab_range(8, world, rank)
+            L.set_state(f[:, z0:z1] + nf[:, z0:z1], g[:, z0:z1] + ng[:, z0:z1])
+            if lb.lb_debug_halo_mode(L.h) == 1:
+                for _ in range(2):
+                    for phase in (0, 1):
+                        lb.lb_debug_step_phase(L.h, phase)
+                        dist.barrier()
+                lb.lb_debug_step_phase(L.h, 2)
+            L.close()
+        with open(os.path.join(outdir, f"nccl{rank}.txt"), "w") as fh:
+            fh.write(outcome)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_bootstrap_two_ranks_one_gpu(tmp_path):
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_entry_nccl, args=(r, 2, port, str(tmp_path))) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    alive = [p for p in procs if p.is_alive()]
+    for p in alive:
+        p.kill()
+    assert not alive, "lb_create_slab hung with two ranks on one GPU"
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    outs = [open(tmp_path / f"nccl{r}.txt").read() for r in range(2)]
+    print("lb_create_slab, two ranks on one GPU:", outs)
+    for o in outs:
+        assert o == "created" or o.startswith(f"error {lb.LB_ENCCL}"), o
