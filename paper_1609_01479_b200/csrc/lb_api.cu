@@ -1227,6 +1227,21 @@ int lb_debug_tune(lb_t* h, int key, int value) {
       }
       if (!h->slabs.empty()) choose_xch(h);
       break;
+    case LB_TUNE_TILE_ROWS: {  // 4 or 8 (0: automatic); the TMA maps are re-encoded for it
+      const int ty = value == 0 ? step_tile_rows(h->G, h->num_sms) : value;
+      if (ty != 4 && ty != 8) return set_err(h, LB_EINVAL, "tile rows must be 4 or 8 (0: automatic)");
+      if (h->lc && ty != 8) return set_err(h, LB_EINVAL, "the liquid-crystal kernel has 32 x 8 tiles");
+      bool ok = true;
+      for (auto& s : h->slabs) {
+        ok = ok && make_step_maps(h->G, s.A, ty, &s.mapsA) && make_step_maps(h->G, s.B, ty, &s.mapsB);
+        if (h->ch) ok = ok && make_ch_maps(h->G, s.A, ty, &s.chA) && make_ch_maps(h->G, s.B, ty, &s.chB);
+      }
+      if (!ok) return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed");
+      h->ty = ty;
+      h->zc = step_zchunk(h->G, h->num_sms, h->ty);
+      if (!h->slabs.empty()) choose_xch(h);
+      break;
+    }
     case LB_TUNE_BAND_ROWS:
       if (value < 1) return set_err(h, LB_EINVAL, "band rows must be >= 1");
       h->order.band = value;

@@ -17,8 +17,8 @@ import torch  # noqa: E402
 from paper_1609_01479_b200 import lb, synth  # noqa: E402
 
 KEYS = {"zc": lb.LB_TUNE_ZCHUNK, "band": lb.LB_TUNE_BAND_ROWS, "resid": lb.LB_TUNE_RESID, "graphs": lb.LB_TUNE_GRAPHS,
-        "box": lb.LB_TUNE_L2_BOX, "ft": lb.LB_TUNE_L2_FTILE, "gt": lb.LB_TUNE_L2_GTILE}
-DEFAULTS = {"zc": 0, "band": 1, "resid": 0, "graphs": 1, "box": 2, "ft": 1, "gt": 1}
+        "box": lb.LB_TUNE_L2_BOX, "ft": lb.LB_TUNE_L2_FTILE, "gt": lb.LB_TUNE_L2_GTILE, "ty": lb.LB_TUNE_TILE_ROWS}
+DEFAULTS = {"zc": 0, "band": 1, "resid": 0, "graphs": 1, "box": 2, "ft": 1, "gt": 1, "ty": 0}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("nx", type=int)
@@ -33,8 +33,10 @@ a = ap.parse_args()
 
 phi = synth.spinodal_phi(a.nx, a.ny, a.nz, seed=0)
 out = {s: [] for s in a.settings}
-with lb.Lattice(a.nx, a.ny, a.nz) as L:
-    lb.lb_debug_step_kernel(L.h, a.kernel)
+Lat = lb.ChLattice if a.collision == "ch" else lb.Lattice
+with Lat(a.nx, a.ny, a.nz) as L:
+    if a.collision != "ch":
+        lb.lb_debug_step_kernel(L.h, a.kernel)
     if a.collision == "mrt":
         lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
     L.init_equilibrium(phi)

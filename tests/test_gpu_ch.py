@@ -167,3 +167,20 @@ def test_ch_parity_bench_launch_sampled():
         fs.append(f1[:, z, y, x]), ps.append(p1[z, y, x])
     assert rel(np.array(fs), np.array(fr)) <= TOL
     assert rel(np.array(ps), np.array(pr)) <= TOL
+
+
+@pytest.mark.parametrize("shape", [(64, 24, 12), (96, 40, 9)])
+def test_ch_tile_rows_bitwise(shape):
+    """32 x 4 tiles (two CTAs per SM) and 32 x 8 tiles (LB_TUNE_TILE_ROWS) give the
+    same bits, and both meet the oracle."""
+    nx, ny, nz = shape
+    f, phi = rough(nx, ny, nz, seed=57)
+    out = []
+    for ty in (4, 8):
+        with lb.ChLattice(nx, ny, nz, cparams(CP.base), CP.tau_s, CP.tau_b, CP.tau_ghost) as L:
+            lb.lb_debug_tune(L.h, lb.LB_TUNE_TILE_ROWS, ty)
+            L.set_state(f, phi)
+            L.step(4)
+            out.append(L.get_state())
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert_parity(out[0], CH.run(f, phi, CP, 4))

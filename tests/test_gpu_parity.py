@@ -251,13 +251,24 @@ def test_block_order_bands_bitwise(kernel, band):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_tile_rows_bitwise(kernel):
+    """32 x 4 tiles (LB_TUNE_TILE_ROWS 4: the TMA maps re-encoded) against the
+    default 32 x 8: the same bits for the tile and warp-specialised kernels."""
+    f, g = rough(96, 40, 12, seed=28)
+    a = gpu_run(f, g, P0, 3, kernel=kernel, tune={lb.LB_TUNE_TILE_ROWS: 4})
+    b = gpu_run(f, g, P0, 3, kernel=kernel)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
 def test_tune_errors_and_graphs_off():
     f, g = rough(32, 12, 10, seed=27)
     a = gpu_run(f, g, P0, 17, tune={lb.LB_TUNE_GRAPHS: 0})
     b = gpu_run(f, g, P0, 17)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     with lb.Lattice(8, 8, 8) as L:
-        for key, val in [(99, 1), (lb.LB_TUNE_ZCHUNK, -1), (lb.LB_TUNE_BAND_ROWS, 0), (lb.LB_TUNE_RESID, -2)]:
+        for key, val in [(99, 1), (lb.LB_TUNE_ZCHUNK, -1), (lb.LB_TUNE_BAND_ROWS, 0), (lb.LB_TUNE_RESID, -2),
+                         (lb.LB_TUNE_TILE_ROWS, 6), (lb.LB_TUNE_L2_BOX, 4)]:
             with pytest.raises(lb.LBError) as e:
                 lb.lb_debug_tune(L.h, key, val)
             assert e.value.code == lb.LB_EINVAL
