@@ -619,7 +619,7 @@ int one_step(lb_ctx* h, bool stream_only = false) {
       Slab& s = h->slabs[r];
       CK(h, timed(h, K_STEP, true, [&]() {
            return launch_step_ch(G, h->dp, s.A, s.B, s.phi, s.phi2, h->zc, health_of(h, r, r == last), &s.chA,
-                                 h->stream);
+                                 h->stream, h->kernel_choice != 1);
          }));
     }
     if (!G.zwrap && (rc = exchange_dist(h))) return rc;
@@ -1195,8 +1195,13 @@ int lb_prepare(lb_t* h) {
 }
 
 int lb_debug_step_kernel(lb_t* h, int which) {
-  if (h && (h->ch || h->lc) && which != 0)
-    return set_err(h, LB_EINVAL, "a Cahn-Hilliard or liquid-crystal handle has one step kernel");
+  if (h && h->lc && which != 0) return set_err(h, LB_EINVAL, "a liquid-crystal handle has one step kernel");
+  if (h && h->ch) {  // 0 auto (warp-specialised for 32 x 8 tiles), 1 tile kernel, 2 warp-specialised
+    if (which < 0 || which > 2) return set_err(h, LB_EINVAL, "a Cahn-Hilliard handle: which must be 0, 1 or 2");
+    h->kernel_choice = which;
+    steps_changed(h);
+    return LB_OK;
+  }
   if (!h || which < 0 || which > 3)
     return set_err(h, LB_EINVAL,
                    "which must be 0 (auto), 1 (tile), 2 (warp-specialised) or 3 (warp-specialised with the phi exchange)");

@@ -252,8 +252,9 @@ struct alignas(64) ChMaps {
   bool ok;
 };
 bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out);
+// ws: the warp-specialised kernel (32 x 8 tiles; same bits), else the tile kernel
 cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
-                           double* phiB, int zc, const Health& hl, const ChMaps* mapsA, cudaStream_t st);
+                           double* phiB, int zc, const Health& hl, const ChMaps* mapsA, cudaStream_t st, bool ws);
 // the liquid-crystal workload (lb_step_lc.cu, NEXT-4): state f (dist buffer, f slots),
 // Q (five components, q[z][c][y][x]) and u (q[z][a][y][x]); 32 x 8 tiles, the f tile
 // by TMA through maps m[0] (5 components) and m[1] (9) of make_step_maps(.., 8, ..)

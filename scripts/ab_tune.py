@@ -35,8 +35,7 @@ phi = synth.spinodal_phi(a.nx, a.ny, a.nz, seed=0)
 out = {s: [] for s in a.settings}
 Lat = lb.ChLattice if a.collision == "ch" else lb.Lattice
 with Lat(a.nx, a.ny, a.nz) as L:
-    if a.collision != "ch":
-        lb.lb_debug_step_kernel(L.h, a.kernel)
+    lb.lb_debug_step_kernel(L.h, a.kernel)
     if a.collision == "mrt":
         lb.lb_set_collision(L.h, 1, 0.8, 1.1, 1.0)
     L.init_equilibrium(phi)

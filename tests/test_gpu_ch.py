@@ -111,7 +111,7 @@ def test_ch_init_equilibrium_and_errors():
         assert np.array_equal(p1, phi)
         assert rel(f1, R.f_equilibrium(np.ones_like(phi), np.zeros((3,) + phi.shape))) <= 1e-15
         for call in (lambda: lb.lb_get_state(L.h), lambda: lb.lb_set_collision(L.h, 1),
-                     lambda: lb.lb_debug_step_kernel(L.h, 2)):
+                     lambda: lb.lb_debug_step_kernel(L.h, 3)):
             with pytest.raises(lb.LBError) as e:
                 call()
             assert e.value.code == lb.LB_EINVAL
@@ -184,3 +184,33 @@ def test_ch_tile_rows_bitwise(shape):
             out.append(L.get_state())
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert_parity(out[0], CH.run(f, phi, CP, 4))
+
+
+def _run_kernel(f, phi, nsteps, kernel, nslabs=1, zchunk=None):
+    nz, ny, nx = f.shape[1:]
+    with lb.ChLattice(nx, ny, nz, cparams(CP.base), CP.tau_s, CP.tau_b, CP.tau_ghost, nslabs=nslabs) as L:
+        lb.lb_debug_step_kernel(L.h, kernel)
+        if zchunk:
+            lb.lb_debug_tune(L.h, lb.LB_TUNE_ZCHUNK, zchunk)
+        L.set_state(f, phi)
+        L.step(nsteps)
+        return L.get_state()
+
+
+@pytest.mark.parametrize("shape,nslabs,zchunk", [((16, 16, 16), 1, None), ((34, 10, 7), 1, None),
+                                                 ((64, 24, 12), 1, 1), ((64, 24, 12), 1, 2), ((96, 40, 9), 1, 4),
+                                                 ((64, 16, 16), 2, None), ((32, 16, 12), 3, None),
+                                                 ((512, 304, 8), 1, None)])
+def test_ch_ws_kernel_bitwise_equal_tile_kernel(shape, nslabs, zchunk):
+    """The warp-specialised Cahn-Hilliard kernel (collision warps: f box, P, MRT,
+    push and every copy; stencil warps: u, mu and the phi update) gives the bits of
+    the tile kernel k_step_ch: one tile, ragged and wrapped tiles, z-chunks of 1, 2
+    and 4 planes, loopback slabs, several waves; and meets the oracle."""
+    nx, ny, nz = shape
+    f, phi = rough(nx, ny, nz, seed=58)
+    steps = 3 if nx * ny * nz > 100_000 else 5
+    a = _run_kernel(f, phi, steps, 2, nslabs, zchunk)
+    b = _run_kernel(f, phi, steps, 1, nslabs, zchunk)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    if nx * ny * nz <= 40_000:
+        assert_parity(a, CH.run(f, phi, CP, steps))
