@@ -969,7 +969,7 @@ int ch_create(int nx, int ny, int nz, const lb_params* params, double tau_shear,
   for (auto& s : h->slabs) {
     if (e == cudaSuccess) e = dev_alloc(h, &s.phi2, phi_doubles(h->G) * sizeof(double));
     if (e == cudaSuccess) e = cudaMemsetAsync(s.phi2, 0xff, phi_doubles(h->G) * sizeof(double), h->stream);
-    maps_ok = maps_ok && make_ch_maps(h->G, s.A, h->ty, &s.chA) && make_ch_maps(h->G, s.B, h->ty, &s.chB);
+    maps_ok = maps_ok && make_ch_maps(h->G, s.A, s.phi, h->ty, &s.chA) && make_ch_maps(h->G, s.B, s.phi2, h->ty, &s.chB);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess || !maps_ok) {
@@ -1239,7 +1239,7 @@ int lb_debug_tune(lb_t* h, int key, int value) {
       bool ok = true;
       for (auto& s : h->slabs) {
         ok = ok && make_step_maps(h->G, s.A, ty, &s.mapsA) && make_step_maps(h->G, s.B, ty, &s.mapsB);
-        if (h->ch) ok = ok && make_ch_maps(h->G, s.A, ty, &s.chA) && make_ch_maps(h->G, s.B, ty, &s.chB);
+        if (h->ch) ok = ok && make_ch_maps(h->G, s.A, s.phi, ty, &s.chA) && make_ch_maps(h->G, s.B, s.phi2, ty, &s.chB);
       }
       if (!ok) return set_err(h, LB_ECUDA, "cuTensorMapEncodeTiled failed");
       h->ty = ty;

@@ -246,12 +246,15 @@ cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, d
                            const XchArgs* xch = nullptr);
 // the finite-difference Cahn-Hilliard variant (lb_step_ch.cu, NEXT-2): state f and
 // a phi field; one TMA map (f box of one component, (32+4) x (ty+2)); one slab
+// m[0]: f box of one component ((32+4) x (ty+2)); m[1], m[2]: the same box over 5
+// and 9 components (the f slot runs); m[3]: the phi box (32+4) x (ty+4) of the phi
+// buffer paired with this distribution buffer (they swap together)
 struct alignas(64) ChMaps {
-  unsigned char m[128];
+  unsigned char m[4][128];
   int ty;
   bool ok;
 };
-bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out);
+bool make_ch_maps(const Geom& G, const double* buf, const double* phibuf, int ty, ChMaps* out);
 // ws: the warp-specialised kernel (32 x 8 tiles; same bits), else the tile kernel
 cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
                            double* phiB, int zc, const Health& hl, const ChMaps* mapsA, cudaStream_t st, bool ws);

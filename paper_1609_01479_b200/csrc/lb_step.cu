@@ -436,6 +436,26 @@ bool encode_dist_map(CUtensorMap* m, const Geom& G, const double* buf, unsigned 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// a phi buffer as a 3-D fp64 tensor {x: nx, y: ny, plane: nzl + 2GP} (ghost planes included)
+bool encode_phi_map(CUtensorMap* m, const Geom& G, const double* phi, unsigned bx, unsigned by) {
+  auto fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)G.nx, (cuuint64_t)G.ny, (cuuint64_t)(G.nzl + 2 * GP)};
+  cuuint64_t strides[2] = {(cuuint64_t)G.nx * 8, (cuuint64_t)G.nxy * 8};
+  cuuint32_t box[3] = {bx, by, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(phi), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Tile rows of the step kernel.  Even nx (TMA rows): 32 x 8 tiles and the
 // warp-specialised kernel for every plane size -- measured in round 1 against
 // 32 x 4 tiles of the tile kernel (two CTAs per SM): +12% at 128^3, +17% at 64^3,

@@ -319,10 +319,16 @@ struct alignas(128) ChWsSmem {
   static constexpr int NBUF = 3;
   static constexpr int TX = kCX, NT = TX * TY;
   static constexpr int FX = TX + 4, FY = TY + 2;
-  static constexpr int FS = ((FX * FY + 15) / 16) * 16;
+  static constexpr int FB = FX * FY;  // one component of the f box
+  // the box as the three f slot runs (5, 9, 5 components, each one TMA copy), each
+  // run starting 128-byte aligned
+  static constexpr int al16(int v) { return (v + 15) / 16 * 16; }
+  static constexpr int RUN1 = al16(5 * FB), RUN2 = al16(RUN1 + 9 * FB), BOXD = al16(RUN2 + 5 * FB);
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;
   static constexpr int UX = TX + 2, UY = TY + 2, NU = UX * UY;
-  alignas(128) double sF[NBUF][Q][FS];
+  // component of rank j (f slot order) in a box
+  __device__ static constexpr int fofs(int j) { return j < 5 ? j * FB : (j < 14 ? RUN1 + (j - 5) * FB : RUN2 + (j - 14) * FB); }
+  alignas(128) double sF[NBUF][BOXD];
   alignas(128) double sPhi[5][NB];
   double sU[3][3][NU];
   double sMu[3][NU];
@@ -342,11 +348,12 @@ template <int TY>
 __global__ void __launch_bounds__(2 * kCX * TY, 1)
     k_step_ch_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
                  const double* __restrict__ phiA, double* __restrict__ phiB, int zc, Health hl,
-                 const __grid_constant__ CUtensorMap tm_f1) {
+                 const __grid_constant__ CUtensorMap tm_f5, const __grid_constant__ CUtensorMap tm_f9,
+                 const __grid_constant__ CUtensorMap tm_phi) {
   using S = ChWsSmem<TY>;
   constexpr int TX = kCX, NT = S::NT;
-  constexpr int FX = S::FX, FY = S::FY, FS = S::FS, BX = S::BX, UX = S::UX, NU = S::NU;
-  constexpr unsigned FBOX_BYTES = Q * FX * FY * 8;
+  constexpr int FX = S::FX, FY = S::FY, BX = S::BX, UX = S::UX, NU = S::NU;
+  constexpr unsigned FBOX_BYTES = Q * S::FB * 8, PBOX_BYTES = S::NB * 8;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
@@ -358,6 +365,7 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
   const int zB = min(zA + zc, G.nzl);
   const long long nxy = G.nxy;
   const bool fbox_tma = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 1 && y0 + TY + 1 <= G.ny;
+  const bool pbox_tma = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
   auto wrapx = [&](int v) { v %= G.nx; return v < 0 ? v + G.nx : v; };
   auto wrapy = [&](int v) { v %= G.ny; return v < 0 ? v + G.ny : v; };
   auto zf = [&](int z) { return G.zwrap ? zwrap1(z, G.nzl) : z; };
@@ -369,7 +377,7 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
 
   if (tid == 0) {
     for (int b = 0; b < 3; ++b) mbar_init(&sm.box_full[b], fbox_tma ? 1 : NT);
-    for (int q = 0; q < 5; ++q) mbar_init(&sm.phi_full[q], NT);
+    for (int q = 0; q < 5; ++q) mbar_init(&sm.phi_full[q], pbox_tma ? 1 : NT);
     for (int d = 0; d < 2; ++d) mbar_init(&sm.sdone[d], NT);
     fence_barrier_init();
   }
@@ -391,19 +399,20 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
       const int row = u / FROWU, cu = u - row * FROWU;
       fb_src[r] = (long long)wrapy(y0 - 1 + row) * G.nx + wrapx(x0 - 2 + cu * 2);
       fb_dst[r] = u < FBU ? row * FX + cu * 2 : -1;
-      LB_CHECK(hl, fb_dst[r] < 0 || (fb_dst[r] + 1 < FS && fb_src[r] >= 0 && fb_src[r] + 1 < nxy));
+      LB_CHECK(hl, fb_dst[r] < 0 || (fb_dst[r] + 1 < S::FB && fb_src[r] >= 0 && fb_src[r] + 1 < nxy));
     }
     auto issue_box = [&](int b) {  // f box of plane b into its slot (b <= zB)
       const int sl = bslot(b);
       const int zs = zf(b);
+      double* box = sm.sF[sl];
       if (fbox_tma) {
-        if (tid == 0) {
+        if (tid == 0) {  // three copies: the f slot runs 0..4, 10..18, 28..32
           fence_proxy_async();
           mbar_expect_tx(&sm.box_full[sl], FBOX_BYTES);
           const int cpl = (zs + GZ) * NSLOT;
-#pragma unroll 1
-          for (int j = 0; j < Q; ++j)
-            tma_load_3d(&sm.sF[sl][j][0], &tm_f1, x0 - 2, y0 - 1, cpl + fslot_of_rank(j), &sm.box_full[sl], pol_f);
+          tma_load_3d(box, &tm_f5, x0 - 2, y0 - 1, cpl, &sm.box_full[sl], pol_f);
+          tma_load_3d(box + S::RUN1, &tm_f9, x0 - 2, y0 - 1, cpl + 10, &sm.box_full[sl], pol_f);
+          tma_load_3d(box + S::RUN2, &tm_f5, x0 - 2, y0 - 1, cpl + 28, &sm.box_full[sl], pol_f);
         }
       } else {
         const double* base = A + (long long)(zs + GZ) * G.plane;
@@ -412,7 +421,7 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
           const double* bj = base + (long long)fslot_of_rank(j) * nxy;
 #pragma unroll
           for (int r = 0; r < FBR; ++r)
-            if (fb_dst[r] >= 0) cp_async_v<2>(&sm.sF[sl][j][fb_dst[r]], bj + fb_src[r]);
+            if (fb_dst[r] >= 0) cp_async_v<2>(box + S::fofs(j) + fb_dst[r], bj + fb_src[r]);
         }
         cp_async_arrive_noinc(&sm.box_full[sl]);
       }
@@ -429,8 +438,16 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
       LB_CHECK(hl, pb_dst[r] < 0 || (pb_dst[r] + 1 < S::NB && pb_src[r] >= 0 && pb_src[r] + 1 < nxy));
     }
     auto issue_phi = [&](int q) {  // phi box of plane q into its ring slot (q <= zB + 1)
-      const double* base = phiA + phi_plane_index(G, zf(q));
       double* ring = sm.sPhi[pslot(q)];
+      if (pbox_tma) {
+        if (tid == 0) {
+          fence_proxy_async();
+          mbar_expect_tx(&sm.phi_full[pslot(q)], PBOX_BYTES);
+          tma_load_3d(ring, &tm_phi, x0 - 2, y0 - 2, zf(q) + GP, &sm.phi_full[pslot(q)], pol_f);
+        }
+        return;
+      }
+      const double* base = phiA + phi_plane_index(G, zf(q));
 #pragma unroll
       for (int r = 0; r < PBR; ++r)
         if (pb_dst[r] >= 0) cp_async_v<2>(&ring[pb_dst[r]], base + pb_src[r]);
@@ -449,7 +466,7 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
       double f[Q];
       mbar_wait(&sm.box_full[bslot(k)], bpar(k));
 #pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = sm.sF[bslot(k)][frank(i)][cf];
+      for (int i = 0; i < Q; ++i) f[i] = sm.sF[bslot(k)][S::fofs(frank(i)) + cf];
       // the stencil is past plane k-1: box k (u, mu(k)) and phi k-2 are free once
       // every collision thread has read f(k) too
       const int jd = k - 1 - (zA - 2);
@@ -489,7 +506,7 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
     const int x = x0 + lx, y = y0 + ly;
     const bool active = x < G.nx && y < G.ny;
     auto make_u_mu_at = [&](int zp, int e) {  // u, mu of plane zp at box site e (k_step_ch's arithmetic)
-      const double(*fb)[FS] = sm.sF[bslot(zp)];
+      const double* fb = sm.sF[bslot(zp)];
       double(*u3)[NU] = sm.sU[rslot<3>(zp)];
       double* mu = sm.sMu[rslot<3>(zp)];
       const double* f0 = sm.sPhi[pslot(zp - 1)];
@@ -500,7 +517,7 @@ __global__ void __launch_bounds__(2 * kCX * TY, 1)
       double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
 #pragma unroll
       for (int i = 0; i < Q; ++i) {  // A.3, canonical order
-        const double v = fb[frank(i)][fi];
+        const double v = fb[S::fofs(frank(i)) + fi];
         rho += v;
         if (cx(i)) jx += cx(i) * v;
         if (cy(i)) jy += cy(i) * v;
@@ -569,7 +586,7 @@ cudaError_t launch_ch_t(const Geom& G, const DevParams& p, const double* A, doub
   if (e != cudaSuccess) return e;
   const int tiles = ((G.nx + kCX - 1) / kCX) * ((G.ny + TY - 1) / TY);
   const int nblk = tiles * ((G.nzl + zc - 1) / zc);
-  kern<<<nblk, kCX * TY, smem, st>>>(G, p, A, B, phiA, phiB, zc, hl, *reinterpret_cast<const CUtensorMap*>(maps->m));
+  kern<<<nblk, kCX * TY, smem, st>>>(G, p, A, B, phiA, phiB, zc, hl, reinterpret_cast<const CUtensorMap*>(maps->m)[0]);
   return cudaGetLastError();
 }
 
@@ -584,7 +601,8 @@ cudaError_t launch_ch_ws_t(const Geom& G, const DevParams& p, const double* A, d
   if (e != cudaSuccess) return e;
   const int tiles = ((G.nx + kCX - 1) / kCX) * ((G.ny + TY - 1) / TY);
   const int nblk = tiles * ((G.nzl + zc - 1) / zc);
-  kern<<<nblk, 2 * kCX * TY, smem, st>>>(G, p, A, B, phiA, phiB, zc, hl, *reinterpret_cast<const CUtensorMap*>(maps->m));
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
+  kern<<<nblk, 2 * kCX * TY, smem, st>>>(G, p, A, B, phiA, phiB, zc, hl, m[1], m[2], m[3]);
   return cudaGetLastError();
 }
 
@@ -599,11 +617,14 @@ cudaError_t prepare_ch_kernels() {
   return e;
 }
 
-bool make_ch_maps(const Geom& G, const double* buf, int ty, ChMaps* out) {
+bool make_ch_maps(const Geom& G, const double* buf, const double* phibuf, int ty, ChMaps* out) {
   out->ok = false;
   out->ty = ty;
   if (G.nx % 2 != 0) return false;
-  if (!encode_dist_map(reinterpret_cast<CUtensorMap*>(out->m), G, buf, kCX + 4, ty + 2, 1)) return false;
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out->m);
+  if (!encode_dist_map(&m[0], G, buf, kCX + 4, ty + 2, 1) || !encode_dist_map(&m[1], G, buf, kCX + 4, ty + 2, 5) ||
+      !encode_dist_map(&m[2], G, buf, kCX + 4, ty + 2, 9) || !encode_phi_map(&m[3], G, phibuf, kCX + 4, ty + 4))
+    return false;
   out->ok = true;
   return true;
 }

@@ -119,5 +119,7 @@ __host__ __device__ constexpr int run_rank0(int r) { return r == 0 ? 0 : (r == 1
 
 // host: 3-D fp64 tensor map of a distribution buffer {x: nx, y: ny, comp-plane: (nzl+2GZ)*38}
 bool encode_dist_map(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsigned by, unsigned bz);
+// host: 3-D fp64 tensor map of a phi buffer {x: nx, y: ny, plane: nzl+2GP}, boxes bx x by x 1
+bool encode_phi_map(CUtensorMap* m, const Geom& G, const double* phi, unsigned bx, unsigned by);
 
 }  // namespace lbk

@@ -1,0 +1,7 @@
+# CH ws kernel with 3-run TMA f boxes and TMA phi boxes: tests, A/B, bench
+mkdir -p gpurun_out
+python -c "from paper_1609_01479_b200 import _build; _build.build(force=True); _build.build(force=True, checked=True)" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_ch.py tests/test_gpu_memsafety.py -q -m gpu -x > gpurun_out/t_ch.log 2>&1; echo tests=$?; tail -3 gpurun_out/t_ch.log
+timeout 300 python scripts/ab_tune.py 512 512 64 zc=0 --kernel 2 --collision ch --rounds 3 > gpurun_out/ab_chws.json 2>&1; cat gpurun_out/ab_chws.json
+timeout 300 python scripts/ab_tune.py 512 512 64 zc=0 --kernel 1 --collision ch --rounds 2 > gpurun_out/ab_chtile.json 2>&1; cat gpurun_out/ab_chtile.json
+timeout 600 python bench.py --collision ch --steps 100 --warmup 5 > gpurun_out/bench_ch.json 2> gpurun_out/bench_ch.err; echo bench=$?; head -c 250 gpurun_out/bench_ch.json; echo
