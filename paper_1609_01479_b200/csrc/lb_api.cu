@@ -69,6 +69,7 @@ struct lb_ctx {
   TileOrder order{0, 1};  // block order of the step kernels (0: the kernel's occupancy)
   L2Pol l2{};             // L2 policies of the warp-specialised kernel's copies
   bool graphs_on = true;  // lb_debug_tune(LB_TUNE_GRAPHS)
+  int variant = 0;        // lb_debug_tune(LB_TUNE_VARIANT): a kernel-internal alternative, for A/B
   bool ch = false;        // NEXT-2 handle: state (f, phi), lb_create_ch
   bool lc = false;        // NEXT-4 handle: state (f, Q, u), lb_create_lc
   int lczc = 1;           // z-chunk of the liquid-crystal step kernel
@@ -619,7 +620,7 @@ int one_step(lb_ctx* h, bool stream_only = false) {
       Slab& s = h->slabs[r];
       CK(h, timed(h, K_STEP, true, [&]() {
            return launch_step_ch(G, h->dp, s.A, s.B, s.phi, s.phi2, h->zc, health_of(h, r, r == last), &s.chA,
-                                 h->stream, h->kernel_choice != 1);
+                                 h->stream, h->kernel_choice != 1, h->variant);
          }));
     }
     if (!G.zwrap && (rc = exchange_dist(h))) return rc;
@@ -1257,6 +1258,10 @@ int lb_debug_tune(lb_t* h, int key, int value) {
       break;
     case LB_TUNE_GRAPHS:
       h->graphs_on = value != 0;
+      break;
+    case LB_TUNE_VARIANT:
+      if (value < 0 || value > 1) return set_err(h, LB_EINVAL, "variant must be 0 or 1");
+      h->variant = value;
       break;
     case LB_TUNE_L2_BOX:
     case LB_TUNE_L2_FTILE:

@@ -255,9 +255,11 @@ struct alignas(64) ChMaps {
   bool ok;
 };
 bool make_ch_maps(const Geom& G, const double* buf, const double* phibuf, int ty, ChMaps* out);
-// ws: the warp-specialised kernel (32 x 8 tiles; same bits), else the tile kernel
+// ws: the warp-specialised kernel (32 x 8 tiles; same bits), else the tile kernel;
+// variant (LB_TUNE_VARIANT, measurement): 1 = the ws kernel with a 5-plane phi ring
 cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, double* B, const double* phiA,
-                           double* phiB, int zc, const Health& hl, const ChMaps* mapsA, cudaStream_t st, bool ws);
+                           double* phiB, int zc, const Health& hl, const ChMaps* mapsA, cudaStream_t st, bool ws,
+                           int variant = 0);
 // the liquid-crystal workload (lb_step_lc.cu, NEXT-4): state f (dist buffer, f slots),
 // Q (five components, q[z][c][y][x]) and u (q[z][a][y][x]); 32 x 8 tiles, the f tile
 // by TMA through maps m[0] (5 components) and m[1] (9) of make_step_maps(.., 8, ..)

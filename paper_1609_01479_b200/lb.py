@@ -232,7 +232,7 @@ def lb_debug_step_kernel(h, which: int) -> None:
 
 # lb_debug_tune keys (include/lb.h)
 LB_TUNE_ZCHUNK, LB_TUNE_BAND_ROWS, LB_TUNE_RESID, LB_TUNE_GRAPHS = 1, 2, 3, 4
-LB_TUNE_L2_BOX, LB_TUNE_L2_FTILE, LB_TUNE_L2_GTILE, LB_TUNE_TILE_ROWS = 5, 6, 7, 8
+LB_TUNE_L2_BOX, LB_TUNE_L2_FTILE, LB_TUNE_L2_GTILE, LB_TUNE_TILE_ROWS, LB_TUNE_VARIANT = 5, 6, 7, 8, 9
 
 
 def lb_debug_tune(h, key: int, value: int) -> None:

@@ -17,8 +17,9 @@ import torch  # noqa: E402
 from paper_1609_01479_b200 import lb, synth  # noqa: E402
 
 KEYS = {"zc": lb.LB_TUNE_ZCHUNK, "band": lb.LB_TUNE_BAND_ROWS, "resid": lb.LB_TUNE_RESID, "graphs": lb.LB_TUNE_GRAPHS,
-        "box": lb.LB_TUNE_L2_BOX, "ft": lb.LB_TUNE_L2_FTILE, "gt": lb.LB_TUNE_L2_GTILE, "ty": lb.LB_TUNE_TILE_ROWS}
-DEFAULTS = {"zc": 0, "band": 1, "resid": 0, "graphs": 1, "box": 2, "ft": 1, "gt": 1, "ty": 0}
+        "box": lb.LB_TUNE_L2_BOX, "ft": lb.LB_TUNE_L2_FTILE, "gt": lb.LB_TUNE_L2_GTILE, "ty": lb.LB_TUNE_TILE_ROWS,
+        "var": lb.LB_TUNE_VARIANT}
+DEFAULTS = {"zc": 0, "band": 1, "resid": 0, "graphs": 1, "box": 2, "ft": 1, "gt": 1, "ty": 0, "var": 0}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("nx", type=int)

@@ -186,10 +186,11 @@ def test_ch_tile_rows_bitwise(shape):
     assert_parity(out[0], CH.run(f, phi, CP, 4))
 
 
-def _run_kernel(f, phi, nsteps, kernel, nslabs=1, zchunk=None):
+def _run_kernel(f, phi, nsteps, kernel, nslabs=1, zchunk=None, variant=0):
     nz, ny, nx = f.shape[1:]
     with lb.ChLattice(nx, ny, nz, cparams(CP.base), CP.tau_s, CP.tau_b, CP.tau_ghost, nslabs=nslabs) as L:
         lb.lb_debug_step_kernel(L.h, kernel)
+        lb.lb_debug_tune(L.h, lb.LB_TUNE_VARIANT, variant)
         if zchunk:
             lb.lb_debug_tune(L.h, lb.LB_TUNE_ZCHUNK, zchunk)
         L.set_state(f, phi)
@@ -211,6 +212,8 @@ def test_ch_ws_kernel_bitwise_equal_tile_kernel(shape, nslabs, zchunk):
     steps = 3 if nx * ny * nz > 100_000 else 5
     a = _run_kernel(f, phi, steps, 2, nslabs, zchunk)
     b = _run_kernel(f, phi, steps, 1, nslabs, zchunk)
+    c = _run_kernel(f, phi, steps, 2, nslabs, zchunk, variant=1)  # 5-plane phi ring
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(c[0], b[0]) and np.array_equal(c[1], b[1])
     if nx * ny * nz <= 40_000:
         assert_parity(a, CH.run(f, phi, CP, steps))
