@@ -638,9 +638,15 @@ cudaError_t launch_step_ch(const Geom& G, const DevParams& p, const double* A, d
                            double* phiB, int zc, const Health& hl, const ChMaps* maps, cudaStream_t st, bool ws,
                            int variant) {
   if (!maps || !maps->ok) return cudaErrorInvalidValue;
-  if (maps->ty == 8 && ws)
-    return variant == 1 ? launch_ch_ws_t<8, 5>(G, p, A, B, phiA, phiB, zc, hl, maps, st)
-                        : launch_ch_ws_t<8, 6>(G, p, A, B, phiA, phiB, zc, hl, maps, st);
+  if (maps->ty == 8 && ws) {
+    // phi ring of 6 planes over several waves (512 x 512 x 64: +2% over 5), of 5 where
+    // every block runs in the first wave (128^3: +2% over 6); variant 1 forces 5
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long nblk = (long long)((G.nx + kCX - 1) / kCX) * ((G.ny + 7) / 8) * ((G.nzl + zc - 1) / zc);
+    return variant == 1 || nblk <= sms ? launch_ch_ws_t<8, 5>(G, p, A, B, phiA, phiB, zc, hl, maps, st)
+                                       : launch_ch_ws_t<8, 6>(G, p, A, B, phiA, phiB, zc, hl, maps, st);
+  }
   if (maps->ty == 8) return launch_ch_t<8>(G, p, A, B, phiA, phiB, zc, hl, maps, st);
   return launch_ch_t<4>(G, p, A, B, phiA, phiB, zc, hl, maps, st);
 }
