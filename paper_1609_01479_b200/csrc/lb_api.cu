@@ -336,7 +336,6 @@ Launch launch_of(const lb_ctx* h) {
   ln.zc = h->zc;
   ln.order = h->order;
   ln.l2 = h->l2;
-  ln.variant = h->variant;
   return ln;
 }
 

@@ -217,8 +217,7 @@ struct L2Pol {
 struct Launch {
   int zc = 1;
   TileOrder order{0, 1};
-  L2Pol l2{};       // warp-specialised kernel
-  int variant = 0;  // LB_TUNE_VARIANT: 1 = the previous alternative of a kernel (A/B)
+  L2Pol l2{};  // warp-specialised kernel
 };
 cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
                         const Launch& ln, const Health& hl, const StepMaps* mapsA, cudaStream_t st,

@@ -71,27 +71,21 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// BOX2: two g-box buffers (the stencil issues box n+2 as soon as phi of box n is
-// summed: a full iteration more lead) paid for by the f tile's buffer -- the
-// collision warps load f of their site straight from global memory (coalesced
-// 256-byte rows per warp and component) at the top of an iteration, so the loads
-// are in flight while they wait for the stencil's hand-off and the g tile.
-template <int TY, int COLL, bool XCH = false, bool BOX2 = false>
+template <int TY, int COLL, bool XCH = false>
 struct alignas(128) WsSmem {
   static constexpr int NPHI = XCH ? kXchLag + 4 : 5;  // phi ring planes (XCH: lag planes more)
   static constexpr int NQ = COLL == 1 ? 8 : 5;  // hand-off values per site
   static constexpr int TX = kWTX, NT = TX * TY;
   static constexpr int BX = TX + 4, BY = TY + 4, NB = BX * BY;  // phi box: tile + 2 halo
   static constexpr int PX = TX + 2, PY = TY + 2, NP = PX * PY;  // P box: tile + 1 halo
-  static constexpr int NBOX = BOX2 ? 2 : 1;
-  alignas(128) double sTf[BOX2 ? 1 : Q][NT];  // f of the tile, f-slot order (TMA boxes TX x TY x 5|9|5)
+  alignas(128) double sTf[Q][NT];  // f of the tile, f-slot order (TMA boxes TX x TY x 5|9|5)
   alignas(128) double sTg[Q][NT];  // g of the tile, g-slot order
   // g on the box, g-slot order (TMA boxes BX x BY x 5|9|5); XCH: two g tiles [Q][NT]
-  alignas(128) double sG[NBOX][Q][XCH ? 2 * NT : NB];
+  alignas(128) double sG[Q][XCH ? 2 * NT : NB];
   double sPhi[NPHI][NB];           // ring of phi planes on the box
   double sP[6][NP];                // chemical stress of one plane on the P box
   double sQ[2][NQ][NT];            // hand-off: phi, mu, then Fx, Fy, Fz (COLL 0) or P (COLL 1)
-  unsigned long long bar_f, bar_g, bar_box[2], bar_xb[2], q_full[2], q_empty[2];
+  unsigned long long bar_f, bar_g, bar_box, bar_xb[2], q_full[2], q_empty[2];
 };
 
 // XCH (phi exchange; one periodic slab, whole 32 x 8 tiles): the stencil warps
@@ -107,15 +101,14 @@ struct alignas(128) WsSmem {
 // one wave (the tiles' CTAs start together and stay within the lag of each
 // other: 128^3, 64^3); over several waves the neighbours drift apart and the
 // fallback sums cost more than the box.
-template <int TY, int COLL, bool XCH = false, bool BOX2 = false>
+template <int TY, int COLL, bool XCH = false>
 __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
               const double* __restrict__ phig, int zc, TileOrder ord, L2Pol l2, Health hl, Peers pr, XchArgs xa,
               const __grid_constant__ CUtensorMap tm_t5, const __grid_constant__ CUtensorMap tm_t9,
               const __grid_constant__ CUtensorMap tm_g5, const __grid_constant__ CUtensorMap tm_g9) {
-  using S = WsSmem<TY, COLL, XCH, BOX2>;
+  using S = WsSmem<TY, COLL, XCH>;
   static_assert(!XCH || (TY == 8 && COLL == 0), "phi exchange: 32 x 8 tiles, BGK");
-  static_assert(!(XCH && BOX2), "the phi exchange has its own two g-tile buffers");
   constexpr int TX = kWTX, NT = S::NT;
   constexpr int BX = S::BX, BY = S::BY, NB = S::NB, PX = S::PX, NP = S::NP;
   constexpr unsigned TILE_BYTES = Q * NT * 8, BOX_BYTES = Q * NB * 8;
@@ -136,8 +129,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
   if (tid == 0) {
     mbar_init(&sm.bar_f, 1);
     mbar_init(&sm.bar_g, 1);
-    mbar_init(&sm.bar_box[0], 1);
-    mbar_init(&sm.bar_box[1], 1);
+    mbar_init(&sm.bar_box, 1);
     mbar_init(&sm.bar_xb[0], 1);
     mbar_init(&sm.bar_xb[1], 1);
     for (int s = 0; s < 2; ++s) {
@@ -200,7 +192,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       if (XCH && !use_box) {
         if (a == 0) {  // the g tile only, in tile layout, into buffer n & 1
           const int cpl = (zs + GZ) * NSLOT;
-          double* dst = &sm.sG[0][0][0] + (n & 1) * Q * NT;
+          double* dst = &sm.sG[0][0] + (n & 1) * Q * NT;
           unsigned long long* bar = &sm.bar_xb[n & 1];
           fence_proxy_async();
           mbar_expect_tx(bar, TILE_BYTES);
@@ -210,41 +202,35 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         }
       } else if (box_interior) {
         if (a == 0) {
-          const int sl = BOX2 ? (n & 1) : 0;
           const int cpl = (zs + GZ) * NSLOT;
           fence_proxy_async();
-          mbar_expect_tx(&sm.bar_box[sl], BOX_BYTES);
-          tma_load_3d(&sm.sG[sl][0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box[sl], pol_last);
-          tma_load_3d(&sm.sG[sl][5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box[sl], pol_last);
-          tma_load_3d(&sm.sG[sl][14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box[sl], pol_last);
+          mbar_expect_tx(&sm.bar_box, BOX_BYTES);
+          tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
+          tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
+          tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
         }
       } else {
-        const int sl = BOX2 ? (n & 1) : 0;
         const double* base = A + (long long)(zs + GZ) * G.plane;
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
           const double* bj = base + (long long)gslot_of_rank(j) * nxy;
 #pragma unroll
           for (int r = 0; r < BOXR; ++r)
-            if (box_dst[r] >= 0) cp_async_v<2>(&sm.sG[sl][j][box_dst[r]], bj + box_src[r]);
+            if (box_dst[r] >= 0) cp_async_v<2>(&sm.sG[j][box_dst[r]], bj + box_src[r]);
         }
         cp_commit();
       }
       return true;
     };
-    // wait for the box, then make it visible to the whole role (BOX2: box n+1 may be
-    // in flight as well -- `next_pending` -- so the cp.async path leaves one group)
-    auto wait_box = [&](bool issued, int n, bool next_pending = false) {
+    // wait for the box, then make it visible to the whole role
+    auto wait_box = [&](bool issued, int n) {
       if (XCH && !use_box) {  // g tile n (always issued: one periodic slab)
         mbar_wait(&sm.bar_xb[n & 1], (ph_xb >> (n & 1)) & 1);
         ph_xb ^= 1u << (n & 1);
       } else if (issued) {
         if (box_interior) {
-          const int sl = BOX2 ? (n & 1) : 0;
-          mbar_wait(&sm.bar_box[sl], (ph_box >> sl) & 1);
-          ph_box ^= 1u << sl;
-        } else if (BOX2 && next_pending) {
-          cp_wait<1>();
+          mbar_wait(&sm.bar_box, ph_box);
+          ph_box ^= 1;
         } else {
           cp_wait<0>();
         }
@@ -259,7 +245,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         double* xp = xa.cur + (long long)zs * nxy;
         double* xo = xa.old + (long long)zs * nxy;
         if (!use_box) {  // phi of the tile from the g tile
-          const double(*gt)[NT] = reinterpret_cast<const double(*)[NT]>(&sm.sG[0][0][0] + (n & 1) * Q * NT);
+          const double(*gt)[NT] = reinterpret_cast<const double(*)[NT]>(&sm.sG[0][0] + (n & 1) * Q * NT);
           for (int s = a; s < NT; s += kNA) {
             double v = gt[grank(0)][s];  // A.3, canonical order (same as phi_sum)
 #pragma unroll
@@ -279,11 +265,9 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           LB_CHECK(hl, zs >= -GP && zs < G.nzl + GP && gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny);
           v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
         } else {
-          constexpr int GS = XCH ? 2 * NT : NB;  // (component stride of sG)
-          const double* gb = &sm.sG[BOX2 ? (n & 1) : 0][0][0];
-          v = gb[grank(0) * GS + b];  // A.3, canonical order (same as phi_sum)
+          v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
 #pragma unroll
-          for (int i = 1; i < Q; ++i) v += gb[grank(i) * GS + b];
+          for (int i = 1; i < Q; ++i) v += sm.sG[grank(i)][b];
         }
         ring[b] = v;
       }
@@ -354,7 +338,6 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     };
     double pf = 0.0;  // the halo site of box hb + 1, loaded an iteration ahead
     bool issued = issue_box(0);
-    bool issued_next = BOX2 && 1 <= nlast ? issue_box(1) : false;  // BOX2: two boxes in flight
     if (XCH && xa.depth == 2 && 1 <= nlast) issue_box(1);  // two g tiles in flight
     for (int nn = 0; nn <= nlast + lag; ++nn) {
       double hv = 0.0;
@@ -366,7 +349,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       }
       if (XCH && h_ring >= 0 && hb + 1 >= 0 && hb + 1 <= nlast) pf = ld_relaxed_f64(xsite(hb + 1));
       if (nn <= nlast) {
-        wait_box(issued, nn, issued_next);  // (also: everyone is past the previous hand-off)
+        wait_box(issued, nn);  // (also: everyone is past the previous hand-off)
         make_phi(zA - 2 + nn, nn);
       } else {
         named_sync(2, kNA);
@@ -374,15 +357,10 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       if (hw) sm.sPhi[wslot<S::NPHI>(zA - 2 + hb)][h_ring] = hv;
       named_sync(2, kNA);  // sG consumed, ring written
       if (nn <= nlast) {
-        if (XCH && xa.depth == 2) {
+        if (XCH && xa.depth == 2)
           issued = nn + 2 <= nlast ? issue_box(nn + 2) : false;
-        } else if (BOX2) {  // into the buffer of box nn, just consumed
-          const bool iss2 = nn + 2 <= nlast ? issue_box(nn + 2) : false;
-          issued = issued_next;
-          issued_next = iss2;
-        } else {
+        else
           issued = nn + 1 <= nlast ? issue_box(nn + 1) : false;
-        }
       }
       const int n = nn - lag, zp = zA - 2 + n;
       if (n < 2) continue;
@@ -469,27 +447,20 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol);
     }
   };
-  if (!BOX2) issue_tile(zA, 0);
+  issue_tile(zA, 0);
   issue_tile(zA, 1);
   const int lx = tid % TX, ly = tid / TX;
   const int x = x0 + lx, y = y0 + ly;
   const bool active = (x < G.nx) && (y < G.ny);
   const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
-  const long long site_xy = (long long)(active ? y : 0) * G.nx + (active ? x : 0);
   for (int k = zA; k < zB; ++k) {
     double f[Q], g[Q];
-    if constexpr (BOX2) {  // f of the site from global memory (last use: evict first)
-      const double* fp = A + (long long)(k + GZ) * G.plane + site_xy;
+    mbar_wait(&sm.bar_f, ph_f);
+    ph_f ^= 1;
 #pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = ldg_hint(fp + (long long)slot(0, i) * nxy, pol_f);
-    } else {
-      mbar_wait(&sm.bar_f, ph_f);
-      ph_f ^= 1;
-#pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
-      named_sync(1, NT);  // sTf consumed
-      if (k + 1 < zB) issue_tile(k + 1, 0);
-    }
+    for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
+    named_sync(1, NT);  // sTf consumed
+    if (k + 1 < zB) issue_tile(k + 1, 0);
     const int q = seq & 1, u = seq >> 1;
     mbar_wait(&sm.q_full[q], u & 1);
     const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];
@@ -533,13 +504,13 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
   }
 }
 
-template <int TY, int COLL, bool XCH = false, bool BOX2 = false>
+template <int TY, int COLL, bool XCH = false>
 cudaError_t launch_ws_t(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
                         const Launch& ln, const Health& hl, const StepMaps* maps, cudaStream_t st, const Peers& pr,
                         const XchArgs* xch = nullptr) {
-  constexpr size_t smem = sizeof(WsSmem<TY, COLL, XCH, BOX2>);
+  constexpr size_t smem = sizeof(WsSmem<TY, COLL, XCH>);
   static_assert(smem <= 232448, "shared memory per CTA exceeds 227 KB");
-  auto kern = k_step_ws<TY, COLL, XCH, BOX2>;
+  auto kern = k_step_ws<TY, COLL, XCH>;
   int resid = 0;
   cudaError_t e = prepare_kernel(reinterpret_cast<const void*>(kern), smem, ws_threads(TY, XCH), &resid);
   if (e != cudaSuccess) return e;
@@ -583,8 +554,6 @@ cudaError_t prepare_ws_kernels() {
   prep(reinterpret_cast<const void*>(k_step_ws<8, 0, false>), sizeof(WsSmem<8, 0, false>), ws_threads(8, false));
   prep(reinterpret_cast<const void*>(k_step_ws<8, 1, false>), sizeof(WsSmem<8, 1, false>), ws_threads(8, false));
   prep(reinterpret_cast<const void*>(k_step_ws<8, 0, true>), sizeof(WsSmem<8, 0, true>), ws_threads(8, true));
-  prep(reinterpret_cast<const void*>(k_step_ws<8, 0, false, true>), sizeof(WsSmem<8, 0, false, true>),
-       ws_threads(8, false));
   prep(reinterpret_cast<const void*>(k_step_ws<4, 0, false>), sizeof(WsSmem<4, 0, false>), ws_threads(4, false));
   prep(reinterpret_cast<const void*>(k_step_ws<4, 1, false>), sizeof(WsSmem<4, 1, false>), ws_threads(4, false));
   return e;
@@ -602,7 +571,6 @@ cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, d
   if (p.coll == 1)
     return t8 ? launch_ws_t<8, 1>(G, p, A, B, phig, ln, hl, maps, st, pr)
               : launch_ws_t<4, 1>(G, p, A, B, phig, ln, hl, maps, st, pr);
-  if (t8 && ln.variant == 0) return launch_ws_t<8, 0, false, true>(G, p, A, B, phig, ln, hl, maps, st, pr);
   return t8 ? launch_ws_t<8, 0>(G, p, A, B, phig, ln, hl, maps, st, pr)
             : launch_ws_t<4, 0>(G, p, A, B, phig, ln, hl, maps, st, pr);
 }
