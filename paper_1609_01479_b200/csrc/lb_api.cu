@@ -1155,6 +1155,10 @@ int lb_init_equilibrium(lb_t* h, const double* rho, const double* u, const doubl
     CK(h, timed(h, K_INIT, true, [&]() {
          return launch_init_eq(G, h->dp, s.phi, rho ? s.B : nullptr, u ? s.B + nloc : nullptr, s.A, h->stream);
        }));
+  // ranks with the peer transport: a neighbour's first K_phi stores into this
+  // rank's phi ghost planes, which the init kernel above reads -- nobody steps
+  // before every rank's init has finished
+  if (h->nranks > 1 && h->halo_mode == 1 && !h->G.zwrap && (rc = halo_barrier(h, K_HALO_PHI))) return rc;
   CK(h, cudaStreamSynchronize(h->stream));
   resolve_pending(h);
   h->have_state = true;
