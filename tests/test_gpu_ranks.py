@@ -38,7 +38,7 @@ def _free_port():
     return port
 
 
-def _entry(rank, world, port, shape, nsteps, kernel, outdir):
+def _entry(rank, world, port, shape, nsteps, kernel, outdir, init=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -53,7 +53,10 @@ def _entry(rank, world, port, shape, nsteps, kernel, outdir):
         with lb.Lattice(nx, ny, nz, params, nranks=world, rank=rank, allgather=D.allgather_bytes) as L:
             assert lb.lb_debug_halo_mode(L.h) == 1  # peer transport mapped and checked end to end
             lb.lb_debug_step_kernel(L.h, kernel)
-            L.set_state(f[:, z0:z1], g[:, z0:z1])
+            if init:  # lb_init_equilibrium: phi ghost planes by P2P copies between the processes
+                L.init_equilibrium(phi[z0:z1])
+            else:
+                L.set_state(f[:, z0:z1], g[:, z0:z1])
             for _ in range(nsteps):
                 for phase in (0, 1):
                     lb.lb_debug_step_phase(L.h, phase)
@@ -67,13 +70,15 @@ def _entry(rank, world, port, shape, nsteps, kernel, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape,kernel", [((32, 16, 16), 0), ((33, 9, 12), 1), ((64, 24, 8), 2)])
-def test_two_ranks_peer_transport_bitwise(shape, kernel, tmp_path):
+@pytest.mark.parametrize("shape,kernel,init", [((32, 16, 16), 0, False), ((33, 9, 12), 1, False),
+                                               ((64, 24, 8), 2, False), ((32, 16, 16), 0, True)])
+def test_two_ranks_peer_transport_bitwise(shape, kernel, init, tmp_path):
     nx, ny, nz = shape
     nsteps = 5
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_entry, args=(r, 2, port, shape, nsteps, kernel, str(tmp_path))) for r in range(2)]
+    procs = [ctx.Process(target=_entry, args=(r, 2, port, shape, nsteps, kernel, str(tmp_path), init))
+             for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
@@ -85,10 +90,15 @@ def test_two_ranks_peer_transport_bitwise(shape, kernel, tmp_path):
     f0, g0 = R.equilibrium_state(rho, u, phi, P0)
     f0, g0 = f0 + nf, g0 + ng
     params = lb.make_params(P0.tau_f, P0.tau_g, P0.A, P0.B, P0.kappa, P0.mobility)
+    if init:
+        f0, g0 = R.equilibrium_state(np.ones_like(phi), np.zeros((3,) + phi.shape), phi, P0)
     for nslabs in (1, 2):
         with lb.Lattice(nx, ny, nz, params, nslabs=nslabs) as L:
             lb.lb_debug_step_kernel(L.h, kernel)
-            L.set_state(f0, g0)
+            if init:
+                L.init_equilibrium(phi)
+            else:
+                L.set_state(f0, g0)
             L.step(nsteps)
             fl, gl = L.get_state()
         assert np.array_equal(f, fl) and np.array_equal(g, gl), nslabs
