@@ -71,13 +71,16 @@ __device__ __forceinline__ void sync_wait_ge(unsigned long long* sync, int w, un
     __nanosleep(200);
   }
 }
-// End of a launch, one thread per CTA after a CTA barrier (every thread's stores
-// into the neighbours done and fenced at system scope): the last CTA of the
+// End of a launch, one thread per CTA after a CTA barrier: the last CTA of the
 // launch advances this slab's epoch `ew` and publishes it to the neighbours'
-// words `to_dn` (in the slab below) and `to_up` (in the slab above).
-__device__ __forceinline__ void sync_publish(const Peers& pr, int done_w, int ew, int to_dn, int to_up) {
+// words `to_dn` (in the slab below) and `to_up` (in the slab above).  A CTA that
+// stored into a neighbour (`remote`) first fences at system scope -- one fence
+// after the barrier covers every thread's stores of the CTA (cumulativity, as in
+// a grid barrier), not one fence per thread; the last CTA fences again before
+// the release, so the neighbour's acquire sees every CTA's stores.
+__device__ __forceinline__ void sync_publish(const Peers& pr, int done_w, int ew, int to_dn, int to_up, bool remote) {
   if (!pr.sync) return;
-  __threadfence_system();
+  if (remote) __threadfence_system();
   if (atomicAdd(pr.sync + done_w, 1ULL) == gridDim.x - 1) {
     pr.sync[done_w] = 0;
     __threadfence_system();

@@ -66,9 +66,8 @@ __global__ void __launch_bounds__(TPB) k_phi_edges(Geom G, const double* __restr
     if (z < GP) pr.phi_dn[phi_plane_index(G, G.nzl + z) + xy] = v;
     if (z >= G.nzl - GP) pr.phi_up[phi_plane_index(G, z - G.nzl) + xy] = v;
   }
-  __threadfence_system();  // this thread's stores into the neighbours, before the CTA's publication
-  __syncthreads();
-  if (threadIdx.x == 0) sync_publish(pr, SW_DONE_PHI, SW_PHI_EPOCH, SW_PHI_FROM_UP, SW_PHI_FROM_DN);
+  __syncthreads();  // every thread's stores into the neighbours before the CTA's publication
+  if (threadIdx.x == 0) sync_publish(pr, SW_DONE_PHI, SW_PHI_EPOCH, SW_PHI_FROM_UP, SW_PHI_FROM_DN, true);
 }
 
 // End of lb_step on a rank: the neighbours' step launches up to this slab's push

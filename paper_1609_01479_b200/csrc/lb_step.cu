@@ -359,11 +359,12 @@ __global__ void __launch_bounds__(TX* TY, 1)
     for (int q = 0; q < 6; ++q) P6_cur[q] = P6_next[q];
   }
   cp_wait<0>();
-  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the publication below
-  __syncthreads();
+  __syncthreads();  // every thread's pushes before the CTA's publication
   if (tid == 0) {
     health_tick(hl);
-    sync_publish(pr, SW_DONE_STEP, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN);
+    // (only a chunk holding plane 0 or nzl - 1 pushed into a neighbour)
+    sync_publish(pr, SW_DONE_STEP, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN,
+                 (pr.dn && zA == 0) || (pr.up && zB == G.nzl));
   }
 }
 

@@ -258,18 +258,30 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           return;
         }
       }
-      for (int b = a; b < NB; b += kNA) {
-        double v;
-        if (ghost) {
+      if (ghost) {
+        for (int b = a; b < NB; b += kNA) {
           const int gx = wrapx(x0 - 2 + b % BX), gy = wrapy(y0 - 2 + b / BX);
           LB_CHECK(hl, zs >= -GP && zs < G.nzl + GP && gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny);
-          v = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
-        } else {
-          v = sm.sG[grank(0)][b];  // A.3, canonical order (same as phi_sum)
-#pragma unroll
-          for (int i = 1; i < Q; ++i) v += sm.sG[grank(i)][b];
+          ring[b] = ldg(phig + phi_plane_index(G, zs) + (long long)gy * G.nx + gx);
         }
-        ring[b] = v;
+        return;
+      }
+      // two neighbouring sites per thread with 16-byte shared loads (BX even: a pair
+      // never straddles a row): every thread of the role has at most one pair, so
+      // phi of the box is ready after 19 loads instead of up to 38 -- and the next
+      // box goes out sooner.  Each site's sum is in the canonical order (A.3, as
+      // phi_sum): the same bits.
+      static_assert(BX % 2 == 0 && NB % 2 == 0, "pairs of box sites");
+      for (int pb = a; pb < NB / 2; pb += kNA) {
+        const int b = 2 * pb;
+        double2 v = *reinterpret_cast<const double2*>(&sm.sG[grank(0)][b]);
+#pragma unroll
+        for (int i = 1; i < Q; ++i) {
+          const double2 w = *reinterpret_cast<const double2*>(&sm.sG[grank(i)][b]);
+          v.x += w.x;
+          v.y += w.y;
+        }
+        *reinterpret_cast<double2*>(&ring[b]) = v;
       }
     };
     auto compute_P = [&](int zp) {
@@ -496,11 +508,12 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       if (!(rho > 0.0) || !isfinite(rho) || !isfinite(ph)) health_report(hl, G, x, y, k);  // R22
     }
   }
-  if (pr.dn || pr.up) __threadfence_system();  // P2P stores visible before the publication below
-  named_sync(1, NT);
+  named_sync(1, NT);  // every thread's pushes before the CTA's publication
   if (tid == 0) {
     health_tick(hl);
-    sync_publish(pr, SW_DONE_STEP, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN);
+    // (only a chunk holding plane 0 or nzl - 1 pushed into a neighbour)
+    sync_publish(pr, SW_DONE_STEP, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN,
+                 (pr.dn && zA == 0) || (pr.up && zB == G.nzl));
   }
 }
 

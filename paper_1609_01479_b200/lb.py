@@ -14,9 +14,11 @@ import os
 
 import numpy as np
 
-# LB_VARIANT=checked loads the bounds-checked test build (liblb_checked.so: device
-# index checks, lb_debug_check) -- the same kernels and results; test support only
-_LIB_NAME = "liblb_checked.so" if os.environ.get("LB_VARIANT") == "checked" else "liblb.so"
+# LB_VARIANT=<name> loads liblb_<name>.so from this directory instead: the
+# bounds-checked test build (checked: device index checks, lb_debug_check), or
+# another build of the same sources kept for an A/B measurement; test support only
+_VARIANT = os.environ.get("LB_VARIANT", "")
+_LIB_NAME = f"liblb_{_VARIANT}.so" if _VARIANT else "liblb.so"
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), _LIB_NAME)
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
