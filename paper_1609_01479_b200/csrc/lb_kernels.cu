@@ -47,24 +47,43 @@ __global__ void __launch_bounds__(TPB) k_phi(Geom G, const double* __restrict__ 
 // (lb_kernels.cuh "SyncWord"): every CTA first waits for both neighbours' step of
 // the previous timestep (their stores into planes 0 / nzl-1 of this slab's state,
 // and their reads of their ghost planes, are then complete); the last CTA
-// publishes this slab's phi epoch.  One thread per site of the 4 planes.
-__global__ void __launch_bounds__(TPB) k_phi_edges(Geom G, const double* __restrict__ A, double* __restrict__ phi,
-                                                   Peers pr) {
+// publishes this slab's phi epoch.
+constexpr int kEdgeThreads = 256, kEdgeUnroll = 4;
+__global__ void __launch_bounds__(kEdgeThreads) k_phi_edges(Geom G, const double* __restrict__ A,
+                                                             double* __restrict__ phi, Peers pr) {
   if (threadIdx.x == 0) {
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + SW_PUSH_EPOCH);
     sync_wait_ge(pr.sync, SW_PUSH_FROM_DN, e);
     sync_wait_ge(pr.sync, SW_PUSH_FROM_UP, e);
   }
   __syncthreads();
-  const long long n = 4 * G.nxy;
-  for (long long t = (long long)blockIdx.x * TPB + threadIdx.x; t < n; t += (long long)gridDim.x * TPB) {
-    const int k = (int)(t / G.nxy);
-    const int z = k < 2 ? k : G.nzl - 4 + k;
-    const long long xy = t - (long long)k * G.nxy;
-    const double v = phi_sum(A + dist_index(G, z, 0, xy), G.nxy);
-    phi[phi_plane_index(G, z) + xy] = v;
-    if (z < GP) pr.phi_dn[phi_plane_index(G, G.nzl + z) + xy] = v;
-    if (z >= G.nzl - GP) pr.phi_up[phi_plane_index(G, z - G.nzl) + xy] = v;
+  // a few CTAs per SM (one acquire at the start and one system fence at the end
+  // each: those cost microseconds, so not one per 128 sites), each thread
+  // summing kEdgeUnroll sites at a time -- all their loads in flight before any store
+  const long long n = 4 * G.nxy, stride = (long long)gridDim.x * kEdgeThreads;
+  for (long long t0 = (long long)blockIdx.x * kEdgeThreads + threadIdx.x; t0 < n; t0 += kEdgeUnroll * stride) {
+    double v[kEdgeUnroll];
+#pragma unroll
+    for (int u = 0; u < kEdgeUnroll; ++u) {
+      const long long t = t0 + u * stride;
+      v[u] = 0.0;
+      if (t < n) {
+        const int k = (int)(t / G.nxy);
+        const int z = k < 2 ? k : G.nzl - 4 + k;
+        v[u] = phi_sum(A + dist_index(G, z, 0, t - (long long)k * G.nxy), G.nxy);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kEdgeUnroll; ++u) {
+      const long long t = t0 + u * stride;
+      if (t >= n) break;
+      const int k = (int)(t / G.nxy);
+      const int z = k < 2 ? k : G.nzl - 4 + k;
+      const long long xy = t - (long long)k * G.nxy;
+      phi[phi_plane_index(G, z) + xy] = v[u];
+      if (z < GP) pr.phi_dn[phi_plane_index(G, G.nzl + z) + xy] = v[u];
+      if (z >= G.nzl - GP) pr.phi_up[phi_plane_index(G, z - G.nzl) + xy] = v[u];
+    }
   }
   __syncthreads();  // every thread's stores into the neighbours before the CTA's publication
   if (threadIdx.x == 0) sync_publish(pr, SW_DONE_PHI, SW_PHI_EPOCH, SW_PHI_FROM_UP, SW_PHI_FROM_DN, true);
@@ -172,12 +191,11 @@ cudaError_t launch_phi_edges(const Geom& G, const double* A, double* phi, cudaSt
                              int num_sms) {
   if (!pr.sync || !pr.sync_dn || !pr.sync_up || !pr.phi_dn || !pr.phi_up || G.zwrap || G.nzl < 2)
     return cudaErrorInvalidValue;
-  // nzl = 2 or 3: the edge pairs overlap; each plane is summed once per occurrence (same bits).
-  // One site per thread: a grid-stride loop over ~14 sites per thread left each
-  // thread's 19 loads of a site waiting for the previous site's (70 us for 4
-  // planes of 512 x 512 against ~20 us).
-  (void)num_sms;
-  k_phi_edges<<<blocks_for(4 * G.nxy), TPB, 0, st>>>(G, A, phi, pr);
+  // nzl = 2 or 3: the edge pairs overlap; each plane is summed once per occurrence (same bits)
+  const long long per = (long long)kEdgeThreads * kEdgeUnroll;
+  const long long need = (4 * G.nxy + per - 1) / per;
+  const unsigned grid = (unsigned)(need < 2LL * num_sms ? need : 2LL * num_sms);
+  k_phi_edges<<<grid, kEdgeThreads, 0, st>>>(G, A, phi, pr);
   return cudaGetLastError();
 }
 
