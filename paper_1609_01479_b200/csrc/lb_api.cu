@@ -640,7 +640,8 @@ int one_step(lb_ctx* h, bool stream_only = false) {
         Slab& s = h->slabs[r];
         const Peers pr = peers_of(h, r);
         if (peer) {  // edge phi into the neighbours' ghost planes, ordered by the sync words (NEXT-1)
-          CK(h, timed(h, K_PHI, true, [&]() { return launch_phi_edges(G, s.A, s.phi, h->stream, pr, h->num_sms); }));
+          CK(h, timed(h, K_PHI, true, [&]() { return launch_phi_edges(G, s.A, s.phi, h->stream, pr); }));
+          h->launches += 2;  // (the one-thread wait and publication around it)
         } else {
           CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, 0, 2, h->stream); }));
           CK(h, timed(h, K_PHI, true, [&]() { return launch_phi(G, s.A, s.phi, G.nzl - 2, G.nzl, h->stream); }));
@@ -654,6 +655,10 @@ int one_step(lb_ctx* h, bool stream_only = false) {
       const Peers pr = peers_of(h, r);
       const Health hl = health_of(h, r, r == last);
       CK(h, timed(h, K_STEP, true, [&]() { return launch_bgk_step(h, s, ln, hl, pr); }));
+      if (peer && pr.sync) {  // the push epoch of this slab, after its step kernel
+        CK(h, launch_publish_push(pr, h->stream));
+        ++h->launches;
+      }
     }
   }
   // peer transport: the step kernels published their pushes (device-side); only
@@ -1073,8 +1078,8 @@ int lb_debug_step_phase(lb_t* h, int phase) {
   const Geom& G = h->G;
   if (phase == 0) {
     for (int r = 0; r < h->nslabs; ++r)
-      CK(h, launch_phi_edges(G, h->slabs[r].A, h->slabs[r].phi, h->stream, peers_of(h, r), h->num_sms));
-    ++h->launches;
+      CK(h, launch_phi_edges(G, h->slabs[r].A, h->slabs[r].phi, h->stream, peers_of(h, r)));
+    h->launches += 3;
     CK(h, cudaStreamSynchronize(h->stream));
     return LB_OK;
   }
@@ -1084,7 +1089,8 @@ int lb_debug_step_phase(lb_t* h, int phase) {
       Slab& s = h->slabs[r];
       const Health hl = health_of(h, r, r == h->nslabs - 1);
       CK(h, launch_bgk_step(h, s, ln, hl, peers_of(h, r)));
-      ++h->launches;
+      CK(h, launch_publish_push(peers_of(h, r), h->stream));
+      h->launches += 2;
     }
     swap_roles(h);
     ++h->steps_done;

@@ -71,25 +71,6 @@ __device__ __forceinline__ void sync_wait_ge(unsigned long long* sync, int w, un
     __nanosleep(200);
   }
 }
-// End of a launch, one thread per CTA after a CTA barrier: the last CTA of the
-// launch advances this slab's epoch `ew` and publishes it to the neighbours'
-// words `to_dn` (in the slab below) and `to_up` (in the slab above).  A CTA that
-// stored into a neighbour (`remote`) first fences at system scope -- one fence
-// after the barrier covers every thread's stores of the CTA (cumulativity, as in
-// a grid barrier), not one fence per thread; the last CTA fences again before
-// the release, so the neighbour's acquire sees every CTA's stores.
-__device__ __forceinline__ void sync_publish(const Peers& pr, int done_w, int ew, int to_dn, int to_up, bool remote) {
-  if (!pr.sync) return;
-  if (remote) __threadfence_system();
-  if (atomicAdd(pr.sync + done_w, 1ULL) == gridDim.x - 1) {
-    pr.sync[done_w] = 0;
-    __threadfence_system();
-    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + ew) + 1;
-    pr.sync[ew] = e;
-    st_release_sys_u64(pr.sync_dn + to_dn, e);
-    st_release_sys_u64(pr.sync_up + to_up, e);
-  }
-}
 // Step kernels: a CTA whose planes need the ghost phi planes of the slab below
 // (zA - 2 < 0) or above (zB + 1 >= nzl) waits for that neighbour's K_phi of this
 // step (this slab's own K_phi ran just before, so its phi epoch is the target).

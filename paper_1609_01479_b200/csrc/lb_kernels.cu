@@ -43,58 +43,43 @@ __global__ void __launch_bounds__(TPB) k_phi(Geom G, const double* __restrict__ 
 }
 
 // K_phi of the peer transport (NEXT-1): phi of planes 0, 1, nzl-2, nzl-1 (A.3),
-// stored here and into the neighbours' ghost planes; ordered by the sync words
-// (lb_kernels.cuh "SyncWord"): every CTA first waits for both neighbours' step of
-// the previous timestep (their stores into planes 0 / nzl-1 of this slab's state,
-// and their reads of their ghost planes, are then complete); the last CTA
-// publishes this slab's phi epoch.
-constexpr int kEdgeThreads = 256, kEdgeUnroll = 4;
-__global__ void __launch_bounds__(kEdgeThreads) k_phi_edges(Geom G, const double* __restrict__ A,
-                                                             double* __restrict__ phi, Peers pr) {
-  if (threadIdx.x == 0) {
-    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + SW_PUSH_EPOCH);
-    sync_wait_ge(pr.sync, SW_PUSH_FROM_DN, e);
-    sync_wait_ge(pr.sync, SW_PUSH_FROM_UP, e);
-  }
-  __syncthreads();
-  // a few CTAs per SM (one acquire at the start and one system fence at the end
-  // each: those cost microseconds, so not one per 128 sites), each thread
-  // summing kEdgeUnroll sites at a time -- all their loads in flight before any store
-  const long long n = 4 * G.nxy, stride = (long long)gridDim.x * kEdgeThreads;
-  for (long long t0 = (long long)blockIdx.x * kEdgeThreads + threadIdx.x; t0 < n; t0 += kEdgeUnroll * stride) {
-    double v[kEdgeUnroll];
-#pragma unroll
-    for (int u = 0; u < kEdgeUnroll; ++u) {
-      const long long t = t0 + u * stride;
-      v[u] = 0.0;
-      if (t < n) {
-        const int k = (int)(t / G.nxy);
-        const int z = k < 2 ? k : G.nzl - 4 + k;
-        v[u] = phi_sum(A + dist_index(G, z, 0, t - (long long)k * G.nxy), G.nxy);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kEdgeUnroll; ++u) {
-      const long long t = t0 + u * stride;
-      if (t >= n) break;
-      const int k = (int)(t / G.nxy);
-      const int z = k < 2 ? k : G.nzl - 4 + k;
-      const long long xy = t - (long long)k * G.nxy;
-      phi[phi_plane_index(G, z) + xy] = v[u];
-      if (z < GP) pr.phi_dn[phi_plane_index(G, G.nzl + z) + xy] = v[u];
-      if (z >= G.nzl - GP) pr.phi_up[phi_plane_index(G, z - G.nzl) + xy] = v[u];
-    }
-  }
-  __syncthreads();  // every thread's stores into the neighbours before the CTA's publication
-  if (threadIdx.x == 0) sync_publish(pr, SW_DONE_PHI, SW_PHI_EPOCH, SW_PHI_FROM_UP, SW_PHI_FROM_DN, true);
+// stored here and into the neighbours' ghost planes; one site per thread.  The
+// ordering is done by the one-thread kernels around it on the same stream
+// (k_sync_wait before it: the neighbours' step of the previous timestep has
+// stored into planes 0 / nzl-1 of this slab and stopped reading its ghost
+// planes; k_sync_publish after it: this slab's phi epoch) -- kernel boundaries
+// order the rest, so no CTA of this kernel waits or fences (in-kernel, one
+// acquire and one system fence per CTA cost 60 us per launch at 512 x 512).
+__global__ void __launch_bounds__(TPB) k_phi_edges(Geom G, const double* __restrict__ A, double* __restrict__ phi,
+                                                   Peers pr) {
+  const long long t = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (t >= 4 * G.nxy) return;
+  const int k = (int)(t / G.nxy);
+  const int z = k < 2 ? k : G.nzl - 4 + k;
+  const long long xy = t - (long long)k * G.nxy;
+  const double v = phi_sum(A + dist_index(G, z, 0, xy), G.nxy);
+  phi[phi_plane_index(G, z) + xy] = v;
+  if (z < GP) pr.phi_dn[phi_plane_index(G, G.nzl + z) + xy] = v;
+  if (z >= G.nzl - GP) pr.phi_up[phi_plane_index(G, z - G.nzl) + xy] = v;
 }
 
-// End of lb_step on a rank: the neighbours' step launches up to this slab's push
-// epoch have completed, so their stores into this slab's state have landed.
-__global__ void k_wait_inbound(Peers pr) {
-  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + SW_PUSH_EPOCH);
-  sync_wait_ge(pr.sync, SW_PUSH_FROM_DN, e);
-  sync_wait_ge(pr.sync, SW_PUSH_FROM_UP, e);
+// One thread: wait until both neighbours' epoch words w_dn, w_up of this slab
+// reach this slab's own epoch `ew` (bounded wait, lb_device.cuh).
+__global__ void k_sync_wait(Peers pr, int w_dn, int w_up, int ew) {
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + ew);
+  sync_wait_ge(pr.sync, w_dn, e);
+  sync_wait_ge(pr.sync, w_up, e);
+}
+
+// One thread, after the kernel whose stores it publishes (stream order: that
+// kernel has completed): a system-scope fence, then this slab's epoch `ew` + 1
+// released into the neighbours' words (to_dn in the slab below, to_up above).
+__global__ void k_sync_publish(Peers pr, int ew, int to_dn, int to_up) {
+  __threadfence_system();
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(pr.sync + ew) + 1;
+  pr.sync[ew] = e;
+  st_release_sys_u64(pr.sync_dn + to_dn, e);
+  st_release_sys_u64(pr.sync_up + to_up, e);
 }
 
 // Propagation only (test support, lb_debug_stream): the push of A.8 with the
@@ -187,21 +172,26 @@ cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int 
   return cudaGetLastError();
 }
 
-cudaError_t launch_phi_edges(const Geom& G, const double* A, double* phi, cudaStream_t st, const Peers& pr,
-                             int num_sms) {
+cudaError_t launch_phi_edges(const Geom& G, const double* A, double* phi, cudaStream_t st, const Peers& pr) {
   if (!pr.sync || !pr.sync_dn || !pr.sync_up || !pr.phi_dn || !pr.phi_up || G.zwrap || G.nzl < 2)
     return cudaErrorInvalidValue;
-  // nzl = 2 or 3: the edge pairs overlap; each plane is summed once per occurrence (same bits)
-  const long long per = (long long)kEdgeThreads * kEdgeUnroll;
-  const long long need = (4 * G.nxy + per - 1) / per;
-  const unsigned grid = (unsigned)(need < 2LL * num_sms ? need : 2LL * num_sms);
-  k_phi_edges<<<grid, kEdgeThreads, 0, st>>>(G, A, phi, pr);
+  // wait for the neighbours' pushes of the previous step; the edges; publish phi
+  // (nzl = 2 or 3: the edge pairs overlap; a plane is summed once per occurrence, same bits)
+  k_sync_wait<<<1, 1, 0, st>>>(pr, SW_PUSH_FROM_DN, SW_PUSH_FROM_UP, SW_PUSH_EPOCH);
+  k_phi_edges<<<blocks_for(4 * G.nxy), TPB, 0, st>>>(G, A, phi, pr);
+  k_sync_publish<<<1, 1, 0, st>>>(pr, SW_PHI_EPOCH, SW_PHI_FROM_UP, SW_PHI_FROM_DN);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_publish_push(const Peers& pr, cudaStream_t st) {
+  if (!pr.sync) return cudaSuccess;
+  k_sync_publish<<<1, 1, 0, st>>>(pr, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN);
   return cudaGetLastError();
 }
 
 cudaError_t launch_wait_inbound(const Peers& pr, cudaStream_t st) {
   if (!pr.sync) return cudaSuccess;
-  k_wait_inbound<<<1, 1, 0, st>>>(pr);
+  k_sync_wait<<<1, 1, 0, st>>>(pr, SW_PUSH_FROM_DN, SW_PUSH_FROM_UP, SW_PUSH_EPOCH);
   return cudaGetLastError();
 }
 

@@ -133,13 +133,14 @@ struct Health {
 // Ordering is device-side (NEXT-1): each slab owns a few 64-bit sync words; a
 // neighbour WRITES its epochs into them (st.release.sys, remote) and the owner
 // POLLS them (ld.acquire.sys, local).  Per step t, with epochs counted per slab:
-//   K_phi(t)  waits for push(dn), push(up) >= its own push epoch (the neighbours'
-//             step t-1 has stored into this slab's state and stopped reading its
-//             phi ghost planes), stores its edge phi planes, and its last CTA
-//             publishes phi epoch t+1 to both neighbours;
+//   K_phi(t)  is preceded by a one-thread wait for push(dn), push(up) >= its own
+//             push epoch (the neighbours' step t-1 has stored into this slab's
+//             state and stopped reading its phi ghost planes), stores its edge phi
+//             planes, and is followed by a one-thread publication of phi epoch t+1
+//             (a system fence, then the release stores);
 //   step(t)   CTAs whose z-chunk reads a ghost phi plane wait for phi(dn) or
-//             phi(up) >= its own phi epoch; interior chunks never wait; its last
-//             CTA publishes push epoch t+1 to both neighbours.
+//             phi(up) >= its own phi epoch; interior chunks never wait; a one-thread
+//             kernel after it publishes push epoch t+1.
 // Waits are bounded (kSyncTimeoutNs): a timeout sets SW_ERR and lb_step fails.
 enum SyncWord {
   SW_PHI_FROM_DN = 0,   // phi epoch of the slab below (it wrote our ghost planes -2, -1)
@@ -148,8 +149,6 @@ enum SyncWord {
   SW_PUSH_FROM_UP = 3,  // push epoch of the slab above (our plane nzl-1)
   SW_PHI_EPOCH = 4,     // own K_phi launches completed
   SW_PUSH_EPOCH = 5,    // own step launches completed
-  SW_DONE_PHI = 6,      // CTAs of the current K_phi launch finished
-  SW_DONE_STEP = 7,     // CTAs of the current step launch finished
   SW_ERR = 8,           // a wait timed out
   SW_WORDS = 16
 };
@@ -179,9 +178,11 @@ __host__ __device__ inline double* push_plane(const Geom& G, double* B, const Pe
 cudaError_t launch_phi(const Geom& G, const double* A, double* phi, int z0, int z1, cudaStream_t st,
                        const Peers& pr = Peers{});
 // K_phi of the peer transport: the two edge planes at each end, stored here and
-// into the neighbours' ghost planes, ordered by the sync words (pr.sync required)
-cudaError_t launch_phi_edges(const Geom& G, const double* A, double* phi, cudaStream_t st, const Peers& pr,
-                             int num_sms);
+// into the neighbours' ghost planes, ordered by the sync words (pr.sync required):
+// a one-thread wait for the neighbours' pushes, the edges, a one-thread publication
+cudaError_t launch_phi_edges(const Geom& G, const double* A, double* phi, cudaStream_t st, const Peers& pr);
+// after a slab's step kernel: one thread publishes its push epoch (pr.sync or nothing)
+cudaError_t launch_publish_push(const Peers& pr, cudaStream_t st);
 // one thread: wait until both neighbours' step launches up to this slab's push
 // epoch have completed (all their stores into this slab have landed)
 cudaError_t launch_wait_inbound(const Peers& pr, cudaStream_t st);

@@ -362,9 +362,6 @@ __global__ void __launch_bounds__(TX* TY, 1)
   __syncthreads();  // every thread's pushes before the CTA's publication
   if (tid == 0) {
     health_tick(hl);
-    // (only a chunk holding plane 0 or nzl - 1 pushed into a neighbour)
-    sync_publish(pr, SW_DONE_STEP, SW_PUSH_EPOCH, SW_PUSH_FROM_UP, SW_PUSH_FROM_DN,
-                 (pr.dn && zA == 0) || (pr.up && zB == G.nzl));
   }
 }
 
