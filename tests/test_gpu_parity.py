@@ -633,6 +633,31 @@ def test_graph_replay_bitwise_equal_plain_steps(nslabs, halo):
     assert na == nb
 
 
+@pytest.mark.parametrize("nslabs", [1, 2])
+def test_prepare_captures_without_stepping(nslabs):
+    """lb_prepare captures the step graphs of both buffer parities and runs nothing:
+    the state is unchanged, and the steps after it give the bits and the kernel
+    count of steps without it."""
+    f, g = rough(32, 12, 16, seed=19)
+    out = []
+    for prep in (True, False):
+        with lb.Lattice(32, 12, 16, cparams(P0), nslabs=nslabs) as L:
+            L.set_state(f, g)
+            n0 = lb.lb_launch_count(L.h)
+            if prep:
+                lb.lb_prepare(L.h)
+                assert lb.lb_launch_count(L.h) == n0
+                f1, g1 = L.get_state()
+                assert np.array_equal(f1, f) and np.array_equal(g1, g)
+                n0 = lb.lb_launch_count(L.h)
+            L.step(3)
+            L.step(17)
+            out.append((L.get_state(), lb.lb_launch_count(L.h) - n0))
+    (a, na), (b, nb) = out
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert na == nb
+
+
 def test_graphs_dropped_on_collision_change():
     """A cached graph of the BGK step must not survive lb_set_collision."""
     f, g = rough(32, 12, 10, seed=10)
