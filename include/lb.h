@@ -357,8 +357,10 @@ int lb_debug_check(lb_t* h);
 /* Block order of the step kernels (host-only): for block L of a launch over ntx x
  * nty tiles and nch z-chunks, out[3L .. 3L+2] = (tile column, tile row, chunk) as
  * the kernels compute it with `resid` CTAs resident and bands of `band` tile rows
- * (LB_TUNE_BAND_ROWS).  Every (tile, chunk) appears exactly once.  out holds
- * 3 * ntx * nty * nch ints.  LB_EINVAL on bad arguments. */
+ * (LB_TUNE_BAND_ROWS); band < 0: bands of -band rows in the order of a z-slab
+ * with the peer transport, whose edge chunks (first and last) run after the
+ * interior ones when there are >= 3.  Every (tile, chunk) appears exactly once.
+ * out holds 3 * ntx * nty * nch ints.  LB_EINVAL on bad arguments. */
 int lb_debug_tile_order(int ntx, int nty, int nch, int resid, int band, int* out);
 
 /* Halo plan of a slab decomposition (host-only; no GPU needed): for rank r of

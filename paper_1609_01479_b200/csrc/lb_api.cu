@@ -335,6 +335,7 @@ Launch launch_of(const lb_ctx* h) {
   Launch ln;
   ln.zc = h->zc;
   ln.order = h->order;
+  ln.order.edge_last = h->halo_mode == 1 && !h->G.zwrap;
   ln.l2 = h->l2;
   return ln;
 }
@@ -1575,10 +1576,12 @@ long long lb_debug_guards(lb_t* h) {
 }
 
 int lb_debug_tile_order(int ntx, int nty, int nch, int resid, int band, int* out) {
-  if (!out || ntx < 1 || nty < 1 || nch < 1 || resid < 1 || band < 1) return LB_EINVAL;
+  if (!out || ntx < 1 || nty < 1 || nch < 1 || resid < 1 || band == 0 || band < -ntx * nty) return LB_EINVAL;
   const int n = ntx * nty * nch;
+  TileOrder o{resid, band < 0 ? -band : band};
+  o.edge_last = band < 0;  // (negative band: the order of a z-slab with the peer transport)
   for (int L = 0; L < n; ++L) {
-    const TileId t = tile_of_block(L, ntx, nty, nch, TileOrder{resid, band});
+    const TileId t = tile_of_block(L, ntx, nty, nch, o);
     out[3 * L] = t.bx, out[3 * L + 1] = t.by, out[3 * L + 2] = t.bz;
   }
   return LB_OK;

@@ -93,6 +93,11 @@ struct TileId {
 struct TileOrder {
   int resid = 148;  // CTAs resident at a time
   int band = 1;     // tile rows per band
+  // z-slab with the peer transport: the chunks that read a neighbour's phi planes
+  // (the first and the last) run after the interior ones -- chunk c of the launch
+  // order is chunk (c + 1) % nch for nch >= 3 -- so the CTAs that may wait for a
+  // neighbour's K_phi come last and the interior work runs meanwhile
+  bool edge_last = false;
 };
 __host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch, TileOrder o) {
   const int ntiles = ntx * nty;
@@ -102,8 +107,9 @@ __host__ __device__ inline TileId tile_of_block(int L, int ntx, int nty, int nch
   const int grp = L / per_group;
   const int r = L - grp * per_group;
   const int rg = ntiles - grp * resid < resid ? ntiles - grp * resid : resid;
-  const int c = r / rg;
-  const int t = grp * resid + (r - c * rg);
+  const int cl = r / rg;
+  const int c = o.edge_last && nch >= 3 ? (cl + 1 == nch ? 0 : cl + 1) : cl;
+  const int t = grp * resid + (r - cl * rg);
   if (o.band <= 1) return TileId{t % ntx, t / ntx, c};
   const int per_band = o.band * ntx;  // tiles of a full band
   const int b = t / per_band, u = t - b * per_band;

@@ -135,3 +135,20 @@ def test_tile_order_is_a_permutation(ntx, nty, nch, resid, band):
         assert o[band].tolist() == [1, 0, 0]
     if band == 1 and resid >= ntx:
         assert o[1].tolist() == [1 % ntx, 1 // ntx, 0]
+
+
+@pytest.mark.parametrize("ntx,nty,nch,resid", [(16, 64, 4, 148), (8, 8, 3, 64), (5, 7, 2, 148), (3, 2, 5, 4)])
+def test_tile_order_edge_chunks_last(ntx, nty, nch, resid):
+    """A z-slab with the peer transport (band < 0): the same permutation with the
+    chunks that read a neighbour's phi planes (0 and nch-1) after the interior
+    chunks of every group, so the CTAs that may wait come last."""
+    o = lb.lb_debug_tile_order(ntx, nty, nch, resid, -1)
+    ref = lb.lb_debug_tile_order(ntx, nty, nch, resid, 1)
+    assert sorted(map(tuple, o.tolist())) == sorted(map(tuple, ref.tolist()))
+    if nch >= 3:
+        ntiles = ntx * nty
+        grp = min(resid, ntiles)
+        first = o[:grp * (nch - 2)]  # the interior chunks of the first group
+        assert all(0 < c < nch - 1 for c in first[:, 2].tolist())
+    else:
+        assert np.array_equal(o, ref)

@@ -261,6 +261,18 @@ def test_tile_rows_bitwise(kernel):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_slab_edge_chunks_last_bitwise(kernel):
+    """Slabs of several z-chunks with the peer transport: the edge chunks (which may
+    wait for a neighbour's K_phi) are launched after the interior ones -- the same
+    bits as one slab and as the exchange transport."""
+    f, g = rough(64, 16, 24, seed=29)
+    ref = gpu_run(f, g, P0, 5, kernel=kernel)
+    for halo in (1, 0):
+        a = gpu_run(f, g, P0, 5, nslabs=2, kernel=kernel, halo=halo, tune={lb.LB_TUNE_ZCHUNK: 3})
+        assert np.array_equal(a[0], ref[0]) and np.array_equal(a[1], ref[1]), halo
+
+
 def test_tune_errors_and_graphs_off():
     f, g = rough(32, 12, 10, seed=27)
     a = gpu_run(f, g, P0, 17, tune={lb.LB_TUNE_GRAPHS: 0})
