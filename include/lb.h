@@ -188,10 +188,8 @@ int lb_debug_stream(lb_t* h, int nsteps);
  * value.  Keys:
  *   LB_TUNE_ZCHUNK    planes per z-chunk of a CTA (0: automatic, step_zchunk)
  *   LB_TUNE_VARIANT   a kernel alternative kept for A/B measurement: 1 = the
- *                     binary-fluid warp-specialised kernel with the halo box
- *                     (lb_step_ws.cu) instead of the g-ring kernel (lb_step_gr.cu),
- *                     and the Cahn-Hilliard warp-specialised kernel with a 5-plane
- *                     phi ring; 0 the default
+ *                     Cahn-Hilliard warp-specialised kernel with a 5-plane phi
+ *                     ring (phi issued 3 planes ahead instead of 4); 0 the default
  *   LB_TUNE_TILE_ROWS tile rows of the binary-fluid and Cahn-Hilliard step kernels,
  *                     4 or 8 (0: automatic); resets the z-chunk to its automatic value
  *   LB_TUNE_BAND_ROWS block order: tiles walked in bands of this many tile rows,

@@ -13,8 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblb.so")
 LIB_CHECKED = os.path.join(PKG, "liblb_checked.so")  # -DLB_CHECKED: device bounds checks (test support)
-SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_step_ws.cu", "lb_step_gr.cu", "lb_step_ch.cu", "lb_step_lc.cu",
-           "lb_api.cu"]
+SOURCES = ["lb_kernels.cu", "lb_step.cu", "lb_step_ws.cu", "lb_step_ch.cu", "lb_step_lc.cu", "lb_api.cu"]
 HEADERS = ["d3q19.cuh", "lb_kernels.cuh", "lb_device.cuh", "lb_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -383,7 +383,6 @@ int create_common(int nx, int ny, int nz, const lb_params* params, int nranks, i
   // every step kernel's per-device preparation now, never inside a graph capture
   e = prepare_step_kernels();
   if (e == cudaSuccess) e = prepare_ws_kernels();
-  if (e == cudaSuccess) e = prepare_gr_kernels();
   if (e == cudaSuccess) e = prepare_ch_kernels();
   if (e == cudaSuccess) e = prepare_lc_kernels();
   if (e != cudaSuccess) {
@@ -588,10 +587,6 @@ cudaError_t launch_bgk_step(lb_ctx* h, Slab& s, const Launch& ln, const Health& 
     const XchArgs xa{h->xphi[k], h->xphi[1 - k], G.nxy * G.nzl <= (1LL << 20) ? 2 : 1};
     return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr, &xa);
   }
-  // the g-ring kernel: kernel 0 (or 2) on 32 x 8 tiles of the BGK + force path, unless
-  // the halo-box kernel is asked for (LB_TUNE_VARIANT 1, A/B)
-  if (ws && h->dp.coll == 0 && h->variant == 0 && step_gr_fits(G, &s.mapsA))
-    return launch_step_gr(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
   if (ws) return launch_step_ws(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
   return launch_step(G, h->dp, s.A, s.B, s.phi, ln, hl, &s.mapsA, h->stream, pr);
 }

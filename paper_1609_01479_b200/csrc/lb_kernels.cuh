@@ -205,11 +205,10 @@ cudaError_t prepare_lc_kernels();
 // buffer whose ghost planes are read when !G.zwrap; zc = z-chunk per CTA
 int step_tile_rows(const Geom& G, int num_sms);  // 4 or 8
 int step_zchunk(const Geom& G, int num_sms, int ty);
-// TMA descriptors of one distribution buffer (CUtensorMap, opaque here): tile
-// boxes TX x TY x {5, 9} components, halo boxes (TX+4) x (TY+4) x {5, 9}, and for
-// 32 x 8 tiles the halo-ring pieces (TX+4) x 2 x {5, 9} and 2 x TY x {5, 9}.
+// TMA descriptors of one distribution buffer (four CUtensorMap, opaque here):
+// tile boxes TX x TY x {5, 9} components, halo boxes (TX+4) x (TY+4) x {5, 9}.
 struct alignas(64) StepMaps {
-  unsigned char m[8][128];
+  unsigned char m[4][128];
   int ty;  // tile rows of the kernel these maps were made for
   bool ok;
 };
@@ -232,11 +231,6 @@ cudaError_t launch_step(const Geom& G, const DevParams& p, const double* A, doub
                         const Peers& pr = Peers{});
 // the warp-specialised variant of the step (lb_step_ws.cu): same maps, nx even.
 bool step_ws_fits(const StepMaps* maps);
-// the g-ring variant (lb_step_gr.cu; BGK + force, 32 x 8 tiles, nx even): the default
-bool step_gr_fits(const Geom& G, const StepMaps* maps);
-cudaError_t prepare_gr_kernels();
-cudaError_t launch_step_gr(const Geom& G, const DevParams& p, const double* A, double* B, const double* phig,
-                           const Launch& ln, const Health& hl, const StepMaps* maps, cudaStream_t st, const Peers& pr);
 // phi exchange (xch, single periodic slab): the stencil warps load only the g tile
 // and take the phi halo from the neighbouring tiles' CTAs through an L2-resident
 // phi array (nx*ny*nzl doubles) whose unwritten sites hold kXchEmpty: `cur` is

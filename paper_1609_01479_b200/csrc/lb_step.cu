@@ -476,11 +476,6 @@ bool make_step_maps(const Geom& G, const double* buf, int ty, StepMaps* out) {
   if (!encode_dist_map(&m[1], G, buf, kTX, ty, 9)) return false;
   if (!encode_dist_map(&m[2], G, buf, BX, BY, 5)) return false;
   if (!encode_dist_map(&m[3], G, buf, BX, BY, 9)) return false;
-  if (ty == 8) {  // halo-ring pieces of the g-ring kernel (lb_step_gr.cu)
-    if (!encode_dist_map(&m[4], G, buf, BX, 2, 5) || !encode_dist_map(&m[5], G, buf, BX, 2, 9) ||
-        !encode_dist_map(&m[6], G, buf, 2, ty, 5) || !encode_dist_map(&m[7], G, buf, 2, ty, 9))
-      return false;
-  }
   out->ok = true;
   return true;
 }

@@ -459,30 +459,20 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       tma_load_3d(&dst[14][0], &tm_t5, x0, y0, cp0 + 28, bar, pol);
     }
   };
-#ifndef LB_WS_FLDG
-#define LB_WS_FLDG 0
-#endif
-  if (!LB_WS_FLDG) issue_tile(zA, 0);
+  issue_tile(zA, 0);
   issue_tile(zA, 1);
   const int lx = tid % TX, ly = tid / TX;
   const int x = x0 + lx, y = y0 + ly;
   const bool active = (x < G.nx) && (y < G.ny);
   const int xm1 = wrapx(x - 1), xp1 = wrapx(x + 1), ym1 = wrapy(y - 1), yp1 = wrapy(y + 1);
-  const long long site_xy = (long long)(active ? y : 0) * G.nx + (active ? x : 0);
   for (int k = zA; k < zB; ++k) {
     double f[Q], g[Q];
-    if (LB_WS_FLDG) {
-      const double* fp = A + (long long)(k + GZ) * G.plane + site_xy;
-#pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = ldg_hint(fp + (long long)slot(0, i) * nxy, pol_f);
-    } else {
     mbar_wait(&sm.bar_f, ph_f);
     ph_f ^= 1;
 #pragma unroll
     for (int i = 0; i < Q; ++i) f[i] = sm.sTf[frank(i)][tid];
     named_sync(1, NT);  // sTf consumed
     if (k + 1 < zB) issue_tile(k + 1, 0);
-    }
     const int q = seq & 1, u = seq >> 1;
     mbar_wait(&sm.q_full[q], u & 1);
     const double ph = sm.sQ[q][0][tid], mu = sm.sQ[q][1][tid];

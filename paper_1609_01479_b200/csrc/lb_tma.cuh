@@ -64,12 +64,6 @@ __device__ __forceinline__ unsigned long long policy_of() {
 __device__ __forceinline__ unsigned long long policy_rt(int kind) {
   return kind == 0 ? policy_of<0>() : (kind == 1 ? policy_of<1>() : (kind == 2 ? policy_of<2>() : policy_of<3>()));
 }
-// read-only global load with an L2 policy (no L1 allocation)
-__device__ __forceinline__ double ldg_hint(const double* a, unsigned long long pol) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
-  return v;
-}
 // store with an L2 policy
 __device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
