@@ -414,6 +414,14 @@ cudaError_t prepare_kernel(const void* fn, size_t smem, int threads, int* resid)
   return cudaSuccess;
 }
 
+// L2 promotion of the TMA copies (the fill granularity of a miss): tiles and halo boxes
+#ifndef LB_TMA_PROMO_TILE
+#define LB_TMA_PROMO_TILE CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+#ifndef LB_TMA_PROMO_BOX
+#define LB_TMA_PROMO_BOX CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 // buffer viewed as a 3-D fp64 tensor {x: nx, y: ny, component-plane: (nzl+2GZ)*38}
 bool encode_dist_map(CUtensorMap* m, const Geom& G, const double* buf, unsigned bx, unsigned by, unsigned bz) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -429,8 +437,9 @@ bool encode_dist_map(CUtensorMap* m, const Geom& G, const double* buf, unsigned 
   cuuint64_t strides[2] = {(cuuint64_t)G.nx * 8, (cuuint64_t)G.nxy * 8};
   cuuint32_t box[3] = {bx, by, bz};
   cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapL2promotion promo = bx % 32 == 0 ? LB_TMA_PROMO_TILE : LB_TMA_PROMO_BOX;  // (tile rows: 32 sites)
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(buf), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

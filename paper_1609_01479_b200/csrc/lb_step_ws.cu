@@ -85,6 +85,11 @@ struct alignas(128) WsSmem {
   double sPhi[NPHI][NB];           // ring of phi planes on the box
   double sP[6][NP];                // chemical stress of one plane on the P box
   double sQ[2][NQ][NT];            // hand-off: phi, mu, then Fx, Fy, Fz (COLL 0) or P (COLL 1)
+  // box of a tile at a periodic edge: the TMA copy fills what lies inside the
+  // lattice (zeros outside); the wrapped column pair (all BY rows) and row pairs
+  // (all BX columns) come here by per-thread copies
+  alignas(16) double sWc[Q][XCH ? 1 : BY][2];
+  alignas(16) double sWr[Q][2][XCH ? 2 : BX];
   unsigned long long bar_f, bar_g, bar_box, bar_xb[2], q_full[2], q_empty[2];
 };
 
@@ -101,6 +106,12 @@ struct alignas(128) WsSmem {
 // one wave (the tiles' CTAs start together and stay within the lag of each
 // other: 128^3, 64^3); over several waves the neighbours drift apart and the
 // fallback sums cost more than the box.
+#ifdef LB_TRACE
+// block schedule trace (measurement build only, scripts/trace_schedule.py): per
+// block start / end globaltimer, SM, tile and first plane
+__device__ unsigned long long lb_trace_buf[1 << 16][4];
+#endif
+
 template <int TY, int COLL, bool XCH = false>
 __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     k_step_ws(Geom G, DevParams p, const double* __restrict__ A, double* __restrict__ B,
@@ -139,6 +150,15 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     fence_barrier_init();
   }
   __syncthreads();
+#ifdef LB_TRACE
+  if (tid == 0 && blockIdx.x < (1u << 16)) {
+    unsigned sm_id;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+    lb_trace_buf[blockIdx.x][0] = globaltimer_ns();
+    lb_trace_buf[blockIdx.x][2] = sm_id;
+    lb_trace_buf[blockIdx.x][3] = ((unsigned long long)tb.bx << 40) | ((unsigned long long)tb.by << 20) | (unsigned)zA;
+  }
+#endif
 
   if (tid >= NT) {
     // ============================ stencil warps ============================
@@ -170,6 +190,15 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     double Pz_prev[SPT][3], Pz_cur[SPT][3], Fxy_cur[SPT][3];
     double P6_cur[SPT][COLL == 1 ? 6 : 1];  // COLL 1: P at the site, plane j
     const bool box_interior = x0 >= 2 && x0 + TX + 2 <= G.nx && y0 >= 2 && y0 + TY + 2 <= G.ny;
+    // a whole tile at an edge of a lattice of >= 2 x 2 tiles: every box column or
+    // row wraps at most once, on one side (the side pieces); otherwise (narrow or
+    // ragged lattices) the whole box by per-thread copies
+    const bool box_side = !box_interior && x0 + TX <= G.nx && y0 + TY <= G.ny && G.nx >= 2 * TX && G.ny >= 2 * TY;
+    const int wcol = x0 == 0 ? 0 : (x0 + TX + 2 > G.nx ? TX + 2 : -1);  // first wrapped box column (a pair)
+    const int nrow_top = y0 < 2 ? 2 - y0 : 0;                           // wrapped box rows at the top ...
+    const int nrow_bot = y0 + TY + 2 > G.ny ? y0 + TY + 2 - G.ny : 0;   // ... and at the bottom (<= 2)
+    auto row_wrapped = [&](int r) { return r < nrow_top || r >= BY - nrow_bot; };
+    auto row_side = [&](int r) { return r < 2 ? r : r - (BY - 2); };  // slot of a wrapped row in sWr
     constexpr bool use_box = !XCH;
     // per-thread copy plan of a wrapped halo box: 16-byte units
     long long box_src[BOXR];
@@ -200,14 +229,33 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           tma_load_3d(dst + 5 * NT, &tm_t9, x0, y0, cpl + 19, bar, pol_last);
           tma_load_3d(dst + 14 * NT, &tm_t5, x0, y0, cpl + 33, bar, pol_last);
         }
-      } else if (box_interior) {
-        if (a == 0) {
+      } else if (box_interior || box_side) {
+        if (a == 0) {  // (at an edge the parts outside the lattice are zero-filled: the side pieces have them)
           const int cpl = (zs + GZ) * NSLOT;
           fence_proxy_async();
           mbar_expect_tx(&sm.bar_box, BOX_BYTES);
           tma_load_3d(&sm.sG[0][0], &tm_g5, x0 - 2, y0 - 2, cpl + 5, &sm.bar_box, pol_last);
           tma_load_3d(&sm.sG[5][0], &tm_g9, x0 - 2, y0 - 2, cpl + 19, &sm.bar_box, pol_last);
           tma_load_3d(&sm.sG[14][0], &tm_g5, x0 - 2, y0 - 2, cpl + 33, &sm.bar_box, pol_last);
+        }
+        if (box_side) {  // 16-byte copies: the wrapped column pair, then the wrapped rows
+          const double* base = A + (long long)(zs + GZ) * G.plane;
+          const int ncu = wcol >= 0 ? Q * BY : 0;
+          const int nrows = nrow_top + nrow_bot, nru = Q * nrows * (BX / 2);
+          for (int u = a; u < ncu + nru; u += kNA) {
+            if (u < ncu) {
+              const int j = u / BY, r = u - j * BY;
+              cp_async_v<2>(&sm.sWc[j][r][0], base + (long long)gslot_of_rank(j) * nxy +
+                                                   (long long)wrapy(y0 - 2 + r) * G.nx + wrapx(x0 - 2 + wcol));
+            } else {
+              const int v = u - ncu, j = v / (nrows * (BX / 2)), w = v - j * (nrows * (BX / 2));
+              const int q = w / (BX / 2), c = 2 * (w - q * (BX / 2));
+              const int r = q < nrow_top ? q : BY - nrow_bot + (q - nrow_top);
+              cp_async_v<2>(&sm.sWr[j][row_side(r)][c], base + (long long)gslot_of_rank(j) * nxy +
+                                                            (long long)wrapy(y0 - 2 + r) * G.nx + wrapx(x0 - 2 + c));
+            }
+          }
+          cp_commit();
         }
       } else {
         const double* base = A + (long long)(zs + GZ) * G.plane;
@@ -228,7 +276,8 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
         mbar_wait(&sm.bar_xb[n & 1], (ph_xb >> (n & 1)) & 1);
         ph_xb ^= 1u << (n & 1);
       } else if (issued) {
-        if (box_interior) {
+        if (box_interior || box_side) {
+          if (box_side) cp_wait<0>();
           mbar_wait(&sm.bar_box, ph_box);
           ph_box ^= 1;
         } else {
@@ -274,10 +323,22 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
       static_assert(BX % 2 == 0 && NB % 2 == 0, "pairs of box sites");
       for (int pb = a; pb < NB / 2; pb += kNA) {
         const int b = 2 * pb;
-        double2 v = *reinterpret_cast<const double2*>(&sm.sG[grank(0)][b]);
+        const double* src = &sm.sG[0][b];  // component rank j of the pair at src + j * stride
+        int stride = NB;
+        if (box_side) {
+          const int r = b / BX, c = b - r * BX;
+          if (wcol >= 0 && (c == wcol)) {
+            src = &sm.sWc[0][r][0];
+            stride = BY * 2;
+          } else if (row_wrapped(r)) {
+            src = &sm.sWr[0][row_side(r)][c];
+            stride = 2 * BX;
+          }
+        }
+        double2 v = *reinterpret_cast<const double2*>(src + grank(0) * stride);
 #pragma unroll
         for (int i = 1; i < Q; ++i) {
-          const double2 w = *reinterpret_cast<const double2*>(&sm.sG[grank(i)][b]);
+          const double2 w = *reinterpret_cast<const double2*>(src + grank(i) * stride);
           v.x += w.x;
           v.y += w.y;
         }
@@ -511,6 +572,9 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
   named_sync(1, NT);  // every thread's pushes before the CTA's publication
   if (tid == 0) {
     health_tick(hl);
+#ifdef LB_TRACE
+    if (blockIdx.x < (1u << 16)) lb_trace_buf[blockIdx.x][1] = globaltimer_ns();
+#endif
   }
 }
 
@@ -586,3 +650,13 @@ cudaError_t launch_step_ws(const Geom& G, const DevParams& p, const double* A, d
 }
 
 }  // namespace lbk
+
+#ifdef LB_TRACE
+// copy the trace of the last launches out and clear it (measurement build only)
+extern "C" int lb_debug_trace_get(unsigned long long* out, int nblocks) {
+  if (nblocks < 0 || nblocks > (1 << 16)) return 1;
+  static unsigned long long zero[1 << 16][4];
+  return cudaMemcpyFromSymbol(out, lbk::lb_trace_buf, (size_t)nblocks * 32) != cudaSuccess ||
+         cudaMemcpyToSymbol(lbk::lb_trace_buf, zero, sizeof(zero)) != cudaSuccess;
+}
+#endif

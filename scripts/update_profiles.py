@@ -69,7 +69,7 @@ with open(traffic_path, "w") as fh:
 # capture of the same call)
 TKEY = {"default": "k_step@c5", "c3": "k_step@c3", "c2": "k_step@c2", "c4": "k_step@c4", "mrt": "k_step@c5-mrt",
         "ch": "k_step@c5-ch", "lc": "k_step@c5-lc"}
-for f in ("default", "c3", "c2", "c4", "ref", "mrt", "ch", "lc"):
+for f in ("default", "c3", "c2", "c4", "c5alt", "ref", "mrt", "ch", "lc"):
     src = os.path.join(G, f"bench_{f}.json")
     if os.path.exists(src) and os.path.getsize(src) > 0:
         dst = os.path.join(P, f"{tag}_bench_{f}.json")
