@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
     unsigned sm_id;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
     lb_trace_buf[blockIdx.x][0] = globaltimer_ns();
-    lb_trace_buf[blockIdx.x][2] = sm_id;
+    lb_trace_buf[blockIdx.x][2] = ((unsigned long long)zB << 32) | sm_id;
     lb_trace_buf[blockIdx.x][3] = ((unsigned long long)tb.bx << 40) | ((unsigned long long)tb.by << 20) | (unsigned)zA;
   }
 #endif

@@ -49,18 +49,19 @@ with lb.Lattice(nx, ny, nz) as L:
         bx = (b[:, 3] >> 40).astype(np.int64)
         by = ((b[:, 3] >> 20) & 0xFFFFF).astype(np.int64)
         zA = (b[:, 3] & 0xFFFFF).astype(np.int64)
+        zb_ = (b[:, 2] >> 32).astype(np.int64)
         dur = (t1 - t0)
         n = len(b)
-        nch = n // ((nx // 32) * (ny // 8))
-        zc = -(-nz // nch)  # planes per block (32 x 8 tiles)
-        pt = dur.mean() / zc  # one plane-time, ns
+        zc = int(np.round(np.mean(zb_ - zA)))  # planes per block (mean)
+        pt = (dur / (zb_ - zA)).mean()  # one plane-time, ns
         # time each (tile, plane) is processed
         ntx, nty = nx // 32, ny // 8
         T = np.full((nty, ntx, nz), np.nan)
         for i in range(n):
-            for j in range(zc):
+            m = zb_[i] - zA[i]
+            for j in range(m):
                 p = (zA[i] + j) % nz
-                T[by[i], bx[i], p] = t0[i] + (j + 0.5) * dur[i] / zc
+                T[by[i], bx[i], p] = t0[i] + (j + 0.5) * dur[i] / m
         dy = np.abs(T - np.roll(T, -1, axis=0)) / pt
         dx = np.abs(T - np.roll(T, -1, axis=1)) / pt
         q = lambda a: [round(float(np.nanpercentile(a, v)), 2) for v in (10, 50, 90, 99)]
@@ -68,7 +69,7 @@ with lb.Lattice(nx, ny, nz) as L:
                   "dur_us_p10_50_90": [round(float(np.percentile(dur, v)) / 1e3, 1) for v in (10, 50, 90)],
                   "y_lag_planes_p10_50_90_99": q(dy), "x_lag_planes_p10_50_90_99": q(dx),
                   "start_spread_first_wave_us": round(float(np.sort(t0)[:148].max()) / 1e3, 2)}
-        sm = b[:, 2].astype(np.int64)
+        sm = (b[:, 2] & 0xFFFFFFFF).astype(np.int64)
         nsm = int(sm.max()) + 1
         sm_end = np.array([t1[sm == i].max() for i in range(nsm) if (sm == i).any()])
         sm_busy = np.array([dur[sm == i].sum() for i in range(nsm) if (sm == i).any()])
