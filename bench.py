@@ -323,22 +323,16 @@ def run_ours(args):
         D.barrier()
         return D.max_over_ranks(e0.elapsed_time(e1)), lb.lb_launch_count(L.h) - n0
 
-    # timed region 1 -> `value`: K steps, no per-launch instrumentation; then REPS
-    # more repetitions of it (min / median / stddev), clocks sampled throughout
+    # timed region 1 -> `value`: K steps, no per-launch instrumentation; region 2
+    # right after it (the same power-capped clock) -> `roofline`; then REPS more
+    # repetitions of region 1 (min / median / stddev); clocks sampled throughout
     clocks = ClockSampler(local)
     time.sleep(0.25)
     clocks.mark("start")
     ms, launches = timed_region()
-    rep_ms = [ms] + [timed_region()[0] for _ in range(REPS)]
-    clocks.mark("end")
-    clk = clocks.stop()
-    reps = {"n": len(rep_ms), "steps_each": K, "ms_per_step_min": min(rep_ms) / K,
-            "ms_per_step_median": statistics.median(rep_ms) / K, "ms_per_step_stddev": statistics.stdev(rep_ms) / K,
-            "mlups_max": nx * ny * nzf(world) * K / (min(rep_ms) * 1e-3) / 1e6,
-            "note": "value = the first region (exactly K steps); these are it and REPS more of the same K steps"}
-    # timed region 2 -> `roofline`: the same K steps with CUDA events around every
-    # kernel launch (per-kernel durations; the events cost ~8 us per step, which is
-    # why region 1 runs without them)
+    # timed region 2: the same K steps with CUDA events around every kernel launch
+    # (per-kernel durations; the events cost ~8 us per step, which is why region 1
+    # runs without them)
     D.barrier()
     torch.cuda.synchronize()
     lb.lb_profile_reset(L.h)
@@ -348,6 +342,14 @@ def run_ours(args):
     D.barrier()
     lb.lb_profile_enable(L.h, False)
     prof = lb.lb_profile(L.h)
+    rep_ms = [ms] + [timed_region()[0] for _ in range(REPS)]
+    clocks.mark("end")
+    clk = clocks.stop()
+    reps = {"n": len(rep_ms), "steps_each": K, "ms_per_step_min": min(rep_ms) / K,
+            "ms_per_step_median": statistics.median(rep_ms) / K, "ms_per_step_stddev": statistics.stdev(rep_ms) / K,
+            "mlups_max": nx * ny * nzf(world) * K / (min(rep_ms) * 1e-3) / 1e6,
+            "note": "value = the first region (exactly K steps); these are it and REPS more of the same K steps, "
+                    "run after the per-launch region that gives `roofline`"}
 
     sites_total = nx * ny * nz
     value = sites_total * K / (ms * 1e-3) / 1e6  # MLUPS, whole job
