@@ -62,6 +62,20 @@ for rep_name, launch_csv, suffix, key, sites, lat in CAPTURES:
         "src_hash": bench.src_hash(),
         "source": f"profiles/{tag}_ncu_full_kstep_{suffix}.txt (ncu --set full, {lat}, 1 launch)"}
     print("traffic:", key, traffic[key])
+# the Cahn-Hilliard kernel: DRAM bytes from a metrics-only capture (scripts/gpu_final_c.sh)
+ch_csv = os.path.join(G, "ncu_ch_dram.csv")
+if not os.path.exists(os.path.join(G, "prof_kstep_ch.ncu-rep")) and os.path.exists(ch_csv):
+    import csv
+    rows = [r for r in csv.reader(open(ch_csv)) if len(r) > 5]
+    i, v = rows[0].index("Metric Name"), rows[0].index("Metric Value")
+    m = {r[i]: float(r[v].replace(",", "")) for r in rows[1:]}
+    rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
+    shutil.copy(ch_csv, os.path.join(P, f"{tag}_ncu_kstep_ch_dram.csv"))
+    traffic["k_step@c5-ch"] = {
+        "dram_bytes_per_launch": rd + wr, "dram_read_bytes_per_site": round(rd / C5, 1),
+        "dram_write_bytes_per_site": round(wr / C5, 1), "src_hash": bench.src_hash(),
+        "source": f"profiles/{tag}_ncu_kstep_ch_dram.csv (ncu --metrics dram__bytes_*, 512x512x64, 1 launch)"}
+    print("traffic:", "k_step@c5-ch", traffic["k_step@c5-ch"])
 with open(traffic_path, "w") as fh:
     json.dump(traffic, fh, indent=1)
 # bench lines: roofline.traffic from the capture above when it was taken on the
