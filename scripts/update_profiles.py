@@ -1,4 +1,4 @@
-"""Refresh profiles/ from the artefacts scripts/gpu_full.sh (and scripts/gpu_lc.sh)
+"""Refresh profiles/ from the artefacts scripts/gpu_final_{a,b,c}.sh
 leave in gpurun_out/: ncu summary + per-line stall/instruction shares of the step
 kernels, the launch lists, traffic.json (keyed to the current source hash) and
 the bench lines.
