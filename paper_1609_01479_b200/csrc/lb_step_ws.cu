@@ -245,14 +245,16 @@ __global__ void __launch_bounds__(ws_threads(TY, XCH), 1)
           for (int u = a; u < ncu + nru; u += kNA) {
             if (u < ncu) {
               const int j = u / BY, r = u - j * BY;
-              cp_async_v<2>(&sm.sWc[j][r][0], base + (long long)gslot_of_rank(j) * nxy +
-                                                   (long long)wrapy(y0 - 2 + r) * G.nx + wrapx(x0 - 2 + wcol));
+              const long long o = (long long)wrapy(y0 - 2 + r) * G.nx + wrapx(x0 - 2 + wcol);
+              LB_CHECK(hl, j < Q && r < BY && o >= 0 && o + 1 < nxy);
+              cp_async_v<2>(&sm.sWc[j][r][0], base + (long long)gslot_of_rank(j) * nxy + o);
             } else {
               const int v = u - ncu, j = v / (nrows * (BX / 2)), w = v - j * (nrows * (BX / 2));
               const int q = w / (BX / 2), c = 2 * (w - q * (BX / 2));
               const int r = q < nrow_top ? q : BY - nrow_bot + (q - nrow_top);
-              cp_async_v<2>(&sm.sWr[j][row_side(r)][c], base + (long long)gslot_of_rank(j) * nxy +
-                                                            (long long)wrapy(y0 - 2 + r) * G.nx + wrapx(x0 - 2 + c));
+              const long long o = (long long)wrapy(y0 - 2 + r) * G.nx + wrapx(x0 - 2 + c);
+              LB_CHECK(hl, j < Q && row_side(r) >= 0 && row_side(r) < 2 && c + 1 < BX && o >= 0 && o + 1 < nxy);
+              cp_async_v<2>(&sm.sWr[j][row_side(r)][c], base + (long long)gslot_of_rank(j) * nxy + o);
             }
           }
           cp_commit();

@@ -53,7 +53,7 @@ def memsafe(L, name):
 
 print("bounds-checked build:", lb.lb_debug_checked(), flush=True)
 for (shape, kernel, nslabs, halo, steps) in [((16, 16, 16), 0, 1, None, 3), ((16, 16, 16), 2, 1, None, 2),
-                                             ((17, 12, 8), 1, 1, None, 2), ((64, 24, 6), 2, 1, None, 1),
+                                             ((17, 12, 8), 1, 1, None, 2), ((64, 24, 6), 2, 1, None, 1), ((96, 41, 6), 2, 1, None, 1),
                                              ((32, 16, 8), 0, 2, 1, 2), ((32, 16, 8), 1, 2, 1, 2),
                                              ((32, 16, 8), 0, 2, 0, 2)]:
     nx, ny, nz = shape

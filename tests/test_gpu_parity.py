@@ -156,6 +156,22 @@ def test_parity_rough_ragged(shape):
     assert_parity(gpu_run(f, g, P0, 5), R.run(f, g, P0, 5))
 
 
+@pytest.mark.parametrize("shape", [(96, 48, 8), (128, 41, 6)])
+def test_parity_edge_and_interior_tiles(shape):
+    """Interior tiles (the halo box by TMA) beside every kind of edge tile (the box
+    by TMA, zero-filled outside the lattice, with the wrapped column pair and rows
+    from side buffers): left / right columns, top / bottom rows -- ny = 41 leaves a
+    single wrapped row below the tile at y0 = 32 and a ragged last tile row (whole
+    box per thread) -- and the four corners, against the oracle at 1e-12; and
+    bitwise equal to the tile kernel (per-thread copies of every box)."""
+    nx, ny, nz = shape
+    f, g = rough(nx, ny, nz, seed=33)
+    ws = gpu_run(f, g, P0, 3, kernel=2)
+    assert_parity(ws, R.run(f, g, P0, 3))
+    tile = gpu_run(f, g, P0, 3, kernel=1)
+    assert np.array_equal(ws[0], tile[0]) and np.array_equal(ws[1], tile[1])
+
+
 def test_parity_64cubed_10_steps():
     f, g = spinodal(64, 64, 64, seed=2)
     assert_parity(gpu_run(f, g, P0, 10), R.run(f, g, P0, 10))
