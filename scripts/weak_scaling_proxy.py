@@ -1,10 +1,14 @@
-"""Weak-scaling proxy on one GPU: the per-rank work of the 512^3-at-8-GPUs weak
-scaling (BASELINE config 5, reading R20: 512 x 512 x 64 per rank) as P loopback
-z-slabs of one 512 x 512 x (64 P) lattice with the peer transport (K_phi edges,
-device-side epochs, P2P-style pushes into the neighbour slab, step kernel).  The
-slabs run one after another on one stream, so time per step / P is what one rank
-spends per step on its own GPU, without NVLink latency or waiting on a
-neighbour; efficiency proxy E(P) = t(1) / (t(P) / P).  One JSON line."""
+"""Scaling proxy on one GPU.  Weak (default): the per-rank work of the
+512^3-at-8-GPUs weak scaling (BASELINE config 5, reading R20: 512 x 512 x 64 per
+rank) as P loopback z-slabs of one 512 x 512 x (64 P) lattice with the peer
+transport (K_phi edges, device-side epochs, P2P-style pushes into the neighbour
+slab, step kernel).  The slabs run one after another on one stream, so time per
+step / P is what one rank spends per step on its own GPU, without NVLink latency
+or waiting on a neighbour; efficiency proxy E(P) = t(1) / (t(P) / P).
+--strong NX NY NZ: the fixed lattice (BASELINE config 4: 256^3) split into P
+slabs; a rank's step is t(P) / P, speed-up t(1) / (t(P) / P), E(P) = t(1) / t(P).
+  python scripts/weak_scaling_proxy.py STEPS P... [--strong NX NY NZ]
+One JSON line."""
 import json
 import os
 import sys
@@ -15,12 +19,18 @@ import torch  # noqa: E402
 
 from paper_1609_01479_b200 import lb, synth  # noqa: E402
 
-nx, ny, nzr = 512, 512, 64
-steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-ps = [int(v) for v in sys.argv[2:]] or [1, 2, 4, 8]
+argv = sys.argv[1:]
+strong = None
+if "--strong" in argv:
+    i = argv.index("--strong")
+    strong = [int(v) for v in argv[i + 1:i + 4]]
+    argv = argv[:i] + argv[i + 4:]
+nx, ny, nzr = strong or (512, 512, 64)
+steps = int(argv[0]) if argv else 20
+ps = [int(v) for v in argv[1:]] or [1, 2, 4, 8]
 out = {}
 for P in ps:
-    nz = nzr * P
+    nz = nzr if strong else nzr * P
     with lb.Lattice(nx, ny, nz, nslabs=P) as L:
         if P > 1:
             lb.lb_debug_halo_mode(L.h, 1)
@@ -44,9 +54,13 @@ for P in ps:
         lb.lb_profile_enable(L.h, False)
         prof = {k: round(v[0] / steps / P, 4) for k, v in lb.lb_profile(L.h).items() if v[1]}
     out[P] = {"ms_per_step": round(best, 4), "ms_per_rank_step": round(best / P, 4),
-              "mlups_per_rank": round(nx * ny * nzr / (best / P * 1e-3) / 1e6, 1), "kernel_ms_per_rank_step": prof}
-t1 = out[ps[0]]["ms_per_rank_step"] if ps[0] == 1 else None
-for P in ps:
-    if t1:
-        out[P]["efficiency_proxy"] = round(t1 / out[P]["ms_per_rank_step"], 4)
-print(json.dumps({"per_rank_lattice": [nx, ny, nzr], "transport": "peer (loopback)", "steps": steps, "by_P": out}))
+              "mlups_per_rank": round(nx * ny * (nz // P) / (best / P * 1e-3) / 1e6, 1),
+              "kernel_ms_per_rank_step": prof}
+if ps[0] == 1:
+    for P in ps:
+        t1, tp = out[1]["ms_per_step"], out[P]["ms_per_step"]
+        out[P]["efficiency_proxy"] = round(t1 / tp if strong else t1 / (tp / P), 4)
+        if strong:
+            out[P]["speedup_proxy"] = round(t1 / (tp / P), 3)
+print(json.dumps({"mode": "strong" if strong else "weak", "lattice" if strong else "per_rank_lattice": [nx, ny, nzr],
+                  "transport": "peer (loopback)", "steps": steps, "by_P": out}))
