@@ -122,11 +122,12 @@ def ncu_traffic(kernel: str, config: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms while running."""
+    """nvidia-smi clocks, throttle reasons and board power sampled every 100 ms
+    while running."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,enforced.power.limit")
 
     def __init__(self, gpu_index: int):
         self.rows, self.marks = [], {}
@@ -164,8 +165,19 @@ class ClockSampler:
         mx = [float(p[1]) for p in inside if p[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for p in inside for k in range(4) if p[3 + k].lower() == "active"})
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        pw = [num(p[7]) for p in inside if len(p) > 7 and num(p[7]) is not None]
+        lim = [num(p[8]) for p in inside if len(p) > 8 and num(p[8]) is not None]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(inside)}
+                "reasons": reasons, "samples": len(inside),
+                "power_w_median": statistics.median(pw) if pw else None,
+                "power_limit_w": max(lim) if lim else None}
 
 
 # ------------------------------------------------------------------------------ oracle arm
