@@ -354,10 +354,13 @@ __global__ void __launch_bounds__(kLT, 1)
       double f[Q];
 #pragma unroll
       for (int i = 0; i < Q; ++i) f[i] = sm.sF[((k) & 1)][frank(i)][tid];
-      // A.8 push targets: periodic in z for a whole lattice, else planes -1 / nzl are
-      // the ghost planes the exchange sends to the neighbouring slabs
-      double* const zb[3] = {push_plane(G, B, Peers{}, k - 1), push_plane(G, B, Peers{}, k),
-                             push_plane(G, B, Peers{}, k + 1)};
+      // A.8 push targets (push_plane of lb_kernels.cuh without peers, spelled out
+      // for the three planes): periodic in z for a whole lattice, else planes -1 /
+      // nzl are the ghost planes the exchange sends to the neighbouring slabs
+      const long long pl = G.plane;
+      double* const zk = B + (long long)(k + GZ) * pl;
+      double* const zb[3] = {G.zwrap && k == 0 ? B + (long long)(G.nzl - 1 + GZ) * pl : zk - pl, zk,
+                             G.zwrap && k == G.nzl - 1 ? B + (long long)GZ * pl : zk + pl};
       const double g0[Q] = {};
       double un[3];
       const double rho = collide(
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(kLT, 1)
             const int xd = cx(i) > 0 ? xp1 : (cx(i) < 0 ? xm1 : x);
             const int yd = cy(i) > 0 ? yp1 : (cy(i) < 0 ? ym1 : y);
             LB_CHECK(hl, xd >= 0 && xd < G.nx && yd >= 0 && yd < G.ny);
-            double* d = zb[cz(i) + 1] + (long long)yd * G.nx + xd;
+            double* d = zb[cz(i) + 1] + (yd * G.nx + xd);  // in-plane offset < nx ny < 2^31
             __stcs(d + (long long)slot(0, i) * nxy, fs);
           },
           un);
@@ -386,14 +389,19 @@ __global__ void __launch_bounds__(kLT, 1)
       const double ufy_p = 0.5 * (uk[1][cu] + uk[1][cu + UX]), ufy_m = 0.5 * (uk[1][cu - UX] + uk[1][cu]);
       const double ufz_p = 0.5 * (uk[2][cu] + up[2]), ufz_m = 0.5 * (um[2] + uk[2][cu]);
       auto J = [](double uf, double qa, double qb) { return uf * (uf > 0.0 ? qa : qb); };
+      // in-plane faces: the upwind site is chosen once per face for all five
+      // components (an offset into the Q box: Qk[c][cq] is q0[c]), so each flux is
+      // one load and one product, the same values as J
+      const int oxp = ufx_p > 0.0 ? cq : cq + 1, oxm = ufx_m > 0.0 ? cq - 1 : cq;
+      const int oyp = ufy_p > 0.0 ? cq : cq + BX, oym = ufy_m > 0.0 ? cq - BX : cq;
       const long long zq = (long long)k * 5 * nxy + (long long)y * G.nx + x;
       double chk = rho;
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         const double v = q0[c];
         double div = 0.0;
-        div = div + (J(ufx_p, v, Qk[c][cq + 1]) - J(ufx_m, Qk[c][cq - 1], v));
-        div = div + (J(ufy_p, v, Qk[c][cq + BX]) - J(ufy_m, Qk[c][cq - BX], v));
+        div = div + (ufx_p * Qk[c][oxp] - ufx_m * Qk[c][oxm]);
+        div = div + (ufy_p * Qk[c][oyp] - ufy_m * Qk[c][oym]);
         div = div + (J(ufz_p, v, q1[c]) - J(ufz_m, qm1[c], v));
         const double qn = ((v - div) + S5[c]) + p.lc_Gamma * H0[c];
         __stcs(qB + zq + c * nxy, qn);
